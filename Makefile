@@ -1,0 +1,34 @@
+# Builds the B200 product library paper_2401_09792_b200/_build/libgwt_b200.so
+# (sm_100a only) and the oracle (test infrastructure).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v
+CXXFLAGS := -O3 -std=c++17 -fPIC -Wall
+PKG := paper_2401_09792_b200
+SRC := $(PKG)/csrc
+OBJ := $(PKG)/_build/obj
+LIB := $(PKG)/_build/libgwt_b200.so
+CU := $(wildcard $(SRC)/*.cu)
+CUO := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU))
+HDR := $(wildcard $(SRC)/*.cuh) include/gwt_b200.h
+
+all: $(LIB) oracle
+
+$(OBJ)/%.o: $(SRC)/%.cu $(HDR)
+	@mkdir -p $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
+
+$(OBJ)/generate.o: $(SRC)/generate.cpp include/gwt_b200.h
+	@mkdir -p $(OBJ)
+	g++ $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(CUO) $(OBJ)/generate.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -lpthread
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf $(PKG)/_build oracle/_build
+
+.PHONY: all oracle clean

@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path (BASELINE.json metric) — one JSON line on rank 0.
+
+Workload: BASELINE.json configs[1] (C2): Nr=4, Nt=64, K=32 submatrices, G=16
+channels/group, 64 groups, 272 subcarriers, ranks (4,24,12), complex64, MMSE
+SINR at 10 dB, 4 streams (J=2, K=G/4 mapping, paper_experiment scope;
+DESIGN.md §2). A "step" is one pass of the compressed-form SINR stage
+(rebuild + precoder + MMSE over all groups x subcarriers) — the headline
+metric "SINR evals/sec" (one eval = one user x one subcarrier, all streams).
+The Tucker stage (groupwise_solve, 20 fixed sweeps, all groups) is timed in
+the same run and reported under "tucker" (Tucker channels/sec).
+
+Multi-GPU (torchrun): weak scaling — each rank compresses and evaluates its
+own C2-sized block of groups (group offset rank*64); no data-path collective;
+one NCCL all_reduce of a small stats vector at the end; times are max over ranks.
+
+--impl reference: times the reference algorithm's CPU implementation (the
+oracle restatement — the reference itself needs Eigen, absent here) on this
+host's cores for the same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], "measured", d
+    except Exception:
+        return 6650.0, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) > 8:
+                for n, v in zip(names, r[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic cost model
+
+def sinr_costs(cfg, cs):
+    """Per stage algorithmic (flops, bytes) for one SINR step over the whole batch."""
+    J, K, m, n, p, P, L = cfg.J, cfg.K, cfg.m, cfg.n, cfg.p, cfg.P, cfg.L
+    links, users, F, g = cfg.G, cfg.G // 2, cfg.F, cfg.groups
+    S = J
+    rebuild_flops = 8 * (m * n * p + P * p) * links * F * g
+    rebuild_bytes = (cs * m * n * links * F + cs * (m * n * p + P * p) * links + 8 * P * links) * g
+    gram_flops = 8 * S * m * m * n * users * F * g
+    gram_bytes = (cs * m * n * links * F + 16 * S * m * m * users * F) * g
+    small_bytes = (16 * S * m * m + 8 * (L + 2 * m * L) * 2 + 16 * L + 4) * users * F * g
+    return dict(rebuild=(rebuild_flops, rebuild_bytes), pair_gram=(gram_flops, gram_bytes),
+                small=(None, small_bytes))
+
+
+def tucker_flops(cfg):
+    """Canonical-order flops of one groupwise_solve (init + S sweeps) per SURVEY.md §8(d)."""
+    M, N, P, m, n, p, S = cfg.M, cfg.N, cfg.P, cfg.m, cfg.n, cfg.p, cfg.sweeps
+    init = M * M * N * P + N * N * M * P + P * P * M * N
+    rx = min(M * N * P * n + M * n * P * p, M * N * P * p + M * N * p * n) + M * M * n * p
+    tx = min(m * M * N * P + m * N * P * p, M * N * P * p + m * M * N * p) + N * N * m * p
+    de = min(m * M * N * P + m * n * N * P, M * N * P * n + m * M * n * P) + P * P * m * n
+    obj = m * n * P * p
+    return 8 * (init + S * (rx + tx + de + obj)) * cfg.links
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args, cfg):
+    import paper_2401_09792_b200 as gw
+    from oracle import oracle as O
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    topo = cfg.topology()
+    dims = dict(J=cfg.J, K=cfg.K, M=cfg.M, N=cfg.N, P=cfg.P, m=cfg.m, n=cfg.n, p=cfg.p)
+    # bounded sample of the same workload: 2*cores groups x 64 subcarriers per step
+    gs = min(cfg.groups, 2 * cores)
+    fs = min(cfg.F, 64)
+    X, tau = gw.generate_channels(topo, gs, seed=0, dtype=np.complex128)
+    if cfg.dtype == "c64":
+        X = X.astype(np.complex64).astype(np.complex128)
+    fo = O.alternating_solve(dims, X, 2, early_stop=False, nthreads=cores)
+    co = O.coeffs_from_tau(tau, cfg.freqs()[:fs])
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.sinr_compressed(dims, fo["C"], fo["G"], co, cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    evals = gs * fs * cfg.J * cfg.K
+    v = evals / statistics.median(times)
+    t0 = time.perf_counter()
+    O.alternating_solve(dims, X[: min(gs, cores)], cfg.sweeps, early_stop=False, nthreads=cores)
+    tuck = min(gs, cores) * cfg.G / (time.perf_counter() - t0)
+    line = {
+        "impl": "reference", "metric": "SINR evals/sec", "value": v, "unit": "evals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
+        "data": "synthetic (BASELINE.json generator, seed 0)",
+        "config": {"workload": cfg.name, "groups": cfg.groups, "subcarriers": cfg.F, "ranks": [cfg.m, cfg.n, cfg.p],
+                   "streams": cfg.L, "snr_db": cfg.snr_db, "scope": "paper_experiment"},
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "port",
+                         "sample": f"{gs} groups x {fs} subcarriers per step (of {cfg.groups} x {cfg.F}); "
+                                   "oracle C++ restatement, one group per std::thread"},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "tucker": {"value": tuck, "unit": "channels/s", "sample": f"{min(gs, cores)} groups x {cfg.sweeps} sweeps"},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_leg(cfg, cores):
+    """Oracle (port) on the host, bounded sample ~10 s; rank 0 at N=1 only."""
+    import paper_2401_09792_b200 as gw
+    from oracle import oracle as O
+    dims = dict(J=cfg.J, K=cfg.K, M=cfg.M, N=cfg.N, P=cfg.P, m=cfg.m, n=cfg.n, p=cfg.p)
+    gs = min(cfg.groups, 2 * cores)
+    fs = min(cfg.F, 64)
+    X, tau = gw.generate_channels(cfg.topology(), gs, seed=0, dtype=np.complex128)
+    if cfg.dtype == "c64":
+        X = X.astype(np.complex64).astype(np.complex128)
+    t0 = time.perf_counter()
+    fo = O.alternating_solve(dims, X, cfg.sweeps, early_stop=False, nthreads=cores)
+    t_tuck = time.perf_counter() - t0
+    co = O.coeffs_from_tau(tau, cfg.freqs()[:fs])
+    t0 = time.perf_counter()
+    O.sinr_compressed(dims, fo["C"], fo["G"], co, cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=cores)
+    t_s = time.perf_counter() - t0
+    return {"value": gs * fs * cfg.J * cfg.K / t_s, "unit": "evals/s", "cores": cores, "kind": "port",
+            "sample": f"SINR: {gs} groups x {fs} subcarriers; Tucker: {gs} groups x {cfg.sweeps} sweeps "
+                      f"(oracle C++ restatement in fp64, one group per std::thread)",
+            "tucker_channels_per_s": gs * cfg.G / t_tuck}
+
+
+def main():
+    args = parse()
+    import paper_2401_09792_b200 as gw
+    cfg = gw.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = gw.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.use_torch_stream()
+    topo, ranks = cfg.topology(), cfg.ranks()
+    npdt = np.complex64 if cfg.dtype == "c64" else np.complex128
+    cs = 8 if cfg.dtype == "c64" else 16
+
+    # inputs: this rank's block of groups, resident in HBM
+    Xh, tau_h = gw.generate_channels(topo, cfg.groups, seed=0, dtype=np.complex128, group0=rank * cfg.groups)
+    Xh = Xh.astype(npdt)
+    X = torch.from_numpy(Xh).to(dev)
+    tau = torch.from_numpy(tau_h).to(dev)
+    freqs = torch.from_numpy(cfg.freqs()).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- Tucker stage (device-resident), fixed 20 sweeps
+    fac = None
+    for _ in range(max(1, args.warmup // 2)):
+        fac = ctx.groupwise_solve(topo, X, ranks, cfg.sweeps, early_stop=False)
+    barrier()
+    tt = []
+    tucker_steps = max(2, min(args.steps, 5))
+    for _ in range(tucker_steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fac = ctx.groupwise_solve(topo, X, ranks, cfg.sweeps, early_stop=False)
+        e1.record(stream)
+        e1.synchronize()
+        tt.append(e0.elapsed_time(e1))
+    tucker_stage = ctx.stage_ms()
+    barrier()
+
+    # ---------------- SINR stage (the step), device-resident inputs
+    for _ in range(args.warmup):
+        rep = ctx.run_compressed_pipeline(topo, fac, ranks, tau=tau, freqs=freqs)
+    barrier()
+    launches0 = ctx.launches
+    step_ms, st_acc = [], np.zeros(8)
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rep = ctx.run_compressed_pipeline(topo, fac, ranks, tau=tau, freqs=freqs)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            st_acc += np.array(rep.stage_ms)
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    launches = ctx.launches - launches0
+    ms = float(np.mean(step_ms))
+    st_acc /= args.steps
+    tk = float(np.mean(tt))
+    stats = torch.tensor([ms, tk, float(rep.status.ne(0).sum())], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)  # only collective: max-over-ranks times + status
+    ms, tk, bad = stats.tolist()
+    evals = cfg.groups * cfg.F * cfg.J * cfg.K * world
+    value = evals / (ms * 1e-3)
+
+    # ---------------- e2e through the public API with pinned host buffers
+    Ch = rep_in = None
+    Ch = fac.delay.cpu().pin_memory()
+    Gh = fac.cores.cpu().pin_memory()
+    tauh = torch.from_numpy(tau_h).pin_memory()
+    fh = torch.from_numpy(cfg.freqs()).pin_memory()
+    ctx_h = gw.Context(local)
+    e2e_ms = []
+    for it in range(max(args.warmup, 1) + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fh_fac = gw.GroupwiseFactorSet(None, None, Ch, Gh)
+        rep_h = ctx_h.run_compressed_pipeline(topo, fh_fac, ranks, tau=tauh, freqs=fh)
+        t1 = time.perf_counter()
+        if it >= max(args.warmup, 1):
+            e2e_ms.append((t1 - t0) * 1e3)
+    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    h2d = Ch.numel() * cs + Gh.numel() * cs + tauh.numel() * 8 + fh.numel() * 8
+    d2h = rep_h.sinr.numel() * 8 * 2 + rep_h.status.numel() * 4
+    # Tucker e2e: host X in, factors out
+    Xpin = torch.from_numpy(Xh).pin_memory()
+    t0 = time.perf_counter()
+    fac_h = ctx_h.groupwise_solve(topo, Xpin, ranks, cfg.sweeps, early_stop=False)
+    tuck_e2e_ms = (time.perf_counter() - t0) * 1e3
+    ctx_h.close()
+
+    # ---------------- roofline of the dominant SINR kernel
+    hbm, peak_kind, pk = peaks()
+    costs = sinr_costs(cfg, cs)
+    stage = {"rebuild": st_acc[4], "pair_gram": st_acc[5], "small": st_acc[6]}
+    dom = max(stage, key=stage.get)
+    fl, by = costs[dom]
+    achieved = by / (stage[dom] * 1e-3) / 1e9
+    roof = {"kernel": {"rebuild": "k_rebuild", "pair_gram": "k_pair_gram", "small": "k_precoder_eig+k_mmse"}[dom],
+            "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": None, "peak_source": peak_kind,
+            "stage_ms": {k: round(v, 4) for k, v in stage.items()},
+            "stage_share": {k: round(v / max(sum(stage.values()), 1e-9), 3) for k, v in stage.items()}}
+    tfl = tucker_flops(cfg) * world
+    fp32_peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    tucker = {"value": cfg.links * world / (tk * 1e-3), "unit": "channels/s", "ms_per_solve": tk,
+              "sweeps": cfg.sweeps, "mode": "fixed sweeps (no early stop)",
+              "algorithmic_tflops": tfl / (tk * 1e-3) / 1e12,
+              "roofline": {"bound": "fp32-cuda-core", "achieved": tfl / (tk * 1e-3) / 1e12, "peak": fp32_peak,
+                           "unit": "TFLOP/s", "frac": tfl / (tk * 1e-3) / 1e12 / fp32_peak,
+                           "peak_source": "derived 148 SMs x 128 FFMA x 2 x max clock (not measured)"},
+              "stage_ms": {"init_obj": tucker_stage[1], "sweeps": tucker_stage[2]},
+              "e2e_ms": tuck_e2e_ms, "e2e_h2d_bytes": Xh.nbytes,
+              "e2e_d2h_bytes": sum(int(np.prod(a.shape)) * cs for a in (fac_h.rx, fac_h.tx, fac_h.delay, fac_h.cores))}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_leg(cfg, os.cpu_count() or 1)
+    if rank == 0:
+        line = {
+            "metric": "SINR evals/sec", "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c64 (fp32 rebuild/products; fp64 Grams and m x m solves)",
+            "data": "synthetic (BASELINE.json generator: 1 ray/tap ULA, exp PDP 0.3, tau U(0,1us), seed 0)",
+            "config": {"workload": cfg.name, "groups_per_gpu": cfg.groups, "subcarriers": cfg.F,
+                       "dims": [cfg.M, cfg.N, cfg.P], "ranks": [cfg.m, cfg.n, cfg.p], "streams": cfg.L,
+                       "snr_db": cfg.snr_db, "scope": "paper_experiment", "J": cfg.J, "K": cfg.K,
+                       "parallelism": f"group-sharded x{world}", "l2": "flushed (256 MB write) between steps"},
+            "e2e": {"value": evals / (e2e_t.item() * 1e-3), "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "tucker": tucker,
+            "clocks": clk.summary(),
+            "status_nonzero": int(bad),
+            "wall_s_timed": t_wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

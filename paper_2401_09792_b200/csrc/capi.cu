@@ -1,0 +1,800 @@
+// extern "C" boundary (include/gwt_b200.h) and host-side orchestration of the
+// B200 kernels. Validation mirrors the reference's exception texts
+// (proj/src/{decompose,sinr,channel}.cpp); no exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gwt_b200.h"
+#include "kernels.cuh"
+
+using namespace gwtk;
+
+namespace {
+
+struct GwtError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw GwtError{code, msg}; }
+[[noreturn]] void invalid(const std::string& msg) { fail(GWT_INVALID_ARGUMENT, msg); }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(GWT_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+struct gwt_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string last_error;
+    int64_t launches = 0;
+    struct Slot {
+        void* p = nullptr;
+        size_t bytes = 0;
+    };
+    std::vector<Slot> slots = std::vector<Slot>(32);
+    cudaEvent_t ev[16] = {};
+    double stage_ms[8] = {};
+
+    void* ws(int slot, size_t bytes) {
+        Slot& s = slots[slot];
+        if (bytes == 0) bytes = 16;
+        if (s.bytes < bytes) {
+            if (s.p) ck(cudaFree(s.p), "cudaFree");
+            s.p = nullptr;
+            s.bytes = 0;
+            ck(cudaMalloc(&s.p, bytes), "cudaMalloc(workspace)");
+            s.bytes = bytes;
+        }
+        return s.p;
+    }
+    void launched(cudaError_t e, int n = 1) {
+        ck(e, "kernel launch");
+        launches += n;
+    }
+};
+
+namespace {
+
+// workspace slots
+enum {
+    WS_X = 0, WS_A, WS_B, WS_C, WS_G, WS_Y1, WS_W, WS_W2, WS_Z, WS_Z2, WS_GRAM, WS_EIGA, WS_EIGZ, WS_EIGX, WS_POOL,
+    WS_ENERGY, WS_CAPT, WS_TRACE, WS_FAIL, WS_FROZEN, WS_TAU, WS_FREQ, WS_COEF, WS_H, WS_PG, WS_EG, WS_SINR, WS_SIG,
+    WS_STATUS, WS_MISC
+};
+
+size_t ws_budget() {
+    const char* e = std::getenv("GWT_WS_BYTES");
+    if (e) return static_cast<size_t>(std::strtoull(e, nullptr, 10));
+    return size_t(16) << 30;  // 16 GiB of the 180 GB HBM for intermediates
+}
+
+template <class F>
+int guarded(gwt_ctx* ctx, F&& f) {
+    if (!ctx) return GWT_INVALID_ARGUMENT;
+    try {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        f();
+        ctx->last_error.clear();
+        return GWT_OK;
+    } catch (const GwtError& e) {
+        ctx->last_error = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        ctx->last_error = e.what();
+        return GWT_RUNTIME_ERROR;
+    }
+}
+
+void validate_topology(const gwt_topology& t) {  // SystemTopology::validate (channel.cpp)
+    if (t.num_cells < 1) invalid("topology: num_cells (J) must be >= 1");
+    if (t.users_per_cell < 1) invalid("topology: users_per_cell (K) must be >= 1");
+    if (t.rx_antennas < 1) invalid("topology: rx_antennas (M) must be >= 1");
+    if (t.tx_antennas < 1) invalid("topology: tx_antennas (N) must be >= 1");
+    if (t.num_taps < 1) invalid("topology: num_taps (P) must be >= 1");
+    if (t.num_streams < 1) invalid("topology: num_streams (L) must be >= 1");
+    if (t.num_streams > std::min(t.rx_antennas, t.tx_antennas))
+        invalid("topology: num_streams (L) must satisfy L <= min(M, N)");
+    if (!(t.noise_std > 0.0)) invalid("topology: noise_std (sigma) must be > 0");
+}
+
+void validate_ranks(const gwt_ranks& r, int d1, int d2, int d3) {  // decompose.cpp:58-68
+    if (r.m < 1 || r.m > d1)
+        invalid("rank m = " + std::to_string(r.m) + " out of range for mode-1 size " + std::to_string(d1));
+    if (r.n < 1 || r.n > d2)
+        invalid("rank n = " + std::to_string(r.n) + " out of range for mode-2 size " + std::to_string(d2));
+    if (r.p < 1 || r.p > d3)
+        invalid("rank p = " + std::to_string(r.p) + " out of range for mode-3 size " + std::to_string(d3));
+}
+
+Topo mk_topo(const gwt_topology& t, const gwt_ranks& r) {
+    Topo o;
+    o.J = t.num_cells; o.K = t.users_per_cell; o.M = t.rx_antennas; o.N = t.tx_antennas; o.P = t.num_taps;
+    o.m = r.m; o.n = r.n; o.p = r.p; o.L = t.num_streams;
+    return o;
+}
+
+struct Timer {
+    gwt_ctx* ctx;
+    int n = 0;
+    explicit Timer(gwt_ctx* c) : ctx(c) {
+        for (auto& e : ctx->ev)
+            if (!e) ck(cudaEventCreate(&e), "cudaEventCreate");
+    }
+    void mark(int i) { ck(cudaEventRecord(ctx->ev[i], ctx->stream), "cudaEventRecord"); }
+    float between(int a, int b) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]);
+        return ms;
+    }
+};
+
+size_t csize(gwt_dtype dt) { return dt == GWT_C64 ? 8 : 16; }
+
+// ---------------------------------------------------------------------------
+// Tucker solve on device pointers for one chunk of groups.
+template <class T>
+void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int sweeps, unsigned flags, void* A, void* B,
+                 void* Cf, void* Gc, double* trace_d, std::vector<int>& iters, std::vector<double>& trace_h,
+                 std::vector<double>& energy_h, double* ms) {
+    using Cx = cplx_t<T>;
+    const size_t cs = sizeof(Cx);
+    cudaStream_t st = ctx->stream;
+    const int links = t.links(), users = t.users();
+    const int64_t MNP = (int64_t)t.M * t.N * t.P;
+    const bool pooled = flags & GWT_SOLVE_POOLED;
+    const bool early = flags & GWT_SOLVE_EARLY_STOP;
+    void* Y1 = ctx->ws(WS_Y1, cs * G * links * t.M * t.N * t.p);
+    void* W = ctx->ws(WS_W, cs * G * links * t.M * t.n * t.p);
+    void* W2 = ctx->ws(WS_W2, cs * G * links * t.m * t.N * t.p);
+    void* Z = ctx->ws(WS_Z, cs * G * links * t.m * t.N * t.P);
+    void* Z2 = ctx->ws(WS_Z2, cs * G * links * t.m * t.n * t.P);
+    const int64_t gram_elems = std::max({(int64_t)G * users * t.M * t.M, (int64_t)G * t.J * t.N * t.N,
+                                         (int64_t)G * links * t.P * t.P});
+    void* gram = ctx->ws(WS_GRAM, cs * gram_elems);
+    const int64_t eig_a = std::max({(int64_t)G * users * t.M * t.M, (int64_t)G * t.J * t.N * t.N,
+                                    (int64_t)G * links * t.P * t.P});
+    const int64_t eig_x = std::max({(int64_t)G * users * t.M * t.m, (int64_t)G * t.J * t.N * t.n,
+                                    (int64_t)G * links * t.P * t.p});
+    double2* eA = (double2*)ctx->ws(WS_EIGA, 16 * eig_a);
+    double* eZ = (double*)ctx->ws(WS_EIGZ, 8 * eig_a);
+    double2* eX = (double2*)ctx->ws(WS_EIGX, 16 * eig_x);
+    void* pool = ctx->ws(WS_POOL, cs * G * std::max(t.M * t.m, t.N * t.n));
+    double* energy = (double*)ctx->ws(WS_ENERGY, 8 * G);
+    double* capt = (double*)ctx->ws(WS_CAPT, 8 * G);
+    int* failp = (int*)ctx->ws(WS_FAIL, 4);
+    ck(cudaMemsetAsync(failp, 0, 4, st), "memset");
+
+    auto gemm = [&](const GemmDesc& d, const void* in, const void* U, void* out) {
+        ctx->launched(launch_cgemm<T>(t, d, G, in, U, out, st));
+    };
+    auto gram_eig = [&](const GramDesc& d, const void* V, int D, int count, void* out_factor, int copies) {
+        // copies > 0: pooled (one set per group) broadcast to `copies` factors
+        const int sets = d.set_kind == FI_USER ? users : d.set_kind == FI_BASE ? t.J : d.set_kind == FI_LINK ? links : 1;
+        ctx->launched(launch_gram<T>(t, d, G, sets, V, gram, st));
+        void* dst = copies > 0 ? pool : out_factor;
+        ctx->launched(launch_heev_topk<T>(D, count, G * sets, gram, dst, nullptr, eA, eZ, eX, failp, st));
+        if (copies > 0) ctx->launched(launch_broadcast<T>(pool, out_factor, (int64_t)D * count, copies, G, st));
+    };
+    // mode-product descriptors
+    GemmDesc dZ{};  // Z = X x1 A^H  (m x N x P)
+    dZ.R = t.N * t.P; dZ.S = 1; dZ.Kd = t.M; dZ.Cols = t.m;
+    dZ.in_item = MNP; dZ.rs_in = t.M; dZ.s_in = 0; dZ.ks_in = 1;
+    dZ.out_item = (int64_t)t.m * t.N * t.P; dZ.rs_out = t.m; dZ.s_out = 0; dZ.cs_out = 1; dZ.fkind = FI_USER;
+    GemmDesc dZ2{};  // Z2 = Z x2 B^H (m x n x P)
+    dZ2.R = t.m; dZ2.S = t.P; dZ2.Kd = t.N; dZ2.Cols = t.n;
+    dZ2.in_item = (int64_t)t.m * t.N * t.P; dZ2.rs_in = 1; dZ2.s_in = (int64_t)t.m * t.N; dZ2.ks_in = t.m;
+    dZ2.out_item = (int64_t)t.m * t.n * t.P; dZ2.rs_out = 1; dZ2.s_out = (int64_t)t.m * t.n; dZ2.cs_out = t.m;
+    dZ2.fkind = FI_BASE;
+    GemmDesc dG{};  // core = Z2 x3 C^H (m x n x p)
+    dG.R = t.m * t.n; dG.S = 1; dG.Kd = t.P; dG.Cols = t.p;
+    dG.in_item = (int64_t)t.m * t.n * t.P; dG.rs_in = 1; dG.s_in = 0; dG.ks_in = (int64_t)t.m * t.n;
+    dG.out_item = (int64_t)t.m * t.n * t.p; dG.rs_out = 1; dG.s_out = 0; dG.cs_out = (int64_t)t.m * t.n;
+    dG.fkind = FI_LINK;
+    GemmDesc dY1{};  // Y1 = X x3 C^H (M x N x p)
+    dY1.R = t.M * t.N; dY1.S = 1; dY1.Kd = t.P; dY1.Cols = t.p;
+    dY1.in_item = MNP; dY1.rs_in = 1; dY1.s_in = 0; dY1.ks_in = (int64_t)t.M * t.N;
+    dY1.out_item = (int64_t)t.M * t.N * t.p; dY1.rs_out = 1; dY1.s_out = 0; dY1.cs_out = (int64_t)t.M * t.N;
+    dY1.fkind = FI_LINK;
+    GemmDesc dW{};  // W = Y1 x2 B^H (M x n x p)
+    dW.R = t.M; dW.S = t.p; dW.Kd = t.N; dW.Cols = t.n;
+    dW.in_item = (int64_t)t.M * t.N * t.p; dW.rs_in = 1; dW.s_in = (int64_t)t.M * t.N; dW.ks_in = t.M;
+    dW.out_item = (int64_t)t.M * t.n * t.p; dW.rs_out = 1; dW.s_out = (int64_t)t.M * t.n; dW.cs_out = t.M;
+    dW.fkind = FI_BASE;
+    GemmDesc dW2{};  // W2 = Y1 x1 A^H (m x N x p)
+    dW2.R = t.N * t.p; dW2.S = 1; dW2.Kd = t.M; dW2.Cols = t.m;
+    dW2.in_item = (int64_t)t.M * t.N * t.p; dW2.rs_in = t.M; dW2.s_in = 0; dW2.ks_in = 1;
+    dW2.out_item = (int64_t)t.m * t.N * t.p; dW2.rs_out = t.m; dW2.s_out = 0; dW2.cs_out = 1; dW2.fkind = FI_USER;
+
+    const int rx_kind = pooled ? FI_GROUP : FI_USER, tx_kind = pooled ? FI_GROUP : FI_BASE;
+    const int rx_copies = pooled ? users : 0, tx_copies = pooled ? t.J : 0;
+
+    Timer tm(ctx);
+    tm.mark(1);
+    ctx->launched(launch_group_sqnorm<T>(X, links * MNP, G, energy, st));
+    if (!(flags & GWT_SOLVE_INIT)) {  // initial_factors (decompose.cpp:248-300)
+        GramDesc g1{t.M, t.N * t.P, 1, MNP, 1, t.M, 0, rx_kind};
+        gram_eig(g1, X, t.M, t.m, A, rx_copies);
+        GramDesc g2{t.N, t.M, t.P, MNP, t.M, 1, (int64_t)t.M * t.N, tx_kind};
+        gram_eig(g2, X, t.N, t.n, B, tx_copies);
+        GramDesc g3{t.P, t.M * t.N, 1, MNP, (int64_t)t.M * t.N, 1, 0, FI_LINK};
+        gram_eig(g3, X, t.P, t.p, Cf, 0);
+    }
+    auto objective = [&](int slot) {
+        gemm(dZ, X, A, Z);
+        gemm(dZ2, Z, B, Z2);
+        gemm(dG, Z2, Cf, Gc);
+        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)links * t.m * t.n * t.p, G, capt, st));
+        ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, slot, st));
+    };
+    objective(0);
+    tm.mark(2);
+    // per-group early-stop bookkeeping (decompose.cpp:363-368)
+    std::vector<char> stopped(G, 0);
+    const size_t a_sz = cs * users * t.M * t.m, b_sz = cs * t.J * t.N * t.n, c_sz = cs * links * t.P * t.p,
+                 g_sz = cs * links * t.m * t.n * t.p;
+    char* frozen = nullptr;
+    if (early) {
+        frozen = (char*)ctx->ws(WS_FROZEN, (a_sz + b_sz + c_sz + g_sz) * G);
+        energy_h.resize(G);
+        ck(cudaMemcpyAsync(energy_h.data(), energy, 8 * G, cudaMemcpyDeviceToHost, st), "D2H");
+    }
+    trace_h.assign((size_t)G * (sweeps + 1), 0.0);
+    iters.assign(G, sweeps);
+    int64_t active = G;
+    for (int s = 0; s < sweeps && active > 0; ++s) {
+        // rx phase: all fresh receive factors from the old tx/delay factors
+        gemm(dY1, X, Cf, Y1);
+        gemm(dW, Y1, B, W);
+        GramDesc grx{t.M, t.n * t.p, 1, (int64_t)t.M * t.n * t.p, 1, t.M, 0, rx_kind};
+        gram_eig(grx, W, t.M, t.m, A, rx_copies);
+        // tx phase with the new receive factors
+        gemm(dW2, Y1, A, W2);
+        GramDesc gtx{t.N, t.m, t.p, (int64_t)t.m * t.N * t.p, t.m, 1, (int64_t)t.m * t.N, tx_kind};
+        gram_eig(gtx, W2, t.N, t.n, B, tx_copies);
+        // delay phase with new rx and tx
+        gemm(dZ, X, A, Z);
+        gemm(dZ2, Z, B, Z2);
+        GramDesc gd{t.P, t.m * t.n, 1, (int64_t)t.m * t.n * t.P, (int64_t)t.m * t.n, 1, 0, FI_LINK};
+        gram_eig(gd, Z2, t.P, t.p, Cf, 0);
+        // objective (energy split ||X||^2 - ||core||^2) and the cores of these factors
+        gemm(dG, Z2, Cf, Gc);
+        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)links * t.m * t.n * t.p, G, capt, st));
+        ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, s + 1, st));
+        if (early) {
+            ck(cudaMemcpyAsync(trace_h.data(), trace_d, 8 * trace_h.size(), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+            for (int64_t g = 0; g < G; ++g) {
+                if (stopped[g]) continue;
+                const double dec = trace_h[g * (sweeps + 1) + s] - trace_h[g * (sweeps + 1) + s + 1];
+                if (dec < 1e-10 * energy_h[g]) {
+                    stopped[g] = 1;
+                    --active;
+                    iters[g] = s + 1;
+                    char* fz = frozen + g * (a_sz + b_sz + c_sz + g_sz);
+                    ck(cudaMemcpyAsync(fz, (char*)A + g * a_sz, a_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                    ck(cudaMemcpyAsync(fz + a_sz, (char*)B + g * b_sz, b_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                    ck(cudaMemcpyAsync(fz + a_sz + b_sz, (char*)Cf + g * c_sz, c_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                    ck(cudaMemcpyAsync(fz + a_sz + b_sz + c_sz, (char*)Gc + g * g_sz, g_sz, cudaMemcpyDeviceToDevice, st),
+                       "D2D");
+                }
+            }
+        }
+    }
+    tm.mark(3);
+    if (early) {
+        for (int64_t g = 0; g < G; ++g) {
+            if (!stopped[g]) continue;
+            char* fz = frozen + g * (a_sz + b_sz + c_sz + g_sz);
+            ck(cudaMemcpyAsync((char*)A + g * a_sz, fz, a_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+            ck(cudaMemcpyAsync((char*)B + g * b_sz, fz + a_sz, b_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+            ck(cudaMemcpyAsync((char*)Cf + g * c_sz, fz + a_sz + b_sz, c_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+            ck(cudaMemcpyAsync((char*)Gc + g * g_sz, fz + a_sz + b_sz + c_sz, g_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+        }
+    }
+    int hfail = 0;
+    ck(cudaMemcpyAsync(&hfail, failp, 4, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    if (hfail) fail(GWT_RUNTIME_ERROR, "leading_eigenvectors: eigendecomposition failed");
+    ms[0] += tm.between(1, 2);
+    ms[1] += tm.between(2, 3);
+}
+
+template <class T>
+void groupwise_solve_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups,
+                          gwt_mem mem, const void* X, int sweeps, unsigned flags, void* A, void* B, void* Cf,
+                          void* Gc, double* trace, int32_t* iters, double* energy) {
+    using Cx = cplx_t<T>;
+    const size_t cs = sizeof(Cx);
+    // reference checks: check_channel_dims, ranks.validate_against, sweeps >= 0 (decompose.cpp:314-318)
+    gwt_topology tt = *topo;
+    if (tt.num_streams < 1) tt.num_streams = 1;
+    if (tt.num_cells < 1 || tt.users_per_cell < 1 || tt.rx_antennas < 1 || tt.tx_antennas < 1 || tt.num_taps < 1)
+        invalid("channel set: inconsistent tensor dims");
+    validate_ranks(*ranks, tt.rx_antennas, tt.tx_antennas, tt.num_taps);
+    if (sweeps < 0) invalid("solve: sweeps must be >= 0");
+    if (ngroups < 0) invalid("solve: ngroups must be >= 0");
+    if (std::max({tt.rx_antennas, tt.tx_antennas, tt.num_taps}) > 256)
+        invalid("solve: mode sizes above 256 are not supported by the batched eigensolver");
+    if (ngroups == 0) return;
+    const Topo t = mk_topo(tt, *ranks);
+    const int links = t.links(), users = t.users();
+    const int64_t x_g = (int64_t)links * t.M * t.N * t.P, a_g = (int64_t)users * t.M * t.m,
+                  b_g = (int64_t)t.J * t.N * t.n, c_g = (int64_t)links * t.P * t.p,
+                  g_g = (int64_t)links * t.m * t.n * t.p;
+    // per-group workspace bytes -> group chunk
+    const int64_t per_group = cs * (links * ((int64_t)t.M * t.N * t.p + (int64_t)t.M * t.n * t.p +
+                                             (int64_t)t.m * t.N * t.p + (int64_t)t.m * t.N * t.P +
+                                             (int64_t)t.m * t.n * t.P) +
+                                    std::max({(int64_t)users * t.M * t.M, (int64_t)t.J * t.N * t.N,
+                                              (int64_t)links * t.P * t.P}) * 3) +
+                              (mem == GWT_MEM_HOST ? cs * (x_g + a_g + b_g + c_g + g_g) : 0);
+    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(ngroups, (int64_t)(ws_budget() / std::max<int64_t>(per_group, 1))));
+    double ms[2] = {0, 0};
+    Timer tm(ctx);
+    tm.mark(0);
+    double h2d_ms = 0;
+    for (int64_t g0 = 0; g0 < ngroups; g0 += chunk) {
+        const int64_t G = std::min(chunk, ngroups - g0);
+        const void* Xd;
+        void *Ad, *Bd, *Cd, *Gd;
+        double* trace_d = (double*)ctx->ws(WS_TRACE, 8 * G * (sweeps + 1));
+        if (mem == GWT_MEM_HOST) {
+            tm.mark(4);
+            void* xb = ctx->ws(WS_X, cs * G * x_g);
+            ck(cudaMemcpyAsync(xb, (const char*)X + cs * g0 * x_g, cs * G * x_g, cudaMemcpyHostToDevice, ctx->stream), "H2D X");
+            Xd = xb;
+            Ad = ctx->ws(WS_A, cs * G * a_g);
+            Bd = ctx->ws(WS_B, cs * G * b_g);
+            Cd = ctx->ws(WS_C, cs * G * c_g);
+            Gd = ctx->ws(WS_G, cs * G * g_g);
+            if (flags & GWT_SOLVE_INIT) {
+                ck(cudaMemcpyAsync(Ad, (const char*)A + cs * g0 * a_g, cs * G * a_g, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+                ck(cudaMemcpyAsync(Bd, (const char*)B + cs * g0 * b_g, cs * G * b_g, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+                ck(cudaMemcpyAsync(Cd, (const char*)Cf + cs * g0 * c_g, cs * G * c_g, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+            }
+            tm.mark(5);
+            ck(cudaStreamSynchronize(ctx->stream), "sync");
+            h2d_ms += tm.between(4, 5);
+        } else {
+            Xd = (const char*)X + cs * g0 * x_g;
+            Ad = (char*)A + cs * g0 * a_g;
+            Bd = (char*)B + cs * g0 * b_g;
+            Cd = (char*)Cf + cs * g0 * c_g;
+            Gd = (char*)Gc + cs * g0 * g_g;
+        }
+        std::vector<int> it;
+        std::vector<double> th, eh;
+        solve_chunk<T>(ctx, t, G, Xd, sweeps, flags, Ad, Bd, Cd, Gd, trace_d, it, th, eh, ms);
+        // trace: entries after an early stop repeat the final objective
+        th.resize((size_t)G * (sweeps + 1));
+        ck(cudaMemcpy(th.data(), trace_d, 8 * th.size(), cudaMemcpyDeviceToHost), "D2H trace");
+        for (int64_t g = 0; g < G; ++g)
+            for (int s = it[g] + 1; s <= sweeps; ++s) th[g * (sweeps + 1) + s] = th[g * (sweeps + 1) + it[g]];
+        double* en = (double*)ctx->ws(WS_ENERGY, 8 * G);
+        std::vector<double> enh(G);
+        ck(cudaMemcpy(enh.data(), en, 8 * G, cudaMemcpyDeviceToHost), "D2H energy");
+        if (mem == GWT_MEM_HOST) {
+            tm.mark(4);
+            ck(cudaMemcpyAsync((char*)A + cs * g0 * a_g, Ad, cs * G * a_g, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            ck(cudaMemcpyAsync((char*)B + cs * g0 * b_g, Bd, cs * G * b_g, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            ck(cudaMemcpyAsync((char*)Cf + cs * g0 * c_g, Cd, cs * G * c_g, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            ck(cudaMemcpyAsync((char*)Gc + cs * g0 * g_g, Gd, cs * G * g_g, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            if (trace) std::memcpy(trace + g0 * (sweeps + 1), th.data(), 8 * th.size());
+            if (iters) for (int64_t g = 0; g < G; ++g) iters[g0 + g] = it[g];
+            if (energy) std::memcpy(energy + g0, enh.data(), 8 * G);
+            tm.mark(5);
+            ck(cudaStreamSynchronize(ctx->stream), "sync");
+            h2d_ms += tm.between(4, 5);
+        } else {
+            if (trace) ck(cudaMemcpyAsync(trace + g0 * (sweeps + 1), th.data(), 8 * th.size(), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+            std::vector<int32_t> it32(it.begin(), it.end());
+            if (iters) ck(cudaMemcpyAsync(iters + g0, it32.data(), 4 * G, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+            if (energy) ck(cudaMemcpyAsync(energy + g0, en, 8 * G, cudaMemcpyDeviceToDevice, ctx->stream), "D2D");
+            ck(cudaStreamSynchronize(ctx->stream), "sync");
+        }
+    }
+    tm.mark(6);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    std::fill(ctx->stage_ms, ctx->stage_ms + 8, 0.0);
+    ctx->stage_ms[0] = tm.between(0, 6);
+    ctx->stage_ms[1] = ms[0];
+    ctx->stage_ms[2] = ms[1];
+    ctx->stage_ms[7] = h2d_ms;
+}
+
+// ---------------------------------------------------------------------------
+// compressed SINR
+void validate_sinr(const gwt_topology& tp, const gwt_ranks& r, int scope) {
+    validate_topology(tp);
+    if (r.m < 1 || r.n < 1 || r.p < 1) invalid("ranks must be >= 1");
+    if (scope != GWT_SCOPE_FULL && scope != GWT_SCOPE_PAPER) invalid("sinr: unknown interference scope");
+    if (tp.num_streams > std::min(r.m, r.n))  // precoder_compressed (sinr.cpp:163-167)
+        invalid("precoder: stream count " + std::to_string(tp.num_streams) + " exceeds compressed channel size " +
+                std::to_string(r.m) + "x" + std::to_string(r.n) + " (ranks chosen below stream count)");
+    if (r.m > 8) invalid("sinr: compressed receive rank m > 8 is not supported by the B200 small-matrix kernel");
+}
+
+template <class T>
+void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups, gwt_mem mem,
+               const void* Cf, const void* Gc, const double* tau, const double* freqs, const void* coeffs, int64_t F,
+               int scope, double* sinr, double* signal, int32_t* status) {
+    using Cx = cplx_t<T>;
+    const size_t cs = sizeof(Cx);
+    const Topo t = mk_topo(*topo, *ranks);
+    cudaStream_t st = ctx->stream;
+    const int links = t.links(), users = t.users();
+    const int S = scope == GWT_SCOPE_PAPER ? t.J : t.J * t.K;
+    const int64_t c_g = (int64_t)links * t.P * t.p, g_g = (int64_t)links * t.m * t.n * t.p;
+    Timer tm(ctx);
+    tm.mark(0);
+    double copy_ms = 0;
+    const void *Cd = Cf, *Gd = Gc, *cod = coeffs;
+    const double *taud = tau, *fd = freqs;
+    double *sd = sinr, *sgd = signal;
+    int* std_ = (int*)status;
+    const int64_t out_rows = ngroups * F * users;
+    if (mem == GWT_MEM_HOST) {
+        tm.mark(4);
+        void* c = ctx->ws(WS_C, cs * ngroups * c_g);
+        void* g = ctx->ws(WS_G, cs * ngroups * g_g);
+        ck(cudaMemcpyAsync(c, Cf, cs * ngroups * c_g, cudaMemcpyHostToDevice, st), "H2D C");
+        ck(cudaMemcpyAsync(g, Gc, cs * ngroups * g_g, cudaMemcpyHostToDevice, st), "H2D G");
+        Cd = c;
+        Gd = g;
+        if (coeffs) {
+            void* co = ctx->ws(WS_COEF, cs * ngroups * F * links * t.P);
+            ck(cudaMemcpyAsync(co, coeffs, cs * ngroups * F * links * t.P, cudaMemcpyHostToDevice, st), "H2D coeffs");
+            cod = co;
+        } else {
+            double* ta = (double*)ctx->ws(WS_TAU, 8 * ngroups * links * t.P);
+            double* fr = (double*)ctx->ws(WS_FREQ, 8 * F);
+            ck(cudaMemcpyAsync(ta, tau, 8 * ngroups * links * t.P, cudaMemcpyHostToDevice, st), "H2D tau");
+            ck(cudaMemcpyAsync(fr, freqs, 8 * F, cudaMemcpyHostToDevice, st), "H2D freqs");
+            taud = ta;
+            fd = fr;
+        }
+        sd = (double*)ctx->ws(WS_SINR, 8 * out_rows * t.L);
+        sgd = (double*)ctx->ws(WS_SIG, 8 * out_rows * t.L);
+        std_ = (int*)ctx->ws(WS_STATUS, 4 * out_rows);
+        tm.mark(5);
+    }
+    // subcarrier chunk from the workspace budget
+    const int64_t per_f = (int64_t)ngroups * ((int64_t)cs * links * t.m * t.n + 16LL * users * S * t.m * t.m +
+                                             8LL * users * (t.L + 2 * t.m * t.L));
+    int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, (int64_t)(std::min<size_t>(ws_budget(), size_t(2) << 30) / std::max<int64_t>(per_f, 1))));
+    void* H = ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
+    double2* PG = (double2*)ctx->ws(WS_PG, 16 * ngroups * Fc * users * S * t.m * t.m);
+    double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * Fc * users * (t.L + 2 * t.m * t.L));
+    double ms_r = 0, ms_p = 0, ms_s = 0;
+    for (int64_t f0 = 0; f0 < F; f0 += Fc) {
+        const int fc = (int)std::min(Fc, F - f0);
+        tm.mark(8);
+        ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
+        tm.mark(9);
+        ctx->launched(launch_pair_gram<T>(t, scope, S, fc, (int)ngroups, H, PG, st));
+        tm.mark(10);
+        ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PG, EG, sd,
+                                        sgd, std_, st),
+                      2);
+        tm.mark(11);
+        ck(cudaEventSynchronize(ctx->ev[11]), "sync");
+        ms_r += tm.between(8, 9);
+        ms_p += tm.between(9, 10);
+        ms_s += tm.between(10, 11);
+    }
+    if (mem == GWT_MEM_HOST) {
+        tm.mark(12);
+        ck(cudaMemcpyAsync(sinr, sd, 8 * out_rows * t.L, cudaMemcpyDeviceToHost, st), "D2H sinr");
+        ck(cudaMemcpyAsync(signal, sgd, 8 * out_rows * t.L, cudaMemcpyDeviceToHost, st), "D2H signal");
+        ck(cudaMemcpyAsync(status, std_, 4 * out_rows, cudaMemcpyDeviceToHost, st), "D2H status");
+        tm.mark(13);
+    }
+    tm.mark(6);
+    ck(cudaStreamSynchronize(st), "sync");
+    if (mem == GWT_MEM_HOST) copy_ms = tm.between(4, 5) + tm.between(12, 13);
+    std::fill(ctx->stage_ms, ctx->stage_ms + 8, 0.0);
+    ctx->stage_ms[0] = tm.between(0, 6);
+    ctx->stage_ms[4] = ms_r;
+    ctx->stage_ms[5] = ms_p;
+    ctx->stage_ms[6] = ms_s;
+    ctx->stage_ms[7] = copy_ms;
+}
+
+void ledger_for(const gwt_topology& tp, const gwt_ranks& r, int path, gwt_ledger* out) {  // sinr.cpp:353-382
+    const int64_t J = tp.num_cells, K = tp.users_per_cell, M = tp.rx_antennas, N = tp.tx_antennas, P = tp.num_taps;
+    const int64_t L = tp.num_streams, m = r.m, n = r.n, p = r.p;
+    const int64_t links = J * J * K, users = J * K;
+    if (path == 0) {
+        out->reconstruct = links * (M * N * P);
+        out->precoder = users * (M * N * L);
+        out->covariance = users * users * (M * N * L + M * M * L);
+        out->inverse = users * (M * M * M);
+        out->filter = users * (M * M * L);
+        out->sinr = users * L * (M * M + 2 * M);
+    } else {
+        out->reconstruct = links * (m * n * p + P * p);
+        out->precoder = users * (m * n * L);
+        out->covariance = users * users * (m * n * L + m * m * L);
+        out->inverse = users * (2 * m * m * m);
+        out->filter = users * (m * m * L + m * L);
+        out->sinr = users * L * (m * m + 2 * m);
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int gwt_ctx_create(gwt_ctx** out, int device) {
+    if (!out) return GWT_INVALID_ARGUMENT;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return GWT_NO_DEVICE;
+    if (device < 0 || device >= n) return GWT_INVALID_ARGUMENT;
+    gwt_ctx* c = new gwt_ctx();
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return GWT_CUDA_ERROR;
+    }
+    c->stream = c->own_stream;
+    *out = c;
+    return GWT_OK;
+}
+
+void gwt_ctx_destroy(gwt_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& s : ctx->slots)
+        if (s.p) cudaFree(s.p);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+const char* gwt_last_error(const gwt_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null gwt_ctx"; }
+
+int gwt_ctx_set_stream(gwt_ctx* ctx, void* stream) {
+    if (!ctx) return GWT_INVALID_ARGUMENT;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return GWT_OK;
+}
+
+int64_t gwt_ctx_launch_count(const gwt_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int gwt_ctx_stage_times(const gwt_ctx* ctx, double* ms8) {
+    if (!ctx || !ms8) return GWT_INVALID_ARGUMENT;
+    std::memcpy(ms8, ctx->stage_ms, sizeof(ctx->stage_ms));
+    return GWT_OK;
+}
+
+int gwt_groupwise_solve(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups,
+                        gwt_dtype dtype, gwt_mem mem, const void* X, int32_t sweeps, uint32_t flags, void* A, void* B,
+                        void* C, void* G, double* trace, int32_t* iters, double* energy) {
+    return guarded(ctx, [&] {
+        if (!topo || !ranks) invalid("groupwise_solve: null topology/ranks");
+        if (dtype == GWT_C64)
+            groupwise_solve_impl<float>(ctx, topo, ranks, ngroups, mem, X, sweeps, flags, A, B, C, G, trace, iters, energy);
+        else
+            groupwise_solve_impl<double>(ctx, topo, ranks, ngroups, mem, X, sweeps, flags, A, B, C, G, trace, iters, energy);
+    });
+}
+
+int gwt_sinr_compressed(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups,
+                        gwt_dtype dtype, gwt_mem mem, const void* C, const void* G, const double* tau,
+                        const double* freqs, int64_t F, gwt_scope scope, double* sinr, double* signal,
+                        int32_t* status, gwt_ledger* ledger) {
+    return guarded(ctx, [&] {
+        if (!topo || !ranks) invalid("sinr: null topology/ranks");
+        validate_sinr(*topo, *ranks, scope);
+        if (F < 0 || ngroups < 0) invalid("sinr: negative batch size");
+        if (ledger) {
+            ledger_for(*topo, *ranks, 1, ledger);
+            const int64_t mul = F * ngroups;
+            ledger->reconstruct *= mul; ledger->precoder *= mul; ledger->covariance *= mul;
+            ledger->inverse *= mul; ledger->filter *= mul; ledger->sinr *= mul;
+        }
+        if (F == 0 || ngroups == 0) return;
+        if (dtype == GWT_C64)
+            sinr_impl<float>(ctx, topo, ranks, ngroups, mem, C, G, tau, freqs, nullptr, F, scope, sinr, signal, status);
+        else
+            sinr_impl<double>(ctx, topo, ranks, ngroups, mem, C, G, tau, freqs, nullptr, F, scope, sinr, signal, status);
+    });
+}
+
+int gwt_sinr_compressed_coeffs(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups,
+                               gwt_dtype dtype, gwt_mem mem, const void* C, const void* G, const void* coeffs,
+                               int64_t F, gwt_scope scope, double* sinr, double* signal, int32_t* status,
+                               gwt_ledger* ledger) {
+    return guarded(ctx, [&] {
+        if (!topo || !ranks) invalid("sinr: null topology/ranks");
+        validate_sinr(*topo, *ranks, scope);
+        if (!coeffs) invalid("assemble_all_compressed: coefficient grid does not match cores");
+        if (ledger) {
+            ledger_for(*topo, *ranks, 1, ledger);
+            const int64_t mul = F * ngroups;
+            ledger->reconstruct *= mul; ledger->precoder *= mul; ledger->covariance *= mul;
+            ledger->inverse *= mul; ledger->filter *= mul; ledger->sinr *= mul;
+        }
+        if (F == 0 || ngroups == 0) return;
+        if (dtype == GWT_C64)
+            sinr_impl<float>(ctx, topo, ranks, ngroups, mem, C, G, nullptr, nullptr, coeffs, F, scope, sinr, signal, status);
+        else
+            sinr_impl<double>(ctx, topo, ranks, ngroups, mem, C, G, nullptr, nullptr, coeffs, F, scope, sinr, signal, status);
+    });
+}
+
+int gwt_assemble_compressed(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups,
+                            gwt_dtype dtype, gwt_mem mem, const void* C, const void* G, const double* tau,
+                            const double* freqs, const void* coeffs, int64_t F, void* H) {
+    return guarded(ctx, [&] {
+        if (!topo || !ranks) invalid("assemble_compressed: null topology/ranks");
+        if (ranks->m < 1 || ranks->n < 1 || ranks->p < 1 || ranks->p > topo->num_taps)
+            invalid("assemble_channel_compressed: delay factor has " + std::to_string(topo->num_taps) +
+                    " rows but core mode-3 size is " + std::to_string(ranks->p));
+        if (F == 0 || ngroups == 0) return;
+        const Topo t = mk_topo(*topo, *ranks);
+        const size_t cs = csize(dtype);
+        const int links = t.links();
+        const int64_t c_g = (int64_t)links * t.P * t.p, g_g = (int64_t)links * t.m * t.n * t.p;
+        const int64_t h_bytes = cs * ngroups * F * links * t.m * t.n;
+        const void *Cd = C, *Gd = G, *cod = coeffs;
+        const double *taud = tau, *fd = freqs;
+        void* Hd = H;
+        cudaStream_t st = ctx->stream;
+        if (mem == GWT_MEM_HOST) {
+            void* c = ctx->ws(WS_C, cs * ngroups * c_g);
+            void* g = ctx->ws(WS_G, cs * ngroups * g_g);
+            ck(cudaMemcpyAsync(c, C, cs * ngroups * c_g, cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(g, G, cs * ngroups * g_g, cudaMemcpyHostToDevice, st), "H2D");
+            Cd = c;
+            Gd = g;
+            if (coeffs) {
+                void* co = ctx->ws(WS_COEF, cs * ngroups * F * links * t.P);
+                ck(cudaMemcpyAsync(co, coeffs, cs * ngroups * F * links * t.P, cudaMemcpyHostToDevice, st), "H2D");
+                cod = co;
+            } else {
+                double* ta = (double*)ctx->ws(WS_TAU, 8 * ngroups * links * t.P);
+                double* fr = (double*)ctx->ws(WS_FREQ, 8 * F);
+                ck(cudaMemcpyAsync(ta, tau, 8 * ngroups * links * t.P, cudaMemcpyHostToDevice, st), "H2D");
+                ck(cudaMemcpyAsync(fr, freqs, 8 * F, cudaMemcpyHostToDevice, st), "H2D");
+                taud = ta;
+                fd = fr;
+            }
+            Hd = ctx->ws(WS_H, h_bytes);
+        }
+        if (dtype == GWT_C64)
+            ctx->launched(launch_rebuild<float>(t, (int)ngroups, (int)F, 0, F, Cd, Gd, taud, fd, cod, Hd, st));
+        else
+            ctx->launched(launch_rebuild<double>(t, (int)ngroups, (int)F, 0, F, Cd, Gd, taud, fd, cod, Hd, st));
+        if (mem == GWT_MEM_HOST) ck(cudaMemcpyAsync(H, Hd, h_bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+int gwt_leading_eigenvectors(gwt_ctx* ctx, int32_t n, int32_t count, int64_t batch, gwt_dtype dtype, gwt_mem mem,
+                             const void* H, void* out, double* evals) {
+    return guarded(ctx, [&] {
+        if (n < 1) invalid("leading_eigenvectors: matrix is not square");
+        if (count < 1 || count > n)  // linalg.cpp:28-32
+            invalid("leading_eigenvectors: count " + std::to_string(count) + " out of range for size " + std::to_string(n));
+        if (n > 256) invalid("leading_eigenvectors: sizes above 256 are not supported by the batched eigensolver");
+        if (batch == 0) return;
+        const size_t cs = csize(dtype);
+        cudaStream_t st = ctx->stream;
+        const void* Hd = H;
+        void* Od = out;
+        double* Ed = evals;
+        if (mem == GWT_MEM_HOST) {
+            void* h = ctx->ws(WS_GRAM, cs * batch * n * n);
+            ck(cudaMemcpyAsync(h, H, cs * batch * n * n, cudaMemcpyHostToDevice, st), "H2D");
+            Hd = h;
+            Od = ctx->ws(WS_POOL, cs * batch * n * count);
+            Ed = evals ? (double*)ctx->ws(WS_MISC, 8 * batch * count) : nullptr;
+        }
+        double2* eA = (double2*)ctx->ws(WS_EIGA, 16 * batch * n * n);
+        double* eZ = (double*)ctx->ws(WS_EIGZ, 8 * batch * n * n);
+        double2* eX = (double2*)ctx->ws(WS_EIGX, 16 * batch * n * count);
+        int* fl = (int*)ctx->ws(WS_FAIL, 4);
+        ck(cudaMemsetAsync(fl, 0, 4, st), "memset");
+        if (dtype == GWT_C64)
+            ctx->launched(launch_heev_topk<float>(n, count, batch, Hd, Od, Ed, eA, eZ, eX, fl, st));
+        else
+            ctx->launched(launch_heev_topk<double>(n, count, batch, Hd, Od, Ed, eA, eZ, eX, fl, st));
+        int hf = 0;
+        ck(cudaMemcpyAsync(&hf, fl, 4, cudaMemcpyDeviceToHost, st), "D2H");
+        if (mem == GWT_MEM_HOST) {
+            ck(cudaMemcpyAsync(out, Od, cs * batch * n * count, cudaMemcpyDeviceToHost, st), "D2H");
+            if (evals) ck(cudaMemcpyAsync(evals, Ed, 8 * batch * count, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        ck(cudaStreamSynchronize(st), "sync");
+        if (hf) fail(GWT_RUNTIME_ERROR, "leading_eigenvectors: eigendecomposition failed");
+    });
+}
+
+int gwt_reconstruct(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups, gwt_dtype dtype,
+                    gwt_mem mem, const void* A, const void* B, const void* C, const void* G, void* X) {
+    return guarded(ctx, [&] {
+        if (!topo || !ranks) invalid("reconstruct: null topology/ranks");
+        validate_ranks(*ranks, topo->rx_antennas, topo->tx_antennas, topo->num_taps);
+        if (ngroups == 0) return;
+        const Topo t = mk_topo(*topo, *ranks);
+        const size_t cs = csize(dtype);
+        const int links = t.links(), users = t.users();
+        const int64_t a_g = (int64_t)users * t.M * t.m, b_g = (int64_t)t.J * t.N * t.n, c_g = (int64_t)links * t.P * t.p,
+                      g_g = (int64_t)links * t.m * t.n * t.p, x_g = (int64_t)links * t.M * t.N * t.P;
+        cudaStream_t st = ctx->stream;
+        const void *Ad = A, *Bd = B, *Cd = C, *Gd = G;
+        void* Xd = X;
+        if (mem == GWT_MEM_HOST) {
+            void* a = ctx->ws(WS_A, cs * ngroups * a_g);
+            void* b = ctx->ws(WS_B, cs * ngroups * b_g);
+            void* c = ctx->ws(WS_C, cs * ngroups * c_g);
+            void* g = ctx->ws(WS_G, cs * ngroups * g_g);
+            ck(cudaMemcpyAsync(a, A, cs * ngroups * a_g, cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(b, B, cs * ngroups * b_g, cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(c, C, cs * ngroups * c_g, cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(g, G, cs * ngroups * g_g, cudaMemcpyHostToDevice, st), "H2D");
+            Ad = a; Bd = b; Cd = c; Gd = g;
+            Xd = ctx->ws(WS_X, cs * ngroups * x_g);
+        }
+        void* T1 = ctx->ws(WS_Z, cs * ngroups * links * t.M * t.n * t.p);
+        void* T2 = ctx->ws(WS_Z2, cs * ngroups * links * t.M * t.N * t.p);
+        // X1 = G x1 A: rows = (d, r) fibers of length m; U(k=c, col=a) = A(a, c) = A[a + M c]
+        GemmDesc d1{};
+        d1.R = t.n * t.p; d1.S = 1; d1.Kd = t.m; d1.Cols = t.M;
+        d1.in_item = (int64_t)t.m * t.n * t.p; d1.rs_in = t.m; d1.s_in = 0; d1.ks_in = 1;
+        d1.out_item = (int64_t)t.M * t.n * t.p; d1.rs_out = t.M; d1.s_out = 0; d1.cs_out = 1; d1.fkind = FI_USER;
+        d1.ublk = (int64_t)t.M * t.m; d1.uk = t.M; d1.ucol = 1; d1.uconj = 0;
+        // X2 = X1 x2 B: rows (a, r); U(k=d, col=b) = B(b, d) = B[b + N d]
+        GemmDesc d2{};
+        d2.R = t.M; d2.S = t.p; d2.Kd = t.n; d2.Cols = t.N;
+        d2.in_item = (int64_t)t.M * t.n * t.p; d2.rs_in = 1; d2.s_in = (int64_t)t.M * t.n; d2.ks_in = t.M;
+        d2.out_item = (int64_t)t.M * t.N * t.p; d2.rs_out = 1; d2.s_out = (int64_t)t.M * t.N; d2.cs_out = t.M;
+        d2.fkind = FI_BASE; d2.ublk = (int64_t)t.N * t.n; d2.uk = t.N; d2.ucol = 1; d2.uconj = 0;
+        // X = X2 x3 C: rows (a,b); U(k=r, col=q) = C(q, r) = C[q + P r]
+        GemmDesc d3{};
+        d3.R = t.M * t.N; d3.S = 1; d3.Kd = t.p; d3.Cols = t.P;
+        d3.in_item = (int64_t)t.M * t.N * t.p; d3.rs_in = 1; d3.s_in = 0; d3.ks_in = (int64_t)t.M * t.N;
+        d3.out_item = x_g / links; d3.rs_out = 1; d3.s_out = 0; d3.cs_out = (int64_t)t.M * t.N;
+        d3.fkind = FI_LINK; d3.ublk = (int64_t)t.P * t.p; d3.uk = t.P; d3.ucol = 1; d3.uconj = 0;
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            ctx->launched(launch_cgemm<T>(t, d1, ngroups, Gd, Ad, T1, st));
+            ctx->launched(launch_cgemm<T>(t, d2, ngroups, T1, Bd, T2, st));
+            ctx->launched(launch_cgemm<T>(t, d3, ngroups, T2, Cd, Xd, st));
+        };
+        if (dtype == GWT_C64) run(float{});
+        else run(double{});
+        if (mem == GWT_MEM_HOST) ck(cudaMemcpyAsync(X, Xd, cs * ngroups * x_g, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+int gwt_flop_estimate(const gwt_topology* topo, const gwt_ranks* ranks, int32_t path, gwt_ledger* out) {
+    if (!topo || !ranks || !out) return GWT_INVALID_ARGUMENT;
+    try {
+        validate_topology(*topo);
+        validate_ranks(*ranks, topo->rx_antennas, topo->tx_antennas, topo->num_taps);
+    } catch (const GwtError& e) {
+        return e.code;
+    }
+    ledger_for(*topo, *ranks, path, out);
+    return GWT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+// Groupwise Tucker compression (hot path a) building blocks, sm_100a.
+//
+// Reference: alternating_solve (proj/src/decompose.cpp:309-373) over
+// rx/tx/delay_update_gram (:146-193), initial_factors (:248-300),
+// compute_cores (:195-204), objective_value (:217-226). The reference forms
+// each mode product through an explicit unfolding copy (tensor.cpp:36-114);
+// here every mode product is ONE strided batched complex GEMM whose operand
+// strides address the unfolding in place (no copies), batched over all links
+// of all groups, and every update Gram is one batched Hermitian rank-k kernel
+// whose reduction runs over all links that share the factor.
+#include "kernels.cuh"
+
+namespace gwtk {
+
+// Tiled strided complex GEMM with conj(U): CTA tile 64 rows x 64 cols,
+// 256 threads, 4x4 outputs per thread, K chunks of 16 staged in smem.
+template <class T>
+__global__ void __launch_bounds__(256) k_cgemm_conjU(Topo t, GemmDesc d, int links, const cplx_t<T>* __restrict__ in,
+                                                      const cplx_t<T>* __restrict__ U, cplx_t<T>* __restrict__ out) {
+    using C = cplx_t<T>;
+    constexpr int TR = 64, TC = 64, KC = 16;
+    __shared__ C sIn[KC][TR + 1];
+    __shared__ C sU[KC][TC + 1];
+    const int64_t item = blockIdx.z;
+    const int64_t g = item / links;
+    const int l = (int)(item % links);
+    const int row0 = blockIdx.x * TR, col0 = blockIdx.y * TC;
+    const int rows = d.R * d.S;
+    const C* inb = in + item * d.in_item;
+    const int64_t ublk = d.ublk >= 0 ? d.ublk : (int64_t)d.Kd * d.Cols;
+    const int64_t ucol = d.ucol >= 0 ? d.ucol : (int64_t)d.Kd;
+    const C* ub = U + factor_index(t, d.fkind, g, l) * ublk;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    C acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = czero<C>();
+    const bool row_fast = d.rs_in == 1;
+    for (int k0 = 0; k0 < d.Kd; k0 += KC) {
+        for (int idx = threadIdx.x; idx < TR * KC; idx += 256) {
+            int r, kk;
+            if (row_fast) { r = idx % TR; kk = idx / TR; }
+            else { kk = idx % KC; r = idx / KC; }
+            const int row = row0 + r, k = k0 + kk;
+            C v = czero<C>();
+            if (row < rows && k < d.Kd)
+                v = inb[(row % d.R) * d.rs_in + (int64_t)(row / d.R) * d.s_in + (int64_t)k * d.ks_in];
+            sIn[kk][r] = v;
+        }
+        for (int idx = threadIdx.x; idx < TC * KC; idx += 256) {
+            const int kk = idx % KC, c = idx / KC;
+            const int col = col0 + c, k = k0 + kk;
+            C v = czero<C>();
+            if (col < d.Cols && k < d.Kd) {
+                v = ub[(int64_t)k * d.uk + (int64_t)col * ucol];
+                if (d.uconj) v = cconj(v);
+            }
+            sU[kk][c] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+            C a[4], b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a[q] = sIn[kk][ty + 16 * q];
+                b[q] = sU[kk][tx + 16 * q];
+            }
+#pragma unroll
+            for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+                for (int qb = 0; qb < 4; ++qb) cfma(acc[qa][qb], a[qa], b[qb]);
+        }
+        __syncthreads();
+    }
+    C* ob = out + item * d.out_item;
+#pragma unroll
+    for (int qa = 0; qa < 4; ++qa) {
+        const int row = row0 + ty + 16 * qa;
+        if (row >= rows) continue;
+        const int64_t ro = (row % d.R) * d.rs_out + (int64_t)(row / d.R) * d.s_out;
+#pragma unroll
+        for (int qb = 0; qb < 4; ++qb) {
+            const int col = col0 + tx + 16 * qb;
+            if (col < d.Cols) ob[ro + (int64_t)col * d.cs_out] = acc[qa][qb];
+        }
+    }
+}
+
+__device__ __forceinline__ int set_size(const Topo& t, int kind) {
+    switch (kind) {
+        case FI_USER: return t.J;
+        case FI_BASE: return t.J * t.K;
+        case FI_LINK: return 1;
+        default: return t.links();
+    }
+}
+// r-th link of set `s` (s local to its group)
+__device__ __forceinline__ int set_link(const Topo& t, int kind, int s, int r) {
+    switch (kind) {
+        case FI_USER: {  // s = i*K + j, r = k
+            const int i = s / t.K, j = s % t.K;
+            return (r * t.J + i) * t.K + j;
+        }
+        case FI_BASE: return s * t.J * t.K + r;  // links (s, i, j) contiguous
+        case FI_LINK: return s;
+        default: return r;
+    }
+}
+
+// Batched Hermitian rank-k accumulation: CTA per (set, 64x64 output tile).
+template <class T>
+__global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_group, const cplx_t<T>* __restrict__ V,
+                                              cplx_t<T>* __restrict__ out) {
+    using C = cplx_t<T>;
+    constexpr int TD = 64, KC = 16;
+    __shared__ C sX[KC][TD + 1];
+    __shared__ C sY[KC][TD + 1];
+    const int64_t set = blockIdx.y;
+    const int64_t g = set / sets_per_group;
+    const int s = (int)(set % sets_per_group);
+    const int tiles = (d.D + TD - 1) / TD;
+    const int x0 = (blockIdx.x % tiles) * TD, y0 = (blockIdx.x / tiles) * TD;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    C acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = czero<C>();
+    const int nl = set_size(t, d.set_kind);
+    const int Tn = d.T1 * d.T2;
+    const bool x_fast = d.xs == 1;
+    for (int r = 0; r < nl; ++r) {
+        const int l = set_link(t, d.set_kind, s, r);
+        const C* vb = V + (g * t.links() + l) * d.v_item;
+        for (int t0 = 0; t0 < Tn; t0 += KC) {
+            for (int idx = threadIdx.x; idx < TD * KC; idx += 256) {
+                int xi, kk;
+                if (x_fast) { xi = idx % TD; kk = idx / TD; }
+                else { kk = idx % KC; xi = idx / KC; }
+                const int tt = t0 + kk;
+                C vx = czero<C>(), vy = czero<C>();
+                if (tt < Tn) {
+                    const int64_t toff = (int64_t)(tt % d.T1) * d.t1s + (int64_t)(tt / d.T1) * d.t2s;
+                    if (x0 + xi < d.D) vx = vb[(int64_t)(x0 + xi) * d.xs + toff];
+                    if (y0 + xi < d.D) vy = vb[(int64_t)(y0 + xi) * d.xs + toff];
+                }
+                sX[kk][xi] = vx;
+                sY[kk][xi] = vy;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int kk = 0; kk < KC; ++kk) {
+                C a[4], b[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    a[q] = sX[kk][ty + 16 * q];
+                    b[q] = sY[kk][tx + 16 * q];
+                }
+#pragma unroll
+                for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+                    for (int qb = 0; qb < 4; ++qb) cfmac(acc[qa][qb], a[qa], b[qb]);
+            }
+            __syncthreads();
+        }
+    }
+    C* ob = out + set * (int64_t)d.D * d.D;
+#pragma unroll
+    for (int qa = 0; qa < 4; ++qa) {
+        const int x = x0 + ty + 16 * qa;
+        if (x >= d.D) continue;
+#pragma unroll
+        for (int qb = 0; qb < 4; ++qb) {
+            const int y = y0 + tx + 16 * qb;
+            if (y < d.D) ob[x + (int64_t)d.D * y] = acc[qa][qb];
+        }
+    }
+}
+
+// Per-group sum of |v|^2 over `per_group` contiguous complex elements:
+// deterministic (fixed tree), fp64 accumulation. One CTA per group.
+template <class T>
+__global__ void __launch_bounds__(256) k_group_sqnorm(const cplx_t<T>* __restrict__ v, int64_t per_group,
+                                                      double* __restrict__ out) {
+    const int64_t g = blockIdx.x;
+    const cplx_t<T>* b = v + g * per_group;
+    double acc = 0.0;
+    for (int64_t e = threadIdx.x; e < per_group; e += 256) {
+        const double2 x = to_d2(b[e]);
+        acc += x.x * x.x + x.y * x.y;
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[g] = red[0];
+}
+
+// trace[g*(stride) + slot] = energy[g] - captured[g]
+__global__ void k_objective(int64_t ngroups, const double* __restrict__ energy, const double* __restrict__ captured,
+                            double* __restrict__ trace, int stride, int slot) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < ngroups) trace[g * stride + slot] = energy[g] - captured[g];
+}
+
+// Broadcast one factor per group to `copies` slots per group (shared model).
+template <class T>
+__global__ void k_broadcast(const cplx_t<T>* __restrict__ src, cplx_t<T>* __restrict__ dst, int64_t elems, int copies,
+                            int64_t ngroups) {
+    const int64_t total = ngroups * copies * elems;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = e / (copies * elems);
+        dst[e] = src[g * elems + e % elems];
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <class T>
+cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, const void* in, const void* U, void* out,
+                         cudaStream_t st) {
+    dim3 grid((d.R * d.S + 63) / 64, (d.Cols + 63) / 64, (unsigned)(ngroups * t.links()));
+    k_cgemm_conjU<T><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
+                                           (cplx_t<T>*)out);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V, void* out,
+                        cudaStream_t st) {
+    const int tiles = (d.D + 63) / 64;
+    dim3 grid(tiles * tiles, (unsigned)(ngroups * sets_per_group));
+    k_gram<T><<<grid, 256, 0, st>>>(t, d, sets_per_group, (const cplx_t<T>*)V, (cplx_t<T>*)out);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_group_sqnorm(const void* v, int64_t per_group, int64_t ngroups, double* out, cudaStream_t st) {
+    k_group_sqnorm<T><<<(unsigned)ngroups, 256, 0, st>>>((const cplx_t<T>*)v, per_group, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_objective(int64_t ngroups, const double* energy, const double* captured, double* trace, int stride,
+                             int slot, cudaStream_t st) {
+    k_objective<<<(unsigned)((ngroups + 255) / 256), 256, 0, st>>>(ngroups, energy, captured, trace, stride, slot);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_broadcast(const void* src, void* dst, int64_t elems, int copies, int64_t ngroups, cudaStream_t st) {
+    const int64_t total = ngroups * copies * elems;
+    const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    k_broadcast<T><<<blocks, 256, 0, st>>>((const cplx_t<T>*)src, (cplx_t<T>*)dst, elems, copies, ngroups);
+    return cudaGetLastError();
+}
+
+#define GWT_INST(T)                                                                                          \
+    template cudaError_t launch_cgemm<T>(const Topo&, const GemmDesc&, int64_t, const void*, const void*, void*, \
+                                         cudaStream_t);                                                      \
+    template cudaError_t launch_gram<T>(const Topo&, const GramDesc&, int64_t, int, const void*, void*,          \
+                                        cudaStream_t);                                                       \
+    template cudaError_t launch_group_sqnorm<T>(const void*, int64_t, int64_t, double*, cudaStream_t);          \
+    template cudaError_t launch_broadcast<T>(const void*, void*, int64_t, int, int64_t, cudaStream_t);
+GWT_INST(float)
+GWT_INST(double)
+
+}  // namespace gwtk

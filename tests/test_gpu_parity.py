@@ -1,0 +1,288 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): per-stream SINR 1e-9 relative for
+complex128, 1e-4 relative for complex64 (c64-rounded inputs, oracle in fp64);
+reconstruction NMSE within 1e-6 absolute. Factors are compared only through
+NMSE/SINR and subspace angles (unique up to phase/rotation).
+"""
+import numpy as np
+import pytest
+
+import paper_2401_09792_b200 as gw
+from oracle import oracle as O
+from tests.helpers import baseline_inputs, dims_of, rel_err
+
+pytestmark = pytest.mark.gpu
+
+SINR_TOL = {"c128": 1e-9, "c64": 1e-4}
+
+
+def _np_dtype(cfg):
+    return np.complex64 if cfg.dtype == "c64" else np.complex128
+
+
+def _oracle_factors(cfg, X128, sweeps=None, early=False):
+    return O.alternating_solve(dims_of(cfg), X128, cfg.sweeps if sweeps is None else sweeps, early_stop=early)
+
+
+def _max_angle(U1, U2):
+    """sin of the largest principal angle between column spaces (oracles.hpp:113-118)."""
+    Q1, _ = np.linalg.qr(U1)
+    Q2, _ = np.linalg.qr(U2)
+    R = Q2 - Q1 @ (Q1.conj().T @ Q2)
+    return np.linalg.svd(R, compute_uv=False)[0] if R.size else 0.0
+
+
+# ---------------------------------------------------------------------------
+# linalg
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8, 17, 24, 32, 64, 128, 256])
+def test_leading_eigenvectors_match_oracle_and_lapack(ctx, n):
+    rng = np.random.default_rng(n)
+    b = 3
+    A = rng.standard_normal((b, n, n)) + 1j * rng.standard_normal((b, n, n))
+    H = A @ np.conj(np.swapaxes(A, 1, 2))
+    count = max(1, n // 2)
+    vec, ev = ctx.leading_eigenvectors(H, count, with_values=True)
+    for k in range(b):
+        w = np.linalg.eigvalsh(H[k])[::-1][:count]
+        assert np.max(np.abs(ev[k] - w)) <= 1e-10 * np.abs(w).max()
+        ref = O.leading_eigenvectors(H[k], count)
+        # same phase convention (linalg.cpp:11-25) => equal vectors for distinct eigenvalues
+        assert np.max(np.abs(vec[k] - ref)) < 1e-8
+        assert np.linalg.norm(vec[k].conj().T @ vec[k] - np.eye(count)) < 1e-10
+
+
+def test_leading_eigenvectors_c64(ctx):
+    rng = np.random.default_rng(5)
+    n = 64
+    A = rng.standard_normal((4, n, n)) + 1j * rng.standard_normal((4, n, n))
+    H = (A @ np.conj(np.swapaxes(A, 1, 2))).astype(np.complex64)
+    vec = ctx.leading_eigenvectors(H, 8)
+    for k in range(4):
+        ref = O.leading_eigenvectors(H[k].astype(np.complex128), 8)
+        assert _max_angle(vec[k].astype(np.complex128), ref) < 1e-3
+
+
+def test_leading_eigenvectors_errors(ctx):
+    H = np.eye(4, dtype=np.complex128)[None]
+    with pytest.raises(gw.InvalidArgument, match="count 5 out of range for size 4"):
+        ctx.leading_eigenvectors(H, 5)
+
+
+# ---------------------------------------------------------------------------
+# compressed assembly
+
+@pytest.mark.parametrize("dt", [np.complex128, np.complex64])
+def test_assemble_compressed_matches_definition(ctx, dt):
+    rng = np.random.default_rng(7)
+    topo = gw.SystemTopology(2, 2, 6, 8, 5, 2, 0.1)
+    ranks = gw.CompressionRanks(4, 5, 3)
+    g, F, links = 2, 3, topo.num_links
+    Cd = (rng.standard_normal((g, links, 3, 5)) + 1j * rng.standard_normal((g, links, 3, 5))).astype(dt)
+    G = (rng.standard_normal((g, links, 3, 5, 4)) + 1j * rng.standard_normal((g, links, 3, 5, 4))).astype(dt)
+    co = (rng.standard_normal((g, F, links, 5)) + 1j * rng.standard_normal((g, F, links, 5))).astype(dt)
+    H = ctx.assemble_compressed(topo, ranks, Cd, G, coeffs=co)
+    # channel.cpp:189-208: d = C^H c, H~ = sum_q G(:,:,q) conj(d_q)
+    d = np.einsum("glqr,gflr->gflq", np.conj(Cd.astype(np.complex128)), co.astype(np.complex128))
+    want = np.einsum("glqba,gflq->gflba", G.astype(np.complex128), np.conj(d))
+    tol = 1e-12 if dt == np.complex128 else 1e-5
+    assert np.max(np.abs(H - want)) <= tol * np.abs(want).max()
+    # oracle cross-check of one item through contract_mode3
+    h_or = O.contract_mode3(np.transpose(G[1, 2].astype(np.complex128), (2, 1, 0)), d[1, 2, 2])
+    assert np.max(np.abs(H[1, 2, 2].T - h_or)) <= tol * np.abs(h_or).max()
+
+
+def test_assemble_from_delays(ctx):
+    cfg = gw.CONFIGS["C1"]
+    rng = np.random.default_rng(3)
+    g, links = 2, cfg.G
+    Cd = rng.standard_normal((g, links, cfg.p, cfg.P)) + 1j * rng.standard_normal((g, links, cfg.p, cfg.P))
+    G = rng.standard_normal((g, links, cfg.p, cfg.n, cfg.m)) + 1j * rng.standard_normal((g, links, cfg.p, cfg.n, cfg.m))
+    tau = rng.uniform(0, 1e-6, (g, links, cfg.P))
+    freqs = cfg.freqs()[:7]
+    H = ctx.assemble_compressed(cfg.topology(), cfg.ranks(), Cd, G, tau=tau, freqs=freqs)
+    co = O.coeffs_from_tau(tau, freqs)
+    d = np.einsum("glqr,gflr->gflq", np.conj(Cd), co)
+    want = np.einsum("glqba,gflq->gflba", G, np.conj(d))
+    assert np.max(np.abs(H - want)) <= 1e-12 * np.abs(want).max()
+
+
+# ---------------------------------------------------------------------------
+# SINR stage parity on identical factors
+
+@pytest.mark.parametrize("name,ngroups,scope", [("C1", None, "paper_experiment"), ("C1", None, "full"),
+                                                ("C2", 2, "paper_experiment"), ("C2d", 2, "paper_experiment")])
+def test_sinr_stage_parity(ctx, name, ngroups, scope):
+    cfg = gw.CONFIGS[name]
+    X, X128, tau = baseline_inputs(cfg, ngroups)
+    fo = _oracle_factors(cfg, X128, sweeps=4)
+    dt = _np_dtype(cfg)
+    Cd, G = fo["C"].astype(dt), fo["G"].astype(dt)
+    freqs = cfg.freqs()
+    oscope = O.SCOPE_FULL if scope == "full" else O.SCOPE_PAPER
+    want, wsig = O.sinr_compressed(dims_of(cfg), Cd.astype(np.complex128), G.astype(np.complex128),
+                                   O.coeffs_from_tau(tau, freqs), cfg.sigma, cfg.L, oscope, nthreads=8)
+    fac = gw.GroupwiseFactorSet(None, None, Cd, G)
+    rep = ctx.run_compressed_pipeline(cfg.topology(), fac, cfg.ranks(), scope, tau=tau, freqs=freqs)
+    assert (np.asarray(rep.status) == 0).all()
+    tol = SINR_TOL[cfg.dtype]
+    assert rel_err(rep.sinr, want).max() <= tol
+    assert rel_err(rep.signal_power, wsig).max() <= tol
+    led = gw.flop_estimate(cfg.topology(), cfg.ranks())
+    assert rep.ledger.total() == led.total() * X.shape[0] * cfg.F
+
+
+def test_sinr_explicit_coefficients_reference_generator(ctx):
+    """Reference-style system (test_sinr.cpp desk_topology, seed 14): coefficient path, ranks (4,5,3)."""
+    topo = gw.SystemTopology(2, 2, 6, 8, 5, 2, 0.1)
+    X, c = O.generate_reference(2, 2, 6, 8, 5, 14)
+    dims = dict(J=2, K=2, M=6, N=8, P=5, m=4, n=5, p=3)
+    fo = O.alternating_solve(dims, X[None], 6)
+    co = c[None, None]
+    for scope, osc in (("paper_experiment", O.SCOPE_PAPER), ("full", O.SCOPE_FULL)):
+        want, _ = O.sinr_compressed(dims, fo["C"], fo["G"], co, 0.1, 2, osc)
+        rep = ctx.run_compressed_pipeline(topo, gw.GroupwiseFactorSet(None, None, fo["C"], fo["G"]),
+                                          gw.CompressionRanks(4, 5, 3), scope, coeffs=co)
+        assert rel_err(rep.sinr, want).max() <= 1e-9
+        # and the reference's strongest pin: compressed == full pipeline on rebuilt channels (test_sinr.cpp:413-425)
+        Hs = []
+        for l, (k, i, j) in enumerate((k, i, j) for k in range(2) for i in range(2) for j in range(2)):
+            u = i * 2 + j
+            A = fo["A"][0, u].T
+            B = fo["B"][0, k].T
+            Cm = fo["C"][0, l].T
+            core = np.transpose(fo["G"][0, l], (2, 1, 0))
+            d = Cm.conj().T @ c[l]
+            hs = np.einsum("abq,q->ab", core, np.conj(d))
+            Hs.append((A @ hs @ B.T).T)
+        ref_full, _ = O.evaluate_assembled(2, 2, 2, 0.1, np.array(Hs), osc)
+        assert rel_err(rep.sinr[0, 0], ref_full).max() <= 1e-8
+
+
+def test_sinr_closed_form_single_link(ctx):
+    """SINR = sigma1^2 / sigma^2 for J=K=1, one stream (test_sinr.cpp:161-174, 391-399)."""
+    topo = gw.SystemTopology(1, 1, 6, 8, 5, 1, 0.3)
+    X, c = O.generate_reference(1, 1, 6, 8, 5, 13)
+    dims = dict(J=1, K=1, M=6, N=8, P=5, m=6, n=8, p=5)
+    fo = O.alternating_solve(dims, X[None], 1)
+    rep = ctx.run_compressed_pipeline(topo, gw.GroupwiseFactorSet(None, None, fo["C"], fo["G"]),
+                                      gw.CompressionRanks(6, 8, 5), "full", coeffs=c[None, None])
+    h = O.contract_mode3(np.transpose(X[0], (2, 1, 0)), c[0])
+    s1 = np.linalg.svd(h, compute_uv=False)[0]
+    assert abs(rep.sinr[0, 0, 0, 0] - s1 * s1 / 0.09) <= 1e-8 * s1 * s1 / 0.09
+
+
+def test_sinr_errors(ctx):
+    topo = gw.SystemTopology(2, 1, 4, 8, 5, 4, 0.1)
+    z = np.zeros((1, 2, 3, 5), np.complex128)
+    G = np.zeros((1, 2, 3, 3, 4), np.complex128)
+    with pytest.raises(gw.InvalidArgument, match="stream count"):
+        ctx.run_compressed_pipeline(topo, gw.GroupwiseFactorSet(None, None, z, G), gw.CompressionRanks(4, 3, 3),
+                                    coeffs=np.zeros((1, 1, 2, 5), np.complex128))
+
+
+# ---------------------------------------------------------------------------
+# Tucker compression parity
+
+@pytest.mark.parametrize("name,ngroups", [("C1", None), ("C2d", 2), ("C2", 2)])
+def test_groupwise_solve_nmse_parity(ctx, name, ngroups):
+    cfg = gw.CONFIGS[name]
+    X, X128, tau = baseline_inputs(cfg, ngroups)
+    fo = _oracle_factors(cfg, X128)
+    res = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), cfg.sweeps, early_stop=False)
+    nmse_gpu = res.trace[:, -1] / res.energy
+    nmse_orc = fo["trace"][:, -1] / fo["energy"]
+    assert np.max(np.abs(nmse_gpu - nmse_orc)) <= 1e-6
+    assert np.max(rel_err(res.energy, fo["energy"])) <= (1e-6 if cfg.dtype == "c64" else 1e-12)
+    # every trace entry (init + each sweep) tracks the oracle
+    assert np.max(np.abs(res.trace / res.energy[:, None] - fo["trace"] / fo["energy"][:, None])) <= 1e-6
+    assert (np.asarray(res.iterations_run) == cfg.sweeps).all()
+    # factors orthonormal, and their subspaces match the oracle's (fp64)
+    if cfg.dtype == "c128":
+        for g in range(X.shape[0]):
+            for k in range(cfg.J):
+                assert _max_angle(res.tx[g, k].T, fo["B"][g, k].T) < 1e-6
+            for u in range(cfg.J * cfg.K):
+                assert _max_angle(res.rx[g, u].T, fo["A"][g, u].T) < 1e-6
+
+
+def test_groupwise_solve_early_stop_and_trace(ctx):
+    cfg = gw.CONFIGS["C1"]
+    X, X128, _ = baseline_inputs(cfg)
+    fo = _oracle_factors(cfg, X128, sweeps=60, early=True)
+    res = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), 60, early_stop=True)
+    assert np.array_equal(np.asarray(res.iterations_run), fo["iters"])
+    tr = np.asarray(res.trace)
+    assert (np.diff(tr, axis=1) <= 1e-9 * res.energy[:, None]).all()  # monotone (decompose.hpp:33-41)
+    assert np.max(np.abs(tr[:, -1] / res.energy - fo["trace"][:, -1] / fo["energy"])) <= 1e-6
+
+
+def test_shared_solve_parity(ctx):
+    cfg = gw.CONFIGS["C1"]
+    X, X128, _ = baseline_inputs(cfg, 2)
+    fo = O.alternating_solve(dims_of(cfg), X128, 5, early_stop=False, pooled=True)
+    res = ctx.shared_solve(cfg.topology(), X, cfg.ranks(), 5, early_stop=False)
+    assert np.max(np.abs(res.trace / res.energy[:, None] - fo["trace"] / fo["energy"][:, None])) <= 1e-9
+    # every user carries the same receive factor
+    assert np.allclose(res.rx[:, :1], res.rx)
+
+
+def test_warm_start_and_zero_sweeps(ctx):
+    cfg = gw.CONFIGS["C1"]
+    X, X128, _ = baseline_inputs(cfg, 2)
+    fo = _oracle_factors(cfg, X128, sweeps=3)
+    init = gw.GroupwiseFactorSet(fo["A"], fo["B"], fo["C"], None)
+    res = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), 0, init=init)
+    assert rel_err(res.trace[:, 0], fo["trace"][:, -1]).max() <= 1e-10
+    assert np.max(np.abs(res.cores - fo["G"])) <= 1e-10 * np.abs(fo["G"]).max()
+
+
+def test_reconstruct_parity(ctx):
+    cfg = gw.CONFIGS["C1"]
+    X, X128, _ = baseline_inputs(cfg, 1)
+    fo = _oracle_factors(cfg, X128, sweeps=2)
+    fac = gw.GroupwiseFactorSet(fo["A"], fo["B"], fo["C"], fo["G"])
+    Xh = ctx.reconstruct(cfg.topology(), cfg.ranks(), fac)
+    for l in range(cfg.G):
+        k, u = l // (cfg.J * cfg.K), l % (cfg.J * cfg.K)
+        want = O.reconstruct(fo["A"][0, u].T, fo["B"][0, k].T, fo["C"][0, l].T, np.transpose(fo["G"][0, l], (2, 1, 0)))
+        got = np.transpose(Xh[0, l], (2, 1, 0))
+        assert np.max(np.abs(got - want)) <= 1e-12 * np.abs(want).max()
+
+
+def test_solver_errors(ctx):
+    cfg = gw.CONFIGS["C1"]
+    X, _, _ = baseline_inputs(cfg, 1)
+    with pytest.raises(gw.InvalidArgument, match="rank m = 5 out of range for mode-1 size 4"):
+        ctx.groupwise_solve(cfg.topology(), X, gw.CompressionRanks(5, 4, 4), 1)
+    with pytest.raises(gw.InvalidArgument, match="sweeps must be >= 0"):
+        ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), -1)
+
+
+def test_end_to_end_compress_then_sinr(ctx):
+    """GPU compress -> GPU SINR against oracle compress -> oracle SINR (C1, fp64)."""
+    cfg = gw.CONFIGS["C1"]
+    X, X128, tau = baseline_inputs(cfg)
+    fo = _oracle_factors(cfg, X128)
+    res = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), cfg.sweeps, early_stop=False)
+    rep = ctx.run_compressed_pipeline(cfg.topology(), res, cfg.ranks(), tau=tau, freqs=cfg.freqs())
+    want, _ = O.sinr_compressed(dims_of(cfg), fo["C"], fo["G"], O.coeffs_from_tau(tau, cfg.freqs()), cfg.sigma,
+                                cfg.L, O.SCOPE_PAPER, nthreads=8)
+    assert rel_err(rep.sinr, want).max() <= 1e-6
+
+
+def test_device_resident_torch_path(ctx):
+    torch = pytest.importorskip("torch")
+    cfg = gw.CONFIGS["C1"]
+    X, X128, tau = baseline_inputs(cfg)
+    Xd = torch.from_numpy(X).cuda()
+    before = ctx.launches
+    res = ctx.groupwise_solve(cfg.topology(), Xd, cfg.ranks(), 3, early_stop=False)
+    rep = ctx.run_compressed_pipeline(cfg.topology(), res, cfg.ranks(), tau=torch.from_numpy(tau).cuda(),
+                                      freqs=torch.from_numpy(cfg.freqs()).cuda())
+    torch.cuda.synchronize()
+    assert ctx.launches > before
+    host = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), 3, early_stop=False)
+    assert np.allclose(res.trace.cpu().numpy(), host.trace, rtol=1e-12, atol=0)
+    assert rep.sinr.is_cuda
