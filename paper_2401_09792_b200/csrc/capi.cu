@@ -471,11 +471,11 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     }
     // subcarrier chunk from the workspace budget
     const int64_t per_f = (int64_t)ngroups * ((int64_t)cs * links * t.m * t.n + 16LL * users * S * t.m * t.m +
-                                             8LL * users * (t.L + 2 * t.m * t.L));
+                                             8LL * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
     int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, (int64_t)(std::min<size_t>(ws_budget(), size_t(2) << 30) / std::max<int64_t>(per_f, 1))));
     void* H = ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
     double2* PG = (double2*)ctx->ws(WS_PG, 16 * ngroups * Fc * users * S * t.m * t.m);
-    double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * Fc * users * (t.L + 2 * t.m * t.L));
+    double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * Fc * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
     double ms_r = 0, ms_p = 0, ms_s = 0;
     for (int64_t f0 = 0; f0 < F; f0 += Fc) {
         const int fc = (int)std::min(Fc, F - f0);

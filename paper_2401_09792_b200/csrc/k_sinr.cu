@@ -199,7 +199,7 @@ __device__ __forceinline__ void jacobi_herm(double2 (&A)[M][M], double2 (&V)[M][
 
 // ---------------------------------------------------------------------------
 // K3a: precoder per (group, subcarrier, user): eig of the serving Gram ->
-// top-L eigenpairs (descending). EG layout per item: lambda[L] then U[M][L]
+// top-L eigenpairs (descending). EG layout per item: lambda[L] (padded to even) then U[M][L]
 // column-major (M x L), fp64.
 template <int M>
 __global__ void __launch_bounds__(128) k_precoder_eig(Topo t, int scope, int S, int64_t items,
@@ -239,8 +239,9 @@ __global__ void __launch_bounds__(128) k_precoder_eig(Topo t, int scope, int S, 
         for (int s = 0; s < M; ++s) rk += (lam[s] > lam[r] || (lam[s] == lam[r] && s < r)) ? 1 : 0;
         rank[r] = rk;
     }
-    double* dst = EG + item * (int64_t)(L + 2 * M * L);
-    double2* du = reinterpret_cast<double2*>(dst + L);
+    const int Lp = (L + 1) & ~1;  // keep the U block 16-byte aligned
+    double* dst = EG + item * (int64_t)(Lp + 2 * M * L);
+    double2* du = reinterpret_cast<double2*>(dst + Lp);
 #pragma unroll
     for (int r = 0; r < M; ++r) {
         if (rank[r] < L) {
@@ -267,9 +268,10 @@ __global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t 
     const int u = (int)(item % users);
     const int64_t gf = item / users;
     const int i = u / t.K, j = u % t.K;
-    const int64_t eg_stride = L + 2 * M * L;
+    const int Lp = (L + 1) & ~1;
+    const int64_t eg_stride = Lp + 2 * M * L;
     const double* own = EG + item * eg_stride;
-    const double2* ownU = reinterpret_cast<const double2*>(own + L);
+    const double2* ownU = reinterpret_cast<const double2*>(own + Lp);
     int st = 0;
     double2 Q[M][M];
     const double s2 = sigma * sigma;
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t 
         scope_slot(t, scope, i, j, s, k, l);
         const int64_t pidx = gf * users + (k * t.K + l);
         const double* pe = EG + pidx * eg_stride;
-        const double2* pU = reinterpret_cast<const double2*>(pe + L);
+        const double2* pU = reinterpret_cast<const double2*>(pe + Lp);
         const double2* X = PG + (item * S + s) * M * M;
         double2 Xr[M][M];
 #pragma unroll
