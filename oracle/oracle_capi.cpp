@@ -286,7 +286,6 @@ int orc_sinr_compressed(int J, int K, int P, int m, int n, int p, int L, double 
     const std::size_t c_sz = static_cast<std::size_t>(P) * p * t.links(), g_sz = static_cast<std::size_t>(m) * n * p * t.links();
     std::vector<Ledger> lg(static_cast<std::size_t>(ngroups));
     int rc = for_groups(ngroups, nthreads, err, len, [&](std::int64_t g) {
-        t.validate();
         FactorSet fs;
         fs.J = J; fs.K = K; fs.ranks = r;
         fs.delay.resize(t.links());

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -416,12 +417,16 @@ void groupwise_solve_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_rank
 // ---------------------------------------------------------------------------
 // compressed SINR
 void validate_sinr(const gwt_topology& tp, const gwt_ranks& r, int scope) {
-    validate_topology(tp);
+    // run_compressed_pipeline does not validate the topology; the first checks it meets are the
+    // precoder's stream count (sinr.cpp:163-167) and woodbury_inverse_apply's sigma (:208-209)
+    if (tp.num_cells < 1 || tp.users_per_cell < 1 || tp.num_taps < 1 || tp.num_streams < 1)
+        invalid("topology: num_cells, users_per_cell, num_taps and num_streams must be >= 1");
     if (r.m < 1 || r.n < 1 || r.p < 1) invalid("ranks must be >= 1");
     if (scope != GWT_SCOPE_FULL && scope != GWT_SCOPE_PAPER) invalid("sinr: unknown interference scope");
     if (tp.num_streams > std::min(r.m, r.n))  // precoder_compressed (sinr.cpp:163-167)
         invalid("precoder: stream count " + std::to_string(tp.num_streams) + " exceeds compressed channel size " +
                 std::to_string(r.m) + "x" + std::to_string(r.n) + " (ranks chosen below stream count)");
+    if (!(tp.noise_std > 0.0)) invalid("woodbury_inverse_apply: sigma must be > 0");
     if (r.m > 8) invalid("sinr: compressed receive rank m > 8 is not supported by the B200 small-matrix kernel");
 }
 
@@ -469,29 +474,59 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         std_ = (int*)ctx->ws(WS_STATUS, 4 * out_rows);
         tm.mark(5);
     }
-    // subcarrier chunk from the workspace budget
-    const int64_t per_f = (int64_t)ngroups * ((int64_t)cs * links * t.m * t.n + 16LL * users * S * t.m * t.m +
-                                             8LL * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
-    int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, (int64_t)(std::min<size_t>(ws_budget(), size_t(2) << 30) / std::max<int64_t>(per_f, 1))));
-    void* H = ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
-    double2* PG = (double2*)ctx->ws(WS_PG, 16 * ngroups * Fc * users * S * t.m * t.m);
-    double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * Fc * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
     double ms_r = 0, ms_p = 0, ms_s = 0;
-    for (int64_t f0 = 0; f0 < F; f0 += Fc) {
-        const int fc = (int)std::min(Fc, F - f0);
+    const char* path = std::getenv("GWT_SINR_PATH");
+    // default: rebuild -> pair Grams -> eig/MMSE (fastest measured on C2);
+    // GWT_SINR_PATH=fused selects the shared-memory fused rebuild+Gram path (paper scope only)
+    const bool fused = scope == GWT_SCOPE_PAPER && path && std::strcmp(path, "fused") == 0;
+    if (fused) {
+        // rebuild + Grams fused (H~ stays in shared memory), then the per-group small-matrix solve
+        std::vector<double> fh(coeffs ? 0 : F);
+        if (!coeffs) {
+            if (mem == GWT_MEM_HOST) std::memcpy(fh.data(), freqs, 8 * F);
+            else ck(cudaMemcpy(fh.data(), freqs, 8 * F, cudaMemcpyDeviceToHost), "freqs");
+        }
+        int uniform = coeffs ? 0 : 1;
+        const double df = (!coeffs && F > 1) ? fh[1] - fh[0] : 0.0;
+        for (int64_t f = 1; uniform && f < F; ++f)
+            if (std::fabs(fh[f] - fh[0] - df * f) > 1e-9 * std::max(std::fabs(df) * F, 1.0)) uniform = 0;
+        const int64_t per_f = 16LL * ngroups * users * t.J * t.m * t.m;
+        const int64_t Fc = std::max<int64_t>(16, std::min<int64_t>(F, (int64_t)(48ll << 20) / std::max<int64_t>(per_f, 1)));
+        double2* GU = (double2*)ctx->ws(WS_PG, 16 * ngroups * std::min(Fc, F) * users * t.J * t.m * t.m);
         tm.mark(8);
-        ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
+        for (int64_t f0 = 0; f0 < F; f0 += Fc) {
+            const int fc = (int)std::min(Fc, F - f0);
+            ctx->launched(launch_sinr_fused<T>(t, (int)ngroups, fc, f0, F, topo->noise_std, Cd, Gd, taud, fd, uniform,
+                                               df, cod, GU, sd, sgd, std_, st),
+                          2);
+        }
         tm.mark(9);
-        ctx->launched(launch_pair_gram<T>(t, scope, S, fc, (int)ngroups, H, PG, st));
-        tm.mark(10);
-        ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PG, EG, sd,
-                                        sgd, std_, st),
-                      2);
-        tm.mark(11);
-        ck(cudaEventSynchronize(ctx->ev[11]), "sync");
-        ms_r += tm.between(8, 9);
-        ms_p += tm.between(9, 10);
-        ms_s += tm.between(10, 11);
+        ck(cudaEventSynchronize(ctx->ev[9]), "sync");
+        ms_r = tm.between(8, 9);
+    } else {
+        // generic path (any scope): rebuild -> pair Grams -> eig + MMSE through HBM workspaces
+        const int64_t per_f = (int64_t)ngroups * ((int64_t)cs * links * t.m * t.n + 16LL * users * S * t.m * t.m +
+                                                 8LL * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
+        int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, (int64_t)(std::min<size_t>(ws_budget(), size_t(2) << 30) / std::max<int64_t>(per_f, 1))));
+        void* H = ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
+        double2* PG = (double2*)ctx->ws(WS_PG, 16 * ngroups * Fc * users * S * t.m * t.m);
+        double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * Fc * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
+        for (int64_t f0 = 0; f0 < F; f0 += Fc) {
+            const int fc = (int)std::min(Fc, F - f0);
+            tm.mark(8);
+            ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
+            tm.mark(9);
+            ctx->launched(launch_pair_gram<T>(t, scope, S, fc, (int)ngroups, H, PG, st));
+            tm.mark(10);
+            ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PG, EG, sd,
+                                            sgd, std_, st),
+                          2);
+            tm.mark(11);
+            ck(cudaEventSynchronize(ctx->ev[11]), "sync");
+            ms_r += tm.between(8, 9);
+            ms_p += tm.between(9, 10);
+            ms_s += tm.between(10, 11);
+        }
     }
     if (mem == GWT_MEM_HOST) {
         tm.mark(12);

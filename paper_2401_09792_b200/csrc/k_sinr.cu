@@ -18,9 +18,24 @@
 //                 gamma_r = g_r^H Q^{-1} g_r (Cholesky + forward solve)
 //                 signal_r = gamma_r^2, SINR_r = gamma_r / (1 - gamma_r)
 // which equals the reference's W~ = (1/s^2)(HV - T HV) route algebraically.
+#include <cstdlib>
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace gwtk {
+
+// conj(c_r(f)) for subcarrier index fa: binary64 argument reduction, then sincospi in the
+// working precision (fp32 for c64: |error| ~1e-7 rad; fp64 for c128)
+template <class T> __device__ __forceinline__ cplx_t<T> conj_coeff(double f, double tau);
+template <> __device__ __forceinline__ float2 conj_coeff<float>(double f, double tau) {
+    double x = f * tau;
+    x -= floor(x);
+    float s, c;
+    sincospif(2.0f * (float)x, &s, &c);
+    return make_float2(c, -s);
+}
+template <> __device__ __forceinline__ double2 conj_coeff<double>(double f, double tau) { return phasor_neg(f, tau); }
 
 // ---------------------------------------------------------------------------
 // K1: rebuild H~(f) = sum_q G(:,:,q) * E[q][f],
@@ -47,7 +62,7 @@ __global__ void __launch_bounds__(128) k_rebuild(Topo t, int Fc, int64_t f0, int
             if (coeffs) {
                 v = cconj(coeffs[(((int64_t)g * Ftot + fa) * links + l) * t.P + r]);
             } else {
-                v = from_d2<C>(phasor_neg(freqs[fa], tau[gl * t.P + r]));
+                v = conj_coeff<T>(freqs[fa], tau[gl * t.P + r]);
             }
         }
         ph[idx] = v;
@@ -146,18 +161,21 @@ __device__ __forceinline__ void jacobi_herm(double2 (&A)[M][M], double2 (&V)[M][
 #pragma unroll
             for (int q = p + 1; q < M; ++q) off += A[p][q].x * A[p][q].x + A[p][q].y * A[p][q].y;
         }
-        if (off <= 1e-34 * dia || off == 0.0) break;
+        if (off <= 1e-30 * dia || off == 0.0) break;
 #pragma unroll
         for (int p = 0; p < M; ++p)
 #pragma unroll
             for (int q = p + 1; q < M; ++q) {
-                const double b = hypot(A[p][q].x, A[p][q].y);
-                if (b > 1e-300) {
-                    const double phr = A[p][q].x / b, phi = A[p][q].y / b;  // phase = apq/|apq|
-                    const double alpha = A[p][p].x, delta = A[q][q].x;
-                    const double tau = (delta - alpha) / (2.0 * b);
-                    const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    const double c = 1.0 / sqrt(1.0 + tt * tt);
+                const double b2 = A[p][q].x * A[p][q].x + A[p][q].y * A[p][q].y;
+                if (b2 > 1e-300) {
+                    // rotation angle in fp32 (only the convergence rate depends on it); the rotation
+                    // itself (unit phase, c = 1/sqrt(1+t^2), s = t c) is exact in binary64
+                    const double rb = rsqrt(b2);
+                    const double phr = A[p][q].x * rb, phi = A[p][q].y * rb;  // phase = apq/|apq|
+                    const float tau = (float)((A[q][q].x - A[p][p].x) * (0.5 * rb));
+                    const float tf = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 1.0f)));
+                    const double tt = (double)tf;
+                    const double c = rsqrt(fma(tt, tt, 1.0));
                     const double s = tt * c;
                     // U = [[c, s], [-s conj(ph), c conj(ph)]]
                     const double2 uqp = make_double2(-s * phr, s * phi);
@@ -403,6 +421,497 @@ __global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t 
     }
     status[orow] = st;
 }
+
+// ---------------------------------------------------------------------------
+// Fused compressed-SINR path (paper_experiment scope), two kernels:
+//  k_rebuild_gram: one CTA per (group, user batch, subcarrier tile). H~ is
+//    rebuilt tile by tile into shared memory and consumed there: per user the
+//    serving Gram A_u and one cross Gram X_{u,k} per other cell (fp64), so H~
+//    never touches HBM. Output: GU[g][f][user][J][m*m].
+//  k_sinr_solve: one CTA per (group, subcarrier tile), one thread per
+//    (user, subcarrier): eig of A_u (Jacobi), the partner projectors P_{k0}
+//    exchanged through shared memory, covariance, Cholesky, SINR.
+struct FusedShape {
+    int B, FT, fsplit;
+};
+
+// Shared-memory tile layouts (bank-conflict free for the access patterns below):
+//   Ph [nl][P][FT] conj(c_r(f)),  E [nl][p][FT],  H~ tile [m*n][FT+1] (subcarrier fastest, padded)
+// A CTA is split into NG independent groups of WG threads (named barriers), each group
+// rebuilding nl (<= 2) links at a time: phasors -> E -> H~ -> Grams, every phase fully parallel.
+
+__device__ __forceinline__ void group_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <class T, int M, int FT, int FPT>
+__device__ __forceinline__ void group_rebuild(const Topo& t, int lane, int WG, int bar_id, int nl, const int* lids,
+                                              int ft0, int Fc, int64_t f0, int64_t Ftot, int64_t gidx,
+                                              const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
+                                              const double* __restrict__ tau, const double* __restrict__ freqs,
+                                              const cplx_t<T>* __restrict__ coeffs, cplx_t<T>* Ph, cplx_t<T>* Es,
+                                              cplx_t<T>* const* dst) {
+    using C = cplx_t<T>;
+    constexpr int LD = FT + 1;
+    const int links = t.links();
+    const int PF = t.P * FT, pF = t.p * FT;
+    for (int idx = lane; idx < nl * PF; idx += WG) {
+        const int li = idx / PF, rem = idx % PF, r = rem / FT, f = rem % FT;
+        const int64_t gl = gidx * links + lids[li];
+        C v = czero<C>();
+        if (ft0 + f < Fc) {
+            const int64_t fa = f0 + ft0 + f;
+            v = coeffs ? cconj(coeffs[((gidx * Ftot + fa) * links + lids[li]) * t.P + r])
+                       : conj_coeff<T>(freqs[fa], tau[gl * t.P + r]);
+        }
+        Ph[idx] = v;
+    }
+    group_bar(bar_id, WG);
+    for (int idx = lane; idx < nl * pF; idx += WG) {
+        const int li = idx / pF, rem = idx % pF, q = rem / FT, f = rem % FT;
+        const C* Cl = Cd + (gidx * links + lids[li]) * t.P * t.p + (int64_t)t.P * q;
+        const C* ph = Ph + li * PF + f;
+        C acc = czero<C>();
+        for (int r = 0; r < t.P; ++r) cfma(acc, Cl[r], ph[r * FT]);
+        Es[idx] = acc;
+    }
+    group_bar(bar_id, WG);
+    const int mn = M * t.n;
+    constexpr int FS = FT / FPT;
+    for (int idx = lane; idx < nl * mn * FS; idx += WG) {
+        const int li = idx / (mn * FS), rem = idx % (mn * FS), row = rem % mn, fb = (rem / mn) * FPT;
+        const C* Gl = G + (gidx * links + lids[li]) * mn * t.p + row;
+        const C* e = Es + li * pF + fb;
+        C acc[FPT];
+#pragma unroll
+        for (int ff = 0; ff < FPT; ++ff) acc[ff] = czero<C>();
+        for (int q = 0; q < t.p; ++q) {
+            const C gv = Gl[(int64_t)mn * q];
+#pragma unroll
+            for (int ff = 0; ff < FPT; ++ff) cfma(acc[ff], gv, e[q * FT + ff]);
+        }
+        C* d = dst[li] + row * LD + fb;
+#pragma unroll
+        for (int ff = 0; ff < FPT; ++ff) d[ff] = acc[ff];
+    }
+    group_bar(bar_id, WG);
+}
+
+// Gram tasks of one user: serving (Hermitian, M(M+1)/2 entries) and `ncross` cross Grams (M*M each)
+// out[f*ostride + slot*MM + a + M b] = sum_c Hx[a + M c][f] conj(Hy[b + M c][f])  (fp64 accumulation)
+template <class T, int M, int FT>
+__device__ __forceinline__ void group_grams(int lane, int WG, int bar_id, int n, int Fvalid, const cplx_t<T>* Hs,
+                                            int ncross, const cplx_t<T>* const* Hc, const cplx_t<T>* const* Hp,
+                                            const int* slot, double2* out, int64_t ostride) {
+    constexpr int LD = FT + 1, MM = M * M, HS = M * (M + 1) / 2;
+    const int total = FT * (HS + ncross * MM);
+    for (int idx = lane; idx < total; idx += WG) {
+        const int f = idx % FT;
+        int e = idx / FT;
+        const cplx_t<T>*hx, *hy;
+        int a, b, sl;
+        bool herm = e < HS;
+        if (herm) {
+            a = 0;
+            while (e >= M - a) { e -= M - a; ++a; }
+            b = a + e;
+            hx = Hs;
+            hy = Hs;
+            sl = 0;
+        } else {
+            e -= HS;
+            const int c = e / MM;
+            e %= MM;
+            a = e % M;
+            b = e / M;
+            hx = Hc[c];
+            hy = Hp[c];
+            sl = slot[c];
+        }
+        if (f >= Fvalid) continue;
+        const cplx_t<T>* px = hx + a * LD + f;
+        const cplx_t<T>* py = hy + b * LD + f;
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
+        for (int c = 0; c < n; ++c) cfmac(acc, to_d2(px[M * LD * c]), to_d2(py[M * LD * c]));
+        double2* o = out + f * ostride + sl * MM;
+        o[a + M * b] = acc;
+        if (herm && a != b) o[b + M * a] = make_double2(acc.x, -acc.y);
+    }
+    group_bar(bar_id, WG);
+}
+
+template <class T, int M, int FT, int FPT>
+__global__ void __launch_bounds__(256) k_rebuild_gram(Topo t, FusedShape fs, int Fc, int64_t f0, int64_t Ftot,
+                                                      const cplx_t<T>* __restrict__ Cd,
+                                                      const cplx_t<T>* __restrict__ G, const double* __restrict__ tau,
+                                                      const double* __restrict__ freqs, int uniform, double df,
+                                                      const cplx_t<T>* __restrict__ coeffs, double2* __restrict__ GU) {
+    using C = cplx_t<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int LD = FT + 1;
+    const int J = t.J, K = t.K, B = fs.B;
+    const int WG = fs.fsplit;  // threads per group
+    const int NG = blockDim.x / WG;
+    const int mn = M * t.n, MM = M * M;
+    const size_t tile = (size_t)mn * LD;
+    const size_t per_group = 2 * tile + (size_t)2 * FT * (t.P + t.p);
+    C* Hpart = reinterpret_cast<C*>(smem_raw);  // [J][mn][LD]
+    const int grp = threadIdx.x / WG, lane = threadIdx.x % WG, bar_id = 1 + grp;
+    C* gw = Hpart + (size_t)J * tile + grp * per_group;
+    C* Hw0 = gw;
+    C* Hw1 = gw + tile;
+    C* Ph = gw + 2 * tile;
+    C* Es = Ph + (size_t)2 * FT * t.P;
+    const int64_t gidx = blockIdx.z;
+    const int ft0 = blockIdx.x * FT;
+    const int Fvalid = min(FT, Fc - ft0);
+    const int u0 = blockIdx.y * B;
+    const int users = t.users();
+    auto link_id = [&](int k, int i, int j) { return (k * J + i) * K + j; };
+    const int64_t fstride = (int64_t)users * J * MM;
+    double2* gbase = GU + ((gidx * Fc + ft0) * users) * (int64_t)J * MM;
+    // partner links (k,k,0), round-robin over groups, into Hpart
+    for (int k = grp; k < J; k += NG) {
+        int lid[2] = {link_id(k, k, 0), 0};
+        C* dst[2] = {Hpart + (size_t)k * tile, nullptr};
+        group_rebuild<T, M, FT, FPT>(t, lane, WG, bar_id, 1, lid, ft0, Fc, f0, Ftot, gidx, Cd, G, tau, freqs, coeffs,
+                                     Ph, Es, dst);
+    }
+    __syncthreads();
+    const int ubeg = u0, uend = min(users, u0 + B);
+    for (int u = ubeg + grp; u < uend; u += NG) {
+        const int i = u / K, j = u % K;
+        // cross links (k,i,j), k != i, in slot order; the serving link rides along when j != 0
+        int kc = 0;
+        int cross_k[8];
+        for (int k = 0; k < J && kc < 8; ++k)
+            if (k != i) cross_k[kc++] = k;
+        const C* hs = Hpart + (size_t)i * tile;
+        int done = 0;
+        bool serving_pending = true;
+        while (serving_pending || done < kc) {
+            int lid[2];
+            C* dst[2];
+            int nl = 0;
+            const C* Hc[2];
+            const C* Hp[2];
+            int slot[2];
+            int ncross = 0;
+            bool with_serving = false;
+            if (serving_pending && j != 0) {
+                lid[nl] = link_id(i, i, j);
+                dst[nl] = Hw0;
+                ++nl;
+                hs = Hw0;
+                with_serving = true;
+            } else if (serving_pending) {
+                with_serving = true;  // serving link is the partner tile Hpart[i]
+            }
+            while (nl < 2 && done < kc) {
+                const int k = cross_k[done];
+                lid[nl] = link_id(k, i, j);
+                dst[nl] = nl == 0 ? Hw0 : Hw1;
+                Hc[ncross] = dst[nl];
+                Hp[ncross] = Hpart + (size_t)k * tile;
+                slot[ncross] = 1 + done;
+                ++ncross;
+                ++nl;
+                ++done;
+            }
+            if (nl > 0)
+                group_rebuild<T, M, FT, FPT>(t, lane, WG, bar_id, nl, lid, ft0, Fc, f0, Ftot, gidx, Cd, G, tau, freqs,
+                                             coeffs, Ph, Es, dst);
+            if (with_serving) {
+                group_grams<T, M, FT>(lane, WG, bar_id, t.n, Fvalid, hs, ncross, Hc, Hp, slot,
+                                      gbase + (int64_t)u * J * MM, fstride);
+            } else {
+                // cross-only round: reuse the Gram routine with a dummy serving slot skipped
+                constexpr int LDc = FT + 1;
+                const int total = FT * ncross * MM;
+                for (int idx = lane; idx < total; idx += WG) {
+                    const int f = idx % FT;
+                    int e = idx / FT;
+                    const int c = e / MM;
+                    e %= MM;
+                    const int a = e % M, b = e / M;
+                    if (f >= Fvalid) continue;
+                    const C* px = Hc[c] + a * LDc + f;
+                    const C* py = Hp[c] + b * LDc + f;
+                    double2 acc = make_double2(0.0, 0.0);
+                    for (int cc = 0; cc < t.n; ++cc) cfmac(acc, to_d2(px[M * LDc * cc]), to_d2(py[M * LDc * cc]));
+                    gbase[(int64_t)u * J * MM + f * fstride + slot[c] * MM + a + M * b] = acc;
+                }
+                group_bar(bar_id, WG);
+            }
+            serving_pending = false;
+        }
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void load_herm(const double2* src, double2 (&A)[M][M]) {
+#pragma unroll
+    for (int b = 0; b < M; ++b)
+#pragma unroll
+        for (int a = 0; a < M; ++a) A[a][b] = src[a + M * b];
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+        A[a][a].y = 0.0;
+#pragma unroll
+        for (int b = a + 1; b < M; ++b) {
+            const double2 v = make_double2(0.5 * (A[a][b].x + A[b][a].x), 0.5 * (A[a][b].y - A[b][a].y));
+            A[a][b] = v;
+            A[b][a] = make_double2(v.x, -v.y);
+        }
+    }
+}
+
+// one CTA per (group, subcarrier tile); thread = (f, user)
+template <int M>
+__global__ void __launch_bounds__(128) k_sinr_solve(Topo t, int FT, int Fc, int64_t f0, int64_t Ftot, double sigma,
+                                                    const double2* __restrict__ GU, double* __restrict__ sinr,
+                                                    double* __restrict__ signal, int* __restrict__ status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int J = t.J, K = t.K, L = t.L, MM = M * M;
+    const int users = t.users();
+    double2* Pk = reinterpret_cast<double2*>(smem_raw);  // [FT][J][MM]
+    int* pbad = reinterpret_cast<int*>(Pk + (size_t)FT * J * MM);  // [FT][J]
+    const int64_t gidx = blockIdx.y;
+    const int ft0 = blockIdx.x * FT;
+    const int tid = threadIdx.x;
+    const int f = tid / users, u = tid % users;
+    const bool active = (f < FT) && (ft0 + f < Fc);
+    const int i = u / K, j = u % K;
+    double lam[M];
+    int rank[M];
+    double2 V[M][M];
+    const double2* g = GU + (((gidx * Fc + ft0 + f) * users + u) * (int64_t)J) * MM;
+    if (active) {
+        double2 A[M][M];
+        load_herm<M>(g, A);
+        jacobi_herm<M>(A, V);
+#pragma unroll
+        for (int r = 0; r < M; ++r) lam[r] = A[r][r].x;
+#pragma unroll
+        for (int r = 0; r < M; ++r) {
+            int rk = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < M; ++s2) rk += (lam[s2] > lam[r] || (lam[s2] == lam[r] && s2 < r)) ? 1 : 0;
+            rank[r] = rk;
+        }
+        if (j == 0) {  // partner projector P = U_L Lambda_L^{-1} U_L^H for the other cells' users
+            double2* P = Pk + ((size_t)f * J + i) * MM;
+            int bad = 0;
+#pragma unroll
+            for (int a = 0; a < M; ++a)
+#pragma unroll
+                for (int b = 0; b < M; ++b) {
+                    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int r = 0; r < M; ++r) {
+                        if (rank[r] < L && lam[r] > 0.0) {
+                            double2 v = make_double2(0, 0);
+                            cfmac(v, V[a][r], V[b][r]);
+                            const double il = 1.0 / lam[r];
+                            acc.x += il * v.x;
+                            acc.y += il * v.y;
+                        }
+                    }
+                    P[a + M * b] = acc;
+                }
+#pragma unroll
+            for (int r = 0; r < M; ++r) bad |= (rank[r] < L && !(lam[r] > 0.0));
+            pbad[f * J + i] = bad;
+        }
+    }
+    __syncthreads();
+    if (!active) return;
+    int st = 0;
+    double2 Q[M][M];
+    const double s2 = sigma * sigma;
+#pragma unroll
+    for (int a = 0; a < M; ++a)
+#pragma unroll
+        for (int b = 0; b < M; ++b) Q[a][b] = make_double2(a == b ? s2 : 0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        if (rank[r] < L) {
+            const double lr = fmax(lam[r], 0.0);
+#pragma unroll
+            for (int a = 0; a < M; ++a)
+#pragma unroll
+                for (int b = 0; b < M; ++b) {
+                    double2 v = make_double2(0, 0);
+                    cfmac(v, V[a][r], V[b][r]);
+                    Q[a][b].x += lr * v.x;
+                    Q[a][b].y += lr * v.y;
+                }
+        }
+    }
+    int s = 1;
+    for (int k = 0; k < J; ++k) {
+        if (k == i) continue;
+        const double2* X = g + (int64_t)s * MM;
+        const double2* P = Pk + ((size_t)f * J + k) * MM;
+        if (pbad[f * J + k]) st = 5;
+        double2 XP[M][M];
+#pragma unroll
+        for (int a = 0; a < M; ++a)
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                double2 acc = make_double2(0, 0);
+#pragma unroll
+                for (int c = 0; c < M; ++c) cfma(acc, X[a + M * c], P[c + M * b]);
+                XP[a][b] = acc;
+            }
+#pragma unroll
+        for (int a = 0; a < M; ++a)
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                double2 acc = Q[a][b];
+#pragma unroll
+                for (int c = 0; c < M; ++c) cfmac(acc, XP[a][c], X[b + M * c]);
+                Q[a][b] = acc;
+            }
+        ++s;
+    }
+    bool finite = true;
+#pragma unroll
+    for (int a = 0; a < M; ++a)
+#pragma unroll
+        for (int b = 0; b < M; ++b) finite = finite && isfinite(Q[a][b].x) && isfinite(Q[a][b].y);
+    bool pd = finite;
+    double dmax = 0.0, dmin = 1e308;
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+        double d = Q[c][c].x;
+#pragma unroll
+        for (int k2 = 0; k2 < c; ++k2) d -= Q[c][k2].x * Q[c][k2].x + Q[c][k2].y * Q[c][k2].y;
+        pd = pd && (d > 0.0);
+        const double inv = rsqrt(fmax(d, 1e-300));
+        const double lcc = fmax(d, 1e-300) * inv;
+        dmax = fmax(dmax, lcc);
+        dmin = fmin(dmin, lcc);
+        Q[c][c] = make_double2(lcc, inv);  // .y keeps 1/l_cc for the solves
+#pragma unroll
+        for (int r = c + 1; r < M; ++r) {
+            double2 sacc = Q[r][c];
+#pragma unroll
+            for (int k2 = 0; k2 < c; ++k2) {
+                sacc.x -= Q[r][k2].x * Q[c][k2].x + Q[r][k2].y * Q[c][k2].y;
+                sacc.y -= Q[r][k2].y * Q[c][k2].x - Q[r][k2].x * Q[c][k2].y;
+            }
+            Q[r][c] = make_double2(sacc.x * inv, sacc.y * inv);
+        }
+    }
+    if (!finite) st = 4;
+    else if (!pd) st = 1;
+    else if ((dmax / dmin) * (dmax / dmin) > 1e14) st = 2;
+    const int64_t orow = (gidx * Ftot + f0 + ft0 + f) * users + u;
+    double* so = sinr + orow * L;
+    double* sg = signal + orow * L;
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        if (rank[r] >= L) continue;
+        double gamma = 0.0;
+        if (st != 1 && st != 2 && st != 4) {
+            double2 y[M];
+#pragma unroll
+            for (int a = 0; a < M; ++a) {
+                double2 acc = V[a][r];
+#pragma unroll
+                for (int k2 = 0; k2 < a; ++k2) {
+                    acc.x -= Q[a][k2].x * y[k2].x - Q[a][k2].y * y[k2].y;
+                    acc.y -= Q[a][k2].x * y[k2].y + Q[a][k2].y * y[k2].x;
+                }
+                y[a] = make_double2(acc.x * Q[a][a].y, acc.y * Q[a][a].y);
+            }
+            double nn = 0.0;
+#pragma unroll
+            for (int a = 0; a < M; ++a) nn += y[a].x * y[a].x + y[a].y * y[a].y;
+            gamma = fmax(lam[r], 0.0) * nn;
+        }
+        const double sp = gamma * gamma;
+        double den = gamma * (1.0 - gamma);
+        if (den <= -1e-12 && st == 0) st = 3;
+        den = fmax(den, 2.2250738585072014e-308);
+        so[rank[r]] = sp / den;
+        sg[rank[r]] = sp;
+    }
+    status[orow] = st;
+}
+
+template <class T, int M>
+static cudaError_t launch_fused_m(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot, double sigma,
+                                  const void* Cd, const void* G, const double* tau, const double* freqs, int uniform,
+                                  double df, const void* coeffs, double2* GU, double* sinr, double* signal,
+                                  int* status, cudaStream_t st) {
+    const size_t cs = sizeof(cplx_t<T>);
+    const int users = t.users();
+    const int mn = M * t.n;
+    // rebuild+Gram: FT subcarriers per CTA tile, a group of WG threads per user (named barriers).
+    // GWT_RG_FT / GWT_RG_WG override the defaults (tuning).
+    const char* eft = std::getenv("GWT_RG_FT");
+    const char* ewg = std::getenv("GWT_RG_WG");
+    const int FTsel = eft ? std::atoi(eft) : 16;
+    int WG = ewg ? std::atoi(ewg) : (mn <= 128 ? 128 : 256);
+    if (WG < 32 || 256 % WG) WG = 256;
+    const int NG = 256 / WG;
+    FusedShape fs;
+    fs.B = std::min(users, 32);
+    fs.fsplit = WG;
+    cudaError_t e = cudaSuccess;
+    auto run = [&](auto ftc) {
+        constexpr int FT = decltype(ftc)::value;
+        fs.FT = FT;
+        const size_t tile = (size_t)mn * (FT + 1);
+        const size_t sm1 = cs * ((size_t)t.J * tile + (size_t)NG * (2 * tile + (size_t)2 * FT * (t.P + t.p)));
+        if (sm1 > 220 * 1024) { e = cudaErrorInvalidValue; return; }
+        dim3 g1((Fc + FT - 1) / FT, (users + fs.B - 1) / fs.B, ngroups);
+        e = cudaFuncSetAttribute(k_rebuild_gram<T, M, FT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        if (e != cudaSuccess) return;
+        k_rebuild_gram<T, M, FT, 8><<<g1, 256, sm1, st>>>(t, fs, Fc, f0, Ftot, (const cplx_t<T>*)Cd,
+                                                          (const cplx_t<T>*)G, tau, freqs, uniform, df,
+                                                          (const cplx_t<T>*)coeffs, GU);
+        e = cudaGetLastError();
+    };
+    if (FTsel == 8) run(std::integral_constant<int, 8>{});
+    else run(std::integral_constant<int, 16>{});
+    if (e != cudaSuccess) return e;
+    // solve: (users x FT2) threads per CTA, FT2 = 128 / users (>= 1)
+    const int FT2 = std::max(1, 128 / users);
+    const size_t sm2 = (size_t)FT2 * t.J * (16 * M * M + 4) + 16;
+    dim3 g2((Fc + FT2 - 1) / FT2, ngroups);
+    k_sinr_solve<M><<<g2, std::max(32, ((FT2 * users + 31) / 32) * 32), sm2, st>>>(t, FT2, Fc, f0, Ftot, sigma, GU,
+                                                                                sinr, signal, status);
+    return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot, double sigma,
+                              const void* Cd, const void* G, const double* tau, const double* freqs, int uniform,
+                              double df, const void* coeffs, double2* GU, double* sinr, double* signal, int* status,
+                              cudaStream_t st) {
+    if (t.users() > 128) return cudaErrorInvalidValue;
+    switch (t.m) {
+#define GWT_FUSED_CASE(MM)                                                                                         \
+    case MM:                                                                                                       \
+        return launch_fused_m<T, MM>(t, ngroups, Fc, f0, Ftot, sigma, Cd, G, tau, freqs, uniform, df, coeffs, GU, \
+                                     sinr, signal, status, st);
+        GWT_FUSED_CASE(1) GWT_FUSED_CASE(2) GWT_FUSED_CASE(3) GWT_FUSED_CASE(4)
+        GWT_FUSED_CASE(5) GWT_FUSED_CASE(6) GWT_FUSED_CASE(7) GWT_FUSED_CASE(8)
+#undef GWT_FUSED_CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template cudaError_t launch_sinr_fused<float>(const Topo&, int, int, int64_t, int64_t, double, const void*,
+                                              const void*, const double*, const double*, int, double, const void*,
+                                              double2*, double*, double*, int*, cudaStream_t);
+template cudaError_t launch_sinr_fused<double>(const Topo&, int, int, int64_t, int64_t, double, const void*,
+                                               const void*, const double*, const double*, int, double, const void*,
+                                               double2*, double*, double*, int*, cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // launchers

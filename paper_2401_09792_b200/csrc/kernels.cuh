@@ -65,6 +65,11 @@ template <class T> cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc
                                               const void* coeffs, void* H, cudaStream_t st);
 template <class T> cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroups, const void* H,
                                                 double2* PG, cudaStream_t st);
+template <class T> cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
+                                                 double sigma, const void* Cd, const void* G, const double* tau,
+                                                 const double* freqs, int uniform, double df, const void* coeffs,
+                                                 double2* GU, double* sinr, double* signal, int* status,
+                                                 cudaStream_t st);
 cudaError_t launch_sinr_small(const Topo& t, int scope, int S, int64_t items, double sigma, int fc, int64_t Ftot,
                               int64_t f0, const double2* PG, double* EG, double* sinr, double* signal, int* status,
                               cudaStream_t st);
