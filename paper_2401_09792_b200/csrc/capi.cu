@@ -163,12 +163,15 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
     const int64_t gram_elems = std::max({(int64_t)G * users * t.M * t.M, (int64_t)G * t.J * t.N * t.N,
                                          (int64_t)G * links * t.P * t.P});
     void* gram = ctx->ws(WS_GRAM, cs * gram_elems);
-    const int64_t eig_a = std::max({(int64_t)G * users * t.M * t.M, (int64_t)G * t.J * t.N * t.N,
-                                    (int64_t)G * links * t.P * t.P});
+    const int64_t eig_a = std::max({(int64_t)G * users * heev_ws_a_elems(t.M), (int64_t)G * t.J * heev_ws_a_elems(t.N),
+                                    (int64_t)G * links * heev_ws_a_elems(t.P)});
+    const int64_t eig_z = std::max({(int64_t)G * users * heev_ws_z_elems(t.M, t.m),
+                                    (int64_t)G * t.J * heev_ws_z_elems(t.N, t.n),
+                                    (int64_t)G * links * heev_ws_z_elems(t.P, t.p)});
     const int64_t eig_x = std::max({(int64_t)G * users * t.M * t.m, (int64_t)G * t.J * t.N * t.n,
                                     (int64_t)G * links * t.P * t.p});
     double2* eA = (double2*)ctx->ws(WS_EIGA, 16 * eig_a);
-    double* eZ = (double*)ctx->ws(WS_EIGZ, 8 * eig_a);
+    double* eZ = (double*)ctx->ws(WS_EIGZ, 8 * eig_z);
     double2* eX = (double2*)ctx->ws(WS_EIGX, 16 * eig_x);
     void* pool = ctx->ws(WS_POOL, cs * G * std::max(t.M * t.m, t.N * t.n));
     double* energy = (double*)ctx->ws(WS_ENERGY, 8 * G);
@@ -741,8 +744,8 @@ int gwt_leading_eigenvectors(gwt_ctx* ctx, int32_t n, int32_t count, int64_t bat
             Od = ctx->ws(WS_POOL, cs * batch * n * count);
             Ed = evals ? (double*)ctx->ws(WS_MISC, 8 * batch * count) : nullptr;
         }
-        double2* eA = (double2*)ctx->ws(WS_EIGA, 16 * batch * n * n);
-        double* eZ = (double*)ctx->ws(WS_EIGZ, 8 * batch * n * n);
+        double2* eA = (double2*)ctx->ws(WS_EIGA, 16 * batch * heev_ws_a_elems(n));
+        double* eZ = (double*)ctx->ws(WS_EIGZ, 8 * batch * heev_ws_z_elems(n, count));
         double2* eX = (double2*)ctx->ws(WS_EIGX, 16 * batch * n * count);
         int* fl = (int*)ctx->ws(WS_FAIL, 4);
         ck(cudaMemsetAsync(fl, 0, 4, st), "memset");

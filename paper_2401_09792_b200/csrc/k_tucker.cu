@@ -179,6 +179,99 @@ __global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_g
     }
 }
 
+// Thin mode-1 product (Kd = KD <= 8, Cols <= 8, fibers contiguous: ks_in == 1):
+// one thread per fiber, conj(U) broadcast from shared memory. Used for X x1 A^H
+// and Y1 x1 A^H, where the generic 64x64 tile would be >90% padding.
+template <class T, int KD>
+__global__ void __launch_bounds__(256) k_mode1_thin(Topo t, GemmDesc d, int links, int64_t items,
+                                                    const cplx_t<T>* __restrict__ in, const cplx_t<T>* __restrict__ U,
+                                                    cplx_t<T>* __restrict__ out) {
+    using C = cplx_t<T>;
+    const int rows = d.R * d.S;
+    const int64_t total = items * rows;
+    const int64_t ublk = d.ublk >= 0 ? d.ublk : (int64_t)d.Kd * d.Cols;
+    const int64_t ucol = d.ucol >= 0 ? d.ucol : (int64_t)d.Kd;
+    for (int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gidx < total;
+         gidx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t item = gidx / rows;
+        const int row = (int)(gidx % rows);
+        const int64_t g = item / links;
+        const int l = (int)(item % links);
+        const C* ub = U + factor_index(t, d.fkind, g, l) * ublk;
+        const C* x = in + item * d.in_item + (row % d.R) * d.rs_in + (int64_t)(row / d.R) * d.s_in;
+        C xv[KD];
+#pragma unroll
+        for (int kk = 0; kk < KD; ++kk) xv[kk] = x[kk];
+        C* o = out + item * d.out_item + (row % d.R) * d.rs_out + (int64_t)(row / d.R) * d.s_out;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (c >= d.Cols) break;
+            C acc = czero<C>();
+#pragma unroll
+            for (int kk = 0; kk < KD; ++kk) {
+                C u = ub[(int64_t)kk * d.uk + (int64_t)c * ucol];
+                if (d.uconj) u = cconj(u);
+                cfma(acc, xv[kk], u);
+            }
+            o[(int64_t)c * d.cs_out] = acc;
+        }
+    }
+}
+
+// Thin Gram (D = MD <= 8, x fastest: xs == 1): one CTA per set; each thread
+// accumulates a private MD x MD partial over strided columns, then a fixed-order
+// shared-memory tree reduction (deterministic).
+template <class T, int MD>
+__global__ void __launch_bounds__(128) k_gram_thin(Topo t, GramDesc d, int sets_per_group,
+                                                  const cplx_t<T>* __restrict__ V, cplx_t<T>* __restrict__ out) {
+    using C = cplx_t<T>;
+    using R = decltype(C{}.x);
+    constexpr int NE = MD * (MD + 1) / 2;
+    __shared__ C red[4][NE];
+    const int64_t set = blockIdx.x;
+    const int64_t g = set / sets_per_group;
+    const int s = (int)(set % sets_per_group);
+    C acc[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) acc[e] = czero<C>();
+    const int nl = set_size(t, d.set_kind);
+    const int Tn = d.T1 * d.T2;
+    for (int r = 0; r < nl; ++r) {
+        const int l = set_link(t, d.set_kind, s, r);
+        const C* vb = V + (g * t.links() + l) * d.v_item;
+        for (int tt = threadIdx.x; tt < Tn; tt += blockDim.x) {
+            const C* col = vb + (int64_t)(tt % d.T1) * d.t1s + (int64_t)(tt / d.T1) * d.t2s;
+            C x[MD];
+#pragma unroll
+            for (int a = 0; a < MD; ++a) x[a] = col[a];
+            int e = 0;
+#pragma unroll
+            for (int a = 0; a < MD; ++a)
+#pragma unroll
+                for (int b = a; b < MD; ++b) cfmac(acc[e++], x[a], x[b]);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        for (int o = 16; o > 0; o >>= 1) {
+            acc[e].x += __shfl_xor_sync(0xffffffffu, acc[e].x, o);
+            acc[e].y += __shfl_xor_sync(0xffffffffu, acc[e].y, o);
+        }
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32][e] = acc[e];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        C* ob = out + set * (int64_t)MD * MD;
+        int e = 0;
+        for (int a = 0; a < MD; ++a)
+            for (int b = a; b < MD; ++b, ++e) {
+                const C v = cadd(cadd(red[0][e], red[1][e]), cadd(red[2][e], red[3][e]));
+                ob[a + MD * b] = v;
+                ob[b + MD * a] = mk((R)v.x, (R)-v.y);
+            }
+    }
+}
+
 // Per-group sum of |v|^2 over `per_group` contiguous complex elements:
 // deterministic (fixed tree), fp64 accumulation. One CTA per group.
 template <class T>
@@ -223,6 +316,18 @@ __global__ void k_broadcast(const cplx_t<T>* __restrict__ src, cplx_t<T>* __rest
 template <class T>
 cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, const void* in, const void* U, void* out,
                          cudaStream_t st) {
+    if (d.ks_in == 1 && d.Kd <= 8 && d.Cols <= 8) {
+        const int64_t items = ngroups * t.links();
+        const int64_t total = items * d.R * d.S;
+        const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+        switch (d.Kd) {
+#define GWT_THIN(KK) \
+    case KK: k_mode1_thin<T, KK><<<blocks, 256, 0, st>>>(t, d, t.links(), items, (const cplx_t<T>*)in, (const cplx_t<T>*)U, (cplx_t<T>*)out); break;
+            GWT_THIN(1) GWT_THIN(2) GWT_THIN(3) GWT_THIN(4) GWT_THIN(5) GWT_THIN(6) GWT_THIN(7) GWT_THIN(8)
+#undef GWT_THIN
+        }
+        return cudaGetLastError();
+    }
     dim3 grid((d.R * d.S + 63) / 64, (d.Cols + 63) / 64, (unsigned)(ngroups * t.links()));
     k_cgemm_conjU<T><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
                                            (cplx_t<T>*)out);
@@ -232,6 +337,16 @@ cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, cons
 template <class T>
 cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V, void* out,
                         cudaStream_t st) {
+    if (d.D <= 8 && d.xs == 1) {
+        const unsigned blocks = (unsigned)(ngroups * sets_per_group);
+        switch (d.D) {
+#define GWT_GT(DD) \
+    case DD: k_gram_thin<T, DD><<<blocks, 128, 0, st>>>(t, d, sets_per_group, (const cplx_t<T>*)V, (cplx_t<T>*)out); break;
+            GWT_GT(1) GWT_GT(2) GWT_GT(3) GWT_GT(4) GWT_GT(5) GWT_GT(6) GWT_GT(7) GWT_GT(8)
+#undef GWT_GT
+        }
+        return cudaGetLastError();
+    }
     const int tiles = (d.D + 63) / 64;
     dim3 grid(tiles * tiles, (unsigned)(ngroups * sets_per_group));
     k_gram<T><<<grid, 256, 0, st>>>(t, d, sets_per_group, (const cplx_t<T>*)V, (cplx_t<T>*)out);

@@ -59,6 +59,8 @@ template <class T> cudaError_t launch_broadcast(const void* src, void* dst, int6
 template <class T> cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, void* out,
                                                 double* evals, double2* ws_a, double* ws_z, double2* ws_x, int* fail,
                                                 cudaStream_t st);
+size_t heev_ws_a_elems(int D);
+size_t heev_ws_z_elems(int D, int count);
 // k_sinr.cu
 template <class T> cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
                                               const void* Cd, const void* G, const double* tau, const double* freqs,
