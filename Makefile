@@ -12,7 +12,12 @@ CU := $(wildcard $(SRC)/*.cu)
 CUO := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU))
 HDR := $(wildcard $(SRC)/*.cuh) include/gwt_b200.h
 
-all: $(LIB) oracle
+HOSTLIB := $(PKG)/_build/libgwtucker_b200.so
+HOSTSRC := $(PKG)/host/src/gwtucker_b200.cpp
+HOSTHDR := $(wildcard $(PKG)/host/include/gwtucker/*.hpp)
+DROPIN := $(PKG)/_build/test_dropin
+
+all: $(LIB) $(HOSTLIB) $(DROPIN) oracle
 
 $(OBJ)/%.o: $(SRC)/%.cu $(HDR)
 	@mkdir -p $(OBJ)
@@ -24,6 +29,12 @@ $(OBJ)/generate.o: $(SRC)/generate.cpp include/gwt_b200.h
 
 $(LIB): $(CUO) $(OBJ)/generate.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart -lpthread
+
+$(HOSTLIB): $(HOSTSRC) $(HOSTHDR) $(LIB) include/gwt_b200.h
+	g++ $(CXXFLAGS) -I$(PKG)/host/include -shared -o $@ $(HOSTSRC) -L$(PKG)/_build -lgwt_b200 -Wl,-rpath,'$$ORIGIN'
+
+$(DROPIN): tests/cpp/test_dropin.cpp $(HOSTLIB)
+	g++ -O2 -std=c++17 -I$(PKG)/host/include -o $@ $< -L$(PKG)/_build -lgwtucker_b200 -lgwt_b200 -Wl,-rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -s -C oracle

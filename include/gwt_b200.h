@@ -20,6 +20,7 @@
  *   gwt_leading_eigenvectors <- gwt::leading_eigenvectors  include/gwtucker/linalg.hpp:16
  *   gwt_reconstruct          <- gwt::reconstruct (decompress)  include/gwtucker/decompose.hpp:84
  *   gwt_flop_estimate        <- gwt::flop_estimate  include/gwtucker/sinr.hpp:148-149
+ *   gwt_mode_product         <- gwt::mode_product  include/gwtucker/tensor.hpp:70 (batched)
  *
  * Layouts. Complex = interleaved (re, im) pairs: float2 for
  * GWT_C64, double2 for GWT_C128 — layout-compatible with std::complex.
@@ -140,6 +141,11 @@ int gwt_leading_eigenvectors(gwt_ctx* ctx, int32_t n, int32_t count, int64_t bat
 int gwt_reconstruct(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups,
                     gwt_dtype dtype, gwt_mem mem, const void* A, const void* B, const void* C, const void* G,
                     void* X);
+
+/* Y[b] = X[b] x_mode U (tensor.hpp:68-70): X [batch][d3][d2][d1] mode-1 fastest, U rows x dim(mode)
+ * column-major, shared by the batch; Y has dim(mode) replaced by `rows`. */
+int gwt_mode_product(gwt_ctx* ctx, gwt_dtype dtype, gwt_mem mem, int64_t batch, int32_t d1, int32_t d2, int32_t d3,
+                     const void* X, int32_t rows, const void* U, int32_t mode, void* Y);
 
 /* Closed-form system ledger (sinr.cpp:353-382); path 0 = full, 1 = compressed. Host only. */
 int gwt_flop_estimate(const gwt_topology* topo, const gwt_ranks* ranks, int32_t path, gwt_ledger* out);

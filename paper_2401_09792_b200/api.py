@@ -333,6 +333,25 @@ class Context:
         vec = out.transpose(-1, -2) if _is_torch(out) else np.swapaxes(out, -1, -2)
         return (vec, ev) if with_values else vec
 
+    def mode_product(self, X, U, mode: int):
+        """Batched gwt::mode_product (tensor.hpp:68-70): X [batch, d3, d2, d1] (mode-1 fastest), U natural
+        [rows, dim(mode)] shared by the batch. Returns Y with dim(mode) replaced by rows."""
+        b, d3, d2, d1 = X.shape
+        rows, dm = U.shape
+        if dm != (d1, d2, d3)[mode - 1] if 1 <= mode <= 3 else True:
+            if not 1 <= mode <= 3:
+                raise InvalidArgument(f"mode_product: mode must be 1, 2 or 3, got {mode}")
+            raise InvalidArgument(f"mode_product: matrix has {dm} cols but tensor mode {mode} has size "
+                                  f"{(d1, d2, d3)[mode - 1]}")
+        Uc = (U.transpose(-1, -2).contiguous() if _is_torch(U) else np.ascontiguousarray(np.swapaxes(U, -1, -2)))
+        o = [d1, d2, d3]
+        o[mode - 1] = rows
+        Y = _like(X, (b, o[2], o[1], o[0]), "c")
+        rc = self.lib.gwt_mode_product(self.h, _dtype_code(X), _mem(X), b, d1, d2, d3, _ptr(X), rows, _ptr(Uc), mode,
+                                       _ptr(Y))
+        self.check(rc)
+        return Y
+
     def reconstruct(self, topo, ranks, factors: GroupwiseFactorSet):
         """gwt::reconstruct (decompose.hpp:84) per link: X^ [g, links, P, N, M]."""
         G = factors.cores

@@ -823,6 +823,52 @@ int gwt_reconstruct(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ran
     });
 }
 
+int gwt_mode_product(gwt_ctx* ctx, gwt_dtype dtype, gwt_mem mem, int64_t batch, int32_t d1, int32_t d2, int32_t d3,
+                     const void* X, int32_t rows, const void* U, int32_t mode, void* Y) {
+    return guarded(ctx, [&] {
+        if (mode < 1 || mode > 3)  // tensor.cpp:96-101
+            invalid("mode_product: mode must be 1, 2 or 3, got " + std::to_string(mode));
+        if (d1 < 1 || d2 < 1 || d3 < 1 || rows < 1) invalid("mode_product: dims must be positive");
+        if (batch == 0) return;
+        const int dm = mode == 1 ? d1 : mode == 2 ? d2 : d3;
+        const size_t cs = csize(dtype);
+        const int o1 = mode == 1 ? rows : d1, o2 = mode == 2 ? rows : d2, o3 = mode == 3 ? rows : d3;
+        const int64_t xn = (int64_t)d1 * d2 * d3, yn = (int64_t)o1 * o2 * o3;
+        cudaStream_t st = ctx->stream;
+        const void *Xd = X, *Ud = U;
+        void* Yd = Y;
+        if (mem == GWT_MEM_HOST) {
+            void* x = ctx->ws(WS_X, cs * batch * xn);
+            void* u = ctx->ws(WS_A, cs * (size_t)rows * dm);
+            ck(cudaMemcpyAsync(x, X, cs * batch * xn, cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(u, U, cs * (size_t)rows * dm, cudaMemcpyHostToDevice, st), "H2D");
+            Xd = x;
+            Ud = u;
+            Yd = ctx->ws(WS_Y1, cs * batch * yn);
+        }
+        // Out(row, col) = sum_k In(row, k) U(col, k): U read transposed, not conjugated, shared (FI_GROUP, 1 link)
+        Topo t{1, 1, d1, d2, d3, 1, 1, 1, 1};
+        GemmDesc d{};
+        d.Kd = dm; d.Cols = rows; d.fkind = FI_GROUP; d.ublk = 0; d.uk = rows; d.ucol = 1; d.uconj = 0;
+        d.in_item = xn; d.out_item = yn;
+        if (mode == 1) {  // rows = fibers (i2,i3), k = i1 contiguous
+            d.R = d2 * d3; d.S = 1; d.rs_in = d1; d.s_in = 0; d.ks_in = 1;
+            d.rs_out = o1; d.s_out = 0; d.cs_out = 1;
+        } else if (mode == 2) {  // rows = (i1, i3)
+            d.R = d1; d.S = d3; d.rs_in = 1; d.s_in = (int64_t)d1 * d2; d.ks_in = d1;
+            d.rs_out = 1; d.s_out = (int64_t)o1 * o2; d.cs_out = o1;
+        } else {  // rows = (i1, i2) flattened, k = i3
+            d.R = d1 * d2; d.S = 1; d.rs_in = 1; d.s_in = 0; d.ks_in = (int64_t)d1 * d2;
+            d.rs_out = 1; d.s_out = 0; d.cs_out = (int64_t)d1 * d2;
+        }
+        // treat the batch as groups of one link each
+        if (dtype == GWT_C64) ctx->launched(launch_cgemm<float>(t, d, batch, Xd, Ud, Yd, st));
+        else ctx->launched(launch_cgemm<double>(t, d, batch, Xd, Ud, Yd, st));
+        if (mem == GWT_MEM_HOST) ck(cudaMemcpyAsync(Y, Yd, cs * batch * yn, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
 int gwt_flop_estimate(const gwt_topology* topo, const gwt_ranks* ranks, int32_t path, gwt_ledger* out) {
     if (!topo || !ranks || !out) return GWT_INVALID_ARGUMENT;
     try {

@@ -91,3 +91,13 @@ def test_configs_follow_baseline():
     assert (c["C4"].m, c["C4"].n, c["C4"].p, c["C4"].L) == (8, 64, 24, 8)
     for k in ("C1", "C2", "C3", "C4", "C5"):
         assert c[k].J * c[k].J * c[k].K == c[k].G
+
+
+def test_cpp_dropin_library_exports_gwt_api():
+    lib = os.path.join(ROOT, "paper_2401_09792_b200", "_build", "libgwtucker_b200.so")
+    assert os.path.exists(lib)
+    out = subprocess.run(["nm", "-DC", lib], capture_output=True, text=True).stdout
+    for sym in ("gwt::groupwise_solve(", "gwt::run_compressed_pipeline(", "gwt::mode_product(", "gwt::hosvd(",
+                "gwt::leading_eigenvectors(", "gwt::assemble_channel_compressed(", "gwt::reconstruct(",
+                "gwt::flop_estimate(", "gwt::shared_solve(", "gwt::truncated_svd("):
+        assert sym in out, sym

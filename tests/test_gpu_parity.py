@@ -286,3 +286,28 @@ def test_device_resident_torch_path(ctx):
     host = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), 3, early_stop=False)
     assert np.allclose(res.trace.cpu().numpy(), host.trace, rtol=1e-12, atol=0)
     assert rep.sinr.is_cuda
+
+
+def test_cpp_dropin_api_on_gpu():
+    """The gwt:: C++ drop-in library (host/) runs the reference's test idioms on the B200."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2401_09792_b200", "_build",
+                       "test_dropin")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASSED" in r.stdout
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_mode_product_matches_oracle(ctx, mode):
+    rng = np.random.default_rng(mode)
+    X = rng.standard_normal((3, 5, 4, 3)) + 1j * rng.standard_normal((3, 5, 4, 3))  # [b, d3, d2, d1]
+    d = (3, 4, 5)[mode - 1]
+    U = rng.standard_normal((2, d)) + 1j * rng.standard_normal((2, d))
+    Y = ctx.mode_product(X, U, mode)
+    for b in range(3):
+        want = O.mode_product(np.transpose(X[b], (2, 1, 0)), U, mode)
+        assert np.max(np.abs(np.transpose(Y[b], (2, 1, 0)) - want)) <= 1e-12 * np.abs(want).max()
+    with pytest.raises(gw.InvalidArgument, match="mode 3 has size 5"):
+        ctx.mode_product(X, np.eye(4, dtype=complex), 3)
