@@ -107,17 +107,34 @@ class ClockSampler:
 # algorithmic cost model
 
 def sinr_costs(cfg, cs):
-    """Per stage algorithmic (flops, bytes) for one SINR step over the whole batch."""
-    J, K, m, n, p, P, L = cfg.J, cfg.K, cfg.m, cfg.n, cfg.p, cfg.P, cfg.L
+    """Per-kernel algorithmic (flops, flop pipe, bytes) for one SINR step over the whole batch."""
+    J, m, n, p, P, L = cfg.J, cfg.m, cfg.n, cfg.p, cfg.P, cfg.L
     links, users, F, g = cfg.G, cfg.G // 2, cfg.F, cfg.groups
     S = J
-    rebuild_flops = 8 * (m * n * p + P * p) * links * F * g
-    rebuild_bytes = (cs * m * n * links * F + cs * (m * n * p + P * p) * links + 8 * P * links) * g
-    gram_flops = 8 * S * m * m * n * users * F * g
-    gram_bytes = (cs * m * n * links * F + 16 * S * m * m * users * F) * g
-    small_bytes = (16 * S * m * m + 8 * (L + 2 * m * L) * 2 + 16 * L + 4) * users * F * g
-    return dict(rebuild=(rebuild_flops, rebuild_bytes), pair_gram=(gram_flops, gram_bytes),
-                small=(None, small_bytes))
+    wp = "fp32" if cs == 8 else "fp64"
+    rebuild = (8 * (m * n * p + P * p) * links * F * g, wp,
+               (cs * m * n * links * F + cs * (m * n * p + P * p) * links + 8 * P * links) * g)
+    pair_gram = (8 * S * m * m * n * users * F * g, "fp64",
+                 (cs * m * n * (2 * J - 1) * users * F + 16 * S * m * m * users * F) * g)
+    # eig (cyclic Jacobi, ~6 sweeps) + covariance/Cholesky/solves, estimated fp64 flops per (user, subcarrier)
+    jac = 6 * (m * (m - 1) // 2) * 48 * m
+    mmse = 8 * (L * m * m + (S - 1) * 2 * m ** 3 + m ** 3 // 3 + L * m * m // 2)
+    Lp = (L + 1) // 2 * 2
+    small = ((jac + mmse) * users * F * g, "fp64",
+             (16 * S * m * m + 8 * (Lp + 2 * m * L) * (1 + (S - 1)) + 16 * L + 4) * users * F * g)
+    return dict(rebuild=rebuild, pair_gram=pair_gram, small=small)
+
+
+def binding_roofline(flops, pipe, nbytes, ms, hbm, peaks_t):
+    """t_roof = max(bytes/BW, flops/peak); report the binding resource's achieved rate vs its peak."""
+    t = ms * 1e-3
+    t_b = nbytes / (hbm * 1e9)
+    t_f = flops / (peaks_t[pipe] * 1e12) if flops else 0.0
+    if t_b >= t_f:
+        ach = nbytes / t / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+    ach = flops / t / 1e12
+    return {"bound": pipe, "achieved": ach, "peak": peaks_t[pipe], "unit": "TFLOP/s", "frac": ach / peaks_t[pipe]}
 
 
 def tucker_flops(cfg):
@@ -315,20 +332,28 @@ def main():
     tuck_e2e_ms = (time.perf_counter() - t0) * 1e3
     ctx_h.close()
 
-    # ---------------- roofline of the dominant SINR kernel
+    # ---------------- roofline of the dominant SINR kernel (binding resource), all stages listed
     hbm, peak_kind, pk = peaks()
+    clk_max = pk.get("sm_max_mhz", 1965.0)
+    peaks_t = {"fp32": 148 * 128 * 2 * clk_max * 1e6 / 1e12, "fp64": 148 * 64 * 2 * clk_max * 1e6 / 1e12}
     costs = sinr_costs(cfg, cs)
     stage = {"rebuild": st_acc[4], "pair_gram": st_acc[5], "small": st_acc[6]}
+    kern = {"rebuild": "k_rebuild", "pair_gram": "k_pair_gram", "small": "k_precoder_eig+k_mmse"}
+    per_stage = {}
+    for k_, ms_k in stage.items():
+        fl, pipe, by = costs[k_]
+        r = binding_roofline(fl, pipe, by, ms_k, hbm, peaks_t)
+        r.update(kernel=kern[k_], ms=round(ms_k, 4), alg_bytes=int(by), alg_flops=int(fl))
+        per_stage[k_] = r
     dom = max(stage, key=stage.get)
-    fl, by = costs[dom]
-    achieved = by / (stage[dom] * 1e-3) / 1e9
-    roof = {"kernel": {"rebuild": "k_rebuild", "pair_gram": "k_pair_gram", "small": "k_precoder_eig+k_mmse"}[dom],
-            "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": None, "peak_source": peak_kind,
-            "stage_ms": {k: round(v, 4) for k, v in stage.items()},
-            "stage_share": {k: round(v / max(sum(stage.values()), 1e-9), 3) for k, v in stage.items()}}
+    roof = dict(per_stage[dom])
+    roof.update(traffic=None, peak_source={"hbm": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                                           "fp32": "derived: 148 SM x 128 FMA/clk x 2 x max clock (not measured)",
+                                           "fp64": "derived: 148 SM x 64 DFMA/clk x 2 x max clock (not measured)"}[roof["bound"]],
+                stage_share={k_: round(v / max(sum(stage.values()), 1e-9), 3) for k_, v in stage.items()},
+                stages=per_stage)
     tfl = tucker_flops(cfg) * world
-    fp32_peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    fp32_peak = peaks_t["fp32" if cs == 8 else "fp64"]
     tucker = {"value": cfg.links * world / (tk * 1e-3), "unit": "channels/s", "ms_per_solve": tk,
               "sweeps": cfg.sweeps, "mode": "fixed sweeps (no early stop)",
               "algorithmic_tflops": tfl / (tk * 1e-3) / 1e12,

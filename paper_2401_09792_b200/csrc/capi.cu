@@ -510,26 +510,41 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         // generic path (any scope): rebuild -> pair Grams -> eig + MMSE through HBM workspaces
         const int64_t per_f = (int64_t)ngroups * ((int64_t)cs * links * t.m * t.n + 16LL * users * S * t.m * t.m +
                                                  8LL * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
-        int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, (int64_t)(std::min<size_t>(ws_budget(), size_t(2) << 30) / std::max<int64_t>(per_f, 1))));
+        // chunk so the H~ / Gram / eig workspaces of one chunk stay resident in the 126 MB L2 between the
+        // producer and consumer kernels (GWT_SINR_CHUNK_BYTES overrides)
+        const char* cb = std::getenv("GWT_SINR_CHUNK_BYTES");
+        const int64_t chunk_bytes = cb ? std::atoll(cb) : (int64_t)(2ll << 30);
+        int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f, 1)));
         void* H = ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
         double2* PG = (double2*)ctx->ws(WS_PG, 16 * ngroups * Fc * users * S * t.m * t.m);
         double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * Fc * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
-        for (int64_t f0 = 0; f0 < F; f0 += Fc) {
+        // stage events per chunk, read back once at the end (no host sync inside the loop)
+        const int64_t nch = (F + Fc - 1) / Fc;
+        std::vector<cudaEvent_t> evs(4 * nch);
+        for (auto& e : evs) ck(cudaEventCreate(&e), "cudaEventCreate");
+        for (int64_t ci = 0, f0 = 0; f0 < F; f0 += Fc, ++ci) {
             const int fc = (int)std::min(Fc, F - f0);
-            tm.mark(8);
+            ck(cudaEventRecord(evs[4 * ci + 0], st), "event");
             ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
-            tm.mark(9);
+            ck(cudaEventRecord(evs[4 * ci + 1], st), "event");
             ctx->launched(launch_pair_gram<T>(t, scope, S, fc, (int)ngroups, H, PG, st));
-            tm.mark(10);
+            ck(cudaEventRecord(evs[4 * ci + 2], st), "event");
             ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PG, EG, sd,
                                             sgd, std_, st),
                           2);
-            tm.mark(11);
-            ck(cudaEventSynchronize(ctx->ev[11]), "sync");
-            ms_r += tm.between(8, 9);
-            ms_p += tm.between(9, 10);
-            ms_s += tm.between(10, 11);
+            ck(cudaEventRecord(evs[4 * ci + 3], st), "event");
         }
+        ck(cudaEventSynchronize(evs.back()), "sync");
+        for (int64_t ci = 0; ci < nch; ++ci) {
+            float a = 0, b = 0, d = 0;
+            cudaEventElapsedTime(&a, evs[4 * ci + 0], evs[4 * ci + 1]);
+            cudaEventElapsedTime(&b, evs[4 * ci + 1], evs[4 * ci + 2]);
+            cudaEventElapsedTime(&d, evs[4 * ci + 2], evs[4 * ci + 3]);
+            ms_r += a;
+            ms_p += b;
+            ms_s += d;
+        }
+        for (auto& e : evs) cudaEventDestroy(e);
     }
     if (mem == GWT_MEM_HOST) {
         tm.mark(12);

@@ -27,6 +27,7 @@
 namespace gwtk {
 
 constexpr int kEigThreads = 256;
+__device__ long long g_eig_phase[8];
 constexpr int kSmemMaxD = 64;
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -87,6 +88,21 @@ __device__ __forceinline__ int sturm_count_fast(int D, const double* d, const do
     return cnt;
 }
 
+// fp32 Sturm count on a scaled tridiagonal: bisection only has to deliver an inverse-iteration
+// shift (~1e-7 relative); the reported eigenvalue is the binary64 Rayleigh quotient.
+__device__ __forceinline__ int sturm_count_f32(int D, const float* d, const float* e2, float x, float pivmin) {
+    int cnt = 0;
+    float q = d[0] - x;
+    if (fabsf(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0f;
+    for (int i = 1; i < D; ++i) {
+        q = d[i] - x - __fdividef(e2[i - 1], q);
+        if (fabsf(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0f;
+    }
+    return cnt;
+}
+
 // in: [batch][D][D] Hermitian (column-major; lower triangle read),
 // out: [batch][count][D] top eigenvectors, evals (nullable): [batch][count].
 // ws_a: [batch][D][D] double2 (used when D > 64), ws_z: [batch][count][6*D] double, ws_x: [batch][count][D] double2
@@ -96,6 +112,7 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
                                                            double2* __restrict__ ws_a, double* __restrict__ ws_z,
                                                            double2* __restrict__ ws_x, int* __restrict__ fail) {
     using C = cplx_t<T>;
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
     __shared__ double2 sv[256];   // Householder vector of the current step
     __shared__ double2 sp[256];   // p / w
     __shared__ double2 salpha[256];
@@ -107,7 +124,7 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
     __shared__ int sround[2];
     const int64_t b = blockIdx.x;
     const int tid = threadIdx.x;
-    double2* A = ws_a + b * (int64_t)D * D;
+    double2* A = D <= kSmemMaxD ? reinterpret_cast<double2*>(smem_dyn) : ws_a + b * (int64_t)D * D;
     const C* H = in + b * (int64_t)D * D;
     for (int idx = tid; idx < D * D; idx += kEigThreads) {
         const int i = idx % D, j = idx / D;
@@ -119,60 +136,79 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         }
     }
     __syncthreads();
-    // 1. Householder tridiagonalisation
+    long long t_ph0 = clock64();
+    // 1. Householder tridiagonalisation: 4 CTA barriers per reflector (warp 0 does the scalar work)
+    __shared__ double sK;
     for (int k = 0; k + 2 < D; ++k) {
         const int len = D - k - 1;
-        double tail = 0.0;
-        for (int r = tid; r < len; r += kEigThreads) {
-            const double2 x = A[(k + 1 + r) + D * k];
-            sv[r] = x;
-            if (r >= 1) tail += x.x * x.x + x.y * x.y;
-        }
-        const double tail2 = block_sum(tail, red);
-        if (tail2 == 0.0) {
+        double2* col = A + (k + 1) + D * k;
+        if (tid < 32) {
+            double tl = 0.0;
+            for (int r = 1 + tid; r < len; r += 32) tl += col[r].x * col[r].x + col[r].y * col[r].y;
+            for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
             if (tid == 0) {
-                stau[k] = 0.0;
-                salpha[k] = A[(k + 1) + D * k];
+                const double2 x0 = col[0];
+                if (tl == 0.0) {
+                    stau[k] = 0.0;
+                    salpha[k] = x0;
+                } else {
+                    const double ax0 = hypot(x0.x, x0.y);
+                    const double xnorm = sqrt(tl + ax0 * ax0);
+                    const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
+                    const double2 al = make_double2(-ph.x * xnorm, -ph.y * xnorm);
+                    const double2 v0 = make_double2(x0.x - al.x, x0.y - al.y);
+                    col[0] = v0;  // the reflector overwrites column k below the diagonal
+                    stau[k] = 2.0 / (tl + v0.x * v0.x + v0.y * v0.y);
+                    salpha[k] = al;
+                }
             }
-            __syncthreads();
-            continue;
-        }
-        if (tid == 0) {
-            const double2 x0 = sv[0];
-            const double ax0 = hypot(x0.x, x0.y);
-            const double xnorm = sqrt(tail2 + ax0 * ax0);
-            const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
-            const double2 alpha = make_double2(-ph.x * xnorm, -ph.y * xnorm);
-            const double2 v0 = make_double2(x0.x - alpha.x, x0.y - alpha.y);
-            sv[0] = v0;
-            stau[k] = 2.0 / (tail2 + v0.x * v0.x + v0.y * v0.y);
-            salpha[k] = alpha;
         }
         __syncthreads();
         const double tau = stau[k];
-        for (int r = tid; r < len; r += kEigThreads) {
-            double2 acc = make_double2(0, 0);
-            const double2* arow = A + (k + 1 + r) + D * (k + 1);
-            for (int c = 0; c < len; ++c) cfma(acc, arow[D * c], sv[c]);
-            sp[r] = make_double2(acc.x * tau, acc.y * tau);
+        if (tau == 0.0) continue;  // uniform: column already reduced
+        for (int r = tid; r < len; r += kEigThreads) sv[r] = col[r];
+        {
+            // p = tau A22 v: SPLIT threads per row (lanes of one warp), partial dots + shuffle reduction
+            const int split = len <= 32 ? 8 : (len <= 64 ? 4 : (len <= 128 ? 2 : 1));
+            const int rows_per_pass = kEigThreads / split;
+            const int sub = tid % split;
+            for (int r0 = 0; r0 < len; r0 += rows_per_pass) {
+                const int r = r0 + tid / split;
+                double2 acc = make_double2(0, 0);
+                if (r < len) {
+                    const double2* arow = A + (k + 1 + r) + D * (k + 1);
+                    for (int c = sub; c < len; c += split) cfma(acc, arow[D * c], col[c]);
+                }
+                for (int o = split / 2; o > 0; o >>= 1) {
+                    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                }
+                if (r < len && sub == 0) sp[r] = make_double2(acc.x * tau, acc.y * tau);
+            }
         }
         __syncthreads();
-        double part = 0.0;
-        for (int r = tid; r < len; r += kEigThreads) part += sv[r].x * sp[r].x + sv[r].y * sp[r].y;
-        const double kk = 0.5 * tau * block_sum(part, red);
-        for (int r = tid; r < len; r += kEigThreads) sp[r] = make_double2(sp[r].x - kk * sv[r].x, sp[r].y - kk * sv[r].y);
+        if (tid < 32) {  // K = tau/2 v^H p (real for Hermitian A22)
+            double part = 0.0;
+            for (int r = tid; r < len; r += 32) part += sv[r].x * sp[r].x + sv[r].y * sp[r].y;
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            if (tid == 0) sK = 0.5 * tau * part;
+        }
         __syncthreads();
+        const double kk = sK;
+        // A22 -= v w^H + w v^H with w = p - K v formed on the fly
         for (int idx = tid; idx < len * len; idx += kEigThreads) {
             const int r = idx % len, c = idx / len;
             double2 a = A[(k + 1 + r) + D * (k + 1 + c)];
-            const double2 vr = sv[r], wr = sp[r], vc = sv[c], wc = sp[c];
+            const double2 vr = sv[r], vc = sv[c];
+            const double2 wr = make_double2(sp[r].x - kk * vr.x, sp[r].y - kk * vr.y);
+            const double2 wc = make_double2(sp[c].x - kk * vc.x, sp[c].y - kk * vc.y);
             a.x -= vr.x * wc.x + vr.y * wc.y + wr.x * vc.x + wr.y * vc.y;
             a.y -= vr.y * wc.x - vr.x * wc.y + wr.y * vc.x - wr.x * vc.y;
             A[(k + 1 + r) + D * (k + 1 + c)] = a;
         }
-        for (int r = tid; r < len; r += kEigThreads) A[(k + 1 + r) + D * k] = sv[r];  // keep the reflector
         __syncthreads();
     }
+    long long t_ph1 = clock64();
     // 2. real symmetric tridiagonal (d, e) via the phase similarity
     for (int r = tid; r < D; r += kEigThreads) sd[r] = A[r + D * r].x;
     __syncthreads();
@@ -221,21 +257,30 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
     const double pivmin = fmax(1e-290, eps * eps * fmax(tnorm, 1e-290));
     glo -= 2.0 * eps * tnorm + pivmin;
     ghi += 2.0 * eps * tnorm + pivmin;
-    // 3a. bisection: thread t -> t-th largest eigenvalue (ascending index D-1-t)
+    // 3a. bisection (fp32, on T / ||T||): thread t -> t-th largest eigenvalue (ascending index D-1-t)
+    __shared__ float fd[256], fe2[256];
+    const double inv_n = tnorm > 0.0 ? 1.0 / tnorm : 1.0;
+    for (int i = tid; i < D; i += kEigThreads) {
+        fd[i] = (float)(sd[i] * inv_n);
+        fe2[i] = (float)(se2[i] * inv_n * inv_n);
+    }
+    __syncthreads();
     double lam = 0.0;
     if (tid < count) {
         const int want = D - 1 - tid;
-        double lo = glo, hi = ghi;
-        for (int it = 0; it < 200; ++it) {
-            const double mid = 0.5 * (lo + hi);
-            if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin || mid <= lo || mid >= hi) break;
-            if (sturm_count_fast(D, sd, se2, mid, pivmin) <= want) lo = mid;
+        const float pivf = 1e-30f;
+        float lo = (float)(glo * inv_n) - 1e-6f, hi = (float)(ghi * inv_n) + 1e-6f;
+        for (int it = 0; it < 64; ++it) {
+            const float mid = 0.5f * (lo + hi);
+            if (hi - lo <= 2e-7f * fmaxf(fmaxf(fabsf(lo), fabsf(hi)), 1e-3f) || mid <= lo || mid >= hi) break;
+            if (sturm_count_f32(D, fd, fe2, mid, pivf) <= want) lo = mid;
             else hi = mid;
         }
-        lam = 0.5 * (lo + hi);
+        lam = 0.5 * ((double)lo + (double)hi) * tnorm;
         sp[tid] = make_double2(lam, 0.0);  // stash for cluster detection
     }
     __syncthreads();
+    long long t_ph2 = clock64();
     // clusters among the wanted eigenvalues (descending order): rounds = position inside the cluster
     if (tid == 0) {
         const double ctol = 1e-3 * fmax(tnorm, 1e-300);
@@ -248,94 +293,103 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         sround[0] = maxr + 1;
     }
     __syncthreads();
-    // 3b. inverse iteration; per-thread LU + vector in the global workspace
-    double* W = ws_z + (b * count + tid) * (int64_t)(6 * D);
-    double* dd = W;           // U diagonal
-    double* du = W + D;       // U first super-diagonal
-    double* du2 = W + 2 * D;  // U second super-diagonal
-    double* ml = W + 3 * D;   // multipliers
-    double* sw = W + 4 * D;   // swap flags (0/1)
-    double* x = W + 5 * D;    // iterate
-    double2* X = ws_x + b * (int64_t)count * D;  // complex eigenvectors (real part = z during iteration)
-    if (tid < count) {
-        const double tiny = fmax(eps * tnorm, 1e-290);
+    // 3b. inverse iteration; LU + iterate in the global workspace, thread (eigenvalue) fastest (coalesced)
+    double* Zw = (D <= kSmemMaxD && count * 6 * D * 8 <= 96 * 1024)
+                     ? reinterpret_cast<double*>(smem_dyn + (size_t)D * D * sizeof(double2))
+                     : ws_z + b * (int64_t)count * 6 * D;
+    double2* X = ws_x + b * (int64_t)count * D;  // [count][D]; real part = z during the iteration
+    const int t = tid;
+#define ZW(arr, i) Zw[((int64_t)(arr) * D + (i)) * count + t]
+    const double tiny = fmax(eps * tnorm, 1e-290);
+    if (t < count) {
         for (int i = 0; i < D; ++i) {
-            dd[i] = sd[i] - lam;
-            du[i] = sl[i];
-            du2[i] = 0.0;
+            ZW(0, i) = sd[i] - lam;
+            ZW(1, i) = sl[i];
+            ZW(2, i) = 0.0;
         }
         for (int i = 0; i + 1 < D; ++i) {
             const double sub = sl[i];
-            if (fabs(dd[i]) >= fabs(sub)) {
-                if (dd[i] == 0.0) dd[i] = tiny;
-                const double mult = sub / dd[i];
-                ml[i] = mult;
-                sw[i] = 0.0;
-                dd[i + 1] -= mult * du[i];
+            double di = ZW(0, i);
+            if (fabs(di) >= fabs(sub)) {
+                if (di == 0.0) di = tiny;
+                const double mult = sub / di;
+                ZW(0, i) = di;
+                ZW(3, i) = mult;
+                ZW(4, i) = 0.0;
+                ZW(0, i + 1) -= mult * ZW(1, i);
             } else {
-                const double mult = dd[i] / sub;
-                ml[i] = mult;
-                sw[i] = 1.0;
-                dd[i] = sub;
-                const double tmp = dd[i + 1];
-                dd[i + 1] = du[i] - mult * tmp;
+                const double mult = di / sub;
+                ZW(3, i) = mult;
+                ZW(4, i) = 1.0;
+                ZW(0, i) = sub;
+                const double tmp = ZW(0, i + 1);
+                ZW(0, i + 1) = ZW(1, i) - mult * tmp;
                 if (i + 2 < D) {
-                    du2[i] = du[i + 1];
-                    du[i + 1] = -mult * du2[i];
+                    ZW(2, i) = ZW(1, i + 1);
+                    ZW(1, i + 1) = -mult * ZW(2, i);
                 }
-                du[i] = tmp;
+                ZW(1, i) = tmp;
             }
         }
-        if (fabs(dd[D - 1]) < tiny) dd[D - 1] = dd[D - 1] < 0 ? -tiny : tiny;
         for (int i = 0; i < D; ++i) {
-            if (fabs(dd[i]) < tiny) dd[i] = dd[i] < 0 ? -tiny : tiny;
-            // deterministic start vector, not orthogonal to any eigenvector in practice
-            x[i] = 1.0 + 0.25 * sin(0.7 * i + 1.3 * tid);
+            const double di = ZW(0, i);
+            if (fabs(di) < tiny) ZW(0, i) = di < 0 ? -tiny : tiny;
+            ZW(5, i) = 1.0 + 0.25 * __sinf(0.7f * i + 1.3f * t);
         }
     }
     const int rounds = sround[0];
     for (int rd = 0; rd < rounds; ++rd) {
-        if (tid < count && scl[tid] == rd) {
+        if (t < count && scl[t] == rd) {
             for (int it = 0; it < 4; ++it) {
-                // orthogonalise against the earlier members of this cluster (already final)
-                for (int s = tid - rd; s < tid; ++s) {
+                for (int s = t - rd; s < t; ++s) {
                     const double2* zs = X + (int64_t)s * D;
                     double dot = 0.0;
-                    for (int i = 0; i < D; ++i) dot += zs[i].x * x[i];
-                    for (int i = 0; i < D; ++i) x[i] -= dot * zs[i].x;
+                    for (int i = 0; i < D; ++i) dot += zs[i].x * ZW(5, i);
+                    for (int i = 0; i < D; ++i) ZW(5, i) -= dot * zs[i].x;
                 }
                 double nn = 0.0;
-                for (int i = 0; i < D; ++i) nn += x[i] * x[i];
-                double inv = nn > 0.0 ? rsqrt(nn) : 1.0;
-                for (int i = 0; i < D; ++i) x[i] *= inv;
+                for (int i = 0; i < D; ++i) nn += ZW(5, i) * ZW(5, i);
+                const double inv = nn > 0.0 ? rsqrt(nn) : 1.0;
+                for (int i = 0; i < D; ++i) ZW(5, i) *= inv;
                 if (it == 3) break;
-                // solve (T - lam I) y = x with the pivoted LU
                 for (int i = 0; i + 1 < D; ++i) {
-                    if (sw[i] != 0.0) {
-                        const double t0 = x[i];
-                        x[i] = x[i + 1];
-                        x[i + 1] = t0 - ml[i] * x[i + 1];
+                    if (ZW(4, i) != 0.0) {
+                        const double t0 = ZW(5, i);
+                        ZW(5, i) = ZW(5, i + 1);
+                        ZW(5, i + 1) = t0 - ZW(3, i) * ZW(5, i + 1);
                     } else {
-                        x[i + 1] -= ml[i] * x[i];
+                        ZW(5, i + 1) -= ZW(3, i) * ZW(5, i);
                     }
                 }
-                x[D - 1] /= dd[D - 1];
-                if (D >= 2) x[D - 2] = (x[D - 2] - du[D - 2] * x[D - 1]) / dd[D - 2];
-                for (int i = D - 3; i >= 0; --i) x[i] = (x[i] - du[i] * x[i + 1] - du2[i] * x[i + 2]) / dd[i];
+                ZW(5, D - 1) /= ZW(0, D - 1);
+                if (D >= 2) ZW(5, D - 2) = (ZW(5, D - 2) - ZW(1, D - 2) * ZW(5, D - 1)) / ZW(0, D - 2);
+                for (int i = D - 3; i >= 0; --i)
+                    ZW(5, i) = (ZW(5, i) - ZW(1, i) * ZW(5, i + 1) - ZW(2, i) * ZW(5, i + 2)) / ZW(0, i);
                 double mx = 0.0;
-                for (int i = 0; i < D; ++i) mx = fmax(mx, fabs(x[i]));
+                for (int i = 0; i < D; ++i) mx = fmax(mx, fabs(ZW(5, i)));
                 if (!(mx > 0.0) || !isfinite(mx)) {
                     if (fail) atomicExch(fail, 1);
                     break;
                 }
                 const double sc = 1.0 / mx;
-                for (int i = 0; i < D; ++i) x[i] *= sc;
+                for (int i = 0; i < D; ++i) ZW(5, i) *= sc;
             }
-            double2* zt = X + (int64_t)tid * D;
-            for (int i = 0; i < D; ++i) zt[i] = make_double2(x[i], 0.0);
+            // Rayleigh quotient z^T T z for the reported eigenvalue
+            double rq = 0.0;
+            for (int i = 0; i < D; ++i) {
+                double tz = sd[i] * ZW(5, i);
+                if (i > 0) tz += sl[i - 1] * ZW(5, i - 1);
+                if (i + 1 < D) tz += sl[i] * ZW(5, i + 1);
+                rq += ZW(5, i) * tz;
+            }
+            sp[t] = make_double2(rq, 0.0);
+            double2* zt = X + (int64_t)t * D;
+            for (int i = 0; i < D; ++i) zt[i] = make_double2(ZW(5, i), 0.0);
         }
         __syncthreads();
     }
+#undef ZW
+    long long t_ph3 = clock64();
     if (evals)
         for (int c = tid; c < count; c += kEigThreads) evals[b * count + c] = sp[c].x;
     // eigenvectors of A: X <- Q diag(delta) z
@@ -391,6 +445,17 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         if (best > 0.0) fac = make_double2(xc[bi].x / best, -xc[bi].y / best);
         for (int r = lane; r < D; r += 32) ob[(int64_t)c * D + r] = from_d2<C>(cmul(xc[r], fac));
     }
+    if (b == 0 && tid == 0) {
+        long long t_ph4 = clock64();
+        g_eig_phase[0] = t_ph1 - t_ph0;
+        g_eig_phase[1] = t_ph2 - t_ph1;
+        g_eig_phase[2] = t_ph3 - t_ph2;
+        g_eig_phase[3] = t_ph4 - t_ph3;
+    }
+}
+
+extern "C" int gwt_debug_eig_phases(long long* out4) {
+    return (int)cudaMemcpyFromSymbol(out4, g_eig_phase, 4 * sizeof(long long));
 }
 
 // ---------------------------------------------------------------------------
@@ -516,16 +581,25 @@ __global__ void __launch_bounds__(256) k_heev_warp(int D, int count, int64_t bat
     const double pivmin = fmax(1e-290, eps * eps * fmax(tnorm, 1e-290));
     const double glo = lo_p - 2.0 * eps * tnorm - pivmin, ghi = hi_p + 2.0 * eps * tnorm + pivmin;
     double* lamv = reinterpret_cast<double*>(pv);  // reuse p/w storage for the wanted eigenvalues
+    float* fd = reinterpret_cast<float*>(alpha);      // alpha (no longer needed) -> fp32 copies of T/||T||
+    float* fe2 = fd + D;
+    const double inv_n = tnorm > 0.0 ? 1.0 / tnorm : 1.0;
+    __syncwarp();
+    for (int i = lane; i < D; i += 32) {
+        fd[i] = (float)(sd[i] * inv_n);
+        fe2[i] = (float)(se2[i] * inv_n * inv_n);
+    }
+    __syncwarp();
     for (int t = lane; t < count; t += 32) {
         const int want = D - 1 - t;
-        double lo = glo, hi = ghi;
-        for (int it = 0; it < 200; ++it) {
-            const double mid = 0.5 * (lo + hi);
-            if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin || mid <= lo || mid >= hi) break;
-            if (sturm_count_fast(D, sd, se2, mid, pivmin) <= want) lo = mid;
+        float lo = (float)(glo * inv_n) - 1e-6f, hi = (float)(ghi * inv_n) + 1e-6f;
+        for (int it = 0; it < 64; ++it) {
+            const float mid = 0.5f * (lo + hi);
+            if (hi - lo <= 2e-7f * fmaxf(fmaxf(fabsf(lo), fabsf(hi)), 1e-3f) || mid <= lo || mid >= hi) break;
+            if (sturm_count_f32(D, fd, fe2, mid, 1e-30f) <= want) lo = mid;
             else hi = mid;
         }
-        lamv[t] = 0.5 * (lo + hi);
+        lamv[t] = 0.5 * ((double)lo + (double)hi) * tnorm;
     }
     __syncwarp();
     int rounds = 1;
@@ -620,6 +694,14 @@ __global__ void __launch_bounds__(256) k_heev_warp(int D, int count, int64_t bat
                 for (int i = 0; i < D; ++i) ZW(5, i) *= sc;
             }
             for (int i = 0; i < D; ++i) XV(i, t) = make_double2(ZW(5, i), 0.0);
+            double rq = 0.0;  // Rayleigh quotient for the reported eigenvalue
+            for (int i = 0; i < D; ++i) {
+                double tz = sd[i] * ZW(5, i);
+                if (i > 0) tz += se[i - 1] * ZW(5, i - 1);
+                if (i + 1 < D) tz += se[i] * ZW(5, i + 1);
+                rq += ZW(5, i) * tz;
+            }
+            lamv[t] = rq;
         }
         __syncwarp();
     }
@@ -922,8 +1004,15 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
                                                                           (cplx_t<T>*)out, evals, ws_z, ws_x, fail);
         return cudaGetLastError();
     }
-    // D > 64 (or forced): CTA per matrix, Householder + bisection + inverse iteration
-    k_heev_topk<T><<<(unsigned)batch, kEigThreads, 0, st>>>(D, count, (const cplx_t<T>*)in, (cplx_t<T>*)out, evals,
+    // D > 32 (or forced): CTA per matrix, Householder + bisection + inverse iteration; A in smem when D <= 64
+    const size_t smA = D <= kSmemMaxD ? sizeof(double2) * D * D +
+                                            ((size_t)count * 6 * D * 8 <= 96 * 1024 ? (size_t)count * 6 * D * 8 : 0)
+                                      : 0;
+    if (smA > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_heev_topk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
+        if (e != cudaSuccess) return e;
+    }
+    k_heev_topk<T><<<(unsigned)batch, kEigThreads, smA, st>>>(D, count, (const cplx_t<T>*)in, (cplx_t<T>*)out, evals,
                                                              ws_a, ws_z, ws_x, fail);
     return cudaGetLastError();
 }

@@ -139,9 +139,15 @@ __global__ void __launch_bounds__(128) k_pair_gram(Topo t, int scope, int S, int
         scope_slot(t, scope, i, j, s, k, l);
         const C* h1 = Hgf + (int64_t)((k * t.J + i) * t.K + j) * mn;  // receive link (k,i,j)
         const C* h2 = Hgf + (int64_t)((k * t.J + k) * t.K + l) * mn;  // partner's serving link (k,k,l)
-        double2 acc = make_double2(0.0, 0.0);
-        for (int c = 0; c < n; ++c) cfmac(acc, to_d2(h1[a + m * c]), to_d2(h2[b + m * c]));
-        PG[(item * S + s) * m * m + a + m * b] = acc;
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        int c = 0;
+#pragma unroll 4
+        for (; c + 1 < n; c += 2) {
+            cfmac(acc0, to_d2(h1[a + m * c]), to_d2(h2[b + m * c]));
+            cfmac(acc1, to_d2(h1[a + m * (c + 1)]), to_d2(h2[b + m * (c + 1)]));
+        }
+        if (c < n) cfmac(acc0, to_d2(h1[a + m * c]), to_d2(h2[b + m * c]));
+        PG[(item * S + s) * m * m + a + m * b] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
     }
 }
 
