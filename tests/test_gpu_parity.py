@@ -311,3 +311,21 @@ def test_mode_product_matches_oracle(ctx, mode):
         assert np.max(np.abs(np.transpose(Y[b], (2, 1, 0)) - want)) <= 1e-12 * np.abs(want).max()
     with pytest.raises(gw.InvalidArgument, match="mode 3 has size 5"):
         ctx.mode_product(X, np.eye(4, dtype=complex), 3)
+
+
+@pytest.mark.parametrize("name,ngroups,sweeps,F", [("C3", 1, 2, 12), ("C4", 1, 1, 8), ("C5", 1, 2, 12)])
+def test_large_configs_parity(ctx, name, ngroups, sweeps, F):
+    """BASELINE C3/C4/C5 shapes (m=8, L=8, N up to 256, P up to 64) on a few groups: NMSE and SINR vs oracle."""
+    cfg = gw.CONFIGS[name]
+    X, X128, tau = baseline_inputs(cfg, ngroups)
+    fo = O.alternating_solve(dims_of(cfg), X128, sweeps, early_stop=False, nthreads=8)
+    res = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), sweeps, early_stop=False)
+    assert np.max(np.abs(res.trace / res.energy[:, None] - fo["trace"] / fo["energy"][:, None])) <= 1e-6
+    freqs = cfg.freqs()[:F]
+    Cd, G = fo["C"].astype(np.complex64), fo["G"].astype(np.complex64)
+    want, _ = O.sinr_compressed(dims_of(cfg), Cd.astype(np.complex128), G.astype(np.complex128),
+                                O.coeffs_from_tau(tau, freqs), cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=8)
+    rep = ctx.run_compressed_pipeline(cfg.topology(), gw.GroupwiseFactorSet(None, None, Cd, G), cfg.ranks(),
+                                      tau=tau, freqs=freqs)
+    assert (np.asarray(rep.status) == 0).all()
+    assert rel_err(rep.sinr, want).max() <= 1e-4
