@@ -21,6 +21,7 @@
  *   gwt_reconstruct          <- gwt::reconstruct (decompress)  include/gwtucker/decompose.hpp:84
  *   gwt_flop_estimate        <- gwt::flop_estimate  include/gwtucker/sinr.hpp:148-149
  *   gwt_mode_product         <- gwt::mode_product  include/gwtucker/tensor.hpp:70 (batched)
+ *   gwt_sinr_full            <- gwt::run_full_pipeline  include/gwtucker/sinr.hpp:134 (batched over F grids)
  *
  * Layouts. Complex = interleaved (re, im) pairs: float2 for
  * GWT_C64, double2 for GWT_C128 — layout-compatible with std::complex.
@@ -126,6 +127,12 @@ int gwt_sinr_compressed_coeffs(gwt_ctx* ctx, const gwt_topology* topo, const gwt
                                gwt_dtype dtype, gwt_mem mem, const void* C, const void* G, const void* coeffs,
                                int64_t F, gwt_scope scope, double* sinr, double* signal, int32_t* status,
                                gwt_ledger* ledger);
+
+/* Full-size SINR on the uncompressed channels H(f) = X x3 c(f)^* (the e_c / R_t comparator).
+ * tau/freqs when coeffs == NULL (coeffs: [groups][F][links][P]). M <= 8. */
+int gwt_sinr_full(gwt_ctx* ctx, const gwt_topology* topo, int64_t ngroups, gwt_dtype dtype, gwt_mem mem,
+                  const void* X, const double* tau, const double* freqs, const void* coeffs, int64_t F,
+                  gwt_scope scope, double* sinr, double* signal, int32_t* status, gwt_ledger* ledger);
 
 /* H~ [groups][F][links][n][m] (column-major m x n per item). tau/freqs when coeffs == NULL. */
 int gwt_assemble_compressed(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups,

@@ -302,6 +302,33 @@ class Context:
             rep.raise_first_error()
         return rep
 
+    def run_full_pipeline(self, topo: SystemTopology, X, scope: str = "paper_experiment", tau=None, freqs=None,
+                          coeffs=None, raise_errors: bool = False) -> SinrReport:
+        """gwt::run_full_pipeline (sinr.hpp:134) batched over groups and F coefficient grids: SINR on the
+        uncompressed channels H(f) = X x3 c(f)^* (the comparator for the paper's e_c and R_t)."""
+        if scope not in SCOPE:
+            raise InvalidArgument(f"unknown interference scope '{scope}'")
+        g = X.shape[0]
+        users, L_ = topo.num_users, topo.num_streams
+        ledger = L.Ledger()
+        if coeffs is not None:
+            F = coeffs.shape[1]
+            tau_p = freqs_p = None
+        else:
+            tau, freqs = _as_f64(X, tau), _as_f64(X, freqs)
+            F = freqs.shape[0]
+            tau_p, freqs_p = _ptr(tau), _ptr(freqs)
+        sinr = _like(X, (g, F, users, L_), "f64")
+        sig = _like(X, (g, F, users, L_), "f64")
+        st = _like(X, (g, F, users), "i32")
+        rc = self.lib.gwt_sinr_full(self.h, C.byref(topo.c()), g, _dtype_code(X), _mem(X), _ptr(X), tau_p, freqs_p,
+                                    _ptr(coeffs), F, SCOPE[scope], _ptr(sinr), _ptr(sig), _ptr(st), C.byref(ledger))
+        self.check(rc)
+        rep = SinrReport(sinr, sig, st, ledger, self.stage_ms())
+        if raise_errors:
+            rep.raise_first_error()
+        return rep
+
     def assemble_compressed(self, topo, ranks, delay, cores, tau=None, freqs=None, coeffs=None):
         """Batched gwt::assemble_channel_compressed (channel.hpp:78-79): H~ [g, F, links, n, m]."""
         g = cores.shape[0]

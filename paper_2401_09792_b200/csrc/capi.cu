@@ -481,7 +481,9 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     const char* path = std::getenv("GWT_SINR_PATH");
     // default: rebuild -> pair Grams -> eig/MMSE (fastest measured on C2);
     // GWT_SINR_PATH=fused selects the shared-memory fused rebuild+Gram path (paper scope only)
-    const bool fused = scope == GWT_SCOPE_PAPER && path && std::strcmp(path, "fused") == 0;
+    // default: rebuild -> pair Grams -> eig/MMSE (fastest measured on C2);
+    // GWT_SINR_PATH=fused selects the shared-memory fused rebuild+Gram kernels (paper scope).
+    const bool fused = scope == GWT_SCOPE_PAPER && t.users() <= 128 && path && std::strcmp(path, "fused") == 0;
     if (fused) {
         // rebuild + Grams fused (H~ stays in shared memory), then the per-group small-matrix solve
         std::vector<double> fh(coeffs ? 0 : F);
@@ -688,6 +690,89 @@ int gwt_sinr_compressed_coeffs(gwt_ctx* ctx, const gwt_topology* topo, const gwt
             sinr_impl<float>(ctx, topo, ranks, ngroups, mem, C, G, nullptr, nullptr, coeffs, F, scope, sinr, signal, status);
         else
             sinr_impl<double>(ctx, topo, ranks, ngroups, mem, C, G, nullptr, nullptr, coeffs, F, scope, sinr, signal, status);
+    });
+}
+
+// Full-size SINR (run_full_pipeline, sinr.cpp:287-294 / evaluate_assembled :259-285): H(f) = X x3 c(f)^*
+// is the compressed rebuild with cores = X and delay factor = I_P, so the same kernels run with
+// ranks (M, N, P); precoder/covariance/filter/SINR act on the M x N channels.
+int gwt_sinr_full(gwt_ctx* ctx, const gwt_topology* topo, int64_t ngroups, gwt_dtype dtype, gwt_mem mem,
+                  const void* X, const double* tau, const double* freqs, const void* coeffs, int64_t F,
+                  gwt_scope scope, double* sinr, double* signal, int32_t* status, gwt_ledger* ledger) {
+    return guarded(ctx, [&] {
+        if (!topo) invalid("sinr_full: null topology");
+        validate_topology(*topo);
+        if (topo->rx_antennas > 8)
+            invalid("sinr_full: receive antennas M > 8 are not supported by the B200 small-matrix kernel");
+        gwt_ranks r{topo->rx_antennas, topo->tx_antennas, topo->num_taps};
+        if (ledger) {
+            ledger_for(*topo, r, 0, ledger);
+            const int64_t mul = F * ngroups;
+            ledger->reconstruct *= mul; ledger->precoder *= mul; ledger->covariance *= mul;
+            ledger->inverse *= mul; ledger->filter *= mul; ledger->sinr *= mul;
+        }
+        if (F == 0 || ngroups == 0) return;
+        const Topo t = mk_topo(*topo, r);
+        const int links = t.links();
+        const size_t cs = csize(dtype);
+        const int64_t x_g = (int64_t)links * t.M * t.N * t.P;
+        cudaStream_t st = ctx->stream;
+        // identity delay factors, device resident
+        std::vector<unsigned char> eye(cs * (size_t)ngroups * links * t.P * t.P, 0);
+        for (int64_t gl = 0; gl < ngroups * links; ++gl)
+            for (int q = 0; q < t.P; ++q) {
+                unsigned char* e = eye.data() + cs * ((size_t)gl * t.P * t.P + (size_t)q * t.P + q);
+                if (dtype == GWT_C64) { const float one = 1.0f; std::memcpy(e, &one, 4); }
+                else { const double one = 1.0; std::memcpy(e, &one, 8); }
+            }
+        void* Cid = ctx->ws(WS_MISC, eye.size());
+        ck(cudaMemcpyAsync(Cid, eye.data(), eye.size(), cudaMemcpyHostToDevice, st), "H2D identity");
+        const void* Xd = X;
+        if (mem == GWT_MEM_HOST) {
+            void* xb = ctx->ws(WS_X, cs * ngroups * x_g);
+            ck(cudaMemcpyAsync(xb, X, cs * ngroups * x_g, cudaMemcpyHostToDevice, st), "H2D X");
+            Xd = xb;
+        }
+        ck(cudaStreamSynchronize(st), "sync");
+        // inputs now on device; run the compressed machinery on (C = I, G = X) with device cores
+        const gwt_mem inner_mem = GWT_MEM_DEVICE;
+        if (mem == GWT_MEM_HOST) {
+            // copy tau/freqs/coeffs and outputs through the host-mode path of sinr_impl: the cores/delay are
+            // already device pointers, so stage the small host inputs here
+            const int64_t out_rows = ngroups * F * t.users();
+            double* sd = (double*)ctx->ws(WS_SINR, 8 * out_rows * t.L);
+            double* sgd = (double*)ctx->ws(WS_SIG, 8 * out_rows * t.L);
+            int* std_ = (int*)ctx->ws(WS_STATUS, 4 * out_rows);
+            const double *taud = nullptr, *fd = nullptr;
+            const void* cod = nullptr;
+            if (coeffs) {
+                void* co = ctx->ws(WS_COEF, cs * ngroups * F * links * t.P);
+                ck(cudaMemcpyAsync(co, coeffs, cs * ngroups * F * links * t.P, cudaMemcpyHostToDevice, st), "H2D");
+                cod = co;
+            } else {
+                double* ta = (double*)ctx->ws(WS_TAU, 8 * ngroups * links * t.P);
+                double* fr = (double*)ctx->ws(WS_FREQ, 8 * F);
+                ck(cudaMemcpyAsync(ta, tau, 8 * ngroups * links * t.P, cudaMemcpyHostToDevice, st), "H2D");
+                ck(cudaMemcpyAsync(fr, freqs, 8 * F, cudaMemcpyHostToDevice, st), "H2D");
+                taud = ta;
+                fd = fr;
+            }
+            if (dtype == GWT_C64)
+                sinr_impl<float>(ctx, topo, &r, ngroups, inner_mem, Cid, Xd, taud, fd, cod, F, scope, sd, sgd, std_);
+            else
+                sinr_impl<double>(ctx, topo, &r, ngroups, inner_mem, Cid, Xd, taud, fd, cod, F, scope, sd, sgd, std_);
+            ck(cudaMemcpyAsync(sinr, sd, 8 * out_rows * t.L, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(signal, sgd, 8 * out_rows * t.L, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(status, std_, 4 * out_rows, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+        } else {
+            if (dtype == GWT_C64)
+                sinr_impl<float>(ctx, topo, &r, ngroups, inner_mem, Cid, Xd, tau, freqs, coeffs, F, scope, sinr, signal,
+                                 status);
+            else
+                sinr_impl<double>(ctx, topo, &r, ngroups, inner_mem, Cid, Xd, tau, freqs, coeffs, F, scope, sinr,
+                                  signal, status);
+        }
     });
 }
 

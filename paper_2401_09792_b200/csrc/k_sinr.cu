@@ -585,6 +585,121 @@ __global__ void __launch_bounds__(256) k_rebuild_gram(Topo t, FusedShape fs, int
     }
 }
 
+// ---------------------------------------------------------------------------
+// Whole-group rebuild + Grams (paper scope, small groups: all links of a group fit in shared
+// memory): one CTA per (group, FT subcarriers); every phase runs over ALL links at once, so
+// the CTA never serialises on per-link barriers. H~ stays in shared memory; output GU as above.
+template <class T, int M, int FT>
+__global__ void __launch_bounds__(256) k_sinr_group(Topo t, int Fc, int64_t f0, int64_t Ftot,
+                                                    const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
+                                                    const double* __restrict__ tau, const double* __restrict__ freqs,
+                                                    const cplx_t<T>* __restrict__ coeffs, double2* __restrict__ GU) {
+    using C = cplx_t<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int LD = FT + 1, MM = M * M, HS = M * (M + 1) / 2;
+    const int J = t.J, K = t.K, links = t.links(), users = t.users();
+    const int mn = M * t.n, P = t.P, p = t.p;
+    C* H = reinterpret_cast<C*>(smem_raw);      // [links][mn][LD]   (phases 3-4)
+    C* Ph = H;                                   // [links][P][FT]    (phases 1-2, aliases H)
+    C* E = H + (size_t)links * mn * LD;          // [links][p][FT]
+    const int64_t gidx = blockIdx.y;
+    const int ft0 = blockIdx.x * FT;
+    const int Fvalid = min(FT, Fc - ft0);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    // 1. conj(c_r(f)) for every link
+    for (int idx = tid; idx < links * P * FT; idx += nt) {
+        const int l = idx / (P * FT), r = (idx / FT) % P, f = idx % FT;
+        C v = czero<C>();
+        if (f < Fvalid) {
+            const int64_t fa = f0 + ft0 + f;
+            v = coeffs ? cconj(coeffs[((gidx * Ftot + fa) * links + l) * P + r])
+                       : conj_coeff<T>(freqs[fa], tau[(gidx * links + l) * P + r]);
+        }
+        Ph[idx] = v;
+    }
+    __syncthreads();
+    // 2. E_l[q][f] = sum_r C_l(r,q) conj(c_r(f))
+    for (int idx = tid; idx < links * p * FT; idx += nt) {
+        const int l = idx / (p * FT), q = (idx / FT) % p, f = idx % FT;
+        const C* Cl = Cd + ((gidx * links + l) * P) * (int64_t)p + (int64_t)P * q;
+        const C* ph = Ph + (size_t)l * P * FT + f;
+        C acc = czero<C>();
+        for (int r = 0; r < P; ++r) cfma(acc, Cl[r], ph[r * FT]);
+        E[idx] = acc;
+    }
+    __syncthreads();
+    // 3. H~_l[row][f] = sum_q G_l[row + mn q] E_l[q][f], all links, one row x FT subcarriers per thread
+    for (int rg = tid; rg < links * mn; rg += nt) {
+        const int l = rg / mn, row = rg % mn;
+        const C* Gl = G + (gidx * links + l) * (int64_t)mn * p + row;
+        const C* e = E + (size_t)l * p * FT;
+        C acc[FT];
+#pragma unroll
+        for (int f = 0; f < FT; ++f) acc[f] = czero<C>();
+        for (int q = 0; q < p; ++q) {
+            const C gv = Gl[(int64_t)mn * q];
+#pragma unroll
+            for (int f = 0; f < FT; ++f) cfma(acc[f], gv, e[q * FT + f]);
+        }
+        C* h = H + (size_t)rg * LD;
+#pragma unroll
+        for (int f = 0; f < FT; ++f) h[f] = acc[f];
+    }
+    __syncthreads();
+    // 4. Grams per user: serving (Hermitian) + one cross Gram per other cell (fp64 accumulation)
+    const int per_user = HS + (J - 1) * MM;
+    const int64_t fstride = (int64_t)users * J * MM;
+    double2* gbase = GU + ((gidx * Fc + ft0) * users) * (int64_t)J * MM;
+    for (int idx = tid; idx < users * per_user * FT; idx += nt) {
+        const int f = idx % FT;
+        int e = (idx / FT) % per_user;
+        const int u = idx / (FT * per_user);
+        if (f >= Fvalid) continue;
+        const int i = u / K, j = u % K;
+        const C *hx, *hy;
+        int a, b, slot;
+        const bool herm = e < HS;
+        if (herm) {
+            a = 0;
+            while (e >= M - a) { e -= M - a; ++a; }
+            b = a + e;
+            hx = hy = H + (size_t)((i * J + i) * K + j) * mn * LD;
+            slot = 0;
+        } else {
+            e -= HS;
+            const int c = e / MM;
+            e %= MM;
+            a = e % M;
+            b = e / M;
+            const int k = c < i ? c : c + 1;  // c-th cell != i
+            hx = H + (size_t)((k * J + i) * K + j) * mn * LD;
+            hy = H + (size_t)((k * J + k) * K + 0) * mn * LD;
+            slot = 1 + c;
+        }
+        const C* px = hx + a * LD + f;
+        const C* py = hy + b * LD + f;
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        int c = 0;
+        for (; c + 1 < t.n; c += 2) {
+            cfmac(acc0, to_d2(px[M * LD * c]), to_d2(py[M * LD * c]));
+            cfmac(acc1, to_d2(px[M * LD * (c + 1)]), to_d2(py[M * LD * (c + 1)]));
+        }
+        if (c < t.n) cfmac(acc0, to_d2(px[M * LD * c]), to_d2(py[M * LD * c]));
+        const double2 acc = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
+        double2* o = gbase + f * fstride + (int64_t)u * J * MM + slot * MM;
+        o[a + M * b] = acc;
+        if (herm && a != b) o[b + M * a] = make_double2(acc.x, -acc.y);
+    }
+}
+
+template <class T, int M>
+static size_t group_smem(const Topo& t, int FT) {
+    const size_t cs = sizeof(cplx_t<T>);
+    const size_t hbytes = cs * (size_t)t.links() * M * t.n * (FT + 1);
+    const size_t phbytes = cs * (size_t)t.links() * t.P * FT;
+    return std::max(hbytes, phbytes) + cs * (size_t)t.links() * t.p * FT;
+}
+
 template <int M>
 __device__ __forceinline__ void load_herm(const double2* src, double2 (&A)[M][M]) {
 #pragma unroll
@@ -786,18 +901,38 @@ static cudaError_t launch_fused_m(const Topo& t, int ngroups, int Fc, int64_t f0
     const size_t cs = sizeof(cplx_t<T>);
     const int users = t.users();
     const int mn = M * t.n;
+    cudaError_t e = cudaSuccess;
+    const char* eft = std::getenv("GWT_RG_FT");
+    int gFT = 0;  // whole-group kernel tile (0 = does not fit)
+    for (int cand : {8, 4, 2})
+        if (!gFT && group_smem<T, M>(t, cand) <= (cand >= 4 ? 110 * 1024 : 200 * 1024)) gFT = cand;
+    if (eft) gFT = std::atoi(eft) == 8 || std::atoi(eft) == 4 || std::atoi(eft) == 2 ? std::atoi(eft) : gFT;
+    if (gFT && group_smem<T, M>(t, gFT) <= 220 * 1024) {
+        auto rung = [&](auto ftc) {
+            constexpr int FT = decltype(ftc)::value;
+            const size_t sm = group_smem<T, M>(t, FT);
+            e = cudaFuncSetAttribute(k_sinr_group<T, M, FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return;
+            dim3 g((Fc + FT - 1) / FT, ngroups);
+            k_sinr_group<T, M, FT><<<g, 256, sm, st>>>(t, Fc, f0, Ftot, (const cplx_t<T>*)Cd, (const cplx_t<T>*)G, tau,
+                                                       freqs, (const cplx_t<T>*)coeffs, GU);
+            e = cudaGetLastError();
+        };
+        if (gFT == 8) rung(std::integral_constant<int, 8>{});
+        else if (gFT == 4) rung(std::integral_constant<int, 4>{});
+        else rung(std::integral_constant<int, 2>{});
+        if (e != cudaSuccess) return e;
+    } else {
     // rebuild+Gram: FT subcarriers per CTA tile, a group of WG threads per user (named barriers).
     // GWT_RG_FT / GWT_RG_WG override the defaults (tuning).
-    const char* eft = std::getenv("GWT_RG_FT");
-    const char* ewg = std::getenv("GWT_RG_WG");
     const int FTsel = eft ? std::atoi(eft) : 16;
+    const char* ewg = std::getenv("GWT_RG_WG");
     int WG = ewg ? std::atoi(ewg) : (mn <= 128 ? 128 : 256);
     if (WG < 32 || 256 % WG) WG = 256;
     const int NG = 256 / WG;
     FusedShape fs;
     fs.B = std::min(users, 32);
     fs.fsplit = WG;
-    cudaError_t e = cudaSuccess;
     auto run = [&](auto ftc) {
         constexpr int FT = decltype(ftc)::value;
         fs.FT = FT;
@@ -815,6 +950,7 @@ static cudaError_t launch_fused_m(const Topo& t, int ngroups, int Fc, int64_t f0
     if (FTsel == 8) run(std::integral_constant<int, 8>{});
     else run(std::integral_constant<int, 16>{});
     if (e != cudaSuccess) return e;
+    }
     // solve: (users x FT2) threads per CTA, FT2 = 128 / users (>= 1)
     const int FT2 = std::max(1, 128 / users);
     const size_t sm2 = (size_t)FT2 * t.J * (16 * M * M + 4) + 16;

@@ -101,3 +101,18 @@ def test_cpp_dropin_library_exports_gwt_api():
                 "gwt::leading_eigenvectors(", "gwt::assemble_channel_compressed(", "gwt::reconstruct(",
                 "gwt::flop_estimate(", "gwt::shared_solve(", "gwt::truncated_svd("):
         assert sym in out, sym
+
+
+def test_paper_metrics_reference_values():
+    """R_s of the paper's Table 2 rows (test_metrics.cpp:38-57 pins these from the count formula)."""
+    from paper_2401_09792_b200 import metrics
+    t = gw.SystemTopology(21, 5, 64, 512, 401, 4, 0.1)
+    assert abs(metrics.storage_ratio(t, gw.CompressionRanks(60, 230, 150)) - 6.1648) < 5e-5
+    assert abs(metrics.storage_ratio(t, gw.CompressionRanks(60, 230, 150), "shared") - 6.1684) < 5e-5
+    assert abs(metrics.storage_ratio(t, gw.CompressionRanks(60, 230, 150), "individual") - 5.8354) < 5e-5
+    t10 = gw.SystemTopology(21, 10, 64, 512, 401, 4, 0.1)
+    assert abs(metrics.storage_ratio(t10, gw.CompressionRanks(60, 270, 190)) - 4.1648) < 5e-5
+    assert metrics.sinr_error([2.0, 4.0], [1.0, 5.0]) == 0.375
+    with pytest.raises(gw.InvalidArgument, match="zero at flat index 1"):
+        metrics.sinr_error([1.0, 0.0], [1.0, 1.0])
+    assert metrics.speedup(6.0, 2.0) == 3.0

@@ -329,3 +329,35 @@ def test_large_configs_parity(ctx, name, ngroups, sweeps, F):
                                       tau=tau, freqs=freqs)
     assert (np.asarray(rep.status) == 0).all()
     assert rel_err(rep.sinr, want).max() <= 1e-4
+
+
+@pytest.mark.parametrize("name,ngroups", [("C1", None), ("C2", 2), ("C2d", 2)])
+def test_full_pipeline_parity(ctx, name, ngroups):
+    """run_full_pipeline (the e_c / R_t comparator) on the uncompressed channels vs the oracle."""
+    cfg = gw.CONFIGS[name]
+    X, X128, tau = baseline_inputs(cfg, ngroups)
+    freqs = cfg.freqs()[:32]
+    want, wsig = O.sinr_full(dims_of(cfg), X128, O.coeffs_from_tau(tau, freqs), cfg.sigma, cfg.L, O.SCOPE_PAPER,
+                             nthreads=8)
+    rep = ctx.run_full_pipeline(cfg.topology(), X, tau=tau, freqs=freqs)
+    assert (np.asarray(rep.status) == 0).all()
+    assert rel_err(rep.sinr, want).max() <= SINR_TOL[cfg.dtype]
+    led = gw.flop_estimate(cfg.topology(), cfg.ranks(), "full")
+    assert rep.ledger.total() == led.total() * X.shape[0] * len(freqs)
+
+
+def test_full_pipeline_reference_generator_and_lossless_identity(ctx):
+    """Reference desk system: full path vs oracle, and lossless compressed == full (test_sinr.cpp:337-365)."""
+    from paper_2401_09792_b200 import metrics
+    topo = gw.SystemTopology(2, 2, 6, 8, 5, 2, 0.1)
+    X, c = O.generate_reference(2, 2, 6, 8, 5, 12)
+    co = c[None, None]
+    for scope, osc in (("paper_experiment", O.SCOPE_PAPER), ("full", O.SCOPE_FULL)):
+        want, _ = O.sinr_full(dict(J=2, K=2, M=6, N=8, P=5), X[None], co, 0.1, 2, osc)
+        full = ctx.run_full_pipeline(topo, X[None], scope, coeffs=co)
+        assert rel_err(full.sinr, want).max() <= 1e-9
+    fac = ctx.groupwise_solve(topo, X[None], gw.CompressionRanks(6, 8, 5), 2)
+    comp = ctx.run_compressed_pipeline(topo, fac, gw.CompressionRanks(6, 8, 5), coeffs=co)
+    full = ctx.run_full_pipeline(topo, X[None], coeffs=co)
+    assert rel_err(comp.sinr, full.sinr).max() <= 1e-8
+    assert metrics.sinr_error(full.sinr, comp.sinr) <= 1e-8
