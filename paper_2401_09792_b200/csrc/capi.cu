@@ -509,44 +509,52 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         ck(cudaEventSynchronize(ctx->ev[9]), "sync");
         ms_r = tm.between(8, 9);
     } else {
-        // generic path (any scope): rebuild -> pair Grams -> eig + MMSE through HBM workspaces
-        const int64_t per_f = (int64_t)ngroups * ((int64_t)cs * links * t.m * t.n + 16LL * users * S * t.m * t.m +
-                                                 8LL * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
-        // chunk so the H~ / Gram / eig workspaces of one chunk stay resident in the 126 MB L2 between the
-        // producer and consumer kernels (GWT_SINR_CHUNK_BYTES overrides)
+        // generic path (any scope): rebuild -> pair Grams per subcarrier chunk sized so H~ stays resident in
+        // L2 between producer and consumer; then ONE eig+MMSE launch over all subcarriers (full occupancy)
+        const int64_t per_f_h = (int64_t)cs * ngroups * links * t.m * t.n;
         const char* cb = std::getenv("GWT_SINR_CHUNK_BYTES");
+        // (measured on C2: L2-sized chunks are slower - fewer CTAs per launch - so default to 2 GiB)
         const int64_t chunk_bytes = cb ? std::atoll(cb) : (int64_t)(2ll << 30);
-        int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f, 1)));
+        const int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f_h, 1)));
         void* H = ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
-        double2* PG = (double2*)ctx->ws(WS_PG, 16 * ngroups * Fc * users * S * t.m * t.m);
-        double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * Fc * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
-        // stage events per chunk, read back once at the end (no host sync inside the loop)
-        const int64_t nch = (F + Fc - 1) / Fc;
-        std::vector<cudaEvent_t> evs(4 * nch);
-        for (auto& e : evs) ck(cudaEventCreate(&e), "cudaEventCreate");
-        for (int64_t ci = 0, f0 = 0; f0 < F; f0 += Fc, ++ci) {
-            const int fc = (int)std::min(Fc, F - f0);
-            ck(cudaEventRecord(evs[4 * ci + 0], st), "event");
-            ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
-            ck(cudaEventRecord(evs[4 * ci + 1], st), "event");
-            ctx->launched(launch_pair_gram<T>(t, scope, S, fc, (int)ngroups, H, PG, st));
-            ck(cudaEventRecord(evs[4 * ci + 2], st), "event");
-            ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PG, EG, sd,
-                                            sgd, std_, st),
+        // pair Grams for a block of Fs subcarriers: [g][Fs][users][S][m*m] (fp64), Fs bounded by ~2 GB
+        const int64_t per_f_pg = (int64_t)ngroups * users * (16LL * S * t.m * t.m + 8LL * (((t.L + 1) & ~1) + 2 * t.m * t.L));
+        const int64_t Fs = std::max<int64_t>(Fc, std::min<int64_t>(F, (int64_t)(2ll << 30) / std::max<int64_t>(per_f_pg, 1)) / Fc * Fc);
+        double2* PG = (double2*)ctx->ws(WS_PG, 16 * ngroups * std::min(Fs, F) * users * S * t.m * t.m);
+        double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * std::min(Fs, F) * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
+        std::vector<cudaEvent_t> evs;
+        auto rec = [&]() {
+            cudaEvent_t ev;
+            ck(cudaEventCreate(&ev), "cudaEventCreate");
+            ck(cudaEventRecord(ev, st), "event");
+            evs.push_back(ev);
+        };
+        std::vector<int> kind;  // 0 rebuild, 1 pair gram, 2 small, per interval
+        rec();
+        for (int64_t F0 = 0; F0 < F; F0 += Fs) {
+            const int64_t fs = std::min(Fs, F - F0);
+            for (int64_t f0 = F0; f0 < F0 + fs; f0 += Fc) {
+                const int fc = (int)std::min(Fc, F0 + fs - f0);
+                ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
+                rec();
+                kind.push_back(0);
+                ctx->launched(launch_pair_gram<T>(t, scope, S, fc, (int)ngroups, f0 - F0, fs, H, PG, st));
+                rec();
+                kind.push_back(1);
+            }
+            ctx->launched(launch_sinr_small(t, scope, S, ngroups * fs * users, topo->noise_std, (int)fs, F, F0, PG, EG,
+                                            sd, sgd, std_, st),
                           2);
-            ck(cudaEventRecord(evs[4 * ci + 3], st), "event");
+            rec();
+            kind.push_back(2);
         }
         ck(cudaEventSynchronize(evs.back()), "sync");
-        for (int64_t ci = 0; ci < nch; ++ci) {
-            float a = 0, b = 0, d = 0;
-            cudaEventElapsedTime(&a, evs[4 * ci + 0], evs[4 * ci + 1]);
-            cudaEventElapsedTime(&b, evs[4 * ci + 1], evs[4 * ci + 2]);
-            cudaEventElapsedTime(&d, evs[4 * ci + 2], evs[4 * ci + 3]);
-            ms_r += a;
-            ms_p += b;
-            ms_s += d;
+        for (size_t i = 0; i < kind.size(); ++i) {
+            float a = 0;
+            cudaEventElapsedTime(&a, evs[i], evs[i + 1]);
+            (kind[i] == 0 ? ms_r : kind[i] == 1 ? ms_p : ms_s) += a;
         }
-        for (auto& e : evs) cudaEventDestroy(e);
+        for (auto& ev : evs) cudaEventDestroy(ev);
     }
     if (mem == GWT_MEM_HOST) {
         tm.mark(12);

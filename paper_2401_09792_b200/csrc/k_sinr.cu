@@ -118,8 +118,9 @@ __device__ __forceinline__ int serving_slot(const Topo& t, int scope, int i, int
 // K2: pair Grams X_{u,s} = H~_{k,i,j} H~_{k,k,l}^H (m x m, fp64 accumulation)
 // one warp per (group, subcarrier, user); lanes over (slot, a, b) entries.
 template <class T>
-__global__ void __launch_bounds__(128) k_pair_gram(Topo t, int scope, int S, int Fc, int64_t items,
-                                                   const cplx_t<T>* __restrict__ H, double2* __restrict__ PG) {
+__global__ void __launch_bounds__(128) k_pair_gram(Topo t, int scope, int S, int Fc, int64_t f0, int64_t Ftot,
+                                                   int64_t items, const cplx_t<T>* __restrict__ H,
+                                                   double2* __restrict__ PG) {
     using C = cplx_t<T>;
     const int64_t item = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (item >= items) return;
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(128) k_pair_gram(Topo t, int scope, int S, int
     const int m = t.m, n = t.n, mn = m * n;
     const C* Hgf = H + gf * links * mn;
     const int total = S * m * m;
+    const int64_t orow = ((gf / Fc) * Ftot + f0 + gf % Fc) * users + u;  // row in the all-subcarrier PG
     for (int e = lane; e < total; e += 32) {
         const int s = e / (m * m);
         const int ab = e % (m * m);
@@ -147,7 +149,56 @@ __global__ void __launch_bounds__(128) k_pair_gram(Topo t, int scope, int S, int
             cfmac(acc1, to_d2(h1[a + m * (c + 1)]), to_d2(h2[b + m * (c + 1)]));
         }
         if (c < n) cfmac(acc0, to_d2(h1[a + m * c]), to_d2(h2[b + m * c]));
-        PG[(item * S + s) * m * m + a + m * b] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
+        PG[(orow * S + s) * m * m + a + m * b] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
+    }
+}
+
+// K2 (paper scope): the item's 2J-1 links (J receive links (k,i,j), J-1 partner links (k,k,0))
+// are staged into shared memory with coalesced loads, then each lane computes one Gram entry.
+template <class T, int M>
+__global__ void __launch_bounds__(128) k_pair_gram_staged(Topo t, int Fc, int64_t f0, int64_t Ftot, int64_t items,
+                                                          const cplx_t<T>* __restrict__ H, double2* __restrict__ PG) {
+    using C = cplx_t<T>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int64_t item = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
+    const int J = t.J, users = t.users(), links = t.links();
+    const int mn = M * t.n, nl = 2 * J - 1;
+    C* sh = reinterpret_cast<C*>(smem_raw) + (size_t)warp * nl * mn;
+    if (item >= items) return;
+    const int u = (int)(item % users);
+    const int64_t gf = item / users;
+    const int i = u / t.K, j = u % t.K;
+    const C* Hgf = H + gf * links * mn;
+    for (int li = 0; li < nl; ++li) {
+        int l;
+        if (li < J) l = (li * J + i) * t.K + j;  // receive link (k = li, i, j)
+        else {
+            int k = li - J;
+            if (k >= i) ++k;
+            l = (k * J + k) * t.K;  // partner (k, k, 0)
+        }
+        const C* src = Hgf + (int64_t)l * mn;
+        C* dst = sh + li * mn;
+        for (int e = lane; e < mn; e += 32) dst[e] = src[e];
+    }
+    __syncwarp();
+    const int64_t orow = ((gf / Fc) * Ftot + f0 + gf % Fc) * users + u;
+    constexpr int MM = M * M;
+    for (int e = lane; e < J * MM; e += 32) {
+        const int s = e / MM, ab = e % MM, a = ab % M, b = ab / M;
+        // slot 0: serving (i,i,j) with itself; slot s>0: cell k (k-th cell != i) receive link vs partner
+        int kcell = s == 0 ? i : (s - 1 < i ? s - 1 : s);
+        const C* h1 = sh + kcell * mn;
+        const C* h2 = s == 0 ? h1 : sh + (J + s - 1) * mn;
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        int c = 0;
+        for (; c + 1 < t.n; c += 2) {
+            cfmac(acc0, to_d2(h1[a + M * c]), to_d2(h2[b + M * c]));
+            cfmac(acc1, to_d2(h1[a + M * (c + 1)]), to_d2(h2[b + M * (c + 1)]));
+        }
+        if (c < t.n) cfmac(acc0, to_d2(h1[a + M * c]), to_d2(h2[b + M * c]));
+        PG[(orow * J + s) * MM + ab] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
     }
 }
 
@@ -1004,11 +1055,27 @@ cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64
 }
 
 template <class T>
-cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroups, const void* H, double2* PG,
-                             cudaStream_t st) {
+cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroups, int64_t f0, int64_t Ftot,
+                             const void* H, double2* PG, cudaStream_t st) {
     const int64_t items = (int64_t)ngroups * Fc * t.users();
     const int wpb = 4;
-    k_pair_gram<T><<<(unsigned)((items + wpb - 1) / wpb), 32 * wpb, 0, st>>>(t, scope, S, Fc, items,
+    const size_t sm = sizeof(cplx_t<T>) * (size_t)wpb * (2 * t.J - 1) * t.m * t.n;
+    if (scope == 1 && sm <= 96 * 1024 && !std::getenv("GWT_PG_UNSTAGED")) {
+        cudaError_t e = cudaSuccess;
+        switch (t.m) {
+#define GWT_PGS(MM)                                                                                                  \
+    case MM:                                                                                                         \
+        e = cudaFuncSetAttribute(k_pair_gram_staged<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);   \
+        if (e != cudaSuccess) return e;                                                                              \
+        k_pair_gram_staged<T, MM><<<(unsigned)((items + wpb - 1) / wpb), 32 * wpb, sm, st>>>(t, Fc, f0, Ftot, items, \
+                                                                                            (const cplx_t<T>*)H, PG); \
+        return cudaGetLastError();
+            GWT_PGS(1) GWT_PGS(2) GWT_PGS(3) GWT_PGS(4) GWT_PGS(5) GWT_PGS(6) GWT_PGS(7) GWT_PGS(8)
+#undef GWT_PGS
+            default: break;
+        }
+    }
+    k_pair_gram<T><<<(unsigned)((items + wpb - 1) / wpb), 32 * wpb, 0, st>>>(t, scope, S, Fc, f0, Ftot, items,
                                                                             (const cplx_t<T>*)H, PG);
     return cudaGetLastError();
 }
@@ -1045,7 +1112,9 @@ template cudaError_t launch_rebuild<float>(const Topo&, int, int, int64_t, int64
                                            const double*, const double*, const void*, void*, cudaStream_t);
 template cudaError_t launch_rebuild<double>(const Topo&, int, int, int64_t, int64_t, const void*, const void*,
                                             const double*, const double*, const void*, void*, cudaStream_t);
-template cudaError_t launch_pair_gram<float>(const Topo&, int, int, int, int, const void*, double2*, cudaStream_t);
-template cudaError_t launch_pair_gram<double>(const Topo&, int, int, int, int, const void*, double2*, cudaStream_t);
+template cudaError_t launch_pair_gram<float>(const Topo&, int, int, int, int, int64_t, int64_t, const void*, double2*,
+                                             cudaStream_t);
+template cudaError_t launch_pair_gram<double>(const Topo&, int, int, int, int, int64_t, int64_t, const void*,
+                                              double2*, cudaStream_t);
 
 }  // namespace gwtk

@@ -65,8 +65,8 @@ size_t heev_ws_z_elems(int D, int count);
 template <class T> cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
                                               const void* Cd, const void* G, const double* tau, const double* freqs,
                                               const void* coeffs, void* H, cudaStream_t st);
-template <class T> cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroups, const void* H,
-                                                double2* PG, cudaStream_t st);
+template <class T> cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroups, int64_t f0,
+                                                int64_t Ftot, const void* H, double2* PG, cudaStream_t st);
 template <class T> cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
                                                  double sigma, const void* Cd, const void* G, const double* tau,
                                                  const double* freqs, int uniform, double df, const void* coeffs,
