@@ -12,13 +12,14 @@
 
 namespace gwtk {
 
-// Tiled strided complex GEMM with conj(U): CTA tile 64 rows x 64 cols,
-// 256 threads, 4x4 outputs per thread, K chunks of 16 staged in smem.
-template <class T>
+// Tiled strided complex GEMM with conj(U): CTA tile (16*RT) rows x (16*CT) cols, 256 threads
+// (16 x 16), RT x CT outputs per thread, K chunks of 16 staged in smem. The tile shape is picked
+// per call from Cols (12/24-wide factor ranks would waste most of a 64-wide tile).
+template <class T, int RT, int CT>
 __global__ void __launch_bounds__(256) k_cgemm_conjU(Topo t, GemmDesc d, int links, const cplx_t<T>* __restrict__ in,
                                                       const cplx_t<T>* __restrict__ U, cplx_t<T>* __restrict__ out) {
     using C = cplx_t<T>;
-    constexpr int TR = 64, TC = 64, KC = 16;
+    constexpr int TR = 16 * RT, TC = 16 * CT, KC = 16;
     __shared__ C sIn[KC][TR + 1];
     __shared__ C sU[KC][TC + 1];
     const int64_t item = blockIdx.z;
@@ -31,11 +32,11 @@ __global__ void __launch_bounds__(256) k_cgemm_conjU(Topo t, GemmDesc d, int lin
     const int64_t ucol = d.ucol >= 0 ? d.ucol : (int64_t)d.Kd;
     const C* ub = U + factor_index(t, d.fkind, g, l) * ublk;
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    C acc[4][4];
+    C acc[RT][CT];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < RT; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = czero<C>();
+        for (int b = 0; b < CT; ++b) acc[a][b] = czero<C>();
     const bool row_fast = d.rs_in == 1;
     for (int k0 = 0; k0 < d.Kd; k0 += KC) {
         for (int idx = threadIdx.x; idx < TR * KC; idx += 256) {
@@ -61,27 +62,26 @@ __global__ void __launch_bounds__(256) k_cgemm_conjU(Topo t, GemmDesc d, int lin
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
-            C a[4], b[4];
+            C a[RT], b[CT];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                a[q] = sIn[kk][ty + 16 * q];
-                b[q] = sU[kk][tx + 16 * q];
-            }
+            for (int q = 0; q < RT; ++q) a[q] = sIn[kk][ty + 16 * q];
 #pragma unroll
-            for (int qa = 0; qa < 4; ++qa)
+            for (int q = 0; q < CT; ++q) b[q] = sU[kk][tx + 16 * q];
 #pragma unroll
-                for (int qb = 0; qb < 4; ++qb) cfma(acc[qa][qb], a[qa], b[qb]);
+            for (int qa = 0; qa < RT; ++qa)
+#pragma unroll
+                for (int qb = 0; qb < CT; ++qb) cfma(acc[qa][qb], a[qa], b[qb]);
         }
         __syncthreads();
     }
     C* ob = out + item * d.out_item;
 #pragma unroll
-    for (int qa = 0; qa < 4; ++qa) {
+    for (int qa = 0; qa < RT; ++qa) {
         const int row = row0 + ty + 16 * qa;
         if (row >= rows) continue;
         const int64_t ro = (row % d.R) * d.rs_out + (int64_t)(row / d.R) * d.s_out;
 #pragma unroll
-        for (int qb = 0; qb < 4; ++qb) {
+        for (int qb = 0; qb < CT; ++qb) {
             const int col = col0 + tx + 16 * qb;
             if (col < d.Cols) ob[ro + (int64_t)col * d.cs_out] = acc[qa][qb];
         }
@@ -109,12 +109,12 @@ __device__ __forceinline__ int set_link(const Topo& t, int kind, int s, int r) {
     }
 }
 
-// Batched Hermitian rank-k accumulation: CTA per (set, 64x64 output tile).
-template <class T>
+// Batched Hermitian rank-k accumulation: CTA per (set, TD x TD output tile), TD = 16*Q.
+template <class T, int Q>
 __global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_group, const cplx_t<T>* __restrict__ V,
                                               cplx_t<T>* __restrict__ out) {
     using C = cplx_t<T>;
-    constexpr int TD = 64, KC = 16;
+    constexpr int TD = 16 * Q, KC = 16;
     __shared__ C sX[KC][TD + 1];
     __shared__ C sY[KC][TD + 1];
     const int64_t set = blockIdx.y;
@@ -123,11 +123,11 @@ __global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_g
     const int tiles = (d.D + TD - 1) / TD;
     const int x0 = (blockIdx.x % tiles) * TD, y0 = (blockIdx.x / tiles) * TD;
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    C acc[4][4];
+    C acc[Q][Q];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < Q; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = czero<C>();
+        for (int b = 0; b < Q; ++b) acc[a][b] = czero<C>();
     const int nl = set_size(t, d.set_kind);
     const int Tn = d.T1 * d.T2;
     const bool x_fast = d.xs == 1;
@@ -152,27 +152,27 @@ __global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_g
             __syncthreads();
 #pragma unroll
             for (int kk = 0; kk < KC; ++kk) {
-                C a[4], b[4];
+                C a[Q], b[Q];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < Q; ++q) {
                     a[q] = sX[kk][ty + 16 * q];
                     b[q] = sY[kk][tx + 16 * q];
                 }
 #pragma unroll
-                for (int qa = 0; qa < 4; ++qa)
+                for (int qa = 0; qa < Q; ++qa)
 #pragma unroll
-                    for (int qb = 0; qb < 4; ++qb) cfmac(acc[qa][qb], a[qa], b[qb]);
+                    for (int qb = 0; qb < Q; ++qb) cfmac(acc[qa][qb], a[qa], b[qb]);
             }
             __syncthreads();
         }
     }
     C* ob = out + set * (int64_t)d.D * d.D;
 #pragma unroll
-    for (int qa = 0; qa < 4; ++qa) {
+    for (int qa = 0; qa < Q; ++qa) {
         const int x = x0 + ty + 16 * qa;
         if (x >= d.D) continue;
 #pragma unroll
-        for (int qb = 0; qb < 4; ++qb) {
+        for (int qb = 0; qb < Q; ++qb) {
             const int y = y0 + tx + 16 * qb;
             if (y < d.D) ob[x + (int64_t)d.D * y] = acc[qa][qb];
         }
@@ -328,9 +328,21 @@ cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, cons
         }
         return cudaGetLastError();
     }
-    dim3 grid((d.R * d.S + 63) / 64, (d.Cols + 63) / 64, (unsigned)(ngroups * t.links()));
-    k_cgemm_conjU<T><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
-                                           (cplx_t<T>*)out);
+    const unsigned items = (unsigned)(ngroups * t.links());
+    const int rows = d.R * d.S;
+    if (d.Cols <= 16) {
+        dim3 grid((rows + 127) / 128, (d.Cols + 15) / 16, items);
+        k_cgemm_conjU<T, 8, 1><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
+                                                      (cplx_t<T>*)out);
+    } else if (d.Cols <= 32) {
+        dim3 grid((rows + 63) / 64, (d.Cols + 31) / 32, items);
+        k_cgemm_conjU<T, 4, 2><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
+                                                      (cplx_t<T>*)out);
+    } else {
+        dim3 grid((rows + 63) / 64, (d.Cols + 63) / 64, items);
+        k_cgemm_conjU<T, 4, 4><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
+                                                      (cplx_t<T>*)out);
+    }
     return cudaGetLastError();
 }
 
@@ -347,9 +359,15 @@ cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int s
         }
         return cudaGetLastError();
     }
-    const int tiles = (d.D + 63) / 64;
-    dim3 grid(tiles * tiles, (unsigned)(ngroups * sets_per_group));
-    k_gram<T><<<grid, 256, 0, st>>>(t, d, sets_per_group, (const cplx_t<T>*)V, (cplx_t<T>*)out);
+    if (d.D <= 32) {
+        const int tiles = (d.D + 31) / 32;
+        dim3 grid(tiles * tiles, (unsigned)(ngroups * sets_per_group));
+        k_gram<T, 2><<<grid, 256, 0, st>>>(t, d, sets_per_group, (const cplx_t<T>*)V, (cplx_t<T>*)out);
+    } else {
+        const int tiles = (d.D + 63) / 64;
+        dim3 grid(tiles * tiles, (unsigned)(ngroups * sets_per_group));
+        k_gram<T, 4><<<grid, 256, 0, st>>>(t, d, sets_per_group, (const cplx_t<T>*)V, (cplx_t<T>*)out);
+    }
     return cudaGetLastError();
 }
 
