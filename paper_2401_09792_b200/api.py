@@ -262,7 +262,43 @@ class Context:
         return GroupwiseFactorSet(A, B, Cd, G, trace, iters, energy)
 
     def shared_solve(self, topo, X, ranks, sweeps, init=None, early_stop=True):
+        """gwt::shared_solve (decompose.hpp:132-134): one rx and one tx factor per group."""
         return self.groupwise_solve(topo, X, ranks, sweeps, init=init, early_stop=early_stop, pooled=True)
+
+    def individual_solve(self, topo, X, ranks, sweeps, init: GroupwiseFactorSet | None = None,
+                         early_stop: bool = True):
+        """gwt::individual_solve (decompose.cpp:389-435): independent per-link HOOI, optionally warm-started
+        from a groupwise solution. Runs as the batched solver on J=K=1 systems (one per link).
+
+        Returns dict: rx [g, links, m, M], tx [g, links, n, N], delay [g, links, p, P], cores [g, links, p, n, m],
+        trace [g, sweeps+1] (per-sweep sum over links; stopped links hold their final value),
+        iterations_run [g] (max over links), link_trace [g, links, sweeps+1]."""
+        J, K = topo.num_cells, topo.users_per_cell
+        g, links = X.shape[0], X.shape[1]
+        one = SystemTopology(1, 1, topo.rx_antennas, topo.tx_antennas, topo.num_taps, 1, topo.noise_std)
+        Xl = X.reshape((g * links, 1) + tuple(X.shape[2:]))
+        ini = None
+        if init is not None:
+            ks = np.arange(links) // (J * K)
+            us = np.arange(links) % (J * K)
+            def per_link(arr, idx):
+                a = arr[:, idx]
+                return a.reshape((g * links, 1) + tuple(a.shape[2:]))
+            ini = GroupwiseFactorSet(per_link(init.rx, us), per_link(init.tx, ks), init.delay.reshape(
+                (g * links, 1) + tuple(init.delay.shape[2:])), None)
+            if _is_torch(X):
+                ini = GroupwiseFactorSet(*(torch.as_tensor(np.ascontiguousarray(x.cpu().numpy() if _is_torch(x) else x),
+                                                           device=X.device) for x in (ini.rx, ini.tx, ini.delay)), None)
+            else:
+                ini = GroupwiseFactorSet(*(np.ascontiguousarray(x.cpu().numpy() if _is_torch(x) else x)
+                                           for x in (ini.rx, ini.tx, ini.delay)), None)
+        r = self.groupwise_solve(one, Xl.contiguous() if _is_torch(Xl) else np.ascontiguousarray(Xl), ranks, sweeps,
+                                 init=ini, early_stop=early_stop)
+        sh = lambda a: a.reshape((g, links) + tuple(a.shape[2:]))
+        tr = r.trace.reshape(g, links, -1)
+        it = r.iterations_run.reshape(g, links)
+        return dict(rx=sh(r.rx), tx=sh(r.tx), delay=sh(r.delay), cores=sh(r.cores), link_trace=tr,
+                    trace=tr.sum(1), iterations_run=it.max(1), energy=r.energy.reshape(g, links).sum(1))
 
     # ------------------------------------------------------------------ SINR
     def run_compressed_pipeline(self, topo: SystemTopology, factors: GroupwiseFactorSet, ranks: CompressionRanks,

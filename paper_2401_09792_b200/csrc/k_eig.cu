@@ -27,7 +27,12 @@
 namespace gwtk {
 
 constexpr int kEigThreads = 256;
+#ifdef GWT_PHASE_TIMERS
 __device__ long long g_eig_phase[8];
+#define GWT_CLK(v) const long long v = clock64()
+#else
+#define GWT_CLK(v)
+#endif
 constexpr int kSmemMaxD = 64;
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -136,7 +141,7 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         }
     }
     __syncthreads();
-    long long t_ph0 = clock64();
+    GWT_CLK(t_ph0);
     // 1. Householder tridiagonalisation: 4 CTA barriers per reflector (warp 0 does the scalar work)
     __shared__ double sK;
     for (int k = 0; k + 2 < D; ++k) {
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         }
         __syncthreads();
     }
-    long long t_ph1 = clock64();
+    GWT_CLK(t_ph1);
     // 2. real symmetric tridiagonal (d, e) via the phase similarity
     for (int r = tid; r < D; r += kEigThreads) sd[r] = A[r + D * r].x;
     __syncthreads();
@@ -280,7 +285,7 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         sp[tid] = make_double2(lam, 0.0);  // stash for cluster detection
     }
     __syncthreads();
-    long long t_ph2 = clock64();
+    GWT_CLK(t_ph2);
     // clusters among the wanted eigenvalues (descending order): rounds = position inside the cluster
     if (tid == 0) {
         const double ctol = 1e-3 * fmax(tnorm, 1e-300);
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         __syncthreads();
     }
 #undef ZW
-    long long t_ph3 = clock64();
+    GWT_CLK(t_ph3);
     if (evals)
         for (int c = tid; c < count; c += kEigThreads) evals[b * count + c] = sp[c].x;
     // eigenvectors of A: X <- Q diag(delta) z
@@ -445,6 +450,7 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         if (best > 0.0) fac = make_double2(xc[bi].x / best, -xc[bi].y / best);
         for (int r = lane; r < D; r += 32) ob[(int64_t)c * D + r] = from_d2<C>(cmul(xc[r], fac));
     }
+#ifdef GWT_PHASE_TIMERS
     if (b == 0 && tid == 0) {
         long long t_ph4 = clock64();
         g_eig_phase[0] = t_ph1 - t_ph0;
@@ -452,11 +458,14 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
         g_eig_phase[2] = t_ph3 - t_ph2;
         g_eig_phase[3] = t_ph4 - t_ph3;
     }
+#endif
 }
 
+#ifdef GWT_PHASE_TIMERS
 extern "C" int gwt_debug_eig_phases(long long* out4) {
     return (int)cudaMemcpyFromSymbol(out4, g_eig_phase, 4 * sizeof(long long));
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // Warp-per-matrix variant for D <= 64: the same algorithm, warp-synchronous

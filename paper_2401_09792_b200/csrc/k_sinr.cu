@@ -42,6 +42,15 @@ template <> __device__ __forceinline__ double2 conj_coeff<double>(double f, doub
 // K1: rebuild H~(f) = sum_q G(:,:,q) * E[q][f],
 //     E[q][f] = sum_r C(r,q) * conj(c_r(f)),  c_r(f) = exp(+j 2 pi f tau_r) or explicit.
 // grid (ceil(Fc/FT), links, groups); one CTA per (link, subcarrier tile).
+#ifdef GWT_PHASE_TIMERS
+__device__ long long g_rb_phase[4];
+extern "C" int gwt_debug_rebuild_phases(long long* out4) {
+    return (int)cudaMemcpyFromSymbol(out4, g_rb_phase, 4 * sizeof(long long));
+}
+#define GWT_CLK(v) const long long v = clock64()
+#else
+#define GWT_CLK(v)
+#endif
 template <class T, int FT>
 __global__ void __launch_bounds__(128) k_rebuild(Topo t, int Fc, int64_t f0, int64_t Ftot,
                                                  const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
@@ -55,6 +64,7 @@ __global__ void __launch_bounds__(128) k_rebuild(Topo t, int Fc, int64_t f0, int
     const int nf = min(FT, Fc - ft0);
     const int links = t.links();
     const int64_t gl = (int64_t)g * links + l;
+    GWT_CLK(c0);
     for (int idx = threadIdx.x; idx < t.P * FT; idx += blockDim.x) {
         const int r = idx / FT, f = idx % FT;
         C v = czero<C>();
@@ -69,6 +79,7 @@ __global__ void __launch_bounds__(128) k_rebuild(Topo t, int Fc, int64_t f0, int
         ph[idx] = v;
     }
     __syncthreads();
+    GWT_CLK(c1);
     const C* Cl = Cd + gl * t.P * t.p;
     for (int idx = threadIdx.x; idx < t.p * FT; idx += blockDim.x) {
         const int q = idx / FT, f = idx % FT;
@@ -77,21 +88,42 @@ __global__ void __launch_bounds__(128) k_rebuild(Topo t, int Fc, int64_t f0, int
         E[idx] = acc;
     }
     __syncthreads();
+    GWT_CLK(c2);
     const int mn = t.m * t.n;
     const C* Gl = G + gl * mn * t.p;
     for (int row = threadIdx.x; row < mn; row += blockDim.x) {
         C acc[FT];
 #pragma unroll
         for (int f = 0; f < FT; ++f) acc[f] = czero<C>();
-        for (int q = 0; q < t.p; ++q) {
-            const C gv = Gl[row + (int64_t)mn * q];
+        const C* gp = Gl + row;
+        for (int q = 0; q < t.p; ++q, gp += mn) {
+            const C gv = *gp;
+            if constexpr (sizeof(C) == 8) {
+                // two complex64 per 128-bit shared load (E row is 16-byte aligned)
+                const float4* e4 = reinterpret_cast<const float4*>(E + q * FT);
 #pragma unroll
-            for (int f = 0; f < FT; ++f) cfma(acc[f], gv, E[q * FT + f]);
+                for (int f = 0; f < FT / 2; ++f) {
+                    const float4 ev = e4[f];
+                    cfma(acc[2 * f], gv, C{ev.x, ev.y});
+                    cfma(acc[2 * f + 1], gv, C{ev.z, ev.w});
+                }
+            } else {
+#pragma unroll
+                for (int f = 0; f < FT; ++f) cfma(acc[f], gv, E[q * FT + f]);
+            }
         }
 #pragma unroll
         for (int f = 0; f < FT; ++f)
             if (f < nf) H[(((int64_t)g * Fc + ft0 + f) * links + l) * mn + row] = acc[f];
     }
+#ifdef GWT_PHASE_TIMERS
+    if (blockIdx.x == 3 && blockIdx.y == 5 && blockIdx.z == 7 && threadIdx.x == 0) {
+        const long long c3 = clock64();
+        g_rb_phase[0] = c1 - c0;
+        g_rb_phase[1] = c2 - c1;
+        g_rb_phase[2] = c3 - c2;
+    }
+#endif
 }
 
 // scope slot s of user (i,j) -> (k,l), mirroring scope_pairs (sinr.cpp:47-62)

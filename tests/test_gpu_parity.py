@@ -361,3 +361,31 @@ def test_full_pipeline_reference_generator_and_lossless_identity(ctx):
     full = ctx.run_full_pipeline(topo, X[None], coeffs=co)
     assert rel_err(comp.sinr, full.sinr).max() <= 1e-8
     assert metrics.sinr_error(full.sinr, comp.sinr) <= 1e-8
+
+
+def test_individual_solve_matches_per_link_hooi(ctx):
+    """individual_solve == single-tensor HOOI per link (test_decompose.cpp:326-335), warm start supported."""
+    cfg = gw.CONFIGS["C1"]
+    X, X128, _ = baseline_inputs(cfg, 1)
+    res = ctx.individual_solve(cfg.topology(), X, cfg.ranks(), 4)
+    for l in (0, 5):
+        *_, tr, it = O.hooi(np.transpose(X128[0, l], (2, 1, 0)), cfg.m, cfg.n, cfg.p, 4)
+        np.testing.assert_allclose(res["link_trace"][0, l], tr, rtol=1e-9, atol=1e-12 * tr[0])
+    fo = O.alternating_solve(dims_of(cfg), X128, 3)
+    warm = ctx.individual_solve(cfg.topology(), X, cfg.ranks(), 0,
+                                init=gw.GroupwiseFactorSet(fo["A"], fo["B"], fo["C"], None))
+    # warm start at the groupwise factors: link objectives sum to the groupwise objective
+    assert abs(warm["trace"][0, 0] - fo["trace"][0, -1]) <= 1e-9 * fo["energy"][0]
+
+
+def test_archive_round_trip_of_gpu_factors(ctx, tmp_path):
+    from paper_2401_09792_b200 import archive as ar
+    cfg = gw.CONFIGS["C1"]
+    X, _, tau = baseline_inputs(cfg, 1)
+    fac = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), 3)
+    co = O.coeffs_from_tau(tau, cfg.freqs()[:1])[0, 0]
+    ar.save_archive(tmp_path / "c.gwtk", "groupwise", fac, co, cfg.J, cfg.K)
+    out = ar.load_archive(tmp_path / "c.gwtk")
+    a = ctx.run_compressed_pipeline(cfg.topology(), fac, cfg.ranks(), coeffs=co[None, None])
+    b = ctx.run_compressed_pipeline(cfg.topology(), out["factors"], cfg.ranks(), coeffs=out["coeffs"][None, None])
+    np.testing.assert_array_equal(a.sinr, b.sinr)
