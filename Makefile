@@ -36,10 +36,14 @@ $(HOSTLIB): $(HOSTSRC) $(HOSTHDR) $(LIB) include/gwt_b200.h
 $(DROPIN): tests/cpp/test_dropin.cpp $(HOSTLIB)
 	g++ -O2 -std=c++17 -I$(PKG)/host/include -o $@ $< -L$(PKG)/_build -lgwtucker_b200 -lgwt_b200 -Wl,-rpath,'$$ORIGIN'
 
+# phase-timer build (tools/eig_phases.py): GWT_LIB_PATH=$(PKG)/_build/phase/libgwt_b200.so
+phase:
+	$(MAKE) OBJ=$(PKG)/_build/phase/obj LIB=$(PKG)/_build/phase/libgwt_b200.so NVFLAGS="$(NVFLAGS) -DGWT_PHASE_TIMERS" $(PKG)/_build/phase/libgwt_b200.so
+
 oracle:
 	$(MAKE) -s -C oracle
 
 clean:
 	rm -rf $(PKG)/_build oracle/_build
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean phase

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libgwt_b200.so")
+LIB_PATH = os.environ.get("GWT_LIB_PATH") or os.path.join(HERE, "_build", "libgwt_b200.so")  # override: profiling builds
 
 GWT_OK, GWT_INVALID_ARGUMENT, GWT_RUNTIME_ERROR, GWT_CUDA_ERROR, GWT_NO_DEVICE = range(5)
 GWT_C64, GWT_C128 = 0, 1

@@ -71,7 +71,7 @@ namespace {
 enum {
     WS_X = 0, WS_A, WS_B, WS_C, WS_G, WS_Y1, WS_W, WS_W2, WS_Z, WS_Z2, WS_GRAM, WS_EIGA, WS_EIGZ, WS_EIGX, WS_POOL,
     WS_ENERGY, WS_CAPT, WS_TRACE, WS_FAIL, WS_FROZEN, WS_TAU, WS_FREQ, WS_COEF, WS_H, WS_PG, WS_EG, WS_SINR, WS_SIG,
-    WS_STATUS, WS_MISC
+    WS_STATUS, WS_MISC, WS_PART
 };
 
 size_t ws_budget() {
@@ -178,6 +178,7 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
     double* capt = (double*)ctx->ws(WS_CAPT, 8 * G);
     int* failp = (int*)ctx->ws(WS_FAIL, 4);
     ck(cudaMemsetAsync(failp, 0, 4, st), "memset");
+    double* part = (double*)ctx->ws(WS_PART, 8 * G * kSqnormMaxBlocks);
 
     auto gemm = [&](const GemmDesc& d, const void* in, const void* U, void* out) {
         ctx->launched(launch_cgemm<T>(t, d, G, in, U, out, st));
@@ -225,7 +226,7 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
 
     Timer tm(ctx);
     tm.mark(1);
-    ctx->launched(launch_group_sqnorm<T>(X, links * MNP, G, energy, st));
+    ctx->launched(launch_group_sqnorm<T>(X, links * MNP, G, energy, part, st));
     if (!(flags & GWT_SOLVE_INIT)) {  // initial_factors (decompose.cpp:248-300)
         GramDesc g1{t.M, t.N * t.P, 1, MNP, 1, t.M, 0, rx_kind};
         gram_eig(g1, X, t.M, t.m, A, rx_copies);
@@ -238,7 +239,7 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
         gemm(dZ, X, A, Z);
         gemm(dZ2, Z, B, Z2);
         gemm(dG, Z2, Cf, Gc);
-        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)links * t.m * t.n * t.p, G, capt, st));
+        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)links * t.m * t.n * t.p, G, capt, part, st));
         ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, slot, st));
     };
     objective(0);
@@ -273,7 +274,7 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
         gram_eig(gd, Z2, t.P, t.p, Cf, 0);
         // objective (energy split ||X||^2 - ||core||^2) and the cores of these factors
         gemm(dG, Z2, Cf, Gc);
-        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)links * t.m * t.n * t.p, G, capt, st));
+        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)links * t.m * t.n * t.p, G, capt, part, st));
         ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, s + 1, st));
         if (early) {
             ck(cudaMemcpyAsync(trace_h.data(), trace_d, 8 * trace_h.size(), cudaMemcpyDeviceToHost, st), "D2H");

@@ -503,6 +503,7 @@ __global__ void __launch_bounds__(256) k_heev_warp(int D, int count, int64_t bat
         }
     }
     __syncwarp();
+    GWT_CLK(t_ph0);
     for (int k = 0; k + 2 < D; ++k) {
         const int len = D - k - 1;
         double2* col = A + (k + 1) + D * k;  // x = A[k+1.., k]; becomes the reflector v
@@ -557,6 +558,7 @@ __global__ void __launch_bounds__(256) k_heev_warp(int D, int count, int64_t bat
         }
         __syncwarp();
     }
+    GWT_CLK(t_ph1);
     for (int r = lane; r < D; r += 32) sd[r] = A[r + D * r].x;
     if (lane == 0) {
         double2 dl = make_double2(1.0, 0.0);
@@ -624,6 +626,7 @@ __global__ void __launch_bounds__(256) k_heev_warp(int D, int count, int64_t bat
     }
     rounds = __shfl_sync(0xffffffffu, rounds, 0);
     __syncwarp();
+    GWT_CLK(t_ph2);
     // per-matrix workspaces, lane (eigenvalue) fastest so every warp access is coalesced:
     //   Zw[arr][i][t] (arr: 0 dd, 1 du, 2 du2, 3 ml, 4 sw, 5 x),  X[i][t] eigenvector t
     double* Zw = ws_z + b * (int64_t)count * 6 * D;
@@ -714,6 +717,7 @@ __global__ void __launch_bounds__(256) k_heev_warp(int D, int count, int64_t bat
         }
         __syncwarp();
     }
+    GWT_CLK(t_ph3);
     if (evals)
         for (int c = lane; c < count; c += 32) evals[b * count + c] = lamv[c];
     // back-transform: lane = column; x <- H_0 ... H_{D-3} diag(delta) z
@@ -759,6 +763,15 @@ __global__ void __launch_bounds__(256) k_heev_warp(int D, int count, int64_t bat
         }
         for (int r = 0; r < D; ++r) ob[(int64_t)c * D + r] = from_d2<C>(cmul(XV(r, c), fac));
     }
+#ifdef GWT_PHASE_TIMERS
+    if (b == 0 && lane == 0) {
+        const long long t_ph4 = clock64();
+        g_eig_phase[0] = t_ph1 - t_ph0;
+        g_eig_phase[1] = t_ph2 - t_ph1;
+        g_eig_phase[2] = t_ph3 - t_ph2;
+        g_eig_phase[3] = t_ph4 - t_ph3;
+    }
+#endif
 #undef ZW
 #undef XV
 }

@@ -8,6 +8,8 @@
 // strides address the unfolding in place (no copies), batched over all links
 // of all groups, and every update Gram is one batched Hermitian rank-k kernel
 // whose reduction runs over all links that share the factor.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace gwtk {
@@ -277,10 +279,13 @@ __global__ void __launch_bounds__(128) k_gram_thin(Topo t, GramDesc d, int sets_
 template <class T>
 __global__ void __launch_bounds__(256) k_group_sqnorm(const cplx_t<T>* __restrict__ v, int64_t per_group,
                                                       double* __restrict__ out) {
+    // grid (groups, blocks per group): block b of group g sums a contiguous slice; out[g * gridDim.y + b]
     const int64_t g = blockIdx.x;
+    const int64_t slice = (per_group + gridDim.y - 1) / gridDim.y;
+    const int64_t e0 = (int64_t)blockIdx.y * slice, e1 = std::min(per_group, e0 + slice);
     const cplx_t<T>* b = v + g * per_group;
     double acc = 0.0;
-    for (int64_t e = threadIdx.x; e < per_group; e += 256) {
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += 256) {
         const double2 x = to_d2(b[e]);
         acc += x.x * x.x + x.y * x.y;
     }
@@ -288,6 +293,18 @@ __global__ void __launch_bounds__(256) k_group_sqnorm(const cplx_t<T>* __restric
     red[threadIdx.x] = acc;
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[g * gridDim.y + blockIdx.y] = red[0];
+}
+
+__global__ void k_sum_partials(const double* __restrict__ part, int nb, double* __restrict__ out) {
+    const int64_t g = blockIdx.x;
+    __shared__ double red[kSqnormMaxBlocks];
+    red[threadIdx.x] = threadIdx.x < nb ? part[g * nb + threadIdx.x] : 0.0;
+    __syncthreads();
+    for (int w = kSqnormMaxBlocks / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
@@ -349,6 +366,12 @@ cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, cons
 template <class T>
 cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V, void* out,
                         cudaStream_t st) {
+    // complex64 Grams with D >= 64 on the tensor cores (3xTF32 tcgen05, k_tc.cu): opt-in (GWT_GRAM_TC=1)
+    // until its staging pipeline beats the CUDA-core kernel
+    if (sizeof(T) == 4 && d.D >= 64) {
+        const char* e = std::getenv("GWT_GRAM_TC");
+        if (e && std::atoi(e) != 0) return launch_gram_tc(t, d, ngroups, sets_per_group, V, out, st);
+    }
     if (d.D <= 8 && d.xs == 1) {
         const unsigned blocks = (unsigned)(ngroups * sets_per_group);
         switch (d.D) {
@@ -372,8 +395,17 @@ cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int s
 }
 
 template <class T>
-cudaError_t launch_group_sqnorm(const void* v, int64_t per_group, int64_t ngroups, double* out, cudaStream_t st) {
-    k_group_sqnorm<T><<<(unsigned)ngroups, 256, 0, st>>>((const cplx_t<T>*)v, per_group, out);
+cudaError_t launch_group_sqnorm(const void* v, int64_t per_group, int64_t ngroups, double* out, double* partial,
+                                cudaStream_t st) {
+    // enough blocks to fill the GPU (~8 per SM), at least 16K elements each, at most kSqnormMaxBlocks per group
+    int64_t nb = std::min<int64_t>((per_group + 16383) / 16384, (148 * 8 + ngroups - 1) / ngroups);
+    nb = std::max<int64_t>(1, std::min<int64_t>(nb, kSqnormMaxBlocks));
+    if (nb == 1) {
+        k_group_sqnorm<T><<<dim3((unsigned)ngroups, 1), 256, 0, st>>>((const cplx_t<T>*)v, per_group, out);
+        return cudaGetLastError();
+    }
+    k_group_sqnorm<T><<<dim3((unsigned)ngroups, (unsigned)nb), 256, 0, st>>>((const cplx_t<T>*)v, per_group, partial);
+    k_sum_partials<<<(unsigned)ngroups, kSqnormMaxBlocks, 0, st>>>(partial, (int)nb, out);
     return cudaGetLastError();
 }
 
@@ -396,7 +428,7 @@ cudaError_t launch_broadcast(const void* src, void* dst, int64_t elems, int copi
                                          cudaStream_t);                                                      \
     template cudaError_t launch_gram<T>(const Topo&, const GramDesc&, int64_t, int, const void*, void*,          \
                                         cudaStream_t);                                                       \
-    template cudaError_t launch_group_sqnorm<T>(const void*, int64_t, int64_t, double*, cudaStream_t);          \
+    template cudaError_t launch_group_sqnorm<T>(const void*, int64_t, int64_t, double*, double*, cudaStream_t);          \
     template cudaError_t launch_broadcast<T>(const void*, void*, int64_t, int, int64_t, cudaStream_t);
 GWT_INST(float)
 GWT_INST(double)

@@ -49,12 +49,17 @@ template <class T> cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, in
                                             const void* U, void* out, cudaStream_t st);
 template <class T> cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group,
                                            const void* V, void* out, cudaStream_t st);
+// per-group ||v||^2 in fp64; deterministic two-level reduction through `partial`
+// (ngroups * kSqnormMaxBlocks doubles) when a group spans many blocks
+constexpr int kSqnormMaxBlocks = 128;
 template <class T> cudaError_t launch_group_sqnorm(const void* v, int64_t per_group, int64_t ngroups, double* out,
-                                                   cudaStream_t st);
+                                                   double* partial, cudaStream_t st);
 cudaError_t launch_objective(int64_t ngroups, const double* energy, const double* captured, double* trace, int stride,
                              int slot, cudaStream_t st);
 template <class T> cudaError_t launch_broadcast(const void* src, void* dst, int64_t elems, int copies, int64_t ngroups,
                                                 cudaStream_t st);
+cudaError_t launch_gram_tc(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V,
+                           void* out, cudaStream_t st);  // k_tc.cu (c64, 3xTF32 tcgen05)
 // k_eig.cu
 template <class T> cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, void* out,
                                                 double* evals, double2* ws_a, double* ws_z, double2* ws_x, int* fail,
