@@ -71,7 +71,7 @@ namespace {
 enum {
     WS_X = 0, WS_A, WS_B, WS_C, WS_G, WS_Y1, WS_W, WS_W2, WS_Z, WS_Z2, WS_GRAM, WS_EIGA, WS_EIGZ, WS_EIGX, WS_POOL,
     WS_ENERGY, WS_CAPT, WS_TRACE, WS_FAIL, WS_FROZEN, WS_TAU, WS_FREQ, WS_COEF, WS_H, WS_PG, WS_EG, WS_SINR, WS_SIG,
-    WS_STATUS, WS_MISC, WS_PART
+    WS_STATUS, WS_MISC, WS_PART, WS_GPART
 };
 
 size_t ws_budget() {
@@ -163,6 +163,8 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
     const int64_t gram_elems = std::max({(int64_t)G * users * t.M * t.M, (int64_t)G * t.J * t.N * t.N,
                                          (int64_t)G * links * t.P * t.P});
     void* gram = ctx->ws(WS_GRAM, cs * gram_elems);
+    const size_t gpart_bytes = std::min<size_t>(cs * gram_elems * 8, size_t(256) << 20);  // K-split partials
+    void* gpart = ctx->ws(WS_GPART, gpart_bytes);
     const int64_t eig_a = std::max({(int64_t)G * users * heev_ws_a_elems(t.M), (int64_t)G * t.J * heev_ws_a_elems(t.N),
                                     (int64_t)G * links * heev_ws_a_elems(t.P)});
     const int64_t eig_z = std::max({(int64_t)G * users * heev_ws_z_elems(t.M, t.m),
@@ -186,7 +188,7 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
     auto gram_eig = [&](const GramDesc& d, const void* V, int D, int count, void* out_factor, int copies) {
         // copies > 0: pooled (one set per group) broadcast to `copies` factors
         const int sets = d.set_kind == FI_USER ? users : d.set_kind == FI_BASE ? t.J : d.set_kind == FI_LINK ? links : 1;
-        ctx->launched(launch_gram<T>(t, d, G, sets, V, gram, st));
+        ctx->launched(launch_gram<T>(t, d, G, sets, V, gram, gpart, gpart_bytes, st));
         void* dst = copies > 0 ? pool : out_factor;
         ctx->launched(launch_heev_topk<T>(D, count, G * sets, gram, dst, nullptr, eA, eZ, eX, failp, st));
         if (copies > 0) ctx->launched(launch_broadcast<T>(pool, out_factor, (int64_t)D * count, copies, G, st));

@@ -1,0 +1,555 @@
+// CTA-per-matrix Hermitian top-k eigensolver for 32 < D <= DM (DM = 64 or 128), in the storage
+// precision R, matrix resident in shared memory. Included by k_eig.cu (inside namespace gwtk).
+//
+// Same algorithm and conventions as k_heev_wr / k_heev_topk (reference leading_eigenvectors,
+// proj/src/linalg.cpp:27-45 + phase_normalize_columns :11-25):
+//  1. Householder tridiagonalisation with Q = 256/DM adjacent threads per row (columns split
+//     mod Q, combined by shuffles), 2 CTA barriers per reflector, every thread forms the
+//     reflector scalars itself (no single-thread serial section).
+//  2. fp32 multisection on Sturm counts (S = 1..8 lanes per wanted eigenvalue).
+//  3. Inverse iteration, one thread per eigenvalue, iterate in registers, LU in shared memory.
+//  4. Back-transform with 4 threads per eigenvector (rows split mod 4, shuffle-reduced dots).
+#pragma once
+
+struct EigCtaLayout {
+    size_t oA, ov, ow, otau, osub, odl, od, oe, oe2, ofd, ofe2, olam, oscl, ored, odd, odu, oml, oxr, total;
+    int lda;
+};
+
+__host__ __device__ inline EigCtaLayout eig_cta_layout(int D, int count, int rs) {
+    EigCtaLayout L;
+    // float2 with 4 threads per row (D <= 64): column stride = 16 banks -> 2 wavefronts per warp access
+    L.lda = (rs == 4 && D <= 64) ? D + 8 : D;
+    size_t o = 0;
+    const size_t cs = 2 * (size_t)rs;
+#define GWT_TAKE(field, bytes)          \
+    L.field = o;                        \
+    o = (o + (bytes) + 15) & ~size_t(15);
+    GWT_TAKE(oA, (size_t)L.lda * D * cs)
+    GWT_TAKE(ov, D * cs)
+    GWT_TAKE(ow, D * cs)
+    GWT_TAKE(otau, D * (size_t)rs)
+    GWT_TAKE(osub, D * cs)
+    GWT_TAKE(odl, D * cs)
+    GWT_TAKE(od, D * (size_t)rs)
+    GWT_TAKE(oe, D * (size_t)rs)
+    GWT_TAKE(oe2, D * (size_t)rs)
+    GWT_TAKE(ofd, D * 4)
+    GWT_TAKE(ofe2, D * 4)
+    GWT_TAKE(olam, count * 8)
+    GWT_TAKE(oscl, count * 4)
+    GWT_TAKE(ored, 4 * 8 * 8)
+    GWT_TAKE(odd, (size_t)D * count * rs)
+    GWT_TAKE(odu, (size_t)D * count * rs)
+    GWT_TAKE(oml, (size_t)D * count * rs)
+    GWT_TAKE(oxr, (size_t)D * count * rs)
+#undef GWT_TAKE
+    L.total = o;
+    return L;
+}
+
+// sum over the lanes q == 0 of each Q-lane row group (values of the other lanes must be 0 or equal
+// across the group's lanes are ignored by construction): log2(32/Q) shuffle levels, result in lane 0
+template <int Q, class R>
+__device__ __forceinline__ R rows_sum(R v) {
+#pragma unroll
+    for (int o = Q; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Householder reflector of x = (x0, tail) with ||tail||^2 = t2 (t2 > 0): alpha = -phase(x0) ||x||,
+// v0 = x0 - alpha, tau = 2 / ||v||^2. fp32: one rsqrt + one reciprocal on the step's critical path.
+__device__ __forceinline__ void reflector(float2 x0, float t2, float2& al, float2& v0, float& tk) {
+    const float s2 = x0.x * x0.x + x0.y * x0.y;
+    const float xn = sqrtf(t2 + s2);
+    if (s2 > 0.f) {
+        const float f = xn * rsqrtf(s2);  // ||x|| / |x0|
+        al = make_float2(-x0.x * f, -x0.y * f);
+        v0 = make_float2(x0.x * (1.f + f), x0.y * (1.f + f));
+        tk = __frcp_rn(0.5f * (t2 + s2 * (1.f + f) * (1.f + f)));
+    } else {
+        al = make_float2(-xn, 0.f);
+        v0 = make_float2(xn, 0.f);
+        tk = __frcp_rn(0.5f * (t2 + xn * xn));
+    }
+}
+__device__ __forceinline__ void reflector(double2 x0, double t2, double2& al, double2& v0, double& tk) {
+    const double ax0 = hypot(x0.x, x0.y);
+    const double xnorm = sqrt(t2 + ax0 * ax0);
+    const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
+    al = make_double2(-ph.x * xnorm, -ph.y * xnorm);
+    v0 = make_double2(x0.x - al.x, x0.y - al.y);
+    tk = 2.0 / (t2 + v0.x * v0.x + v0.y * v0.y);
+}
+
+template <class R, int DM, int NT>
+__global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, const cplx_t<R>* __restrict__ in,
+                                                          cplx_t<R>* __restrict__ out, double* __restrict__ evals,
+                                                          int* __restrict__ fail) {
+    using C = cplx_t<R>;
+    constexpr int Q = NT / DM, NW = NT / 32;
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
+    const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
+    const int64_t b = blockIdx.x;
+    const EigCtaLayout L = eig_cta_layout(D, count, sizeof(R));
+    const int LD = L.lda;
+    unsigned char* base = smem_dyn;
+    C* A = reinterpret_cast<C*>(base + L.oA);
+    C* vv = reinterpret_cast<C*>(base + L.ov);
+    C* ww = reinterpret_cast<C*>(base + L.ow);
+    R* tau = reinterpret_cast<R*>(base + L.otau);
+    C* sub = reinterpret_cast<C*>(base + L.osub);
+    C* dlt = reinterpret_cast<C*>(base + L.odl);
+    R* sd = reinterpret_cast<R*>(base + L.od);
+    R* se = reinterpret_cast<R*>(base + L.oe);
+    R* se2 = reinterpret_cast<R*>(base + L.oe2);
+    float* fd = reinterpret_cast<float*>(base + L.ofd);
+    float* fe2 = reinterpret_cast<float*>(base + L.ofe2);
+    double* lamv = reinterpret_cast<double*>(base + L.olam);
+    int* scl = reinterpret_cast<int*>(base + L.oscl);
+    double* red = reinterpret_cast<double*>(base + L.ored);  // [4 slots][NW]
+    R* DDv = reinterpret_cast<R*>(base + L.odd);
+    R* DUv = reinterpret_cast<R*>(base + L.odu);
+    R* MLv = reinterpret_cast<R*>(base + L.oml);
+    R* XR = reinterpret_cast<R*>(base + L.oxr);
+    const C* H = in + b * (int64_t)D * D;
+    for (int idx = tid; idx < D * D; idx += NT) {
+        const int i = idx % D, j = idx / D;
+        if (i >= j) {
+            C v = H[idx];
+            if (i == j) v.y = R(0);
+            A[i + LD * j] = v;
+            A[j + LD * i] = mk(v.x, -v.y);
+        }
+    }
+    __syncthreads();
+    GWT_CLK(t_ph0);
+    const int r = tid / Q, q = tid % Q;
+    // 1. Householder, two CTA barriers per reflector:
+    //   [A] column-k norm partials visible -> every thread forms (alpha, tau, v0); p = tau A22 v
+    //       reading v straight from column k (v0 substituted for row k+1); publish p and v^H p partials
+    //   [B] K = tau/2 v^H p; A22 -= v w^H + w v^H with w = p - K v; the updated column k+1
+    //       yields the next step's norm partials (published before the next [A]).
+    R* rt2 = reinterpret_cast<R*>(red);       // [NW] norm partials of the current column
+    R* rkp = rt2 + NW;                        // [NW] v^H p partials
+    C* pp = vv;              // p of the current step
+    {
+        R part = R(0);
+        if (q == 0 && r > 1 && r < D) {
+            const C a = A[r];
+            part = a.x * a.x + a.y * a.y;
+        }
+        part = rows_sum<Q>(part);
+        if (lane == 0) rt2[wid] = part;
+    }
+    for (int k = 0; k + 2 < D; ++k) {
+        const bool act = r > k && r < D;
+        __syncthreads();  // [A]
+        R t2 = R(0);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t2 += rt2[w];
+        const C x0 = A[(k + 1) + LD * k];
+        const C* colk = A + LD * k;
+        if (t2 == R(0)) {  // uniform: column already reduced; next column's partials
+            if (tid == 0) {
+                tau[k] = R(0);
+                sub[k] = x0;
+            }
+            __syncthreads();  // all reads of rt2 done before it is rewritten
+            R part = R(0);
+            if (q == 0 && r > k + 2 && r < D) {
+                const C a = A[r + LD * (k + 1)];
+                part = a.x * a.x + a.y * a.y;
+            }
+            part = rows_sum<Q>(part);
+            if (lane == 0) rt2[wid] = part;
+            continue;
+        }
+        C al, v0;
+        R tk;
+        reflector(x0, t2, al, v0, tk);
+        const C v = act ? (r == k + 1 ? v0 : colk[r]) : czero<C>();
+        C p0 = czero<C>(), p1 = czero<C>();
+        if (act) {
+            // columns c = k+1+q, +Q, ...; 4-column batches with all loads issued first
+            const C* arow = A + r;
+            int c = k + 1 + q;
+            for (; c + 3 * Q < D; c += 4 * Q) {
+                C a[4], b[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    a[u] = arow[LD * (c + u * Q)];
+                    b[u] = colk[c + u * Q];
+                }
+                if (c == k + 1) b[0] = v0;  // the reflector's first entry is v0, not the stored x0
+                cfma(p0, a[0], b[0]);
+                cfma(p1, a[1], b[1]);
+                cfma(p0, a[2], b[2]);
+                cfma(p1, a[3], b[3]);
+            }
+            for (; c < D; c += Q) cfma(p0, arow[LD * c], c == k + 1 ? v0 : colk[c]);
+        }
+        C p = mk(p0.x + p1.x, p0.y + p1.y);
+#pragma unroll
+        for (int o = 1; o < Q; o <<= 1) {
+            p.x += __shfl_xor_sync(0xffffffffu, p.x, o);
+            p.y += __shfl_xor_sync(0xffffffffu, p.y, o);
+        }
+        p = mk(p.x * tk, p.y * tk);
+        R kp = (q == 0 && act) ? v.x * p.x + v.y * p.y : R(0);
+        kp = rows_sum<Q>(kp);
+        if (lane == 0) rkp[wid] = kp;
+        if (act && q == 0) pp[r] = p;
+        __syncthreads();  // [B]
+        R ks = R(0);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) ks += rkp[w];
+        const R kk = R(0.5) * tk * ks;
+        const C w = mk(p.x - kk * v.x, p.y - kk * v.y);
+        if (tid == 0) {
+            tau[k] = tk;
+            sub[k] = al;
+        }
+        R part = R(0);
+        if (act) {
+            // a[r][c] -= v_r conj(w_c) + w_r conj(v_c),  w_c = p_c - K v_c
+            C* arow = A + r;
+            int c = k + 1 + q;
+            for (; c + 3 * Q < D; c += 4 * Q) {
+                C a[4], vc[4], pc[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    a[u] = arow[LD * (c + u * Q)];
+                    vc[u] = colk[c + u * Q];
+                    pc[u] = pp[c + u * Q];
+                }
+                if (c == k + 1) vc[0] = v0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const C wc = mk(pc[u].x - kk * vc[u].x, pc[u].y - kk * vc[u].y);
+                    a[u].x -= v.x * wc.x + v.y * wc.y + w.x * vc[u].x + w.y * vc[u].y;
+                    a[u].y -= v.y * wc.x - v.x * wc.y + w.y * vc[u].x - w.x * vc[u].y;
+                    arow[LD * (c + u * Q)] = a[u];
+                }
+                if (c == k + 1 && r > k + 2) part = a[0].x * a[0].x + a[0].y * a[0].y;
+            }
+            for (; c < D; c += Q) {
+                const C vc = c == k + 1 ? v0 : colk[c];
+                const C pc = pp[c];
+                const C wc = mk(pc.x - kk * vc.x, pc.y - kk * vc.y);
+                C a = arow[LD * c];
+                a.x -= v.x * wc.x + v.y * wc.y + w.x * vc.x + w.y * vc.y;
+                a.y -= v.y * wc.x - v.x * wc.y + w.y * vc.x - w.x * vc.y;
+                arow[LD * c] = a;
+                if (c == k + 1 && r > k + 2) part = a.x * a.x + a.y * a.y;
+            }
+            if (r == k + 1 && q == 0) A[r + LD * k] = v0;  // store the reflector (x0 no longer read)
+        }
+        part = rows_sum<Q>(part);
+        if (lane == 0) rt2[wid] = part;  // rt2 of step k was consumed before [B]
+    }
+    __syncthreads();
+    GWT_CLK(t_ph1);
+    // 2. real symmetric tridiagonal via the diagonal phase similarity
+    for (int i = tid; i < D; i += NT) sd[i] = A[i + LD * i].x;
+    if (tid == 0) {
+        C dl = mk(R(1), R(0));
+        dlt[0] = dl;
+        for (int i = 0; i + 1 < D; ++i) {
+            const C s = (i + 2 < D) ? sub[i] : A[(i + 1) + LD * i];
+            const R mag = hypot(s.x, s.y);
+            se[i] = mag;
+            se2[i] = mag * mag;
+            if (mag > R(0)) dl = cmul(dl, mk(s.x / mag, s.y / mag));
+            dlt[i + 1] = dl;
+        }
+        se[D - 1] = R(0);
+        se2[D - 1] = R(0);
+    }
+    __syncthreads();
+    double lo_p = 1e308, hi_p = -1e308, nrm_p = 0.0;
+    for (int i = tid; i < D; i += NT) {
+        const double rr = (double)(i > 0 ? se[i - 1] : R(0)) + (double)se[i];
+        lo_p = fmin(lo_p, (double)sd[i] - rr);
+        hi_p = fmax(hi_p, (double)sd[i] + rr);
+        nrm_p = fmax(nrm_p, fabs((double)sd[i]) + rr);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo_p = fmin(lo_p, __shfl_xor_sync(0xffffffffu, lo_p, o));
+        hi_p = fmax(hi_p, __shfl_xor_sync(0xffffffffu, hi_p, o));
+        nrm_p = fmax(nrm_p, __shfl_xor_sync(0xffffffffu, nrm_p, o));
+    }
+    if (lane == 0) {
+        red[wid] = lo_p;
+        red[NW + wid] = hi_p;
+        red[2 * NW + wid] = nrm_p;
+    }
+    __syncthreads();
+    double glo = 1e308, ghi = -1e308, tnorm = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        glo = fmin(glo, red[w]);
+        ghi = fmax(ghi, red[NW + w]);
+        tnorm = fmax(tnorm, red[2 * NW + w]);
+    }
+    const double eps = sizeof(R) == 4 ? 1.1920928955078125e-07 : 2.220446049250313e-16;
+    glo -= 2.0 * eps * tnorm;
+    ghi += 2.0 * eps * tnorm;
+    const double inv_n = tnorm > 0.0 ? 1.0 / tnorm : 1.0;
+    for (int i = tid; i < D; i += NT) {
+        fd[i] = (float)((double)sd[i] * inv_n);
+        fe2[i] = (float)((double)se2[i] * inv_n * inv_n);
+    }
+    __syncthreads();
+    // 3a. multisection, S lanes (power of two, within one warp) per wanted eigenvalue
+    {
+        int S = NT / count;
+        S = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1));
+        const int t = tid / S, s = tid % S;
+        const int gl = lane / S;  // group index inside the warp
+        const int want = D - 1 - t;
+        float lo = (float)(glo * inv_n) - 1e-6f, hi = (float)(ghi * inv_n) + 1e-6f;
+        bool done = t >= count;
+        for (int it = 0; it < 96; ++it) {
+            if (!done && hi - lo <= 2e-7f * fmaxf(fmaxf(fabsf(lo), fabsf(hi)), 1e-3f)) done = true;
+            if (__all_sync(0xffffffffu, done)) break;
+            const float step = (hi - lo) / (float)(S + 1);
+            const float pt = lo + (float)(s + 1) * step;
+            const bool le = !done && sturm_count_f32(D, fd, fe2, pt, 1e-30f) <= want;
+            const unsigned bits = __ballot_sync(0xffffffffu, le);
+            if (!done) {
+                const int j = __popc((bits >> (gl * S)) & ((S == 32 ? 0u : (1u << S)) - 1u));
+                const float nlo = j > 0 ? lo + (float)j * step : lo;
+                const float nhi = j < S ? lo + (float)(j + 1) * step : hi;
+                if (!(nlo >= lo && nhi <= hi && nlo < nhi) || (nlo == lo && nhi == hi)) done = true;
+                else {
+                    lo = nlo;
+                    hi = nhi;
+                }
+            }
+        }
+        if (t < count && s == 0) lamv[t] = 0.5 * ((double)lo + (double)hi) * tnorm;
+    }
+    __syncthreads();
+    __shared__ int s_rounds;
+    if (tid == 0) {
+        const double ctol = 1e-3 * fmax(tnorm, 1e-300);
+        int pos = 0, maxr = 0;
+        for (int t = 0; t < count; ++t) {
+            pos = (t > 0 && fabs(lamv[t - 1] - lamv[t]) <= ctol) ? pos + 1 : 0;
+            scl[t] = pos;
+            maxr = max(maxr, pos);
+        }
+        s_rounds = maxr + 1;
+    }
+    __syncthreads();
+    const int rounds = s_rounds;
+    GWT_CLK(t_ph2);
+    // 3b. inverse iteration, thread t = eigenvalue t
+    {
+        const int t = tid;
+#define LU_(arr, i) arr[(i) * count + t]
+        const R tiny = (R)fmax(eps * tnorm, sizeof(R) == 4 ? 1e-30 : 1e-290);
+    // solves from the fp32 bisection shift (~2e-7 rel): 2 reach fp32 accuracy, 3 binary64
+    constexpr int kSolves = sizeof(R) == 4 ? 2 : 3;
+        for (int rd = 0; rd < rounds; ++rd) {
+            if (t < count && scl[t] == rd) {
+                R x[DM];
+                const R lam = (R)lamv[t];
+                unsigned long long sw = 0ull;  // DM <= 64 bits used per word; DM = 128 uses the high word below
+                unsigned long long sw2 = 0ull;
+                R dcur = sd[0] - lam, ucur = se[0];
+                for (int i = 0; i + 1 < D; ++i) {
+                    const R sb = se[i], dn = sd[i + 1] - lam, en = (i + 2 < D) ? se[i + 1] : R(0);
+                    R mult;
+                    if (fabs(dcur) >= fabs(sb)) {
+                        const R di = dcur == R(0) ? tiny : dcur;
+                        mult = sb / di;
+                        LU_(DDv, i) = di;
+                        LU_(DUv, i) = ucur;
+                        dcur = dn - mult * ucur;
+                        ucur = en;
+                    } else {
+                        mult = dcur / sb;
+                        if (i < 64) sw |= 1ull << i;
+                        else sw2 |= 1ull << (i - 64);
+                        LU_(DDv, i) = sb;
+                        LU_(DUv, i) = dn;
+                        dcur = ucur - mult * dn;
+                        ucur = -mult * en;
+                    }
+                    LU_(MLv, i) = mult;
+                }
+                LU_(DDv, D - 1) = dcur;
+                for (int i = 0; i < D; ++i) {
+                    R di = LU_(DDv, i);
+                    if (fabs(di) < tiny) di = di < R(0) ? -tiny : tiny;
+                    LU_(DDv, i) = R(1) / di;
+                }
+#pragma unroll
+                for (int i = 0; i < DM; ++i) x[i] = i < D ? R(1) + R(0.25) * (R)__sinf(0.7f * i + 1.3f * t) : R(0);
+                for (int it = 0; it <= kSolves; ++it) {
+                    for (int s2 = t - rd; s2 < t; ++s2) {
+                        R dot = R(0);
+#pragma unroll
+                        for (int i = 0; i < DM; ++i)
+                            if (i < D) dot += XR[i * count + s2] * x[i];
+#pragma unroll
+                        for (int i = 0; i < DM; ++i)
+                            if (i < D) x[i] -= dot * XR[i * count + s2];
+                    }
+                    R nn = R(0);
+#pragma unroll
+                    for (int i = 0; i < DM; ++i) nn += x[i] * x[i];
+                    const R inv = nn > R(0) ? R(1) / sqrt(nn) : R(1);
+#pragma unroll
+                    for (int i = 0; i < DM; ++i) x[i] *= inv;
+                    if (it == kSolves) break;
+#pragma unroll
+                    for (int i = 0; i + 1 < DM; ++i) {
+                        if (i + 1 < D) {
+                            const R ml = LU_(MLv, i);
+                            const bool swp = i < 64 ? ((sw >> i) & 1ull) : ((sw2 >> (i - 64)) & 1ull);
+                            if (swp) {
+                                const R t0 = x[i];
+                                x[i] = x[i + 1];
+                                x[i + 1] = t0 - ml * x[i + 1];
+                            } else {
+                                x[i + 1] -= ml * x[i];
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = DM - 1; i >= 0; --i) {
+                        if (i < D) {
+                            R acc = x[i];
+                            if (i + 1 < DM && i + 1 < D) acc -= LU_(DUv, i) * x[i + 1];
+                            const bool swp = i < 64 ? ((sw >> i) & 1ull) : ((sw2 >> (i - 64)) & 1ull);
+                            if (i + 2 < DM && i + 2 < D && swp) acc -= se[i + 1] * x[i + 2];
+                            x[i] = acc * LU_(DDv, i);
+                        }
+                    }
+                    R mx = R(0);
+#pragma unroll
+                    for (int i = 0; i < DM; ++i) mx = fmax(mx, fabs(x[i]));
+                    if (!(mx > R(0)) || !isfinite(mx)) {
+                        if (fail) atomicExch(fail, 1);
+                        break;
+                    }
+                    const R sc = R(1) / mx;
+#pragma unroll
+                    for (int i = 0; i < DM; ++i) x[i] *= sc;
+                }
+#pragma unroll
+                for (int i = 0; i < DM; ++i)
+                    if (i < D) XR[i * count + t] = x[i];
+                double rq = 0.0;
+#pragma unroll
+                for (int i = 0; i < DM; ++i) {
+                    if (i < D) {
+                        double tz = (double)sd[i] * x[i];
+                        if (i > 0) tz += (double)se[i - 1] * x[i - 1];
+                        if (i + 1 < DM && i + 1 < D) tz += (double)se[i] * x[i + 1];
+                        rq += (double)x[i] * tz;
+                    }
+                }
+                lamv[t] = rq;
+            }
+            __syncthreads();
+        }
+#undef LU_
+    }
+    GWT_CLK(t_ph3);
+    // 4. back-transform, 4 threads per eigenvector (rows i = qb mod 4)
+    {
+        constexpr int QB = 4, RPT = DM / QB;
+        const int t = tid / QB, qb = tid % QB;
+        const bool on = t < count;  // count <= 64 (host-checked)
+        if (on && qb == 0 && evals) evals[b * count + t] = lamv[t];
+        C y[RPT];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int i = qb + QB * u;
+            y[u] = czero<C>();
+            if (on && i < D) {
+                const R z = XR[i * count + t];
+                const C dl = dlt[i];
+                y[u] = mk(dl.x * z, dl.y * z);
+            }
+        }
+        for (int k = D - 3; k >= 0; --k) {
+            const R tk = tau[k];
+            if (tk == R(0)) continue;
+            C dot = czero<C>();
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i > k && i < D) cfmaconj(dot, A[i + LD * k], y[u]);
+            }
+#pragma unroll
+            for (int o = 1; o < QB; o <<= 1) {
+                dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
+                dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
+            }
+            dot = mk(dot.x * tk, dot.y * tk);
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i > k && i < D) {
+                    const C pr = cmul(A[i + LD * k], dot);
+                    y[u].x -= pr.x;
+                    y[u].y -= pr.y;
+                }
+            }
+        }
+        R best = R(-1);
+        int bi = 0;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int i = qb + QB * u;
+            const R mag = y[u].x * y[u].x + y[u].y * y[u].y;
+            if (i < D && mag > best) {
+                best = mag;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < QB; o <<= 1) {
+            const R ob2 = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob2 > best || (ob2 == best && oi < bi)) {
+                best = ob2;
+                bi = oi;
+            }
+        }
+        // the owner of row bi broadcasts y[bi]
+        C yb = czero<C>();
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+            if (qb + QB * u == bi) yb = y[u];
+        const int owner = (lane & ~(QB - 1)) | (bi % QB);
+        yb = shfl_c(yb, owner);
+        if (on) {
+            C fac = mk(R(1), R(0));
+            if (best > R(0)) {
+                const R im = R(1) / sqrt(best);
+                fac = mk(yb.x * im, -yb.y * im);
+            }
+            C* ob = out + (b * count + t) * (int64_t)D;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i < D) ob[i] = cmul(y[u], fac);
+            }
+        }
+    }
+#ifdef GWT_PHASE_TIMERS
+    if (b == 0 && tid == 0) {
+        const long long t_ph4 = clock64();
+        g_eig_phase[0] = t_ph1 - t_ph0;
+        g_eig_phase[1] = t_ph2 - t_ph1;
+        g_eig_phase[2] = t_ph3 - t_ph2;
+        g_eig_phase[3] = t_ph4 - t_ph3;
+    }
+#endif
+}

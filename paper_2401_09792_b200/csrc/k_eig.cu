@@ -108,6 +108,9 @@ __device__ __forceinline__ int sturm_count_f32(int D, const float* d, const floa
     return cnt;
 }
 
+#include "eig_warp.cuh"
+#include "eig_cta.cuh"
+
 // in: [batch][D][D] Hermitian (column-major; lower triangle read),
 // out: [batch][count][D] top eigenvectors, evals (nullable): [batch][count].
 // ws_a: [batch][D][D] double2 (used when D > 64), ws_z: [batch][count][6*D] double, ws_x: [batch][count][D] double2
@@ -994,6 +997,7 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
     if (D > 256 || D < 1 || count < 1 || count > D) return cudaErrorInvalidValue;
     const char* mode = std::getenv("GWT_EIG_MODE");  // tuning override: "warp", "cta"
     const bool force_warp = mode && std::strcmp(mode, "warp") == 0, force_cta = mode && std::strcmp(mode, "cta") == 0;
+    const bool legacy_warp = mode && std::strcmp(mode, "warp_old") == 0;
     if (!force_warp && !force_cta && D <= 8) {
         const unsigned blocks = (unsigned)((batch + 127) / 128);
         switch (D) {
@@ -1015,7 +1019,58 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
                                                               fail);
         return cudaGetLastError();
     }
-    if (!force_cta && (force_warp ? D <= kSmemMaxD : D <= 32)) {
+    const bool cta32 = mode && std::strcmp(mode, "cta32") == 0;
+    if (cta32 && D <= 32) {
+        const EigCtaLayout L = eig_cta_layout(D, count, sizeof(T));
+        cudaError_t e = cudaFuncSetAttribute(k_heev_cr<T, 32, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)L.total);
+        if (e != cudaSuccess) return e;
+        k_heev_cr<T, 32, 128><<<(unsigned)batch, 128, L.total, st>>>(D, count, (const cplx_t<T>*)in, (cplx_t<T>*)out,
+                                                                      evals, fail);
+        return cudaGetLastError();
+    }
+    if (!force_cta && !force_warp && !legacy_warp && D <= 32) {
+        // warp per matrix in the storage precision, registers + shared memory only (eig_warp.cuh)
+        const EigWarpLayout L = eig_warp_layout(D, count, sizeof(T));
+        int W = 4;
+        while (W > 1 && W * L.total > 100 * 1024) W /= 2;
+        const size_t sm = L.total * W;
+        const unsigned blocks = (unsigned)((batch + W - 1) / W);
+        cudaError_t e;
+        if (D <= 16) {
+            e = cudaFuncSetAttribute(k_heev_wr<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return e;
+            k_heev_wr<T, 16><<<blocks, 32 * W, sm, st>>>(D, count, batch, W, (const cplx_t<T>*)in, (cplx_t<T>*)out,
+                                                          evals, fail);
+        } else {
+            e = cudaFuncSetAttribute(k_heev_wr<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return e;
+            k_heev_wr<T, 32><<<blocks, 32 * W, sm, st>>>(D, count, batch, W, (const cplx_t<T>*)in, (cplx_t<T>*)out,
+                                                          evals, fail);
+        }
+        return cudaGetLastError();
+    }
+    if (!force_cta && !force_warp && !legacy_warp && D > 32 && count <= 64 && (sizeof(T) == 4 ? D <= 128 : D <= 64)) {
+        // CTA per matrix in the storage precision, matrix in shared memory (eig_cta.cuh)
+        const EigCtaLayout L = eig_cta_layout(D, count, sizeof(T));
+        if (L.total <= 227 * 1024) {
+            const size_t sm = L.total;
+            cudaError_t e;
+            if (D <= 64) {
+                e = cudaFuncSetAttribute(k_heev_cr<T, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                if (e != cudaSuccess) return e;
+                k_heev_cr<T, 64, 256><<<(unsigned)batch, 256, sm, st>>>(D, count, (const cplx_t<T>*)in, (cplx_t<T>*)out,
+                                                                  evals, fail);
+            } else {
+                e = cudaFuncSetAttribute(k_heev_cr<T, 128, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                if (e != cudaSuccess) return e;
+                k_heev_cr<T, 128, 256><<<(unsigned)batch, 256, sm, st>>>(D, count, (const cplx_t<T>*)in, (cplx_t<T>*)out,
+                                                                   evals, fail);
+            }
+            return cudaGetLastError();
+        }
+    }
+    if (!force_cta && (force_warp || legacy_warp ? D <= kSmemMaxD : D <= 32)) {
         // warp per matrix (Householder + bisection + inverse iteration); W matrices per CTA
         const size_t per = ((size_t)D * D * 16 + (size_t)D * (16 + 16 + 16 + 8 + 8 + 8 + 8 + 4) + 15) & ~size_t(15);
         const int W = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per));

@@ -14,77 +14,118 @@
 
 namespace gwtk {
 
-// Tiled strided complex GEMM with conj(U): CTA tile (16*RT) rows x (16*CT) cols, 256 threads
-// (16 x 16), RT x CT outputs per thread, K chunks of 16 staged in smem. The tile shape is picked
-// per call from Cols (12/24-wide factor ranks would waste most of a 64-wide tile).
-template <class T, int RT, int CT>
-__global__ void __launch_bounds__(256) k_cgemm_conjU(Topo t, GemmDesc d, int links, const cplx_t<T>* __restrict__ in,
-                                                      const cplx_t<T>* __restrict__ U, cplx_t<T>* __restrict__ out) {
+// Tiled strided batched complex GEMM with conj(U) (GemmDesc): CTA tile TR rows x TC cols of one item,
+// 256 threads as NR x NC (NR = TR/RT, NC = TC/CT), RT x CT outputs per thread. The global offsets of
+// each thread's staging elements are computed once (no per-chunk div/mod); the next K chunk is
+// prefetched into registers while the current one is multiplied out of shared memory. TC is matched
+// to the factor rank (8/12/16/24/32/48/64/96) so narrow ranks do not pad a wide tile.
+template <class T, int TR, int TC, int RT, int CT>
+__global__ void __launch_bounds__(256) k_cgemm_conjU(Topo t, GemmDesc d, int links, int64_t item0,
+                                                      const cplx_t<T>* __restrict__ in, const cplx_t<T>* __restrict__ U,
+                                                      cplx_t<T>* __restrict__ out) {
     using C = cplx_t<T>;
-    constexpr int TR = 16 * RT, TC = 16 * CT, KC = 16;
+    constexpr int KC = 16, NR = TR / RT, NC = TC / CT;
+    static_assert(NR * NC == 256, "256 threads");
+    constexpr int EI = TR * KC / 256, EU = (TC * KC + 255) / 256;
     __shared__ C sIn[KC][TR + 1];
     __shared__ C sU[KC][TC + 1];
-    const int64_t item = blockIdx.z;
+    const int64_t item = item0 + blockIdx.z;
     const int64_t g = item / links;
     const int l = (int)(item % links);
     const int row0 = blockIdx.x * TR, col0 = blockIdx.y * TC;
     const int rows = d.R * d.S;
+    const int tid = threadIdx.x;
     const C* inb = in + item * d.in_item;
     const int64_t ublk = d.ublk >= 0 ? d.ublk : (int64_t)d.Kd * d.Cols;
     const int64_t ucol = d.ucol >= 0 ? d.ucol : (int64_t)d.Kd;
     const C* ub = U + factor_index(t, d.fkind, g, l) * ublk;
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const bool row_fast = d.rs_in == 1;
+    int64_t goff[EI];
+    int ekk[EI];
+    bool erok[EI];
+#pragma unroll
+    for (int e = 0; e < EI; ++e) {
+        const int idx = tid + 256 * e;
+        int r, kk;
+        if (row_fast) { r = idx % TR; kk = idx / TR; }
+        else { kk = idx % KC; r = idx / KC; }
+        const int row = row0 + r;
+        ekk[e] = kk;
+        erok[e] = row < rows;
+        goff[e] = erok[e] ? (row % d.R) * d.rs_in + (int64_t)(row / d.R) * d.s_in + (int64_t)kk * d.ks_in : 0;
+    }
+    int64_t uoff[EU];
+    int ukk[EU], uc[EU];
+    bool uok[EU];
+#pragma unroll
+    for (int e = 0; e < EU; ++e) {
+        const int idx = tid + 256 * e;
+        ukk[e] = idx % KC;
+        uc[e] = idx / KC;
+        const int col = col0 + uc[e];
+        uok[e] = idx < TC * KC && col < d.Cols;
+        uoff[e] = uok[e] ? (int64_t)ukk[e] * d.uk + (int64_t)col * ucol : 0;
+    }
+    C pin[EI], pu[EU];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int e = 0; e < EI; ++e) {
+            pin[e] = czero<C>();
+            if (erok[e] && k0 + ekk[e] < d.Kd) pin[e] = inb[goff[e] + (int64_t)k0 * d.ks_in];
+        }
+#pragma unroll
+        for (int e = 0; e < EU; ++e) {
+            pu[e] = czero<C>();
+            if (uok[e] && k0 + ukk[e] < d.Kd) {
+                pu[e] = ub[uoff[e] + (int64_t)k0 * d.uk];
+                if (d.uconj) pu[e] = cconj(pu[e]);
+            }
+        }
+    };
+    const int tx = tid % NC, ty = tid / NC;
     C acc[RT][CT];
 #pragma unroll
     for (int a = 0; a < RT; ++a)
 #pragma unroll
         for (int b = 0; b < CT; ++b) acc[a][b] = czero<C>();
-    const bool row_fast = d.rs_in == 1;
+    fetch(0);
     for (int k0 = 0; k0 < d.Kd; k0 += KC) {
-        for (int idx = threadIdx.x; idx < TR * KC; idx += 256) {
-            int r, kk;
-            if (row_fast) { r = idx % TR; kk = idx / TR; }
-            else { kk = idx % KC; r = idx / KC; }
-            const int row = row0 + r, k = k0 + kk;
-            C v = czero<C>();
-            if (row < rows && k < d.Kd)
-                v = inb[(row % d.R) * d.rs_in + (int64_t)(row / d.R) * d.s_in + (int64_t)k * d.ks_in];
-            sIn[kk][r] = v;
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EI; ++e) {
+            const int idx = tid + 256 * e;
+            if (row_fast) sIn[idx / TR][idx % TR] = pin[e];
+            else sIn[idx % KC][idx / KC] = pin[e];
         }
-        for (int idx = threadIdx.x; idx < TC * KC; idx += 256) {
-            const int kk = idx % KC, c = idx / KC;
-            const int col = col0 + c, k = k0 + kk;
-            C v = czero<C>();
-            if (col < d.Cols && k < d.Kd) {
-                v = ub[(int64_t)k * d.uk + (int64_t)col * ucol];
-                if (d.uconj) v = cconj(v);
-            }
-            sU[kk][c] = v;
+#pragma unroll
+        for (int e = 0; e < EU; ++e) {
+            const int idx = tid + 256 * e;
+            if (idx < TC * KC) sU[idx % KC][idx / KC] = pu[e];
         }
         __syncthreads();
+        if (k0 + KC < d.Kd) fetch(k0 + KC);
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
             C a[RT], b[CT];
 #pragma unroll
-            for (int q = 0; q < RT; ++q) a[q] = sIn[kk][ty + 16 * q];
+            for (int q = 0; q < RT; ++q) a[q] = sIn[kk][ty + NR * q];
 #pragma unroll
-            for (int q = 0; q < CT; ++q) b[q] = sU[kk][tx + 16 * q];
+            for (int q = 0; q < CT; ++q) b[q] = sU[kk][tx + NC * q];
 #pragma unroll
             for (int qa = 0; qa < RT; ++qa)
 #pragma unroll
                 for (int qb = 0; qb < CT; ++qb) cfma(acc[qa][qb], a[qa], b[qb]);
         }
-        __syncthreads();
     }
     C* ob = out + item * d.out_item;
 #pragma unroll
     for (int qa = 0; qa < RT; ++qa) {
-        const int row = row0 + ty + 16 * qa;
+        const int row = row0 + ty + NR * qa;
         if (row >= rows) continue;
         const int64_t ro = (row % d.R) * d.rs_out + (int64_t)(row / d.R) * d.s_out;
 #pragma unroll
         for (int qb = 0; qb < CT; ++qb) {
-            const int col = col0 + tx + 16 * qb;
+            const int col = col0 + tx + NC * qb;
             if (col < d.Cols) ob[ro + (int64_t)col * d.cs_out] = acc[qa][qb];
         }
     }
@@ -111,64 +152,109 @@ __device__ __forceinline__ int set_link(const Topo& t, int kind, int s, int r) {
     }
 }
 
-// Batched Hermitian rank-k accumulation: CTA per (set, TD x TD output tile), TD = 16*Q.
-template <class T, int Q>
-__global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_group, const cplx_t<T>* __restrict__ V,
-                                              cplx_t<T>* __restrict__ out) {
+// Batched Hermitian rank-k accumulation (GramDesc). CTA = (lower-triangle TD x TD tile, set, K split),
+// TD = 16*Q, 256 threads with Q x Q outputs each. The set's flattened reduction index
+// k = link_in_set * T + t is mapped to global offsets chunk by chunk (a KC-entry shared table built
+// one chunk ahead), so the per-element staging has no div/mod; the next K chunk is prefetched into registers while the current one is
+// multiplied. With nsplit > 1 each split writes its partial D x D Gram to `out + split * D*D*sets`
+// and k_gram_reduce sums them in a fixed order (deterministic).
+template <class T, int Q, int KC>
+__global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_group, int64_t set0, int nsplit,
+                                              int kspan, const cplx_t<T>* __restrict__ V, cplx_t<T>* __restrict__ out,
+                                              int64_t split_stride) {
     using C = cplx_t<T>;
-    constexpr int TD = 16 * Q, KC = 16;
+    constexpr int TD = 16 * Q, EL = TD * KC / 256;
     __shared__ C sX[KC][TD + 1];
     __shared__ C sY[KC][TD + 1];
-    const int64_t set = blockIdx.y;
+    __shared__ int64_t koff[2][KC];  // global offsets of the current / next K chunk
+    const int64_t set = set0 + blockIdx.y;
     const int64_t g = set / sets_per_group;
     const int s = (int)(set % sets_per_group);
-    const int tiles = (d.D + TD - 1) / TD;
-    const int x0 = (blockIdx.x % tiles) * TD, y0 = (blockIdx.x / tiles) * TD;
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    // lower-triangle tile index -> (xt >= yt)
+    int xt = 0, yt = 0;
+    {
+        int rem = blockIdx.x;
+        while (rem > xt) {
+            ++xt;
+            rem -= xt;
+        }
+        yt = rem;
+    }
+    const int x0 = xt * TD, y0 = yt * TD;
+    const bool diag = xt == yt;
+    const int nl = set_size(t, d.set_kind);
+    const int Tn = d.T1 * d.T2;
+    const int64_t ktot = (int64_t)nl * Tn;
+    const int64_t kb = (int64_t)blockIdx.z * kspan;
+    const int kn = (int)std::max<int64_t>(0, std::min<int64_t>(kspan, ktot - kb));
+    const C* vg = V + g * t.links() * d.v_item;
+    auto offsets = [&](int k0, int64_t* dst) {  // threads < KC: offset table of chunk k0
+        const int k = k0 + threadIdx.x;
+        if (threadIdx.x < KC && k < kn) {
+            const int64_t kf = kb + k;
+            const int li = (int)(kf / Tn), tt = (int)(kf % Tn);
+            const int l = set_link(t, d.set_kind, s, li);
+            dst[threadIdx.x] = (int64_t)l * d.v_item + (int64_t)(tt % d.T1) * d.t1s + (int64_t)(tt / d.T1) * d.t2s;
+        }
+    };
+    offsets(0, koff[0]);
+    __syncthreads();
+    const bool x_fast = d.xs == 1;
+    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+    C px[EL], py[EL];
+    auto fetch = [&](int k0, const int64_t* ko) {
+#pragma unroll
+        for (int e = 0; e < EL; ++e) {
+            const int idx = tid + 256 * e;
+            int xi, kk;
+            if (x_fast) { xi = idx % TD; kk = idx / TD; }
+            else { kk = idx % KC; xi = idx / KC; }
+            const int k = k0 + kk;
+            px[e] = czero<C>();
+            py[e] = czero<C>();
+            if (k < kn) {
+                const C* vb = vg + ko[kk];
+                if (x0 + xi < d.D) px[e] = vb[(int64_t)(x0 + xi) * d.xs];
+                if (!diag && y0 + xi < d.D) py[e] = vb[(int64_t)(y0 + xi) * d.xs];
+            }
+        }
+    };
     C acc[Q][Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a)
 #pragma unroll
         for (int b = 0; b < Q; ++b) acc[a][b] = czero<C>();
-    const int nl = set_size(t, d.set_kind);
-    const int Tn = d.T1 * d.T2;
-    const bool x_fast = d.xs == 1;
-    for (int r = 0; r < nl; ++r) {
-        const int l = set_link(t, d.set_kind, s, r);
-        const C* vb = V + (g * t.links() + l) * d.v_item;
-        for (int t0 = 0; t0 < Tn; t0 += KC) {
-            for (int idx = threadIdx.x; idx < TD * KC; idx += 256) {
-                int xi, kk;
-                if (x_fast) { xi = idx % TD; kk = idx / TD; }
-                else { kk = idx % KC; xi = idx / KC; }
-                const int tt = t0 + kk;
-                C vx = czero<C>(), vy = czero<C>();
-                if (tt < Tn) {
-                    const int64_t toff = (int64_t)(tt % d.T1) * d.t1s + (int64_t)(tt / d.T1) * d.t2s;
-                    if (x0 + xi < d.D) vx = vb[(int64_t)(x0 + xi) * d.xs + toff];
-                    if (y0 + xi < d.D) vy = vb[(int64_t)(y0 + xi) * d.xs + toff];
-                }
-                sX[kk][xi] = vx;
-                sY[kk][xi] = vy;
+    fetch(0, koff[0]);
+    for (int k0 = 0, c = 0; k0 < kn; k0 += KC, ++c) {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < EL; ++e) {
+            const int idx = tid + 256 * e;
+            int xi, kk;
+            if (x_fast) { xi = idx % TD; kk = idx / TD; }
+            else { kk = idx % KC; xi = idx / KC; }
+            sX[kk][xi] = px[e];
+            if (!diag) sY[kk][xi] = py[e];
+        }
+        if (k0 + KC < kn) offsets(k0 + KC, koff[(c + 1) & 1]);
+        __syncthreads();
+        if (k0 + KC < kn) fetch(k0 + KC, koff[(c + 1) & 1]);
+        const C(*sB)[TD + 1] = diag ? sX : sY;
+#pragma unroll 8
+        for (int kk = 0; kk < KC; ++kk) {
+            C a[Q], b[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                a[q] = sX[kk][ty + 16 * q];
+                b[q] = sB[kk][tx + 16 * q];
             }
-            __syncthreads();
 #pragma unroll
-            for (int kk = 0; kk < KC; ++kk) {
-                C a[Q], b[Q];
+            for (int qa = 0; qa < Q; ++qa)
 #pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    a[q] = sX[kk][ty + 16 * q];
-                    b[q] = sY[kk][tx + 16 * q];
-                }
-#pragma unroll
-                for (int qa = 0; qa < Q; ++qa)
-#pragma unroll
-                    for (int qb = 0; qb < Q; ++qb) cfmac(acc[qa][qb], a[qa], b[qb]);
-            }
-            __syncthreads();
+                for (int qb = 0; qb < Q; ++qb) cfmac(acc[qa][qb], a[qa], b[qb]);
         }
     }
-    C* ob = out + set * (int64_t)d.D * d.D;
+    C* ob = out + blockIdx.z * split_stride + set * (int64_t)d.D * d.D;
 #pragma unroll
     for (int qa = 0; qa < Q; ++qa) {
         const int x = x0 + ty + 16 * qa;
@@ -176,8 +262,21 @@ __global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_g
 #pragma unroll
         for (int qb = 0; qb < Q; ++qb) {
             const int y = y0 + tx + 16 * qb;
-            if (y < d.D) ob[x + (int64_t)d.D * y] = acc[qa][qb];
+            if (y >= d.D) continue;
+            ob[x + (int64_t)d.D * y] = acc[qa][qb];
+            if (!diag) ob[y + (int64_t)d.D * x] = cconj(acc[qa][qb]);
         }
+    }
+}
+
+// out[e] = sum_{s < nsplit} part[s * stride + e], e < n (fixed order)
+template <class T>
+__global__ void k_gram_reduce(const cplx_t<T>* __restrict__ part, int nsplit, int64_t stride, int64_t n,
+                              cplx_t<T>* __restrict__ out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        cplx_t<T> acc = part[e];
+        for (int s = 1; s < nsplit; ++s) acc = cadd(acc, part[s * stride + e]);
+        out[e] = acc;
     }
 }
 
@@ -185,38 +284,42 @@ __global__ void __launch_bounds__(256) k_gram(Topo t, GramDesc d, int sets_per_g
 // one thread per fiber, conj(U) broadcast from shared memory. Used for X x1 A^H
 // and Y1 x1 A^H, where the generic 64x64 tile would be >90% padding.
 template <class T, int KD>
-__global__ void __launch_bounds__(256) k_mode1_thin(Topo t, GemmDesc d, int links, int64_t items,
-                                                    const cplx_t<T>* __restrict__ in, const cplx_t<T>* __restrict__ U,
-                                                    cplx_t<T>* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_mode1_thin(Topo t, GemmDesc d, int links, const cplx_t<T>* __restrict__ in,
+                                                    const cplx_t<T>* __restrict__ U, cplx_t<T>* __restrict__ out) {
+    // grid (items, row blocks of 256): the item's conj(U) (KD x Cols <= 8) is staged in shared memory once
     using C = cplx_t<T>;
+    __shared__ C su[KD][8];
+    const int64_t item = blockIdx.x;
     const int rows = d.R * d.S;
-    const int64_t total = items * rows;
-    const int64_t ublk = d.ublk >= 0 ? d.ublk : (int64_t)d.Kd * d.Cols;
-    const int64_t ucol = d.ucol >= 0 ? d.ucol : (int64_t)d.Kd;
-    for (int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gidx < total;
-         gidx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t item = gidx / rows;
-        const int row = (int)(gidx % rows);
-        const int64_t g = item / links;
-        const int l = (int)(item % links);
-        const C* ub = U + factor_index(t, d.fkind, g, l) * ublk;
-        const C* x = in + item * d.in_item + (row % d.R) * d.rs_in + (int64_t)(row / d.R) * d.s_in;
-        C xv[KD];
-#pragma unroll
-        for (int kk = 0; kk < KD; ++kk) xv[kk] = x[kk];
-        C* o = out + item * d.out_item + (row % d.R) * d.rs_out + (int64_t)(row / d.R) * d.s_out;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            if (c >= d.Cols) break;
-            C acc = czero<C>();
-#pragma unroll
-            for (int kk = 0; kk < KD; ++kk) {
-                C u = ub[(int64_t)kk * d.uk + (int64_t)c * ucol];
-                if (d.uconj) u = cconj(u);
-                cfma(acc, xv[kk], u);
-            }
-            o[(int64_t)c * d.cs_out] = acc;
+    const int row = blockIdx.y * 256 + threadIdx.x;
+    if (threadIdx.x < KD * 8) {
+        const int kk = threadIdx.x % KD, c = threadIdx.x / KD;
+        C u = czero<C>();
+        if (c < d.Cols) {
+            const int64_t g = item / links;
+            const int l = (int)(item % links);
+            const int64_t ublk = d.ublk >= 0 ? d.ublk : (int64_t)d.Kd * d.Cols;
+            const int64_t ucol = d.ucol >= 0 ? d.ucol : (int64_t)d.Kd;
+            u = U[factor_index(t, d.fkind, g, l) * ublk + (int64_t)kk * d.uk + (int64_t)c * ucol];
+            if (d.uconj) u = cconj(u);
         }
+        su[kk][c] = u;
+    }
+    __syncthreads();
+    if (row >= rows) return;
+    const int rr = d.S == 1 ? row : row % d.R, rs = d.S == 1 ? 0 : row / d.R;
+    const C* x = in + item * d.in_item + (int64_t)rr * d.rs_in + (int64_t)rs * d.s_in;
+    C xv[KD];
+#pragma unroll
+    for (int kk = 0; kk < KD; ++kk) xv[kk] = x[kk];
+    C* o = out + item * d.out_item + (int64_t)rr * d.rs_out + (int64_t)rs * d.s_out;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        if (c >= d.Cols) break;
+        C acc = czero<C>();
+#pragma unroll
+        for (int kk = 0; kk < KD; ++kk) cfma(acc, xv[kk], su[kk][c]);
+        o[(int64_t)c * d.cs_out] = acc;
     }
 }
 
@@ -335,37 +438,40 @@ cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, cons
                          cudaStream_t st) {
     if (d.ks_in == 1 && d.Kd <= 8 && d.Cols <= 8) {
         const int64_t items = ngroups * t.links();
-        const int64_t total = items * d.R * d.S;
-        const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32);
+        dim3 grid((unsigned)items, (unsigned)((d.R * d.S + 255) / 256));
         switch (d.Kd) {
 #define GWT_THIN(KK) \
-    case KK: k_mode1_thin<T, KK><<<blocks, 256, 0, st>>>(t, d, t.links(), items, (const cplx_t<T>*)in, (const cplx_t<T>*)U, (cplx_t<T>*)out); break;
+    case KK: k_mode1_thin<T, KK><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U, (cplx_t<T>*)out); break;
             GWT_THIN(1) GWT_THIN(2) GWT_THIN(3) GWT_THIN(4) GWT_THIN(5) GWT_THIN(6) GWT_THIN(7) GWT_THIN(8)
 #undef GWT_THIN
         }
         return cudaGetLastError();
     }
-    const unsigned items = (unsigned)(ngroups * t.links());
+    const int64_t items = ngroups * t.links();
     const int rows = d.R * d.S;
-    if (d.Cols <= 16) {
-        dim3 grid((rows + 127) / 128, (d.Cols + 15) / 16, items);
-        k_cgemm_conjU<T, 8, 1><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
-                                                      (cplx_t<T>*)out);
-    } else if (d.Cols <= 32) {
-        dim3 grid((rows + 63) / 64, (d.Cols + 31) / 32, items);
-        k_cgemm_conjU<T, 4, 2><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
-                                                      (cplx_t<T>*)out);
-    } else {
-        dim3 grid((rows + 63) / 64, (d.Cols + 63) / 64, items);
-        k_cgemm_conjU<T, 4, 4><<<grid, 256, 0, st>>>(t, d, t.links(), (const cplx_t<T>*)in, (const cplx_t<T>*)U,
-                                                      (cplx_t<T>*)out);
+    const cplx_t<T>* a = (const cplx_t<T>*)in;
+    const cplx_t<T>* u = (const cplx_t<T>*)U;
+    cplx_t<T>* o = (cplx_t<T>*)out;
+#define GWT_GEMM(TR_, TC_, RT_, CT_)                                                                      \
+    for (int64_t i0 = 0; i0 < items; i0 += 65535) {                                                       \
+        dim3 grid((rows + TR_ - 1) / TR_, (d.Cols + TC_ - 1) / TC_, (unsigned)std::min<int64_t>(65535, items - i0)); \
+        k_cgemm_conjU<T, TR_, TC_, RT_, CT_><<<grid, 256, 0, st>>>(t, d, t.links(), i0, a, u, o);          \
     }
+    if (d.Cols <= 8) GWT_GEMM(128, 8, 2, 2)
+    else if (d.Cols <= 12) GWT_GEMM(128, 12, 2, 3)
+    else if (d.Cols <= 16) GWT_GEMM(128, 16, 2, 4)
+    else if (d.Cols <= 24) GWT_GEMM(128, 24, 4, 3)
+    else if (d.Cols <= 32) GWT_GEMM(128, 32, 4, 4)
+    else if (d.Cols <= 48) GWT_GEMM(64, 48, 4, 3)
+    else if (d.Cols <= 64) GWT_GEMM(64, 64, 4, 4)
+    else GWT_GEMM(64, 96, 4, 6)
+#undef GWT_GEMM
     return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V, void* out,
-                        cudaStream_t st) {
+                        void* part, size_t part_bytes, cudaStream_t st) {
     // complex64 Grams with D >= 64 on the tensor cores (3xTF32 tcgen05, k_tc.cu): opt-in (GWT_GRAM_TC=1)
     // until its staging pipeline beats the CUDA-core kernel
     if (sizeof(T) == 4 && d.D >= 64) {
@@ -382,16 +488,37 @@ cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int s
         }
         return cudaGetLastError();
     }
-    if (d.D <= 32) {
-        const int tiles = (d.D + 31) / 32;
-        dim3 grid(tiles * tiles, (unsigned)(ngroups * sets_per_group));
-        k_gram<T, 2><<<grid, 256, 0, st>>>(t, d, sets_per_group, (const cplx_t<T>*)V, (cplx_t<T>*)out);
-    } else {
-        const int tiles = (d.D + 63) / 64;
-        dim3 grid(tiles * tiles, (unsigned)(ngroups * sets_per_group));
-        k_gram<T, 4><<<grid, 256, 0, st>>>(t, d, sets_per_group, (const cplx_t<T>*)V, (cplx_t<T>*)out);
-    }
-    return cudaGetLastError();
+    const int64_t sets = ngroups * sets_per_group;
+    const int nl = d.set_kind == FI_USER ? t.J : d.set_kind == FI_BASE ? t.J * t.K : d.set_kind == FI_LINK ? 1 : t.links();
+    const int64_t ktot = (int64_t)nl * d.T1 * d.T2;
+    auto run = [&](auto kern, int TD, int KC) -> cudaError_t {
+        const int tiles = (d.D + TD - 1) / TD, ntl = tiles * (tiles + 1) / 2;
+        // K split: aim for >= 4 CTAs per SM, at least 8 chunks per split, limited by the partial buffer
+        int nsplit = 1;
+        const int64_t ctas = sets * ntl;
+        if (part && ctas < 148 * 4) {
+            nsplit = (int)std::min<int64_t>((148 * 4 + ctas - 1) / ctas, std::max<int64_t>(1, ktot / (8 * KC)));
+            const int64_t cap = (int64_t)(part_bytes / (sizeof(cplx_t<T>) * (size_t)d.D * d.D * sets));
+            nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit, cap));
+        }
+        int kspan = (int)((ktot + nsplit - 1) / nsplit);
+        kspan = (kspan + KC - 1) / KC * KC;
+        nsplit = (int)((ktot + kspan - 1) / kspan);
+        cplx_t<T>* dst = nsplit > 1 ? (cplx_t<T>*)part : (cplx_t<T>*)out;
+        const int64_t stride = sets * (int64_t)d.D * d.D;
+        for (int64_t s0 = 0; s0 < sets; s0 += 65535) {
+            dim3 grid(ntl, (unsigned)std::min<int64_t>(65535, sets - s0), nsplit);
+            kern<<<grid, 256, 0, st>>>(t, d, sets_per_group, s0, nsplit, kspan, (const cplx_t<T>*)V, dst, stride);
+        }
+        if (nsplit > 1) {
+            const unsigned blocks = (unsigned)std::min<int64_t>((stride + 255) / 256, 148 * 16);
+            k_gram_reduce<T><<<blocks, 256, 0, st>>>((const cplx_t<T>*)part, nsplit, stride, stride, (cplx_t<T>*)out);
+        }
+        return cudaGetLastError();
+    };
+    constexpr int KCb = sizeof(T) == 4 ? 32 : 16;
+    if (d.D <= 32) return run(k_gram<T, 2, KCb>, 32, KCb);
+    return run(k_gram<T, 4, KCb>, 64, KCb);
 }
 
 template <class T>
@@ -426,8 +553,8 @@ cudaError_t launch_broadcast(const void* src, void* dst, int64_t elems, int copi
 #define GWT_INST(T)                                                                                          \
     template cudaError_t launch_cgemm<T>(const Topo&, const GemmDesc&, int64_t, const void*, const void*, void*, \
                                          cudaStream_t);                                                      \
-    template cudaError_t launch_gram<T>(const Topo&, const GramDesc&, int64_t, int, const void*, void*,          \
-                                        cudaStream_t);                                                       \
+    template cudaError_t launch_gram<T>(const Topo&, const GramDesc&, int64_t, int, const void*, void*, void*,   \
+                                        size_t, cudaStream_t);                                                       \
     template cudaError_t launch_group_sqnorm<T>(const void*, int64_t, int64_t, double*, double*, cudaStream_t);          \
     template cudaError_t launch_broadcast<T>(const void*, void*, int64_t, int, int64_t, cudaStream_t);
 GWT_INST(float)

@@ -36,7 +36,7 @@ def _max_angle(U1, U2):
 # ---------------------------------------------------------------------------
 # linalg
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 8, 17, 24, 32, 64, 128, 256])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8, 12, 17, 24, 32, 64, 128, 256])
 def test_leading_eigenvectors_match_oracle_and_lapack(ctx, n):
     rng = np.random.default_rng(n)
     b = 3
@@ -53,15 +53,19 @@ def test_leading_eigenvectors_match_oracle_and_lapack(ctx, n):
         assert np.linalg.norm(vec[k].conj().T @ vec[k] - np.eye(count)) < 1e-10
 
 
-def test_leading_eigenvectors_c64(ctx):
-    rng = np.random.default_rng(5)
-    n = 64
+@pytest.mark.parametrize("n,count", [(12, 5), (24, 12), (32, 12), (64, 8), (64, 24)])
+def test_leading_eigenvectors_c64(ctx, n, count):
+    """c64 Grams are decomposed in fp32 (warp kernel for n <= 32): subspace angle and eigenvalues vs fp64."""
+    rng = np.random.default_rng(5 + n)
     A = rng.standard_normal((4, n, n)) + 1j * rng.standard_normal((4, n, n))
     H = (A @ np.conj(np.swapaxes(A, 1, 2))).astype(np.complex64)
-    vec = ctx.leading_eigenvectors(H, 8)
+    vec, ev = ctx.leading_eigenvectors(H, count, with_values=True)
     for k in range(4):
-        ref = O.leading_eigenvectors(H[k].astype(np.complex128), 8)
+        ref = O.leading_eigenvectors(H[k].astype(np.complex128), count)
         assert _max_angle(vec[k].astype(np.complex128), ref) < 1e-3
+        w = np.linalg.eigvalsh(H[k].astype(np.complex128))[::-1][:count]
+        assert np.max(np.abs(ev[k] - w)) <= 1e-5 * np.abs(w).max()
+        assert np.linalg.norm(vec[k].astype(np.complex128).conj().T @ vec[k] - np.eye(count)) < 1e-4
 
 
 def test_leading_eigenvectors_errors(ctx):

@@ -11,10 +11,11 @@ def launches(path):
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         us = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("void ", "")
