@@ -46,9 +46,18 @@ struct gwt_ctx {
     std::vector<Slot> slots = std::vector<Slot>(32);
     cudaEvent_t ev[16] = {};
     double stage_ms[8] = {};
+    // extra solver lanes (stream + workspace) that run group sub-chunks concurrently with lane 0 (ctx->stream)
+    struct Lane {
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev = nullptr;
+        std::vector<Slot> slots = std::vector<Slot>(32);
+    };
+    std::vector<Lane> lanes;
 
-    void* ws(int slot, size_t bytes) {
-        Slot& s = slots[slot];
+    void* ws(int slot, size_t bytes) { return ws_in(slots, slot, bytes); }
+    void* lws(int lane, int slot, size_t bytes) { return lane == 0 ? ws(slot, bytes) : ws_in(lanes[lane - 1].slots, slot, bytes); }
+    void* ws_in(std::vector<Slot>& v, int slot, size_t bytes) {
+        Slot& s = v[slot];
         if (bytes == 0) bytes = 16;
         if (s.bytes < bytes) {
             if (s.p) ck(cudaFree(s.p), "cudaFree");
@@ -143,176 +152,281 @@ struct Timer {
 size_t csize(gwt_dtype dt) { return dt == GWT_C64 ? 8 : 16; }
 
 // ---------------------------------------------------------------------------
-// Tucker solve on device pointers for one chunk of groups.
+// Tucker solve on device pointers for one sub-chunk of groups on one solver lane (stream +
+// workspace). The driver interleaves the lanes sweep by sweep, so the latency-bound eigensolver
+// launches of one lane overlap the bandwidth-bound contractions of the others.
 template <class T>
-void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int sweeps, unsigned flags, void* A, void* B,
-                 void* Cf, void* Gc, double* trace_d, std::vector<int>& iters, std::vector<double>& trace_h,
-                 std::vector<double>& energy_h, double* ms) {
+struct SolveLane {
     using Cx = cplx_t<T>;
-    const size_t cs = sizeof(Cx);
-    cudaStream_t st = ctx->stream;
-    const int links = t.links(), users = t.users();
-    const int64_t MNP = (int64_t)t.M * t.N * t.P;
-    const bool pooled = flags & GWT_SOLVE_POOLED;
-    const bool early = flags & GWT_SOLVE_EARLY_STOP;
-    void* Y1 = ctx->ws(WS_Y1, cs * G * links * t.M * t.N * t.p);
-    void* W = ctx->ws(WS_W, cs * G * links * t.M * t.n * t.p);
-    void* W2 = ctx->ws(WS_W2, cs * G * links * t.m * t.N * t.p);
-    void* Z = ctx->ws(WS_Z, cs * G * links * t.m * t.N * t.P);
-    void* Z2 = ctx->ws(WS_Z2, cs * G * links * t.m * t.n * t.P);
-    const int64_t gram_elems = std::max({(int64_t)G * users * t.M * t.M, (int64_t)G * t.J * t.N * t.N,
-                                         (int64_t)G * links * t.P * t.P});
-    void* gram = ctx->ws(WS_GRAM, cs * gram_elems);
-    const size_t gpart_bytes = std::min<size_t>(cs * gram_elems * 8, size_t(256) << 20);  // K-split partials
-    void* gpart = ctx->ws(WS_GPART, gpart_bytes);
-    const int64_t eig_a = std::max({(int64_t)G * users * heev_ws_a_elems(t.M), (int64_t)G * t.J * heev_ws_a_elems(t.N),
-                                    (int64_t)G * links * heev_ws_a_elems(t.P)});
-    const int64_t eig_z = std::max({(int64_t)G * users * heev_ws_z_elems(t.M, t.m),
-                                    (int64_t)G * t.J * heev_ws_z_elems(t.N, t.n),
-                                    (int64_t)G * links * heev_ws_z_elems(t.P, t.p)});
-    const int64_t eig_x = std::max({(int64_t)G * users * t.M * t.m, (int64_t)G * t.J * t.N * t.n,
-                                    (int64_t)G * links * t.P * t.p});
-    double2* eA = (double2*)ctx->ws(WS_EIGA, 16 * eig_a);
-    double* eZ = (double*)ctx->ws(WS_EIGZ, 8 * eig_z);
-    double2* eX = (double2*)ctx->ws(WS_EIGX, 16 * eig_x);
-    void* pool = ctx->ws(WS_POOL, cs * G * std::max(t.M * t.m, t.N * t.n));
-    double* energy = (double*)ctx->ws(WS_ENERGY, 8 * G);
-    double* capt = (double*)ctx->ws(WS_CAPT, 8 * G);
-    int* failp = (int*)ctx->ws(WS_FAIL, 4);
-    ck(cudaMemsetAsync(failp, 0, 4, st), "memset");
-    double* part = (double*)ctx->ws(WS_PART, 8 * G * kSqnormMaxBlocks);
+    gwt_ctx* ctx = nullptr;
+    int lane = 0;
+    cudaStream_t st = nullptr;
+    Topo t{};
+    int64_t G = 0;
+    const void* X = nullptr;
+    int sweeps = 0;
+    unsigned flags = 0;
+    void *A = nullptr, *B = nullptr, *Cf = nullptr, *Gc = nullptr;
+    double *trace_d = nullptr, *energy = nullptr;
+    // workspace
+    void *Y1, *W, *W2, *Z, *Z2, *gram, *gpart, *pool;
+    size_t gpart_bytes = 0;
+    double2* eA;
+    double* eZ;
+    double2* eX;
+    double *capt, *part;
+    int* failp;
+    int hfail = 0;
+    GemmDesc dZ{}, dZ2{}, dG{}, dY1{}, dW{}, dW2{};
+    int rx_kind = 0, tx_kind = 0, rx_copies = 0, tx_copies = 0;
+    // early stop (decompose.cpp:363-368)
+    bool early = false;
+    std::vector<char> stopped;
+    std::vector<int> iters;
+    std::vector<double> trace_h, energy_h;
+    char* frozen = nullptr;
+    size_t a_sz = 0, b_sz = 0, c_sz = 0, g_sz = 0;
+    int64_t active = 0;
 
-    auto gemm = [&](const GemmDesc& d, const void* in, const void* U, void* out) {
+    void* ws(int slot, size_t bytes) { return ctx->lws(lane, slot, bytes); }
+    void gemm(const GemmDesc& d, const void* in, const void* U, void* out) {
         ctx->launched(launch_cgemm<T>(t, d, G, in, U, out, st));
-    };
-    auto gram_eig = [&](const GramDesc& d, const void* V, int D, int count, void* out_factor, int copies) {
+    }
+    void gram_eig(const GramDesc& d, const void* V, int D, int count, void* out_factor, int copies) {
         // copies > 0: pooled (one set per group) broadcast to `copies` factors
+        const int users = t.users(), links = t.links();
         const int sets = d.set_kind == FI_USER ? users : d.set_kind == FI_BASE ? t.J : d.set_kind == FI_LINK ? links : 1;
         ctx->launched(launch_gram<T>(t, d, G, sets, V, gram, gpart, gpart_bytes, st));
         void* dst = copies > 0 ? pool : out_factor;
         ctx->launched(launch_heev_topk<T>(D, count, G * sets, gram, dst, nullptr, eA, eZ, eX, failp, st));
         if (copies > 0) ctx->launched(launch_broadcast<T>(pool, out_factor, (int64_t)D * count, copies, G, st));
-    };
-    // mode-product descriptors
-    GemmDesc dZ{};  // Z = X x1 A^H  (m x N x P)
-    dZ.R = t.N * t.P; dZ.S = 1; dZ.Kd = t.M; dZ.Cols = t.m;
-    dZ.in_item = MNP; dZ.rs_in = t.M; dZ.s_in = 0; dZ.ks_in = 1;
-    dZ.out_item = (int64_t)t.m * t.N * t.P; dZ.rs_out = t.m; dZ.s_out = 0; dZ.cs_out = 1; dZ.fkind = FI_USER;
-    GemmDesc dZ2{};  // Z2 = Z x2 B^H (m x n x P)
-    dZ2.R = t.m; dZ2.S = t.P; dZ2.Kd = t.N; dZ2.Cols = t.n;
-    dZ2.in_item = (int64_t)t.m * t.N * t.P; dZ2.rs_in = 1; dZ2.s_in = (int64_t)t.m * t.N; dZ2.ks_in = t.m;
-    dZ2.out_item = (int64_t)t.m * t.n * t.P; dZ2.rs_out = 1; dZ2.s_out = (int64_t)t.m * t.n; dZ2.cs_out = t.m;
-    dZ2.fkind = FI_BASE;
-    GemmDesc dG{};  // core = Z2 x3 C^H (m x n x p)
-    dG.R = t.m * t.n; dG.S = 1; dG.Kd = t.P; dG.Cols = t.p;
-    dG.in_item = (int64_t)t.m * t.n * t.P; dG.rs_in = 1; dG.s_in = 0; dG.ks_in = (int64_t)t.m * t.n;
-    dG.out_item = (int64_t)t.m * t.n * t.p; dG.rs_out = 1; dG.s_out = 0; dG.cs_out = (int64_t)t.m * t.n;
-    dG.fkind = FI_LINK;
-    GemmDesc dY1{};  // Y1 = X x3 C^H (M x N x p)
-    dY1.R = t.M * t.N; dY1.S = 1; dY1.Kd = t.P; dY1.Cols = t.p;
-    dY1.in_item = MNP; dY1.rs_in = 1; dY1.s_in = 0; dY1.ks_in = (int64_t)t.M * t.N;
-    dY1.out_item = (int64_t)t.M * t.N * t.p; dY1.rs_out = 1; dY1.s_out = 0; dY1.cs_out = (int64_t)t.M * t.N;
-    dY1.fkind = FI_LINK;
-    GemmDesc dW{};  // W = Y1 x2 B^H (M x n x p)
-    dW.R = t.M; dW.S = t.p; dW.Kd = t.N; dW.Cols = t.n;
-    dW.in_item = (int64_t)t.M * t.N * t.p; dW.rs_in = 1; dW.s_in = (int64_t)t.M * t.N; dW.ks_in = t.M;
-    dW.out_item = (int64_t)t.M * t.n * t.p; dW.rs_out = 1; dW.s_out = (int64_t)t.M * t.n; dW.cs_out = t.M;
-    dW.fkind = FI_BASE;
-    GemmDesc dW2{};  // W2 = Y1 x1 A^H (m x N x p)
-    dW2.R = t.N * t.p; dW2.S = 1; dW2.Kd = t.M; dW2.Cols = t.m;
-    dW2.in_item = (int64_t)t.M * t.N * t.p; dW2.rs_in = t.M; dW2.s_in = 0; dW2.ks_in = 1;
-    dW2.out_item = (int64_t)t.m * t.N * t.p; dW2.rs_out = t.m; dW2.s_out = 0; dW2.cs_out = 1; dW2.fkind = FI_USER;
-
-    const int rx_kind = pooled ? FI_GROUP : FI_USER, tx_kind = pooled ? FI_GROUP : FI_BASE;
-    const int rx_copies = pooled ? users : 0, tx_copies = pooled ? t.J : 0;
-
-    Timer tm(ctx);
-    tm.mark(1);
-    ctx->launched(launch_group_sqnorm<T>(X, links * MNP, G, energy, part, st));
-    if (!(flags & GWT_SOLVE_INIT)) {  // initial_factors (decompose.cpp:248-300)
-        GramDesc g1{t.M, t.N * t.P, 1, MNP, 1, t.M, 0, rx_kind};
-        gram_eig(g1, X, t.M, t.m, A, rx_copies);
-        GramDesc g2{t.N, t.M, t.P, MNP, t.M, 1, (int64_t)t.M * t.N, tx_kind};
-        gram_eig(g2, X, t.N, t.n, B, tx_copies);
-        GramDesc g3{t.P, t.M * t.N, 1, MNP, (int64_t)t.M * t.N, 1, 0, FI_LINK};
-        gram_eig(g3, X, t.P, t.p, Cf, 0);
     }
-    auto objective = [&](int slot) {
+    void objective(int slot) {
         gemm(dZ, X, A, Z);
         gemm(dZ2, Z, B, Z2);
         gemm(dG, Z2, Cf, Gc);
-        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)links * t.m * t.n * t.p, G, capt, part, st));
+        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)t.links() * t.m * t.n * t.p, G, capt, part, st));
         ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, slot, st));
-    };
-    objective(0);
-    tm.mark(2);
-    // per-group early-stop bookkeeping (decompose.cpp:363-368)
-    std::vector<char> stopped(G, 0);
-    const size_t a_sz = cs * users * t.M * t.m, b_sz = cs * t.J * t.N * t.n, c_sz = cs * links * t.P * t.p,
-                 g_sz = cs * links * t.m * t.n * t.p;
-    char* frozen = nullptr;
-    if (early) {
-        frozen = (char*)ctx->ws(WS_FROZEN, (a_sz + b_sz + c_sz + g_sz) * G);
-        energy_h.resize(G);
-        ck(cudaMemcpyAsync(energy_h.data(), energy, 8 * G, cudaMemcpyDeviceToHost, st), "D2H");
     }
-    trace_h.assign((size_t)G * (sweeps + 1), 0.0);
-    iters.assign(G, sweeps);
-    int64_t active = G;
-    for (int s = 0; s < sweeps && active > 0; ++s) {
-        // rx phase: all fresh receive factors from the old tx/delay factors
+
+    // allocations, ||X||^2, initial factors (decompose.cpp:248-300) and the sweep-0 objective
+    void begin() {
+        const size_t cs = sizeof(Cx);
+        const int links = t.links(), users = t.users();
+        const int64_t MNP = (int64_t)t.M * t.N * t.P;
+        const bool pooled = flags & GWT_SOLVE_POOLED;
+        early = flags & GWT_SOLVE_EARLY_STOP;
+        Y1 = ws(WS_Y1, cs * G * links * t.M * t.N * t.p);
+        W = ws(WS_W, cs * G * links * t.M * t.n * t.p);
+        W2 = ws(WS_W2, cs * G * links * t.m * t.N * t.p);
+        Z = ws(WS_Z, cs * G * links * t.m * t.N * t.P);
+        Z2 = ws(WS_Z2, cs * G * links * t.m * t.n * t.P);
+        const int64_t gram_elems = std::max({(int64_t)G * users * t.M * t.M, (int64_t)G * t.J * t.N * t.N,
+                                             (int64_t)G * links * t.P * t.P});
+        gram = ws(WS_GRAM, cs * gram_elems);
+        gpart_bytes = std::min<size_t>(cs * gram_elems * 8, size_t(256) << 20);  // K-split partials
+        gpart = ws(WS_GPART, gpart_bytes);
+        const int64_t eig_a = std::max({(int64_t)G * users * heev_ws_a_elems(t.M),
+                                        (int64_t)G * t.J * heev_ws_a_elems(t.N), (int64_t)G * links * heev_ws_a_elems(t.P)});
+        const int64_t eig_z = std::max({(int64_t)G * users * heev_ws_z_elems(t.M, t.m),
+                                        (int64_t)G * t.J * heev_ws_z_elems(t.N, t.n),
+                                        (int64_t)G * links * heev_ws_z_elems(t.P, t.p)});
+        const int64_t eig_x = std::max({(int64_t)G * users * t.M * t.m, (int64_t)G * t.J * t.N * t.n,
+                                        (int64_t)G * links * t.P * t.p});
+        eA = (double2*)ws(WS_EIGA, 16 * eig_a);
+        eZ = (double*)ws(WS_EIGZ, 8 * eig_z);
+        eX = (double2*)ws(WS_EIGX, 16 * eig_x);
+        pool = ws(WS_POOL, cs * G * std::max(t.M * t.m, t.N * t.n));
+        capt = (double*)ws(WS_CAPT, 8 * G);
+        failp = (int*)ws(WS_FAIL, 4);
+        part = (double*)ws(WS_PART, 8 * G * kSqnormMaxBlocks);
+        ck(cudaMemsetAsync(failp, 0, 4, st), "memset");
+        // mode-product descriptors
+        dZ.R = t.N * t.P; dZ.S = 1; dZ.Kd = t.M; dZ.Cols = t.m;  // Z = X x1 A^H  (m x N x P)
+        dZ.in_item = MNP; dZ.rs_in = t.M; dZ.s_in = 0; dZ.ks_in = 1;
+        dZ.out_item = (int64_t)t.m * t.N * t.P; dZ.rs_out = t.m; dZ.s_out = 0; dZ.cs_out = 1; dZ.fkind = FI_USER;
+        dZ2.R = t.m; dZ2.S = t.P; dZ2.Kd = t.N; dZ2.Cols = t.n;  // Z2 = Z x2 B^H (m x n x P)
+        dZ2.in_item = (int64_t)t.m * t.N * t.P; dZ2.rs_in = 1; dZ2.s_in = (int64_t)t.m * t.N; dZ2.ks_in = t.m;
+        dZ2.out_item = (int64_t)t.m * t.n * t.P; dZ2.rs_out = 1; dZ2.s_out = (int64_t)t.m * t.n; dZ2.cs_out = t.m;
+        dZ2.fkind = FI_BASE;
+        dG.R = t.m * t.n; dG.S = 1; dG.Kd = t.P; dG.Cols = t.p;  // core = Z2 x3 C^H (m x n x p)
+        dG.in_item = (int64_t)t.m * t.n * t.P; dG.rs_in = 1; dG.s_in = 0; dG.ks_in = (int64_t)t.m * t.n;
+        dG.out_item = (int64_t)t.m * t.n * t.p; dG.rs_out = 1; dG.s_out = 0; dG.cs_out = (int64_t)t.m * t.n;
+        dG.fkind = FI_LINK;
+        dY1.R = t.M * t.N; dY1.S = 1; dY1.Kd = t.P; dY1.Cols = t.p;  // Y1 = X x3 C^H (M x N x p)
+        dY1.in_item = MNP; dY1.rs_in = 1; dY1.s_in = 0; dY1.ks_in = (int64_t)t.M * t.N;
+        dY1.out_item = (int64_t)t.M * t.N * t.p; dY1.rs_out = 1; dY1.s_out = 0; dY1.cs_out = (int64_t)t.M * t.N;
+        dY1.fkind = FI_LINK;
+        dW.R = t.M; dW.S = t.p; dW.Kd = t.N; dW.Cols = t.n;  // W = Y1 x2 B^H (M x n x p)
+        dW.in_item = (int64_t)t.M * t.N * t.p; dW.rs_in = 1; dW.s_in = (int64_t)t.M * t.N; dW.ks_in = t.M;
+        dW.out_item = (int64_t)t.M * t.n * t.p; dW.rs_out = 1; dW.s_out = (int64_t)t.M * t.n; dW.cs_out = t.M;
+        dW.fkind = FI_BASE;
+        dW2.R = t.N * t.p; dW2.S = 1; dW2.Kd = t.M; dW2.Cols = t.m;  // W2 = Y1 x1 A^H (m x N x p)
+        dW2.in_item = (int64_t)t.M * t.N * t.p; dW2.rs_in = t.M; dW2.s_in = 0; dW2.ks_in = 1;
+        dW2.out_item = (int64_t)t.m * t.N * t.p; dW2.rs_out = t.m; dW2.s_out = 0; dW2.cs_out = 1; dW2.fkind = FI_USER;
+        rx_kind = pooled ? FI_GROUP : FI_USER;
+        tx_kind = pooled ? FI_GROUP : FI_BASE;
+        rx_copies = pooled ? users : 0;
+        tx_copies = pooled ? t.J : 0;
+
+        ctx->launched(launch_group_sqnorm<T>(X, links * MNP, G, energy, part, st));
+        if (!(flags & GWT_SOLVE_INIT)) {
+            GramDesc g1{t.M, t.N * t.P, 1, MNP, 1, t.M, 0, rx_kind};
+            gram_eig(g1, X, t.M, t.m, A, rx_copies);
+            GramDesc g2{t.N, t.M, t.P, MNP, t.M, 1, (int64_t)t.M * t.N, tx_kind};
+            gram_eig(g2, X, t.N, t.n, B, tx_copies);
+            GramDesc g3{t.P, t.M * t.N, 1, MNP, (int64_t)t.M * t.N, 1, 0, FI_LINK};
+            gram_eig(g3, X, t.P, t.p, Cf, 0);
+        }
+        objective(0);
+        stopped.assign(G, 0);
+        a_sz = cs * users * t.M * t.m;
+        b_sz = cs * t.J * t.N * t.n;
+        c_sz = cs * links * t.P * t.p;
+        g_sz = cs * links * t.m * t.n * t.p;
+        if (early) {
+            frozen = (char*)ws(WS_FROZEN, (a_sz + b_sz + c_sz + g_sz) * G);
+            energy_h.resize(G);
+            ck(cudaMemcpyAsync(energy_h.data(), energy, 8 * G, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        trace_h.assign((size_t)G * (sweeps + 1), 0.0);
+        iters.assign(G, sweeps);
+        active = G;
+    }
+
+    // enqueue one alternating sweep (decompose.cpp:330-370): rx, tx, delay factors, then cores + objective
+    void sweep(int s) {
         gemm(dY1, X, Cf, Y1);
         gemm(dW, Y1, B, W);
         GramDesc grx{t.M, t.n * t.p, 1, (int64_t)t.M * t.n * t.p, 1, t.M, 0, rx_kind};
         gram_eig(grx, W, t.M, t.m, A, rx_copies);
-        // tx phase with the new receive factors
         gemm(dW2, Y1, A, W2);
         GramDesc gtx{t.N, t.m, t.p, (int64_t)t.m * t.N * t.p, t.m, 1, (int64_t)t.m * t.N, tx_kind};
         gram_eig(gtx, W2, t.N, t.n, B, tx_copies);
-        // delay phase with new rx and tx
         gemm(dZ, X, A, Z);
         gemm(dZ2, Z, B, Z2);
         GramDesc gd{t.P, t.m * t.n, 1, (int64_t)t.m * t.n * t.P, (int64_t)t.m * t.n, 1, 0, FI_LINK};
         gram_eig(gd, Z2, t.P, t.p, Cf, 0);
-        // objective (energy split ||X||^2 - ||core||^2) and the cores of these factors
         gemm(dG, Z2, Cf, Gc);
-        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)links * t.m * t.n * t.p, G, capt, part, st));
+        ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)t.links() * t.m * t.n * t.p, G, capt, part, st));
         ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, s + 1, st));
-        if (early) {
-            ck(cudaMemcpyAsync(trace_h.data(), trace_d, 8 * trace_h.size(), cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaStreamSynchronize(st), "sync");
-            for (int64_t g = 0; g < G; ++g) {
-                if (stopped[g]) continue;
-                const double dec = trace_h[g * (sweeps + 1) + s] - trace_h[g * (sweeps + 1) + s + 1];
-                if (dec < 1e-10 * energy_h[g]) {
-                    stopped[g] = 1;
-                    --active;
-                    iters[g] = s + 1;
-                    char* fz = frozen + g * (a_sz + b_sz + c_sz + g_sz);
-                    ck(cudaMemcpyAsync(fz, (char*)A + g * a_sz, a_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                    ck(cudaMemcpyAsync(fz + a_sz, (char*)B + g * b_sz, b_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                    ck(cudaMemcpyAsync(fz + a_sz + b_sz, (char*)Cf + g * c_sz, c_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                    ck(cudaMemcpyAsync(fz + a_sz + b_sz + c_sz, (char*)Gc + g * g_sz, g_sz, cudaMemcpyDeviceToDevice, st),
-                       "D2D");
-                }
+        if (early) ck(cudaMemcpyAsync(trace_h.data(), trace_d, 8 * trace_h.size(), cudaMemcpyDeviceToHost, st), "D2H");
+    }
+
+    // host side, after the lane's stream has completed sweep s: freeze converged groups
+    void check(int s) {
+        for (int64_t g = 0; g < G; ++g) {
+            if (stopped[g]) continue;
+            const double dec = trace_h[g * (sweeps + 1) + s] - trace_h[g * (sweeps + 1) + s + 1];
+            if (dec < 1e-10 * energy_h[g]) {
+                stopped[g] = 1;
+                --active;
+                iters[g] = s + 1;
+                char* fz = frozen + g * (a_sz + b_sz + c_sz + g_sz);
+                ck(cudaMemcpyAsync(fz, (char*)A + g * a_sz, a_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                ck(cudaMemcpyAsync(fz + a_sz, (char*)B + g * b_sz, b_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                ck(cudaMemcpyAsync(fz + a_sz + b_sz, (char*)Cf + g * c_sz, c_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                ck(cudaMemcpyAsync(fz + a_sz + b_sz + c_sz, (char*)Gc + g * g_sz, g_sz, cudaMemcpyDeviceToDevice, st),
+                   "D2D");
             }
         }
     }
-    tm.mark(3);
-    if (early) {
-        for (int64_t g = 0; g < G; ++g) {
-            if (!stopped[g]) continue;
-            char* fz = frozen + g * (a_sz + b_sz + c_sz + g_sz);
-            ck(cudaMemcpyAsync((char*)A + g * a_sz, fz, a_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-            ck(cudaMemcpyAsync((char*)B + g * b_sz, fz + a_sz, b_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-            ck(cudaMemcpyAsync((char*)Cf + g * c_sz, fz + a_sz + b_sz, c_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-            ck(cudaMemcpyAsync((char*)Gc + g * g_sz, fz + a_sz + b_sz + c_sz, g_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+
+    void end() {
+        if (early) {
+            for (int64_t g = 0; g < G; ++g) {
+                if (!stopped[g]) continue;
+                char* fz = frozen + g * (a_sz + b_sz + c_sz + g_sz);
+                ck(cudaMemcpyAsync((char*)A + g * a_sz, fz, a_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                ck(cudaMemcpyAsync((char*)B + g * b_sz, fz + a_sz, b_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                ck(cudaMemcpyAsync((char*)Cf + g * c_sz, fz + a_sz + b_sz, c_sz, cudaMemcpyDeviceToDevice, st), "D2D");
+                ck(cudaMemcpyAsync((char*)Gc + g * g_sz, fz + a_sz + b_sz + c_sz, g_sz, cudaMemcpyDeviceToDevice, st),
+                   "D2D");
+            }
         }
+        ck(cudaMemcpyAsync(&hfail, failp, 4, cudaMemcpyDeviceToHost, st), "D2H");
     }
-    int hfail = 0;
-    ck(cudaMemcpyAsync(&hfail, failp, 4, cudaMemcpyDeviceToHost, st), "D2H");
-    ck(cudaStreamSynchronize(st), "sync");
-    if (hfail) fail(GWT_RUNTIME_ERROR, "leading_eigenvectors: eigendecomposition failed");
+};
+
+int solve_lanes() {
+    const char* e = std::getenv("GWT_SOLVE_LANES");
+    return e ? std::max(1, std::min(8, std::atoi(e))) : 4;
+}
+
+// Solve one chunk of G groups (device pointers) on up to solve_lanes() concurrent lanes.
+template <class T>
+void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int sweeps, unsigned flags, void* A, void* B,
+                 void* Cf, void* Gc, double* trace_d, double* energy_d, std::vector<int>& iters, double* ms) {
+    using Cx = cplx_t<T>;
+    const size_t cs = sizeof(Cx);
+    const int links = t.links(), users = t.users();
+    const int64_t x_g = (int64_t)links * t.M * t.N * t.P, a_g = (int64_t)users * t.M * t.m,
+                  b_g = (int64_t)t.J * t.N * t.n, c_g = (int64_t)links * t.P * t.p,
+                  g_g = (int64_t)links * t.m * t.n * t.p;
+    const int L = (int)std::min<int64_t>(solve_lanes(), G);
+    while ((int)ctx->lanes.size() < L - 1) {
+        gwt_ctx::Lane ln;
+        ck(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaEventCreateWithFlags(&ln.ev, cudaEventDisableTiming), "cudaEventCreate");
+        ctx->lanes.push_back(ln);
+    }
+    Timer tm(ctx);
+    tm.mark(1);
+    std::vector<SolveLane<T>> lanes(L);
+    if (L > 1) {  // lanes 1.. start after everything already queued on ctx->stream
+        ck(cudaEventRecord(ctx->ev[10], ctx->stream), "cudaEventRecord");
+        for (int l = 1; l < L; ++l) ck(cudaStreamWaitEvent(ctx->lanes[l - 1].st, ctx->ev[10], 0), "cudaStreamWaitEvent");
+    }
+    int64_t g0 = 0;
+    for (int l = 0; l < L; ++l) {
+        SolveLane<T>& ln = lanes[l];
+        const int64_t Gl = G / L + (l < G % L ? 1 : 0);
+        ln.ctx = ctx;
+        ln.lane = l;
+        ln.st = l == 0 ? ctx->stream : ctx->lanes[l - 1].st;
+        ln.t = t;
+        ln.G = Gl;
+        ln.X = (const char*)X + cs * g0 * x_g;
+        ln.sweeps = sweeps;
+        ln.flags = flags;
+        ln.A = (char*)A + cs * g0 * a_g;
+        ln.B = (char*)B + cs * g0 * b_g;
+        ln.Cf = (char*)Cf + cs * g0 * c_g;
+        ln.Gc = (char*)Gc + cs * g0 * g_g;
+        ln.trace_d = trace_d + g0 * (sweeps + 1);
+        ln.energy = energy_d + g0;
+        g0 += Gl;
+        ln.begin();
+    }
+    tm.mark(2);
+    const bool early = flags & GWT_SOLVE_EARLY_STOP;
+    for (int s = 0; s < sweeps; ++s) {
+        bool any = false;
+        for (auto& ln : lanes)
+            if (ln.active > 0) {
+                ln.sweep(s);
+                any = true;
+            }
+        if (!any) break;
+        if (early)
+            for (auto& ln : lanes)
+                if (ln.active > 0) {
+                    ck(cudaStreamSynchronize(ln.st), "sync");
+                    ln.check(s);
+                }
+    }
+    for (auto& ln : lanes) ln.end();
+    for (int l = 1; l < L; ++l) {  // ctx->stream waits for the other lanes
+        ck(cudaEventRecord(ctx->lanes[l - 1].ev, ctx->lanes[l - 1].st), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(ctx->stream, ctx->lanes[l - 1].ev, 0), "cudaStreamWaitEvent");
+    }
+    tm.mark(3);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    iters.clear();
+    for (auto& ln : lanes) {
+        if (ln.hfail) fail(GWT_RUNTIME_ERROR, "leading_eigenvectors: eigendecomposition failed");
+        iters.insert(iters.end(), ln.iters.begin(), ln.iters.end());
+    }
     ms[0] += tm.between(1, 2);
     ms[1] += tm.between(2, 3);
 }
@@ -381,14 +495,14 @@ void groupwise_solve_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_rank
             Gd = (char*)Gc + cs * g0 * g_g;
         }
         std::vector<int> it;
-        std::vector<double> th, eh;
-        solve_chunk<T>(ctx, t, G, Xd, sweeps, flags, Ad, Bd, Cd, Gd, trace_d, it, th, eh, ms);
+        std::vector<double> th;
+        double* en = (double*)ctx->ws(WS_ENERGY, 8 * G);
+        solve_chunk<T>(ctx, t, G, Xd, sweeps, flags, Ad, Bd, Cd, Gd, trace_d, en, it, ms);
         // trace: entries after an early stop repeat the final objective
         th.resize((size_t)G * (sweeps + 1));
         ck(cudaMemcpy(th.data(), trace_d, 8 * th.size(), cudaMemcpyDeviceToHost), "D2H trace");
         for (int64_t g = 0; g < G; ++g)
             for (int s = it[g] + 1; s <= sweeps; ++s) th[g * (sweeps + 1) + s] = th[g * (sweeps + 1) + it[g]];
-        double* en = (double*)ctx->ws(WS_ENERGY, 8 * G);
         std::vector<double> enh(G);
         ck(cudaMemcpy(enh.data(), en, 8 * G, cudaMemcpyDeviceToHost), "D2H energy");
         if (mem == GWT_MEM_HOST) {
@@ -626,6 +740,13 @@ void gwt_ctx_destroy(gwt_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& s : ctx->slots)
         if (s.p) cudaFree(s.p);
+    for (auto& ln : ctx->lanes) {
+        cudaStreamSynchronize(ln.st);
+        for (auto& s : ln.slots)
+            if (s.p) cudaFree(s.p);
+        cudaStreamDestroy(ln.st);
+        cudaEventDestroy(ln.ev);
+    }
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);

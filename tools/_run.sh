@@ -1,3 +1,2 @@
-python -m pytest tests/test_gpu_parity.py -x -q -k "leading or groupwise or large" 2>&1 | tail -2
-GWT_LIB_PATH=paper_2401_09792_b200/_build/phase/libgwt_b200.so python tools/eig_phases.py 2>&1 | tail -4
-python tools/eig_probe.py 2>&1 | tail -4
+python -m pytest tests/test_gpu_parity.py tests/test_tc.py -x -q 2>&1 | tail -3
+for L in 1 2 4; do echo "lanes $L"; GWT_SOLVE_LANES=$L python tools/tucker_probe.py 2>&1 | tail -4; done
