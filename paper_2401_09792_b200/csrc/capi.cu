@@ -633,7 +633,8 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         // (measured on C2: L2-sized chunks are slower - fewer CTAs per launch - so default to 2 GiB)
         const int64_t chunk_bytes = cb ? std::atoll(cb) : (int64_t)(2ll << 30);
         const int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f_h, 1)));
-        void* H = ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
+        const bool rg = scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
+        void* H = rg ? nullptr : ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
         // pair Grams for a block of Fs subcarriers: [g][Fs][users][S][m*m] (fp64), Fs bounded by ~2 GB
         const int64_t per_f_pg = (int64_t)ngroups * users * (16LL * S * t.m * t.m + 8LL * (((t.L + 1) & ~1) + 2 * t.m * t.L));
         const int64_t Fs = std::max<int64_t>(Fc, std::min<int64_t>(F, (int64_t)(2ll << 30) / std::max<int64_t>(per_f_pg, 1)) / Fc * Fc);
@@ -647,10 +648,16 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
             evs.push_back(ev);
         };
         std::vector<int> kind;  // 0 rebuild, 1 pair gram, 2 small, per interval
+        // rg: paper scope with small groups -> rebuild + pair Grams fused in shared memory (H~ never in HBM)
         rec();
         for (int64_t F0 = 0; F0 < F; F0 += Fs) {
             const int64_t fs = std::min(Fs, F - F0);
-            for (int64_t f0 = F0; f0 < F0 + fs; f0 += Fc) {
+            if (rg) {
+                ctx->launched(launch_rebuild_pg<T>(t, (int)ngroups, (int)fs, F0, F, 0, fs, Cd, Gd, taud, fd, cod, PG, st));
+                rec();
+                kind.push_back(1);
+            }
+            for (int64_t f0 = F0; !rg && f0 < F0 + fs; f0 += Fc) {
                 const int fc = (int)std::min(Fc, F0 + fs - f0);
                 ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
                 rec();

@@ -126,6 +126,94 @@ __global__ void __launch_bounds__(128) k_rebuild(Topo t, int Fc, int64_t f0, int
 #endif
 }
 
+// K1 (persistent per link): one CTA per (link, group, subcarrier range) keeps the link's delay
+// factor C_l (P x p), core G_l (mn x p) and delays in shared memory and walks its subcarriers in
+// tiles of FT: phasors -> E (p x FT) -> H~ rows. Every global read happens once per CTA; the inner
+// loops only touch shared memory (E read as 16-byte pairs of subcarriers). 128 threads; work items
+// (row, 8-subcarrier block) for the rebuild, (q, subcarrier pair) for E.
+template <class T, int FT>
+__global__ void __launch_bounds__(128) k_rebuild_link(Topo t, int Fc, int64_t f0, int64_t Ftot, int frange,
+                                                      const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
+                                                      const double* __restrict__ tau, const double* __restrict__ freqs,
+                                                      cplx_t<T>* __restrict__ H) {
+    using C = cplx_t<T>;
+    constexpr int NT = 128, FB = 8, NB = FT / FB;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int P = t.P, p = t.p, mn = t.m * t.n, links = t.links();
+    C* ph = reinterpret_cast<C*>(smem_raw);   // [P][FT]
+    C* E = ph + (size_t)P * FT;               // [p][FT]
+    C* sG = E + (size_t)p * FT;               // [p][mn]
+    C* sC = sG + (size_t)p * mn;              // [p][P]  (C_l column-major P x p)
+    double* st = reinterpret_cast<double*>(sC + (size_t)p * P);  // [P]
+    const int l = blockIdx.x;
+    const int64_t g = blockIdx.y;
+    const int64_t gl = g * links + l;
+    const int tid = threadIdx.x;
+    const C* Gl = G + gl * (int64_t)mn * p;
+    const C* Cl = Cd + gl * (int64_t)P * p;
+    for (int e = tid; e < mn * p; e += NT) sG[e] = Gl[e];
+    for (int e = tid; e < P * p; e += NT) sC[e] = Cl[e];
+    for (int e = tid; e < P; e += NT) st[e] = tau[gl * P + e];
+    const int fbeg = blockIdx.z * frange, fend = min(Fc, fbeg + frange);
+    const int64_t fstride = (int64_t)links * mn;  // H~ stride between subcarriers
+    for (int ft0 = fbeg; ft0 < fend; ft0 += FT) {
+        const int nf = min(FT, fend - ft0);
+        __syncthreads();  // previous tile's E consumed (and staging done on the first pass)
+        for (int idx = tid; idx < P * FT; idx += NT) {
+            const int r = idx / FT, f = idx % FT;
+            ph[idx] = f < nf ? conj_coeff<T>(freqs[f0 + ft0 + f], st[r]) : czero<C>();
+        }
+        __syncthreads();
+        // E[q][f..f+1] = sum_r C_l(r, q) ph[r][f..f+1]
+        for (int idx = tid; idx < p * (FT / 2); idx += NT) {
+            const int q = idx / (FT / 2), f = 2 * (idx % (FT / 2));
+            const C* cq = sC + (size_t)P * q;
+            C a0 = czero<C>(), a1 = czero<C>(), b0 = czero<C>(), b1 = czero<C>();
+            int r = 0;
+            for (; r + 1 < P; r += 2) {
+                const C c0 = cq[r], c1 = cq[r + 1];
+                cfma(a0, c0, ph[r * FT + f]);
+                cfma(a1, c0, ph[r * FT + f + 1]);
+                cfma(b0, c1, ph[(r + 1) * FT + f]);
+                cfma(b1, c1, ph[(r + 1) * FT + f + 1]);
+            }
+            if (r < P) {
+                cfma(a0, cq[r], ph[r * FT + f]);
+                cfma(a1, cq[r], ph[r * FT + f + 1]);
+            }
+            E[q * FT + f] = cadd(a0, b0);
+            E[q * FT + f + 1] = cadd(a1, b1);
+        }
+        __syncthreads();
+        for (int w = tid; w < mn * NB; w += NT) {
+            const int row = w % mn, fb = (w / mn) * FB;
+            C acc[FB];
+#pragma unroll
+            for (int f = 0; f < FB; ++f) acc[f] = czero<C>();
+            for (int q = 0; q < p; ++q) {
+                const C gv = sG[(size_t)q * mn + row];
+                const C* eq = E + q * FT + fb;
+                if constexpr (sizeof(C) == 8) {
+                    const float4* e4 = reinterpret_cast<const float4*>(eq);
+#pragma unroll
+                    for (int f = 0; f < FB / 2; ++f) {
+                        const float4 ev = e4[f];
+                        cfma(acc[2 * f], gv, C{ev.x, ev.y});
+                        cfma(acc[2 * f + 1], gv, C{ev.z, ev.w});
+                    }
+                } else {
+#pragma unroll
+                    for (int f = 0; f < FB; ++f) cfma(acc[f], gv, eq[f]);
+                }
+            }
+            C* hp = H + ((g * Fc + ft0 + fb) * links + l) * (int64_t)mn + row;
+#pragma unroll
+            for (int f = 0; f < FB; ++f, hp += fstride)
+                if (fb + f < nf) *hp = acc[f];
+        }
+    }
+}
+
 // scope slot s of user (i,j) -> (k,l), mirroring scope_pairs (sinr.cpp:47-62)
 __device__ __forceinline__ void scope_slot(const Topo& t, int scope, int i, int j, int s, int& k, int& l) {
     if (scope == 0) {  // full: all (k,l) k-major
@@ -196,7 +284,7 @@ __global__ void __launch_bounds__(128) k_pair_gram_staged(Topo t, int Fc, int64_
     const int64_t item = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
     const int J = t.J, users = t.users(), links = t.links();
     const int mn = M * t.n, nl = 2 * J - 1;
-    C* sh = reinterpret_cast<C*>(smem_raw) + (size_t)warp * nl * mn;
+    double2* sh = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * nl * mn;  // binary64 once, at staging
     if (item >= items) return;
     const int u = (int)(item % users);
     const int64_t gf = item / users;
@@ -211,8 +299,8 @@ __global__ void __launch_bounds__(128) k_pair_gram_staged(Topo t, int Fc, int64_
             l = (k * J + k) * t.K;  // partner (k, k, 0)
         }
         const C* src = Hgf + (int64_t)l * mn;
-        C* dst = sh + li * mn;
-        for (int e = lane; e < mn; e += 32) dst[e] = src[e];
+        double2* dst = sh + li * mn;
+        for (int e = lane; e < mn; e += 32) dst[e] = to_d2(src[e]);
     }
     __syncwarp();
     const int64_t orow = ((gf / Fc) * Ftot + f0 + gf % Fc) * users + u;
@@ -221,18 +309,229 @@ __global__ void __launch_bounds__(128) k_pair_gram_staged(Topo t, int Fc, int64_
         const int s = e / MM, ab = e % MM, a = ab % M, b = ab / M;
         // slot 0: serving (i,i,j) with itself; slot s>0: cell k (k-th cell != i) receive link vs partner
         int kcell = s == 0 ? i : (s - 1 < i ? s - 1 : s);
-        const C* h1 = sh + kcell * mn;
-        const C* h2 = s == 0 ? h1 : sh + (J + s - 1) * mn;
+        const double2* h1 = sh + kcell * mn;
+        const double2* h2 = s == 0 ? h1 : sh + (J + s - 1) * mn;
         double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
         int c = 0;
         for (; c + 1 < t.n; c += 2) {
-            cfmac(acc0, to_d2(h1[a + M * c]), to_d2(h2[b + M * c]));
-            cfmac(acc1, to_d2(h1[a + M * (c + 1)]), to_d2(h2[b + M * (c + 1)]));
+            cfmac(acc0, h1[a + M * c], h2[b + M * c]);
+            cfmac(acc1, h1[a + M * (c + 1)], h2[b + M * (c + 1)]);
         }
-        if (c < t.n) cfmac(acc0, to_d2(h1[a + M * c]), to_d2(h2[b + M * c]));
+        if (c < t.n) cfmac(acc0, h1[a + M * c], h2[b + M * c]);
         PG[(orow * J + s) * MM + ab] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
     }
 }
+
+// K2 (paper scope, whole subcarrier): one CTA per (group, subcarrier) stages every link of that
+// H~(f) (one contiguous links*m*n block, 16-byte vector loads, converted to binary64 once) and
+// computes all users' J pair Grams, one thread per Gram entry. No partner link is read twice.
+template <class T, int M>
+__global__ void __launch_bounds__(256) k_pair_gram_gf(Topo t, int Fc, int64_t f0, int64_t Ftot,
+                                                      const cplx_t<T>* __restrict__ H, double2* __restrict__ PG) {
+    using C = cplx_t<T>;
+    constexpr int MM = M * M;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* sh = reinterpret_cast<double2*>(smem_raw);  // [links][mn]
+    const int J = t.J, K = t.K, links = t.links(), users = t.users();
+    const int n = t.n, mn = M * n;
+    const int f = blockIdx.x;
+    const int64_t g = blockIdx.y;
+    const C* Hf = H + ((g * Fc + f) * links) * (int64_t)mn;
+    const int tot = links * mn;
+    if constexpr (sizeof(C) == 8) {
+        const float4* h4 = reinterpret_cast<const float4*>(Hf);  // mn even for m*n even; else scalar tail
+        const int n4 = tot / 2;
+        for (int e = threadIdx.x; e < n4; e += blockDim.x) {
+            const float4 v = h4[e];
+            sh[2 * e] = make_double2(v.x, v.y);
+            sh[2 * e + 1] = make_double2(v.z, v.w);
+        }
+        if ((tot & 1) && threadIdx.x == 0) sh[tot - 1] = to_d2(Hf[tot - 1]);
+    } else {
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) sh[e] = to_d2(Hf[e]);
+    }
+    __syncthreads();
+    const int64_t orow0 = (g * Ftot + f0 + f) * users;
+    for (int e = threadIdx.x; e < users * J * MM; e += blockDim.x) {
+        const int u = e / (J * MM), s = (e / MM) % J, ab = e % MM, a = ab % M, b = ab / M;
+        const int i = u / K, j = u % K;
+        int lx, ly;
+        if (s == 0) {
+            lx = ly = (i * J + i) * K + j;  // serving (i,i,j)
+        } else {
+            const int k = s - 1 < i ? s - 1 : s;  // s-th cell != i (scope_pairs order)
+            lx = (k * J + i) * K + j;
+            ly = (k * J + k) * K;
+        }
+        const double2* h1 = sh + (size_t)lx * mn + a;
+        const double2* h2 = sh + (size_t)ly * mn + b;
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        int c = 0;
+        for (; c + 1 < n; c += 2) {
+            cfmac(acc0, h1[M * c], h2[M * c]);
+            cfmac(acc1, h1[M * (c + 1)], h2[M * (c + 1)]);
+        }
+        if (c < n) cfmac(acc0, h1[M * c], h2[M * c]);
+        PG[((orow0 + u) * J + s) * MM + ab] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1+K2 fused (opt-in GWT_SINR_PATH=rg; measured slower than K1 -> K2 on C2): one CTA (512
+// threads) per (group, FT-subcarrier tile): phasors -> E -> every link's H~ for the tile (binary64
+// in shared memory) -> the J pair Grams of every user, 4 threads per (user, slot, subcarrier).
+template <int M>
+__host__ __device__ inline size_t rg_smem(const Topo& t, int FT, int csize) {
+    const size_t hd = (size_t)t.links() * M * t.n * FT * 16;
+    const size_t ph = (size_t)t.links() * t.P * FT * csize;
+    return (hd > ph ? hd : ph) + (size_t)t.links() * t.p * FT * csize;
+}
+
+template <class T, int M, int FT>
+__global__ void __launch_bounds__(512, 1) k_rebuild_pg(Topo t, int Fc, int64_t f0, int64_t Ftot, int64_t pf0, int64_t pfs,
+                                                     const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
+                                                     const double* __restrict__ tau, const double* __restrict__ freqs,
+                                                     const cplx_t<T>* __restrict__ coeffs, double2* __restrict__ PG) {
+    using C = cplx_t<T>;
+    constexpr int NT = 512, MM = M * M;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int J = t.J, K = t.K, links = t.links(), users = t.users();
+    const int n = t.n, mn = M * n, P = t.P, p = t.p;
+    double2* Hd = reinterpret_cast<double2*>(smem_raw);  // [links][mn][FT]   (phases 3-4)
+    C* Ph = reinterpret_cast<C*>(smem_raw);              // [links][P][FT]    (phases 1-2, aliases Hd)
+    const size_t hd_bytes = (size_t)links * mn * FT * 16, ph_bytes = (size_t)links * P * FT * sizeof(C);
+    C* E = reinterpret_cast<C*>(smem_raw + (hd_bytes > ph_bytes ? hd_bytes : ph_bytes));  // [links][p][FT]
+    const int64_t g = blockIdx.y;
+    const int ft0 = blockIdx.x * FT;
+    const int nf = min(FT, Fc - ft0);
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < links * P * FT; idx += NT) {
+        const int l = idx / (P * FT), r = (idx / FT) % P, f = idx % FT;
+        C v = czero<C>();
+        if (f < nf) {
+            const int64_t fa = f0 + ft0 + f;
+            v = coeffs ? cconj(coeffs[((g * Ftot + fa) * links + l) * P + r])
+                       : conj_coeff<T>(freqs[fa], tau[(g * links + l) * P + r]);
+        }
+        Ph[idx] = v;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < links * p * FT; idx += NT) {
+        const int l = idx / (p * FT), q = (idx / FT) % p, f = idx % FT;
+        const C* Cl = Cd + ((g * links + l) * P) * (int64_t)p + (int64_t)P * q;
+        const C* ph = Ph + (size_t)l * P * FT + f;
+        C acc = czero<C>();
+        for (int r = 0; r < P; ++r) cfma(acc, Cl[r], ph[r * FT]);
+        E[idx] = acc;
+    }
+    __syncthreads();
+    for (int rg = tid; rg < links * mn; rg += NT) {
+        const int l = rg / mn, row = rg % mn;
+        const C* Gl = G + (g * links + l) * (int64_t)mn * p + row;
+        const C* e = E + (size_t)l * p * FT;
+        C acc[FT];
+#pragma unroll
+        for (int f = 0; f < FT; ++f) acc[f] = czero<C>();
+        for (int q = 0; q < p; ++q) {
+            const C gv = Gl[(int64_t)mn * q];
+#pragma unroll
+            for (int f = 0; f < FT; ++f) cfma(acc[f], gv, e[q * FT + f]);
+        }
+        double2* h = Hd + (size_t)rg * FT;
+#pragma unroll
+        for (int f = 0; f < FT; ++f) h[f] = to_d2(acc[f]);
+    }
+    __syncthreads();
+    const int ntask = users * J * FT * 4;
+    for (int w = tid; w < ntask; w += NT) {
+        const int h = w & 3, f = (w >> 2) % FT, task = (w >> 2) / FT;
+        const int u = task / J, s = task % J;
+        const int i = u / K, j = u % K;
+        int lx, ly;
+        if (s == 0) {
+            lx = ly = (i * J + i) * K + j;
+        } else {
+            const int k = s - 1 < i ? s - 1 : s;
+            lx = (k * J + i) * K + j;
+            ly = (k * J + k) * K;
+        }
+        const double2* hx = Hd + (size_t)lx * mn * FT + f;
+        const double2* hy = Hd + (size_t)ly * mn * FT + f;
+        double2 acc[M][M];
+#pragma unroll
+        for (int a = 0; a < M; ++a)
+#pragma unroll
+            for (int b = 0; b < M; ++b) acc[a][b] = make_double2(0.0, 0.0);
+        for (int c = h; c < n; c += 4) {
+            double2 xa[M], yb[M];
+#pragma unroll
+            for (int a = 0; a < M; ++a) {
+                xa[a] = hx[(size_t)(a + M * c) * FT];
+                yb[a] = hy[(size_t)(a + M * c) * FT];
+            }
+#pragma unroll
+            for (int a = 0; a < M; ++a)
+#pragma unroll
+                for (int b = 0; b < M; ++b) cfmac(acc[a][b], xa[a], yb[b]);
+        }
+#pragma unroll
+        for (int a = 0; a < M; ++a)
+#pragma unroll
+            for (int b = 0; b < M; ++b)
+#pragma unroll
+                for (int o = 1; o < 4; o <<= 1) {
+                    acc[a][b].x += __shfl_xor_sync(0xffffffffu, acc[a][b].x, o);
+                    acc[a][b].y += __shfl_xor_sync(0xffffffffu, acc[a][b].y, o);
+                }
+        if (f < nf) {
+            double2* o = PG + (((g * pfs + pf0 + ft0 + f) * users + u) * J + s) * MM;
+#pragma unroll
+            for (int e = 0; e < MM; ++e)
+                if ((e & 3) == h) o[e] = acc[e % M][e / M];
+        }
+    }
+}
+
+template <class T>
+cudaError_t launch_rebuild_pg(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot, int64_t pf0, int64_t pfs,
+                              const void* Cd, const void* G, const double* tau, const double* freqs, const void* coeffs,
+                              double2* PG, cudaStream_t st) {
+    constexpr int FT = 8;
+    if (t.m > 4) return cudaErrorNotSupported;
+    const size_t cs = sizeof(cplx_t<T>);
+    dim3 grid((Fc + FT - 1) / FT, ngroups);
+    cudaError_t e = cudaErrorNotSupported;
+    switch (t.m) {
+#define GWT_RPG(MM)                                                                                                   \
+    case MM: {                                                                                                        \
+        const size_t sm = rg_smem<MM>(t, FT, (int)cs);                                                                \
+        if (sm > 227 * 1024) return cudaErrorNotSupported;                                                            \
+        e = cudaFuncSetAttribute(k_rebuild_pg<T, MM, FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
+        if (e != cudaSuccess) return e;                                                                               \
+        k_rebuild_pg<T, MM, FT><<<grid, 512, sm, st>>>(t, Fc, f0, Ftot, pf0, pfs, (const cplx_t<T>*)Cd,              \
+                                                       (const cplx_t<T>*)G, tau, freqs, (const cplx_t<T>*)coeffs, PG); \
+        return cudaGetLastError();                                                                                    \
+    }
+        GWT_RPG(1) GWT_RPG(2) GWT_RPG(3) GWT_RPG(4)
+#undef GWT_RPG
+    }
+    return e;
+}
+bool rebuild_pg_fits(const Topo& t, size_t csize) {
+    if (t.m > 4) return false;
+    switch (t.m) {
+        case 1: return rg_smem<1>(t, 8, (int)csize) <= 227 * 1024;
+        case 2: return rg_smem<2>(t, 8, (int)csize) <= 227 * 1024;
+        case 3: return rg_smem<3>(t, 8, (int)csize) <= 227 * 1024;
+        default: return rg_smem<4>(t, 8, (int)csize) <= 227 * 1024;
+    }
+}
+template cudaError_t launch_rebuild_pg<float>(const Topo&, int, int, int64_t, int64_t, int64_t, int64_t, const void*,
+                                              const void*, const double*, const double*, const void*, double2*,
+                                              cudaStream_t);
+template cudaError_t launch_rebuild_pg<double>(const Topo&, int, int, int64_t, int64_t, int64_t, int64_t, const void*,
+                                               const void*, const double*, const double*, const void*, double2*,
+                                               cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // K3a: precoder per (group, subcarrier, user): eig of the serving Gram ->
@@ -1077,6 +1376,24 @@ cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64
                            cudaStream_t st) {
     using C = cplx_t<T>;
     constexpr int FT = 16;
+    {
+        constexpr int FTL = 32;
+        const size_t sm = sizeof(C) * ((size_t)t.p * t.m * t.n + (size_t)t.p * t.P + (size_t)t.P * FTL + (size_t)t.p * FTL) +
+                          8 * (size_t)t.P;
+        if (!coeffs && sm <= 200 * 1024 && !std::getenv("GWT_REBUILD_TILED")) {
+            // split the subcarriers so the grid covers >= ~8 CTAs per SM
+            const int64_t base = (int64_t)ngroups * t.links();
+            int nz = (int)std::max<int64_t>(1, std::min<int64_t>((148 * 8 + base - 1) / base, (Fc + 2 * FTL - 1) / (2 * FTL)));
+            int frange = (Fc + nz - 1) / nz;
+            frange = (frange + FTL - 1) / FTL * FTL;
+            nz = (Fc + frange - 1) / frange;
+            cudaError_t e = cudaFuncSetAttribute(k_rebuild_link<T, FTL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return e;
+            dim3 g2(t.links(), ngroups, nz);
+            k_rebuild_link<T, FTL><<<g2, 128, sm, st>>>(t, Fc, f0, Ftot, frange, (const C*)Cd, (const C*)G, tau, freqs, (C*)H);
+            return cudaGetLastError();
+        }
+    }
     dim3 grid((Fc + FT - 1) / FT, t.links(), ngroups);
     const size_t sm = sizeof(C) * (size_t)(t.P + t.p) * FT;
     if (sm > 48 * 1024)
@@ -1091,7 +1408,23 @@ cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroup
                              const void* H, double2* PG, cudaStream_t st) {
     const int64_t items = (int64_t)ngroups * Fc * t.users();
     const int wpb = 4;
-    const size_t sm = sizeof(cplx_t<T>) * (size_t)wpb * (2 * t.J - 1) * t.m * t.n;
+    const size_t smf = sizeof(double2) * (size_t)t.links() * t.m * t.n;
+    if (scope == 1 && smf <= 64 * 1024 && t.m <= 8 && !std::getenv("GWT_PG_STAGED")) {
+        const int thr = (int)std::min<int64_t>(256, ((int64_t)t.users() * t.J * t.m * t.m + 31) / 32 * 32);
+        dim3 grid(Fc, ngroups);
+        cudaError_t e = cudaSuccess;
+        switch (t.m) {
+#define GWT_PGF(MM)                                                                                              \
+    case MM:                                                                                                     \
+        e = cudaFuncSetAttribute(k_pair_gram_gf<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf);  \
+        if (e != cudaSuccess) return e;                                                                          \
+        k_pair_gram_gf<T, MM><<<grid, thr, smf, st>>>(t, Fc, f0, Ftot, (const cplx_t<T>*)H, PG);                 \
+        return cudaGetLastError();
+            GWT_PGF(1) GWT_PGF(2) GWT_PGF(3) GWT_PGF(4) GWT_PGF(5) GWT_PGF(6) GWT_PGF(7) GWT_PGF(8)
+#undef GWT_PGF
+        }
+    }
+    const size_t sm = sizeof(double2) * (size_t)wpb * (2 * t.J - 1) * t.m * t.n;
     if (scope == 1 && sm <= 96 * 1024 && !std::getenv("GWT_PG_UNSTAGED")) {
         cudaError_t e = cudaSuccess;
         switch (t.m) {

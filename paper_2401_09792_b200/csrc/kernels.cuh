@@ -71,6 +71,11 @@ size_t heev_ws_z_elems(int D, int count);
 template <class T> cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
                                               const void* Cd, const void* G, const double* tau, const double* freqs,
                                               const void* coeffs, void* H, cudaStream_t st);
+template <class T> cudaError_t launch_rebuild_pg(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
+                                                 int64_t pf0, int64_t pfs, const void* Cd, const void* G,
+                                                 const double* tau, const double* freqs, const void* coeffs,
+                                                 double2* PG, cudaStream_t st);  // k_sinr.cu, fused K1+K2
+bool rebuild_pg_fits(const Topo& t, size_t csize);
 template <class T> cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroups, int64_t f0,
                                                 int64_t Ftot, const void* H, double2* PG, cudaStream_t st);
 template <class T> cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,

@@ -41,7 +41,10 @@ def main(path, top=30):
         key = (fname, line)
         text[key] = r[1].strip()[:90]
         h = {n: i for i, n in enumerate(header)}
-        s = int(r[h["Warp Stall Sampling (All Samples)"]] or 0)
+        try:
+            s = int(r[h["Warp Stall Sampling (All Samples)"]] or 0)
+        except (ValueError, IndexError):
+            continue  # source text with unescaped quotes breaks the CSV row
         if s == 0:
             continue
         total += s
