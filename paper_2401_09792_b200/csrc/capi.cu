@@ -550,6 +550,78 @@ void validate_sinr(const gwt_topology& tp, const gwt_ranks& r, int scope) {
     if (r.m > 8) invalid("sinr: compressed receive rank m > 8 is not supported by the B200 small-matrix kernel");
 }
 
+// Generic device pipeline (any scope) for ngroups groups on device pointers, on solver/SINR lane
+// `lane` (stream st + its workspace): rebuild -> pair Grams per subcarrier chunk, then ONE eig+MMSE
+// launch per pair-Gram block. timing: per-stage CUDA events (host waits at the end).
+template <class T>
+void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const gwt_topology* topo, int64_t ngroups,
+                 const void* Cd, const void* Gd, const double* taud, const double* fd, const void* cod, int64_t F,
+                 int scope, double* sd, double* sgd, int* std_, bool timing, double& ms_r, double& ms_p, double& ms_s) {
+    using Cx = cplx_t<T>;
+    const size_t cs = sizeof(Cx);
+    const int links = t.links(), users = t.users();
+    const int S = scope == GWT_SCOPE_PAPER ? t.J : t.J * t.K;
+    const char* path = std::getenv("GWT_SINR_PATH");
+    {
+        // generic path (any scope): rebuild -> pair Grams per subcarrier chunk sized so H~ stays resident in
+        // L2 between producer and consumer; then ONE eig+MMSE launch over all subcarriers (full occupancy)
+        const int64_t per_f_h = (int64_t)cs * ngroups * links * t.m * t.n;
+        const char* cb = std::getenv("GWT_SINR_CHUNK_BYTES");
+        // (measured on C2: L2-sized chunks are slower - fewer CTAs per launch - so default to 2 GiB)
+        const int64_t chunk_bytes = cb ? std::atoll(cb) : (int64_t)(2ll << 30);
+        const int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f_h, 1)));
+        const bool rg = scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
+        void* H = rg ? nullptr : ctx->lws(lane, WS_H, cs * ngroups * Fc * links * t.m * t.n);
+        // pair Grams for a block of Fs subcarriers: [g][Fs][users][S][m*m] (fp64), Fs bounded by ~2 GB
+        const int64_t per_f_pg = (int64_t)ngroups * users * (16LL * S * t.m * t.m + 8LL * (((t.L + 1) & ~1) + 2 * t.m * t.L));
+        const int64_t Fs = std::max<int64_t>(Fc, std::min<int64_t>(F, (int64_t)(2ll << 30) / std::max<int64_t>(per_f_pg, 1)) / Fc * Fc);
+        double2* PG = (double2*)ctx->lws(lane, WS_PG, 16 * ngroups * std::min(Fs, F) * users * S * t.m * t.m);
+        double* EG = (double*)ctx->lws(lane, WS_EG, 8 * ngroups * std::min(Fs, F) * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
+        std::vector<cudaEvent_t> evs;
+        auto rec = [&]() {
+            if (!timing) return;
+            cudaEvent_t ev;
+            ck(cudaEventCreate(&ev), "cudaEventCreate");
+            ck(cudaEventRecord(ev, st), "event");
+            evs.push_back(ev);
+        };
+        std::vector<int> kind;  // 0 rebuild, 1 pair gram, 2 small, per interval
+        // rg: paper scope with small groups -> rebuild + pair Grams fused in shared memory (H~ never in HBM)
+        rec();
+        for (int64_t F0 = 0; F0 < F; F0 += Fs) {
+            const int64_t fs = std::min(Fs, F - F0);
+            if (rg) {
+                ctx->launched(launch_rebuild_pg<T>(t, (int)ngroups, (int)fs, F0, F, 0, fs, Cd, Gd, taud, fd, cod, PG, st));
+                rec();
+                kind.push_back(1);
+            }
+            for (int64_t f0 = F0; !rg && f0 < F0 + fs; f0 += Fc) {
+                const int fc = (int)std::min(Fc, F0 + fs - f0);
+                ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
+                rec();
+                kind.push_back(0);
+                ctx->launched(launch_pair_gram<T>(t, scope, S, fc, (int)ngroups, f0 - F0, fs, H, PG, st));
+                rec();
+                kind.push_back(1);
+            }
+            ctx->launched(launch_sinr_small(t, scope, S, ngroups * fs * users, topo->noise_std, (int)fs, F, F0, PG, EG,
+                                            sd, sgd, std_, st),
+                          2);
+            rec();
+            kind.push_back(2);
+        }
+        if (timing) {
+            ck(cudaEventSynchronize(evs.back()), "sync");
+            for (size_t i = 0; i < kind.size(); ++i) {
+                float a = 0;
+                cudaEventElapsedTime(&a, evs[i], evs[i + 1]);
+                (kind[i] == 0 ? ms_r : kind[i] == 1 ? ms_p : ms_s) += a;
+            }
+        }
+        for (auto& ev : evs) cudaEventDestroy(ev);
+    }
+}
+
 template <class T>
 void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups, gwt_mem mem,
                const void* Cf, const void* Gc, const double* tau, const double* freqs, const void* coeffs, int64_t F,
@@ -569,6 +641,66 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     double *sd = sinr, *sgd = signal;
     int* std_ = (int*)status;
     const int64_t out_rows = ngroups * F * users;
+    const char* path0 = std::getenv("GWT_SINR_PATH");
+    const bool fused0 = scope == GWT_SCOPE_PAPER && t.users() <= 128 && path0 && std::strcmp(path0, "fused") == 0;
+    const char* pl = std::getenv("GWT_SINR_PIPELINE");
+    const int64_t nch = std::min<int64_t>(ngroups, pl ? std::max(1, std::atoi(pl)) : 8);
+    if (mem == GWT_MEM_HOST && !fused0 && nch > 1) {
+        // host buffers: group chunks round-robin over 3 stream lanes, each chunk H2D -> device
+        // pipeline -> D2H on its lane, so copies in both directions overlap the other chunks' kernels
+        const int NS = (int)std::min<int64_t>(3, nch);
+        while ((int)ctx->lanes.size() < NS - 1) {
+            gwt_ctx::Lane ln;
+            ck(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking), "cudaStreamCreate");
+            ck(cudaEventCreateWithFlags(&ln.ev, cudaEventDisableTiming), "cudaEventCreate");
+            ctx->lanes.push_back(ln);
+        }
+        auto lane_st = [&](int l) { return l == 0 ? ctx->stream : ctx->lanes[l - 1].st; };
+        ck(cudaEventRecord(ctx->ev[10], ctx->stream), "cudaEventRecord");
+        for (int l = 1; l < NS; ++l) ck(cudaStreamWaitEvent(lane_st(l), ctx->ev[10], 0), "cudaStreamWaitEvent");
+        const int64_t cg = (ngroups + nch - 1) / nch;
+        double dr = 0, dp = 0, ds = 0;
+        for (int64_t c = 0, g0 = 0; g0 < ngroups; ++c, g0 += cg) {
+            const int l = (int)(c % NS);
+            cudaStream_t s2 = lane_st(l);
+            const int64_t G = std::min(cg, ngroups - g0), rows = G * F * users;
+            void* cdv = ctx->lws(l, WS_C, cs * cg * c_g);
+            void* gdv = ctx->lws(l, WS_G, cs * cg * g_g);
+            ck(cudaMemcpyAsync(cdv, (const char*)Cf + cs * g0 * c_g, cs * G * c_g, cudaMemcpyHostToDevice, s2), "H2D C");
+            ck(cudaMemcpyAsync(gdv, (const char*)Gc + cs * g0 * g_g, cs * G * g_g, cudaMemcpyHostToDevice, s2), "H2D G");
+            const void* codv = nullptr;
+            const double *tav = nullptr, *frv = nullptr;
+            if (coeffs) {
+                void* co = ctx->lws(l, WS_COEF, cs * cg * F * links * t.P);
+                ck(cudaMemcpyAsync(co, (const char*)coeffs + cs * g0 * F * links * t.P, cs * G * F * links * t.P,
+                                   cudaMemcpyHostToDevice, s2), "H2D coeffs");
+                codv = co;
+            } else {
+                double* ta = (double*)ctx->lws(l, WS_TAU, 8 * cg * links * t.P);
+                double* fr = (double*)ctx->lws(l, WS_FREQ, 8 * F);
+                ck(cudaMemcpyAsync(ta, tau + g0 * links * t.P, 8 * G * links * t.P, cudaMemcpyHostToDevice, s2), "H2D tau");
+                ck(cudaMemcpyAsync(fr, freqs, 8 * F, cudaMemcpyHostToDevice, s2), "H2D freqs");
+                tav = ta;
+                frv = fr;
+            }
+            double* so = (double*)ctx->lws(l, WS_SINR, 8 * cg * F * users * t.L);
+            double* sg = (double*)ctx->lws(l, WS_SIG, 8 * cg * F * users * t.L);
+            int* stt = (int*)ctx->lws(l, WS_STATUS, 4 * cg * F * users);
+            sinr_device<T>(ctx, l, s2, t, topo, G, cdv, gdv, tav, frv, codv, F, scope, so, sg, stt, false, dr, dp, ds);
+            ck(cudaMemcpyAsync(sinr + g0 * F * users * t.L, so, 8 * rows * t.L, cudaMemcpyDeviceToHost, s2), "D2H sinr");
+            ck(cudaMemcpyAsync(signal + g0 * F * users * t.L, sg, 8 * rows * t.L, cudaMemcpyDeviceToHost, s2), "D2H signal");
+            ck(cudaMemcpyAsync(status + g0 * F * users, stt, 4 * rows, cudaMemcpyDeviceToHost, s2), "D2H status");
+        }
+        for (int l = 1; l < NS; ++l) {
+            ck(cudaEventRecord(ctx->lanes[l - 1].ev, lane_st(l)), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(ctx->stream, ctx->lanes[l - 1].ev, 0), "cudaStreamWaitEvent");
+        }
+        tm.mark(6);
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        std::fill(ctx->stage_ms, ctx->stage_ms + 8, 0.0);
+        ctx->stage_ms[0] = tm.between(0, 6);
+        return;
+    }
     if (mem == GWT_MEM_HOST) {
         tm.mark(4);
         void* c = ctx->ws(WS_C, cs * ngroups * c_g);
@@ -626,59 +758,8 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         ck(cudaEventSynchronize(ctx->ev[9]), "sync");
         ms_r = tm.between(8, 9);
     } else {
-        // generic path (any scope): rebuild -> pair Grams per subcarrier chunk sized so H~ stays resident in
-        // L2 between producer and consumer; then ONE eig+MMSE launch over all subcarriers (full occupancy)
-        const int64_t per_f_h = (int64_t)cs * ngroups * links * t.m * t.n;
-        const char* cb = std::getenv("GWT_SINR_CHUNK_BYTES");
-        // (measured on C2: L2-sized chunks are slower - fewer CTAs per launch - so default to 2 GiB)
-        const int64_t chunk_bytes = cb ? std::atoll(cb) : (int64_t)(2ll << 30);
-        const int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f_h, 1)));
-        const bool rg = scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
-        void* H = rg ? nullptr : ctx->ws(WS_H, cs * ngroups * Fc * links * t.m * t.n);
-        // pair Grams for a block of Fs subcarriers: [g][Fs][users][S][m*m] (fp64), Fs bounded by ~2 GB
-        const int64_t per_f_pg = (int64_t)ngroups * users * (16LL * S * t.m * t.m + 8LL * (((t.L + 1) & ~1) + 2 * t.m * t.L));
-        const int64_t Fs = std::max<int64_t>(Fc, std::min<int64_t>(F, (int64_t)(2ll << 30) / std::max<int64_t>(per_f_pg, 1)) / Fc * Fc);
-        double2* PG = (double2*)ctx->ws(WS_PG, 16 * ngroups * std::min(Fs, F) * users * S * t.m * t.m);
-        double* EG = (double*)ctx->ws(WS_EG, 8 * ngroups * std::min(Fs, F) * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
-        std::vector<cudaEvent_t> evs;
-        auto rec = [&]() {
-            cudaEvent_t ev;
-            ck(cudaEventCreate(&ev), "cudaEventCreate");
-            ck(cudaEventRecord(ev, st), "event");
-            evs.push_back(ev);
-        };
-        std::vector<int> kind;  // 0 rebuild, 1 pair gram, 2 small, per interval
-        // rg: paper scope with small groups -> rebuild + pair Grams fused in shared memory (H~ never in HBM)
-        rec();
-        for (int64_t F0 = 0; F0 < F; F0 += Fs) {
-            const int64_t fs = std::min(Fs, F - F0);
-            if (rg) {
-                ctx->launched(launch_rebuild_pg<T>(t, (int)ngroups, (int)fs, F0, F, 0, fs, Cd, Gd, taud, fd, cod, PG, st));
-                rec();
-                kind.push_back(1);
-            }
-            for (int64_t f0 = F0; !rg && f0 < F0 + fs; f0 += Fc) {
-                const int fc = (int)std::min(Fc, F0 + fs - f0);
-                ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
-                rec();
-                kind.push_back(0);
-                ctx->launched(launch_pair_gram<T>(t, scope, S, fc, (int)ngroups, f0 - F0, fs, H, PG, st));
-                rec();
-                kind.push_back(1);
-            }
-            ctx->launched(launch_sinr_small(t, scope, S, ngroups * fs * users, topo->noise_std, (int)fs, F, F0, PG, EG,
-                                            sd, sgd, std_, st),
-                          2);
-            rec();
-            kind.push_back(2);
-        }
-        ck(cudaEventSynchronize(evs.back()), "sync");
-        for (size_t i = 0; i < kind.size(); ++i) {
-            float a = 0;
-            cudaEventElapsedTime(&a, evs[i], evs[i + 1]);
-            (kind[i] == 0 ? ms_r : kind[i] == 1 ? ms_p : ms_s) += a;
-        }
-        for (auto& ev : evs) cudaEventDestroy(ev);
+        sinr_device<T>(ctx, 0, st, t, topo, ngroups, Cd, Gd, taud, fd, cod, F, scope, sd, sgd, std_, true, ms_r, ms_p,
+                       ms_s);
     }
     if (mem == GWT_MEM_HOST) {
         tm.mark(12);

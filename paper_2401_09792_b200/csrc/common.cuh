@@ -65,6 +65,18 @@ __device__ __forceinline__ double2 phasor_neg(double f, double tau) {
     return make_double2(c, -s);
 }
 
+// conj(c_r(f)) for subcarrier index fa: binary64 argument reduction, then sincospi in the
+// working precision (fp32 for c64: |error| ~1e-7 rad; fp64 for c128)
+template <class T> __device__ __forceinline__ cplx_t<T> conj_coeff(double f, double tau);
+template <> __device__ __forceinline__ float2 conj_coeff<float>(double f, double tau) {
+    double x = f * tau;
+    x -= floor(x);
+    float s, c;
+    sincospif(2.0f * (float)x, &s, &c);
+    return make_float2(c, -s);
+}
+template <> __device__ __forceinline__ double2 conj_coeff<double>(double f, double tau) { return phasor_neg(f, tau); }
+
 // Topology helpers shared by the kernels: link = (k*J + i)*K + j, user = i*K + j.
 struct Topo {
     int J, K, M, N, P, m, n, p, L;

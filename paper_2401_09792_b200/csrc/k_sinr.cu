@@ -26,17 +26,6 @@
 
 namespace gwtk {
 
-// conj(c_r(f)) for subcarrier index fa: binary64 argument reduction, then sincospi in the
-// working precision (fp32 for c64: |error| ~1e-7 rad; fp64 for c128)
-template <class T> __device__ __forceinline__ cplx_t<T> conj_coeff(double f, double tau);
-template <> __device__ __forceinline__ float2 conj_coeff<float>(double f, double tau) {
-    double x = f * tau;
-    x -= floor(x);
-    float s, c;
-    sincospif(2.0f * (float)x, &s, &c);
-    return make_float2(c, -s);
-}
-template <> __device__ __forceinline__ double2 conj_coeff<double>(double f, double tau) { return phasor_neg(f, tau); }
 
 // ---------------------------------------------------------------------------
 // K1: rebuild H~(f) = sum_q G(:,:,q) * E[q][f],
@@ -1376,6 +1365,13 @@ cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64
                            cudaStream_t st) {
     using C = cplx_t<T>;
     constexpr int FT = 16;
+    const char* rtc = std::getenv("GWT_REBUILD_TC");
+    if (sizeof(T) == 4 && !coeffs && rtc && std::atoi(rtc) != 0) {
+        // tensor-core rebuild (k_tc.cu, opt-in) when the shape fits; else the CUDA-core kernels below
+        cudaError_t e = launch_rebuild_tc(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
     {
         constexpr int FTL = 32;
         const size_t sm = sizeof(C) * ((size_t)t.p * t.m * t.n + (size_t)t.p * t.P + (size_t)t.P * FTL + (size_t)t.p * FTL) +

@@ -61,6 +61,8 @@ template <class T> cudaError_t launch_broadcast(const void* src, void* dst, int6
                                                 cudaStream_t st);
 cudaError_t launch_gram_tc(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V,
                            void* out, cudaStream_t st);  // k_tc.cu (c64, 3xTF32 tcgen05)
+cudaError_t launch_rebuild_tc(const Topo& t, int ngroups, int Fc, int64_t f0, const void* Cd, const void* G,
+                              const double* tau, const double* freqs, void* H, cudaStream_t st);  // k_tc.cu
 // k_eig.cu
 template <class T> cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, void* out,
                                                 double* evals, double2* ws_a, double* ws_z, double2* ws_x, int* fail,
