@@ -346,9 +346,11 @@ def main():
     d2h = rep_h.sinr.numel() * 8 * 2 + rep_h.status.numel() * 4
     # Tucker e2e: host X in, factors out
     Xpin = torch.from_numpy(Xh).pin_memory()
+    fac_h = ctx_h.groupwise_solve(topo, Xpin, ranks, cfg.sweeps, early_stop=False)  # warm (workspaces, pinned outs)
     t0 = time.perf_counter()
-    fac_h = ctx_h.groupwise_solve(topo, Xpin, ranks, cfg.sweeps, early_stop=False)
-    tuck_e2e_ms = (time.perf_counter() - t0) * 1e3
+    for _ in range(2):
+        fac_h = ctx_h.groupwise_solve(topo, Xpin, ranks, cfg.sweeps, early_stop=False)
+    tuck_e2e_ms = (time.perf_counter() - t0) * 1e3 / 2
     ctx_h.close()
 
     # ---------------- roofline of the dominant SINR kernel (binding resource), all stages listed
@@ -357,7 +359,7 @@ def main():
     peaks_t = {"fp32": 148 * 128 * 2 * clk_max * 1e6 / 1e12, "fp64": 148 * 64 * 2 * clk_max * 1e6 / 1e12}
     costs = sinr_costs(cfg, cs)
     stage = {"rebuild": st_acc[4], "pair_gram": st_acc[5], "small": st_acc[6]}
-    kern = {"rebuild": "k_rebuild", "pair_gram": "k_pair_gram", "small": "k_precoder_eig+k_mmse"}
+    kern = {"rebuild": "k_rebuild_link", "pair_gram": "k_pair_gram_gf", "small": "k_precoder_eig+k_mmse"}
     per_stage = {}
     for k_, ms_k in stage.items():
         fl, pipe, by = costs[k_]

@@ -311,33 +311,100 @@ __global__ void __launch_bounds__(128) k_pair_gram_staged(Topo t, int Fc, int64_
     }
 }
 
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// K2 (paper scope, c64), persistent and double-buffered: each CTA walks (group, subcarrier) slices
+// with stride gridDim.x; slice it+1's H~(f) block (contiguous links*m*n complex64) is fetched with
+// cp.async into a raw buffer while slice it is converted once to binary64 and reduced into the J
+// pair Grams of every user (one thread per Gram entry).
+template <int M>
+__global__ void __launch_bounds__(256) k_pair_gram_pipe(Topo t, int Fc, int64_t f0, int64_t Ftot, int64_t nslices,
+                                                        const float2* __restrict__ H, double2* __restrict__ PG) {
+    constexpr int MM = M * M;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int J = t.J, K = t.K, links = t.links(), users = t.users();
+    const int n = t.n, mn = M * n, tot = links * mn;  // complex elements per slice (tot % 2 == 0 checked)
+    float2* raw[2] = {reinterpret_cast<float2*>(smem_raw), reinterpret_cast<float2*>(smem_raw) + tot};
+    double2* sh = reinterpret_cast<double2*>(smem_raw + 2 * (size_t)tot * sizeof(float2));
+    const int nchunk = tot / 2;  // 16-byte chunks per slice
+    auto fetch = [&](int64_t sl, float2* dst) {
+        if (sl < nslices) {
+            const float2* src = H + sl * (int64_t)tot;  // slice = g * Fc + f (H~ layout [g][Fc][links][mn])
+            for (int c = threadIdx.x; c < nchunk; c += blockDim.x) cp_async16(dst + 2 * c, src + 2 * c);
+        }
+        cp_async_commit();
+    };
+    int64_t sl = blockIdx.x;
+    fetch(sl, raw[0]);
+    for (int it = 0; sl < nslices; ++it, sl += gridDim.x) {
+        fetch(sl + gridDim.x, raw[(it + 1) & 1]);
+        cp_async_wait1();
+        __syncthreads();
+        const float2* r = raw[it & 1];
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) sh[e] = make_double2(r[e].x, r[e].y);
+        __syncthreads();
+        const int64_t g = sl / Fc, f = sl % Fc;
+        const int64_t orow0 = (g * Ftot + f0 + f) * users;
+        for (int e = threadIdx.x; e < users * J * MM; e += blockDim.x) {
+            const int u = e / (J * MM), s = (e / MM) % J, ab = e % MM, a = ab % M, b = ab / M;
+            const int i = u / K, j = u % K;
+            int lx, ly;
+            if (s == 0) {
+                lx = ly = (i * J + i) * K + j;
+            } else {
+                const int k = s - 1 < i ? s - 1 : s;
+                lx = (k * J + i) * K + j;
+                ly = (k * J + k) * K;
+            }
+            const double2* h1 = sh + (size_t)lx * mn + a;
+            const double2* h2 = sh + (size_t)ly * mn + b;
+            double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+            int c = 0;
+            for (; c + 1 < n; c += 2) {
+                cfmac(acc0, h1[M * c], h2[M * c]);
+                cfmac(acc1, h1[M * (c + 1)], h2[M * (c + 1)]);
+            }
+            if (c < n) cfmac(acc0, h1[M * c], h2[M * c]);
+            PG[((orow0 + u) * J + s) * MM + ab] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
+        }
+        __syncthreads();  // sh and raw[it&1] reused by the next iterations
+    }
+}
+
 // K2 (paper scope, whole subcarrier): one CTA per (group, subcarrier) stages every link of that
 // H~(f) (one contiguous links*m*n block, 16-byte vector loads, converted to binary64 once) and
 // computes all users' J pair Grams, one thread per Gram entry. No partner link is read twice.
 template <class T, int M>
-__global__ void __launch_bounds__(256) k_pair_gram_gf(Topo t, int Fc, int64_t f0, int64_t Ftot,
+__global__ void __launch_bounds__(256) k_pair_gram_gf(Topo t, int Fc, int64_t f0, int64_t Ftot, int LS,
                                                       const cplx_t<T>* __restrict__ H, double2* __restrict__ PG) {
+    // LS: padded per-link stride (LS % 8 == 4) so the two Gram tasks of a warp, which read different
+    // links at the same offsets, hit disjoint shared-memory banks
     using C = cplx_t<T>;
     constexpr int MM = M * M;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* sh = reinterpret_cast<double2*>(smem_raw);  // [links][mn]
+    double2* sh = reinterpret_cast<double2*>(smem_raw);  // [links][LS]
     const int J = t.J, K = t.K, links = t.links(), users = t.users();
     const int n = t.n, mn = M * n;
     const int f = blockIdx.x;
     const int64_t g = blockIdx.y;
     const C* Hf = H + ((g * Fc + f) * links) * (int64_t)mn;
     const int tot = links * mn;
-    if constexpr (sizeof(C) == 8) {
-        const float4* h4 = reinterpret_cast<const float4*>(Hf);  // mn even for m*n even; else scalar tail
+    if (sizeof(C) == 8 && (mn % 2) == 0) {
+        const float4* h4 = reinterpret_cast<const float4*>(Hf);
         const int n4 = tot / 2;
         for (int e = threadIdx.x; e < n4; e += blockDim.x) {
             const float4 v = h4[e];
-            sh[2 * e] = make_double2(v.x, v.y);
-            sh[2 * e + 1] = make_double2(v.z, v.w);
+            const int l = (2 * e) / mn, r = (2 * e) % mn;
+            sh[l * LS + r] = make_double2(v.x, v.y);
+            sh[l * LS + r + 1] = make_double2(v.z, v.w);
         }
-        if ((tot & 1) && threadIdx.x == 0) sh[tot - 1] = to_d2(Hf[tot - 1]);
     } else {
-        for (int e = threadIdx.x; e < tot; e += blockDim.x) sh[e] = to_d2(Hf[e]);
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) sh[(e / mn) * LS + e % mn] = to_d2(Hf[e]);
     }
     __syncthreads();
     const int64_t orow0 = (g * Ftot + f0 + f) * users;
@@ -352,8 +419,8 @@ __global__ void __launch_bounds__(256) k_pair_gram_gf(Topo t, int Fc, int64_t f0
             lx = (k * J + i) * K + j;
             ly = (k * J + k) * K;
         }
-        const double2* h1 = sh + (size_t)lx * mn + a;
-        const double2* h2 = sh + (size_t)ly * mn + b;
+        const double2* h1 = sh + (size_t)lx * LS + a;
+        const double2* h2 = sh + (size_t)ly * LS + b;
         double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
         int c = 0;
         for (; c + 1 < n; c += 2) {
@@ -1405,16 +1472,38 @@ cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroup
     const int64_t items = (int64_t)ngroups * Fc * t.users();
     const int wpb = 4;
     const size_t smf = sizeof(double2) * (size_t)t.links() * t.m * t.n;
+    if (sizeof(T) == 4 && scope == 1 && smf <= 48 * 1024 && t.m <= 8 && ((t.links() * t.m * t.n) % 2 == 0) &&
+        std::getenv("GWT_PG_PIPE")) {
+        const size_t sm = 2 * smf;  // two raw complex64 buffers + one binary64 buffer
+        const int64_t nsl = (int64_t)ngroups * Fc;
+        const int thr = (int)std::min<int64_t>(256, ((int64_t)t.users() * t.J * t.m * t.m + 31) / 32 * 32);
+        int per_sm = 0;
+        cudaError_t e = cudaSuccess;
+        switch (t.m) {
+#define GWT_PGP(MM)                                                                                               \
+    case MM:                                                                                                      \
+        e = cudaFuncSetAttribute(k_pair_gram_pipe<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
+        if (e != cudaSuccess) return e;                                                                           \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pair_gram_pipe<MM>, thr, sm);                   \
+        k_pair_gram_pipe<MM><<<(unsigned)std::min<int64_t>(nsl, 148 * std::max(per_sm, 1)), thr, sm, st>>>(       \
+            t, Fc, f0, Ftot, nsl, (const float2*)H, PG);                                                          \
+        return cudaGetLastError();
+            GWT_PGP(1) GWT_PGP(2) GWT_PGP(3) GWT_PGP(4) GWT_PGP(5) GWT_PGP(6) GWT_PGP(7) GWT_PGP(8)
+#undef GWT_PGP
+        }
+    }
     if (scope == 1 && smf <= 64 * 1024 && t.m <= 8 && !std::getenv("GWT_PG_STAGED")) {
+        const int mn = t.m * t.n, LS = mn + ((4 - mn % 8) + 8) % 8;
+        const size_t smp = sizeof(double2) * (size_t)t.links() * LS;
         const int thr = (int)std::min<int64_t>(256, ((int64_t)t.users() * t.J * t.m * t.m + 31) / 32 * 32);
         dim3 grid(Fc, ngroups);
         cudaError_t e = cudaSuccess;
         switch (t.m) {
 #define GWT_PGF(MM)                                                                                              \
     case MM:                                                                                                     \
-        e = cudaFuncSetAttribute(k_pair_gram_gf<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf);  \
+        e = cudaFuncSetAttribute(k_pair_gram_gf<T, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);  \
         if (e != cudaSuccess) return e;                                                                          \
-        k_pair_gram_gf<T, MM><<<grid, thr, smf, st>>>(t, Fc, f0, Ftot, (const cplx_t<T>*)H, PG);                 \
+        k_pair_gram_gf<T, MM><<<grid, thr, smp, st>>>(t, Fc, f0, Ftot, LS, (const cplx_t<T>*)H, PG);             \
         return cudaGetLastError();
             GWT_PGF(1) GWT_PGF(2) GWT_PGF(3) GWT_PGF(4) GWT_PGF(5) GWT_PGF(6) GWT_PGF(7) GWT_PGF(8)
 #undef GWT_PGF
