@@ -797,6 +797,306 @@ __global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t 
 }
 
 // ---------------------------------------------------------------------------
+// K3 for m > 4 (C3/C4: m = 8): one CTA per SPC (group, subcarrier) slices, 8 lanes per user
+// (lane = matrix column), all matrices in fp64.
+//  a) precoder: parallel cyclic Jacobi on the serving Gram (round-robin pairing, 7 rounds of 4
+//     disjoint rotations per sweep; the rotation of jacobi_herm / the reference test oracle),
+//     columns exchanged between partner lanes by shuffles; eigenpairs ranked and kept in smem.
+//  b) MMSE: lane j builds column j of Q (partners' precoders read from smem), right-looking
+//     Cholesky with the reference's PD / condition / finite checks, one lane per stream solves
+//     L y = u_r for gamma_r.
+template <class V>
+__device__ __forceinline__ V sel8(const V (&a)[8], int i) {
+    V r = a[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k)
+        if (k == i) r = a[k];
+    return r;
+}
+__device__ __forceinline__ double2 shfl_d2(double2 v, int src) {
+    return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__host__ __device__ constexpr int rr_partner(int i, int r) {  // round-robin pairing of 8 indices, round r < 7
+    return i == 7 ? r : (i == r ? 7 : ((2 * r - i) % 7 + 7) % 7);
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) k_small_grp(Topo t, int scope, int S, int64_t nslices, int spc, double sigma,
+                                                   int fc, int64_t Ftot, int64_t f0, const double2* __restrict__ PG,
+                                                   double* __restrict__ sinr, double* __restrict__ signal,
+                                                   int* __restrict__ status) {
+    constexpr int MM = M * M;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int users = t.users(), L = t.L;
+    const int tid = threadIdx.x, lane = tid & 31, j = tid & 7, base = lane & ~7;
+    const int sl_local = tid / (users * 8), u = (tid / 8) % users;
+    const int64_t sl = (int64_t)blockIdx.x * spc + sl_local;
+    // per slice: U [users][8][8] double2, L-factor scratch [users][8][8] double2, lambda [users][8]
+    const size_t per_slice = (size_t)users * (64 * 16 * 2 + 8 * 8);
+    double2* sU = reinterpret_cast<double2*>(smem_raw + sl_local * per_slice);
+    double2* sL = sU + (size_t)users * 64;
+    double* slam = reinterpret_cast<double*>(sL + (size_t)users * 64);
+    const bool valid = sl_local < spc && sl < nslices;
+    const int64_t item = (sl < nslices ? sl : 0) * users + u;
+    const int i_cell = u / t.K, j_user = u % t.K;
+    // ---- a) precoder eig of the serving Gram (symmetrised), lane j holds column j
+    double2 acol[8], vcol[8];
+    {
+        const int ss = serving_slot(t, scope, i_cell, j_user);
+        const double2* src = PG + (item * S + ss) * MM;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            double2 a = make_double2(0.0, 0.0);
+            if (valid && i < M && j < M) {
+                const double2 x = src[i + M * j], y = src[j + M * i];
+                a = make_double2(0.5 * (x.x + y.x), 0.5 * (x.y - y.y));
+                if (i == j) a.y = 0.0;
+            }
+            acol[i] = a;
+            vcol[i] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+        }
+    }
+    for (int sweep = 0; sweep < 32; ++sweep) {
+        double off = 0.0, dia = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (i < j) off += acol[i].x * acol[i].x + acol[i].y * acol[i].y;
+            if (i == j) dia += acol[i].x * acol[i].x;
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            off += __shfl_xor_sync(0xffffffffu, off, o);
+            dia += __shfl_xor_sync(0xffffffffu, dia, o);
+        }
+        const bool conv = off <= kJacobiTol * dia || off == 0.0;
+        if (__all_sync(0xffffffffu, conv)) break;
+#pragma unroll
+        for (int r = 0; r < 7; ++r) {
+            const int q = rr_partner(j, r);
+            const bool lead = j < q;
+            double2 pc[8], pv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                pc[i] = shfl_d2(acol[i], base + q);
+                pv[i] = shfl_d2(vcol[i], base + q);
+            }
+            // rotation parameters from the leader's column and the other lane's diagonal
+            const double2 app = lead ? sel8(acol, j) : sel8(pc, q);
+            const double2 aqq = lead ? sel8(pc, q) : sel8(acol, j);
+            const double2 aqp = lead ? sel8(acol, q) : sel8(pc, j);  // A[q][p] of the leader's column
+            const double2 apq = make_double2(aqp.x, -aqp.y);
+            double c = 1.0, sn = 0.0, phr = 1.0, phi = 0.0;
+            const double b2 = apq.x * apq.x + apq.y * apq.y;
+            if (b2 > 1e-300) {
+                const double rb = rsqrt(b2);
+                phr = apq.x * rb;
+                phi = apq.y * rb;
+                const float tau = (float)((aqq.x - app.x) * (0.5 * rb));
+                const float tf = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 1.0f)));
+                const double tt = (double)tf;
+                c = rsqrt(fma(tt, tt, 1.0));
+                sn = tt * c;
+            }
+            const double2 uqp = make_double2(-sn * phr, sn * phi), uqq = make_double2(c * phr, -c * phi);
+            // A <- A U and V <- V U: columns p (leader) and q
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double2 na, nv;
+                if (lead) {
+                    na = make_double2(c * acol[i].x, c * acol[i].y);
+                    cfma(na, pc[i], uqp);
+                    nv = make_double2(c * vcol[i].x, c * vcol[i].y);
+                    cfma(nv, pv[i], uqp);
+                } else {
+                    na = make_double2(sn * pc[i].x, sn * pc[i].y);
+                    cfma(na, acol[i], uqq);
+                    nv = make_double2(sn * pv[i].x, sn * pv[i].y);
+                    cfma(nv, vcol[i], uqq);
+                }
+                acol[i] = na;
+                vcol[i] = nv;
+            }
+            // A <- U^H A: rows p, q of my column for every pair of this round (parameters from leaders)
+#pragma unroll
+            for (int pp = 0; pp < 8; ++pp) {
+                const int qq = rr_partner(pp, r);
+                if (pp < qq) {
+                    const double cl = __shfl_sync(0xffffffffu, c, base + pp);
+                    const double sl2 = __shfl_sync(0xffffffffu, sn, base + pp);
+                    const double pr = __shfl_sync(0xffffffffu, phr, base + pp);
+                    const double pi = __shfl_sync(0xffffffffu, phi, base + pp);
+                    const double2 up = make_double2(-sl2 * pr, sl2 * pi), uq = make_double2(cl * pr, -cl * pi);
+                    const double2 apc = acol[pp], aqc = acol[qq];
+                    double2 np = make_double2(cl * apc.x, cl * apc.y);
+                    cfmaconj(np, up, aqc);
+                    double2 nq = make_double2(sl2 * apc.x, sl2 * apc.y);
+                    cfmaconj(nq, uq, aqc);
+                    acol[pp] = np;
+                    acol[qq] = nq;
+                }
+            }
+        }
+    }
+    // rank eigenvalues (descending, lower index first on ties) and keep the top L
+    {
+        const double lam = sel8(acol, j).x;
+        int rank = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double lk = __shfl_sync(0xffffffffu, lam, base + k);
+            if (k < M && j < M) rank += (lk > lam || (lk == lam && k < j)) ? 1 : 0;
+        }
+        if (valid && j < M && rank < L) {
+            slam[u * 8 + rank] = fmax(lam, 0.0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sU[(u * 8 + rank) * 8 + i] = vcol[i];
+        }
+    }
+    __syncthreads();
+    // ---- b) covariance column j, Cholesky, per-stream gamma
+    int st = 0;
+    const double s2 = sigma * sigma;
+    double2 qcol[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qcol[i] = make_double2(i == j ? s2 : 0.0, 0.0);
+    if (valid && j < M) {
+        for (int r = 0; r < L; ++r) {
+            const double lr = slam[u * 8 + r];
+            const double2* ur = sU + (u * 8 + r) * 8;
+            const double2 uj = ur[j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double2 v = make_double2(0.0, 0.0);
+                cfmac(v, ur[i], uj);
+                qcol[i].x += lr * v.x;
+                qcol[i].y += lr * v.y;
+            }
+        }
+    }
+    const int ss = serving_slot(t, scope, i_cell, j_user);
+    for (int s = 0; s < S; ++s) {
+        if (s == ss) continue;
+        int k, l;
+        scope_slot(t, scope, i_cell, j_user, s, k, l);
+        const int pu = k * t.K + l;
+        double2 xrow[8];
+        const double2* X = PG + (item * S + s) * MM;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) xrow[b] = (valid && j < M && b < M) ? X[j + M * b] : make_double2(0.0, 0.0);
+        for (int r = 0; r < L; ++r) {  // warp-uniform trip count: every lane reaches the shuffles
+            const double lr = valid ? slam[pu * 8 + r] : 1.0;
+            const bool ok = lr > 0.0;
+            if (!ok) st = st ? st : 5;
+            const double sc = ok ? 1.0 / sqrt(lr) : 0.0;
+            const double2* ur = sU + (pu * 8 + r) * 8;
+            double2 zj = make_double2(0.0, 0.0);
+            if (valid && ok) {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) cfma(zj, xrow[b], ur[b]);
+            }
+            zj = make_double2(zj.x * sc, zj.y * sc);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double2 zi = shfl_d2(zj, base + i);
+                cfmac(qcol[i], zi, zj);
+            }
+        }
+    }
+    // non-finite check over the item's Q (check_finite(q, "woodbury_inverse_apply"))
+    bool finite;
+    {
+        bool fin = true;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) fin = fin && isfinite(qcol[i].x) && isfinite(qcol[i].y);
+        const unsigned bad = __ballot_sync(0xffffffffu, !fin);
+        finite = ((bad >> base) & 0xffu) == 0u;
+    }
+    // right-looking Cholesky (Eigen::LLT semantics: d_c = Q_cc - sum_k |L_ck|^2 > 0), lane = column
+    bool pd = finite;
+    double dmax = 0.0, dmin = 1e308;
+#pragma unroll
+    for (int kc = 0; kc < M; ++kc) {
+        double dh = 0.0;
+        if (j == kc) {
+            dh = qcol[kc].x;
+            const double lkk = sqrt(fmax(dh, 1e-300));
+            qcol[kc] = make_double2(lkk, 0.0);
+            const double inv = 1.0 / lkk;
+#pragma unroll
+            for (int i = kc + 1; i < 8; ++i) qcol[i] = make_double2(qcol[i].x * inv, qcol[i].y * inv);
+        }
+        const double d = __shfl_sync(0xffffffffu, dh, base + kc);
+        double2 lk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) lk[i] = shfl_d2(qcol[i], base + kc);
+        pd = pd && (d > 0.0);
+        dmax = fmax(dmax, lk[kc].x);
+        dmin = fmin(dmin, lk[kc].x);
+        if (j > kc && j < M) {
+            const double2 ljv = sel8(lk, j);  // L[j][kc]
+#pragma unroll
+            for (int i = kc + 1; i < 8; ++i) {
+                if (i >= j) {  // Q[i][j] -= L[i][kc] conj(L[j][kc])
+                    qcol[i].x -= lk[i].x * ljv.x + lk[i].y * ljv.y;
+                    qcol[i].y -= lk[i].y * ljv.x - lk[i].x * ljv.y;
+                }
+            }
+        }
+    }
+    if (valid && j < M)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sL[(u * 8 + j) * 8 + i] = qcol[i];  // column j of L
+    __syncwarp();
+    if (!finite) st = 4;
+    else if (!pd) st = 1;
+    else if ((dmax / dmin) * (dmax / dmin) > 1e14) st = 2;
+    const int64_t gf = item / users;
+    const int64_t g = gf / fc, fl = gf % fc;
+    const int64_t orow = (g * Ftot + f0 + fl) * users + u;
+    if (valid && j < L) {
+        const int r = j;
+        double gamma = 0.0;
+        const double lr = slam[u * 8 + r];
+        if (st != 1 && st != 2 && st != 4) {
+            const double2* ur = sU + (u * 8 + r) * 8;
+            double2 y[8];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                if (a < M) {
+                    double2 acc = ur[a];
+#pragma unroll
+                    for (int k2 = 0; k2 < a; ++k2) {
+                        double2 pr = make_double2(0, 0);
+                        cfma(pr, sL[(u * 8 + k2) * 8 + a], y[k2]);
+                        acc.x -= pr.x;
+                        acc.y -= pr.y;
+                    }
+                    const double laa = sL[(u * 8 + a) * 8 + a].x;
+                    y[a] = make_double2(acc.x / laa, acc.y / laa);
+                } else {
+                    y[a] = make_double2(0.0, 0.0);
+                }
+            }
+            double nn = 0.0;
+#pragma unroll
+            for (int a = 0; a < 8; ++a) nn += y[a].x * y[a].x + y[a].y * y[a].y;
+            gamma = lr * nn;
+        }
+        const double sp = gamma * gamma;
+        double den = gamma * (1.0 - gamma);
+        if (den <= -1e-12 && st == 0) st = 3;
+        den = fmax(den, 2.2250738585072014e-308);
+        sinr[orow * L + r] = sp / den;
+        signal[orow * L + r] = sp;
+    }
+    // status: lanes agree on 5/4/1/2; a negative denominator (3) can come from any stream lane
+    {
+        const unsigned any3 = __ballot_sync(0xffffffffu, st == 3);
+        if (valid && j == 0) status[orow] = (st == 0 && ((any3 >> base) & 0xffu)) ? 3 : st;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Fused compressed-SINR path (paper_experiment scope), two kernels:
 //  k_rebuild_gram: one CTA per (group, user batch, subcarrier tile). H~ is
 //    rebuilt tile by tile into shared memory and consumed there: per user the
@@ -1542,9 +1842,40 @@ static cudaError_t launch_small_m(const Topo& t, int scope, int S, int64_t items
     return cudaGetLastError();
 }
 
+template <int M>
+static cudaError_t launch_small_grp(const Topo& t, int scope, int S, int64_t items, double sigma, int fc,
+                                    int64_t Ftot, int64_t f0, const double2* PG, double* sinr, double* signal,
+                                    int* status, cudaStream_t st) {
+    const int users = t.users();
+    const int64_t nsl = items / users;
+    const int spc = std::max(1, 128 / (users * 8));
+    const size_t per_slice = (size_t)users * (64 * 16 * 2 + 8 * 8);
+    const size_t sm = per_slice * spc;
+    cudaError_t e = cudaFuncSetAttribute(k_small_grp<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_small_grp<M><<<(unsigned)((nsl + spc - 1) / spc), users * 8 * spc, sm, st>>>(t, scope, S, nsl, spc, sigma, fc,
+                                                                                   Ftot, f0, PG, sinr, signal, status);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sinr_small(const Topo& t, int scope, int S, int64_t items, double sigma, int fc, int64_t Ftot,
                               int64_t f0, const double2* PG, double* EG, double* sinr, double* signal, int* status,
                               cudaStream_t st) {
+    const char* grp = std::getenv("GWT_SMALL_GRP");  // 1: force the 8-lanes-per-user kernel, 0: never
+    const bool use_grp = t.users() * 8 <= 256 && (grp ? std::atoi(grp) != 0 : t.m > 4);
+    if (use_grp) {
+        switch (t.m) {
+            case 1: return launch_small_grp<1>(t, scope, S, items, sigma, fc, Ftot, f0, PG, sinr, signal, status, st);
+            case 2: return launch_small_grp<2>(t, scope, S, items, sigma, fc, Ftot, f0, PG, sinr, signal, status, st);
+            case 3: return launch_small_grp<3>(t, scope, S, items, sigma, fc, Ftot, f0, PG, sinr, signal, status, st);
+            case 4: return launch_small_grp<4>(t, scope, S, items, sigma, fc, Ftot, f0, PG, sinr, signal, status, st);
+            case 5: return launch_small_grp<5>(t, scope, S, items, sigma, fc, Ftot, f0, PG, sinr, signal, status, st);
+            case 6: return launch_small_grp<6>(t, scope, S, items, sigma, fc, Ftot, f0, PG, sinr, signal, status, st);
+            case 7: return launch_small_grp<7>(t, scope, S, items, sigma, fc, Ftot, f0, PG, sinr, signal, status, st);
+            case 8: return launch_small_grp<8>(t, scope, S, items, sigma, fc, Ftot, f0, PG, sinr, signal, status, st);
+            default: break;
+        }
+    }
     switch (t.m) {
         case 1: return launch_small_m<1>(t, scope, S, items, sigma, fc, Ftot, f0, PG, EG, sinr, signal, status, st);
         case 2: return launch_small_m<2>(t, scope, S, items, sigma, fc, Ftot, f0, PG, EG, sinr, signal, status, st);

@@ -6,6 +6,10 @@
 
 namespace gwtk {
 
+// Jacobi stop: sum_{p<q} |a_pq|^2 <= tol * sum_p a_pp^2. 1e-22 leaves eigenvector errors ~1e-11/gap
+// (the c128 SINR parity bound is 1e-9); 1e-30 (full convergence) costs ~1-2 extra sweeps.
+constexpr double kJacobiTol = 1e-22;
+
 // ---------------------------------------------------------------------------
 // Per-thread small Hermitian eigensolver (cyclic complex Jacobi, fp64), the
 // rotation of the reference test oracle (proj/tests/support/oracles.hpp:31-97).
@@ -23,7 +27,7 @@ __device__ __forceinline__ void jacobi_herm(double2 (&A)[M][M], double2 (&V)[M][
 #pragma unroll
             for (int q = p + 1; q < M; ++q) off += A[p][q].x * A[p][q].x + A[p][q].y * A[p][q].y;
         }
-        if (off <= 1e-30 * dia || off == 0.0) break;
+        if (off <= kJacobiTol * dia || off == 0.0) break;
 #pragma unroll
         for (int p = 0; p < M; ++p)
 #pragma unroll
