@@ -1,0 +1,471 @@
+// CTA-per-matrix Hermitian top-k eigensolver for 128 < D <= 256 in fp32 (c64 Grams, e.g. the C4
+// transmit factor, N = 256). Included by k_eig.cu (inside namespace gwtk) after eig_cta.cuh.
+//
+// Same algorithm and conventions as k_heev_cr (reference leading_eigenvectors,
+// proj/src/linalg.cpp:27-45 + phase_normalize_columns :11-25). The 256x256 complex64 matrix
+// (512 KB) does not fit in shared memory, so it lives in the per-matrix global workspace where
+// it stays L2-resident (148 concurrent matrices = 76 MB of the 126 MB L2); everything on the
+// serial chains is in shared memory or registers:
+//  1. Householder, 512 threads = 2 per row, 2 CTA barriers per reflector (as k_heev_cr), loads of
+//     4-column batches issued before use.
+//  2. fp32 multisection on Sturm counts (8 lanes per wanted eigenvalue).
+//  3. Inverse iteration, thread per eigenvalue, iterate in shared memory ([i][t], conflict free),
+//     pivoted LU in the global workspace (L1-resident per thread column).
+//  4. Back-transform with 8 threads per eigenvector (32 rows each in registers).
+#pragma once
+
+constexpr int kBigNT = 512;
+
+__host__ __device__ inline size_t eig_big_smem(int D, int count) {
+    // tau, sub, dlt, sd, se, se2, fd, fe2, lam, scl, red, pp, XR
+    return (size_t)D * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4) + (size_t)count * (8 + 4) + 2 * 16 * 8 + (size_t)D * 8 +
+           (size_t)D * count * 4 + 64;
+}
+
+__global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, const float2* __restrict__ in,
+                                                        float2* __restrict__ out, double* __restrict__ evals,
+                                                        float2* __restrict__ ws_a, float* __restrict__ ws_lu,
+                                                        int* __restrict__ fail) {
+    using R = float;
+    using C = float2;
+    constexpr int NT = kBigNT, DM = 256, Q = NT / DM, NW = NT / 32;
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
+    const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
+    const int64_t b = blockIdx.x;
+    const int LD = D;
+    // shared carve-up
+    unsigned char* p = smem_dyn;
+    auto take = [&](size_t bytes) {
+        unsigned char* r = p;
+        p += (bytes + 15) & ~size_t(15);
+        return r;
+    };
+    R* tau = reinterpret_cast<R*>(take((size_t)D * 4));
+    C* sub = reinterpret_cast<C*>(take((size_t)D * 8));
+    C* dlt = reinterpret_cast<C*>(take((size_t)D * 8));
+    R* sd = reinterpret_cast<R*>(take((size_t)D * 4));
+    R* se = reinterpret_cast<R*>(take((size_t)D * 4));
+    R* se2 = reinterpret_cast<R*>(take((size_t)D * 4));
+    float* fd = reinterpret_cast<float*>(take((size_t)D * 4));
+    float* fe2 = reinterpret_cast<float*>(take((size_t)D * 4));
+    double* lamv = reinterpret_cast<double*>(take((size_t)count * 8));
+    int* scl = reinterpret_cast<int*>(take((size_t)count * 4));
+    R* red = reinterpret_cast<R*>(take(2 * 16 * 8));
+    C* pp = reinterpret_cast<C*>(take((size_t)D * 8));
+    R* XR = reinterpret_cast<R*>(take((size_t)D * count * 4));  // [i][t] iterate / final z
+    __shared__ int s_rounds;
+    C* A = ws_a + b * (int64_t)D * D;
+    const C* H = in + b * (int64_t)D * D;
+    for (int idx = tid; idx < D * D; idx += NT) {
+        const int i = idx % D, j = idx / D;
+        if (i >= j) {
+            C v = H[idx];
+            if (i == j) v.y = 0.f;
+            A[i + LD * j] = v;
+            A[j + LD * i] = make_float2(v.x, -v.y);
+        }
+    }
+    __syncthreads();
+    GWT_CLK(t_ph0);
+    const int r = tid / Q, q = tid % Q;
+    R* rt2 = red;
+    R* rkp = red + NW;
+    {
+        R part = 0.f;
+        if (q == 0 && r > 1 && r < D) {
+            const C a = A[r];
+            part = a.x * a.x + a.y * a.y;
+        }
+        part = rows_sum<Q>(part);
+        if (lane == 0) rt2[wid] = part;
+    }
+    for (int k = 0; k + 2 < D; ++k) {
+        const bool act = r > k && r < D;
+        __syncthreads();  // [A]
+        R t2 = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t2 += rt2[w];
+        const C x0 = A[(k + 1) + LD * k];
+        const C* colk = A + LD * k;
+        if (t2 == 0.f) {
+            if (tid == 0) {
+                tau[k] = 0.f;
+                sub[k] = x0;
+            }
+            __syncthreads();
+            R part = 0.f;
+            if (q == 0 && r > k + 2 && r < D) {
+                const C a = A[r + LD * (k + 1)];
+                part = a.x * a.x + a.y * a.y;
+            }
+            part = rows_sum<Q>(part);
+            if (lane == 0) rt2[wid] = part;
+            continue;
+        }
+        C al, v0;
+        R tk;
+        reflector(x0, t2, al, v0, tk);
+        const C v = act ? (r == k + 1 ? v0 : colk[r]) : make_float2(0.f, 0.f);
+        C p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
+        if (act) {
+            const C* arow = A + r;
+            int c = k + 1 + q;
+            for (; c + 3 * Q < D; c += 4 * Q) {
+                C a[4], bb[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    a[u] = arow[LD * (c + u * Q)];
+                    bb[u] = colk[c + u * Q];
+                }
+                if (c == k + 1) bb[0] = v0;
+                cfma(p0, a[0], bb[0]);
+                cfma(p1, a[1], bb[1]);
+                cfma(p0, a[2], bb[2]);
+                cfma(p1, a[3], bb[3]);
+            }
+            for (; c < D; c += Q) cfma(p0, arow[LD * c], c == k + 1 ? v0 : colk[c]);
+        }
+        C pv = make_float2(p0.x + p1.x, p0.y + p1.y);
+#pragma unroll
+        for (int o = 1; o < Q; o <<= 1) {
+            pv.x += __shfl_xor_sync(0xffffffffu, pv.x, o);
+            pv.y += __shfl_xor_sync(0xffffffffu, pv.y, o);
+        }
+        pv = make_float2(pv.x * tk, pv.y * tk);
+        R kp = (q == 0 && act) ? v.x * pv.x + v.y * pv.y : 0.f;
+        kp = rows_sum<Q>(kp);
+        if (lane == 0) rkp[wid] = kp;
+        if (act && q == 0) pp[r] = pv;
+        __syncthreads();  // [B]
+        R ks = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) ks += rkp[w];
+        const R kk = 0.5f * tk * ks;
+        const C w = make_float2(pv.x - kk * v.x, pv.y - kk * v.y);
+        if (tid == 0) {
+            tau[k] = tk;
+            sub[k] = al;
+        }
+        R part = 0.f;
+        if (act) {
+            C* arow = A + r;
+            int c = k + 1 + q;
+            for (; c + 3 * Q < D; c += 4 * Q) {
+                C a[4], vc[4], pc[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    a[u] = arow[LD * (c + u * Q)];
+                    vc[u] = colk[c + u * Q];
+                    pc[u] = pp[c + u * Q];
+                }
+                if (c == k + 1) vc[0] = v0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const C wc = make_float2(pc[u].x - kk * vc[u].x, pc[u].y - kk * vc[u].y);
+                    a[u].x -= v.x * wc.x + v.y * wc.y + w.x * vc[u].x + w.y * vc[u].y;
+                    a[u].y -= v.y * wc.x - v.x * wc.y + w.y * vc[u].x - w.x * vc[u].y;
+                    arow[LD * (c + u * Q)] = a[u];
+                }
+                if (c == k + 1 && r > k + 2) part = a[0].x * a[0].x + a[0].y * a[0].y;
+            }
+            for (; c < D; c += Q) {
+                const C vc = c == k + 1 ? v0 : colk[c];
+                const C pc = pp[c];
+                const C wc = make_float2(pc.x - kk * vc.x, pc.y - kk * vc.y);
+                C a = arow[LD * c];
+                a.x -= v.x * wc.x + v.y * wc.y + w.x * vc.x + w.y * vc.y;
+                a.y -= v.y * wc.x - v.x * wc.y + w.y * vc.x - w.x * vc.y;
+                arow[LD * c] = a;
+                if (c == k + 1 && r > k + 2) part = a.x * a.x + a.y * a.y;
+            }
+            if (r == k + 1 && q == 0) A[r + LD * k] = v0;
+        }
+        part = rows_sum<Q>(part);
+        if (lane == 0) rt2[wid] = part;
+    }
+    __syncthreads();
+    GWT_CLK(t_ph1);
+    // 2. tridiagonal + phases
+    for (int i = tid; i < D; i += NT) sd[i] = A[i + LD * i].x;
+    if (tid == 0) {
+        C dl = make_float2(1.f, 0.f);
+        dlt[0] = dl;
+        for (int i = 0; i + 1 < D; ++i) {
+            const C s = (i + 2 < D) ? sub[i] : A[(i + 1) + LD * i];
+            const R mag = hypotf(s.x, s.y);
+            se[i] = mag;
+            se2[i] = mag * mag;
+            if (mag > 0.f) dl = cmul(dl, make_float2(s.x / mag, s.y / mag));
+            dlt[i + 1] = dl;
+        }
+        se[D - 1] = 0.f;
+        se2[D - 1] = 0.f;
+    }
+    __syncthreads();
+    double lo_p = 1e308, hi_p = -1e308, nrm_p = 0.0;
+    for (int i = tid; i < D; i += NT) {
+        const double rr = (double)(i > 0 ? se[i - 1] : 0.f) + (double)se[i];
+        lo_p = fmin(lo_p, (double)sd[i] - rr);
+        hi_p = fmax(hi_p, (double)sd[i] + rr);
+        nrm_p = fmax(nrm_p, fabs((double)sd[i]) + rr);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo_p = fmin(lo_p, __shfl_xor_sync(0xffffffffu, lo_p, o));
+        hi_p = fmax(hi_p, __shfl_xor_sync(0xffffffffu, hi_p, o));
+        nrm_p = fmax(nrm_p, __shfl_xor_sync(0xffffffffu, nrm_p, o));
+    }
+    __shared__ double bred[3][NW];
+    if (lane == 0) {
+        bred[0][wid] = lo_p;
+        bred[1][wid] = hi_p;
+        bred[2][wid] = nrm_p;
+    }
+    __syncthreads();
+    double glo = 1e308, ghi = -1e308, tnorm = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) {
+        glo = fmin(glo, bred[0][w2]);
+        ghi = fmax(ghi, bred[1][w2]);
+        tnorm = fmax(tnorm, bred[2][w2]);
+    }
+    const double eps = 1.1920928955078125e-07;
+    glo -= 2.0 * eps * tnorm;
+    ghi += 2.0 * eps * tnorm;
+    const double inv_n = tnorm > 0.0 ? 1.0 / tnorm : 1.0;
+    for (int i = tid; i < D; i += NT) {
+        fd[i] = (float)((double)sd[i] * inv_n);
+        fe2[i] = (float)((double)se2[i] * inv_n * inv_n);
+    }
+    __syncthreads();
+    {
+        int S = NT / count;
+        S = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1));
+        const int t = tid / S, s = tid % S;
+        const int gl = lane / S;
+        const int want = D - 1 - t;
+        float lo = (float)(glo * inv_n) - 1e-6f, hi = (float)(ghi * inv_n) + 1e-6f;
+        bool done = t >= count;
+        for (int it = 0; it < 96; ++it) {
+            if (!done && hi - lo <= 2e-7f * fmaxf(fmaxf(fabsf(lo), fabsf(hi)), 1e-3f)) done = true;
+            if (__all_sync(0xffffffffu, done)) break;
+            const float step = (hi - lo) / (float)(S + 1);
+            const float pt = lo + (float)(s + 1) * step;
+            const bool le = !done && sturm_count_f32(D, fd, fe2, pt, 1e-30f) <= want;
+            const unsigned bits = __ballot_sync(0xffffffffu, le);
+            if (!done) {
+                const int j = __popc((bits >> (gl * S)) & ((1u << S) - 1u));
+                const float nlo = j > 0 ? lo + (float)j * step : lo;
+                const float nhi = j < S ? lo + (float)(j + 1) * step : hi;
+                if (!(nlo >= lo && nhi <= hi && nlo < nhi) || (nlo == lo && nhi == hi)) done = true;
+                else {
+                    lo = nlo;
+                    hi = nhi;
+                }
+            }
+        }
+        if (t < count && s == 0) lamv[t] = 0.5 * ((double)lo + (double)hi) * tnorm;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const double ctol = 1e-3 * fmax(tnorm, 1e-300);
+        int pos = 0, maxr = 0;
+        for (int t = 0; t < count; ++t) {
+            pos = (t > 0 && fabs(lamv[t - 1] - lamv[t]) <= ctol) ? pos + 1 : 0;
+            scl[t] = pos;
+            maxr = max(maxr, pos);
+        }
+        s_rounds = maxr + 1;
+    }
+    __syncthreads();
+    const int rounds = s_rounds;
+    GWT_CLK(t_ph2);
+    // 3b. inverse iteration: thread t = eigenvalue t; x in XR[i][t]; LU in the global workspace
+    {
+        const int t = tid;
+        R* DDv = ws_lu + b * (int64_t)count * 3 * D;
+        R* DUv = DDv + (int64_t)count * D;
+        R* MLv = DUv + (int64_t)count * D;
+#define LU_(arr, i) arr[(int64_t)(i) * count + t]
+#define XV(i) XR[(i) * count + t]
+        const R tiny = (R)fmax(eps * tnorm, 1e-30);
+        constexpr int kSolves = 2;
+        for (int rd = 0; rd < rounds; ++rd) {
+            if (t < count && scl[t] == rd) {
+                const R lam = (R)lamv[t];
+                uint32_t sw[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                R dcur = sd[0] - lam, ucur = se[0];
+                for (int i = 0; i + 1 < D; ++i) {
+                    const R sb = se[i], dn = sd[i + 1] - lam, en = (i + 2 < D) ? se[i + 1] : 0.f;
+                    R mult;
+                    if (fabsf(dcur) >= fabsf(sb)) {
+                        const R di = dcur == 0.f ? tiny : dcur;
+                        mult = sb / di;
+                        LU_(DDv, i) = di;
+                        LU_(DUv, i) = ucur;
+                        dcur = dn - mult * ucur;
+                        ucur = en;
+                    } else {
+                        mult = dcur / sb;
+                        sw[i >> 5] |= 1u << (i & 31);
+                        LU_(DDv, i) = sb;
+                        LU_(DUv, i) = dn;
+                        dcur = ucur - mult * dn;
+                        ucur = -mult * en;
+                    }
+                    LU_(MLv, i) = mult;
+                }
+                LU_(DDv, D - 1) = dcur;
+                for (int i = 0; i < D; ++i) {
+                    R di = LU_(DDv, i);
+                    if (fabsf(di) < tiny) di = di < 0.f ? -tiny : tiny;
+                    LU_(DDv, i) = 1.f / di;
+                }
+                for (int i = 0; i < D; ++i) XV(i) = 1.f + 0.25f * __sinf(0.7f * i + 1.3f * t);
+                for (int it = 0; it <= kSolves; ++it) {
+                    for (int s2 = t - rd; s2 < t; ++s2) {
+                        R dot = 0.f;
+                        for (int i = 0; i < D; ++i) dot += XR[i * count + s2] * XV(i);
+                        for (int i = 0; i < D; ++i) XV(i) -= dot * XR[i * count + s2];
+                    }
+                    R nn = 0.f;
+                    for (int i = 0; i < D; ++i) nn += XV(i) * XV(i);
+                    const R inv = nn > 0.f ? rsqrtf(nn) : 1.f;
+                    for (int i = 0; i < D; ++i) XV(i) *= inv;
+                    if (it == kSolves) break;
+                    for (int i = 0; i + 1 < D; ++i) {
+                        const R ml = LU_(MLv, i);
+                        if ((sw[i >> 5] >> (i & 31)) & 1u) {
+                            const R t0 = XV(i);
+                            XV(i) = XV(i + 1);
+                            XV(i + 1) = t0 - ml * XV(i + 1);
+                        } else {
+                            XV(i + 1) -= ml * XV(i);
+                        }
+                    }
+                    R x2 = 0.f, x1 = 0.f;  // x[i+2], x[i+1]
+                    for (int i = D - 1; i >= 0; --i) {
+                        R acc = XV(i);
+                        if (i + 1 < D) acc -= LU_(DUv, i) * x1;
+                        if (i + 2 < D && ((sw[i >> 5] >> (i & 31)) & 1u)) acc -= se[i + 1] * x2;
+                        const R xi = acc * LU_(DDv, i);
+                        XV(i) = xi;
+                        x2 = x1;
+                        x1 = xi;
+                    }
+                    R mx = 0.f;
+                    for (int i = 0; i < D; ++i) mx = fmaxf(mx, fabsf(XV(i)));
+                    if (!(mx > 0.f) || !isfinite(mx)) {
+                        if (fail) atomicExch(fail, 1);
+                        break;
+                    }
+                    const R sc = 1.f / mx;
+                    for (int i = 0; i < D; ++i) XV(i) *= sc;
+                }
+                double rq = 0.0;
+                for (int i = 0; i < D; ++i) {
+                    double tz = (double)sd[i] * XV(i);
+                    if (i > 0) tz += (double)se[i - 1] * XV(i - 1);
+                    if (i + 1 < D) tz += (double)se[i] * XV(i + 1);
+                    rq += (double)XV(i) * tz;
+                }
+                lamv[t] = rq;
+            }
+            __syncthreads();
+        }
+#undef LU_
+#undef XV
+    }
+    GWT_CLK(t_ph3);
+    // 4. back-transform, 8 threads per eigenvector (rows i = qb mod 8)
+    {
+        constexpr int QB = 8, RPT = DM / QB;
+        const int t = tid / QB, qb = tid % QB;
+        const bool on = t < count;  // count <= 64
+        if (on && qb == 0 && evals) evals[b * count + t] = lamv[t];
+        C y[RPT];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int i = qb + QB * u;
+            y[u] = make_float2(0.f, 0.f);
+            if (on && i < D) {
+                const R z = XR[i * count + t];
+                const C dl = dlt[i];
+                y[u] = make_float2(dl.x * z, dl.y * z);
+            }
+        }
+        for (int k = D - 3; k >= 0; --k) {
+            const R tk = tau[k];
+            if (tk == 0.f) continue;
+            const C* vk = A + LD * k;
+            C dot = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i > k && i < D) cfmaconj(dot, vk[i], y[u]);
+            }
+#pragma unroll
+            for (int o = 1; o < QB; o <<= 1) {
+                dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
+                dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
+            }
+            dot = make_float2(dot.x * tk, dot.y * tk);
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i > k && i < D) {
+                    const C pr = cmul(vk[i], dot);
+                    y[u].x -= pr.x;
+                    y[u].y -= pr.y;
+                }
+            }
+        }
+        R best = -1.f;
+        int bi = 0;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int i = qb + QB * u;
+            const R mag = y[u].x * y[u].x + y[u].y * y[u].y;
+            if (i < D && mag > best) {
+                best = mag;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < QB; o <<= 1) {
+            const R ob2 = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob2 > best || (ob2 == best && oi < bi)) {
+                best = ob2;
+                bi = oi;
+            }
+        }
+        C yb = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+            if (qb + QB * u == bi) yb = y[u];
+        const int owner = (lane & ~(QB - 1)) | (bi % QB);
+        yb = shfl_c(yb, owner);
+        if (on) {
+            C fac = make_float2(1.f, 0.f);
+            if (best > 0.f) {
+                const R im = rsqrtf(best);
+                fac = make_float2(yb.x * im, -yb.y * im);
+            }
+            C* ob = out + (b * count + t) * (int64_t)D;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i < D) ob[i] = cmul(y[u], fac);
+            }
+        }
+    }
+#ifdef GWT_PHASE_TIMERS
+    if (b == 0 && tid == 0) {
+        const long long t_ph4 = clock64();
+        g_eig_phase[0] = t_ph1 - t_ph0;
+        g_eig_phase[1] = t_ph2 - t_ph1;
+        g_eig_phase[2] = t_ph3 - t_ph2;
+        g_eig_phase[3] = t_ph4 - t_ph3;
+    }
+#endif
+}

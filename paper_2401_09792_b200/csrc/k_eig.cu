@@ -110,6 +110,7 @@ __device__ __forceinline__ int sturm_count_f32(int D, const float* d, const floa
 
 #include "eig_warp.cuh"
 #include "eig_cta.cuh"
+#include "eig_big.cuh"
 
 // in: [batch][D][D] Hermitian (column-major; lower triangle read),
 // out: [batch][count][D] top eigenvectors, evals (nullable): [batch][count].
@@ -1069,6 +1070,18 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
             }
             return cudaGetLastError();
         }
+    }
+    const bool cr_fits = D <= 128 && count <= 64 && eig_cta_layout(D, count, sizeof(T)).total <= 227 * 1024;
+    if (sizeof(T) == 4 && !force_cta && !force_warp && !legacy_warp && D > 64 && D <= 256 && count <= 64 &&
+        !(D <= 128 && cr_fits)) {
+        // fp32, matrix in the (L2-resident) global workspace (eig_big.cuh)
+        const size_t sm = eig_big_smem(D, count);
+        cudaError_t e = cudaFuncSetAttribute(k_heev_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        k_heev_big<<<(unsigned)batch, kBigNT, sm, st>>>(D, count, (const float2*)in, (float2*)out, evals,
+                                                        reinterpret_cast<float2*>(ws_a), reinterpret_cast<float*>(ws_z),
+                                                        fail);
+        return cudaGetLastError();
     }
     if (!force_cta && (force_warp || legacy_warp ? D <= kSmemMaxD : D <= 32)) {
         // warp per matrix (Householder + bisection + inverse iteration); W matrices per CTA
