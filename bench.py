@@ -368,7 +368,15 @@ def main():
         per_stage[k_] = r
     dom = max(stage, key=stage.get)
     roof = dict(per_stage[dom])
-    roof.update(traffic=None, peak_source={"hbm": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+    # measured DRAM traffic per launch of the dominant kernel from the committed ncu capture (same config)
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")))
+        if tj.get("config") == args.config:
+            traffic = tj["bytes_per_launch"].get(kern[dom])
+    except (OSError, ValueError, KeyError):
+        traffic = None
+    roof.update(traffic=traffic, traffic_source="profiles/r01_traffic.json" if traffic else None, peak_source={"hbm": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                                            "fp32": "derived: 148 SM x 128 FMA/clk x 2 x max clock (not measured)",
                                            "fp64": "derived: 148 SM x 64 DFMA/clk x 2 x max clock (not measured)"}[roof["bound"]],
                 stage_share={k_: round(v / max(sum(stage.values()), 1e-9), 3) for k_, v in stage.items()},
