@@ -67,6 +67,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
         : "memory");
 }
 
+// plain (non-tensor) arrival on an mbarrier from a generic thread
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(mbar))
+                 : "memory");
+}
+// named barrier over `n` threads (multiple of 32)
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

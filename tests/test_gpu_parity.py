@@ -53,7 +53,7 @@ def test_leading_eigenvectors_match_oracle_and_lapack(ctx, n):
         assert np.linalg.norm(vec[k].conj().T @ vec[k] - np.eye(count)) < 1e-10
 
 
-@pytest.mark.parametrize("n,count", [(12, 5), (24, 12), (32, 12), (64, 8), (64, 24)])
+@pytest.mark.parametrize("n,count", [(12, 5), (24, 12), (32, 12), (64, 8), (64, 24), (128, 40), (128, 64), (200, 48), (256, 64)])
 def test_leading_eigenvectors_c64(ctx, n, count):
     """c64 Grams are decomposed in fp32 (warp kernel for n <= 32): subspace angle and eigenvalues vs fp64."""
     rng = np.random.default_rng(5 + n)

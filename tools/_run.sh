@@ -1,2 +1,1 @@
-timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/b.log 2>&1; python tools/show_bench.py gpurun_out/b.log 2>/dev/null | head -4; python -c "import json; d=json.loads(open('gpurun_out/b.log').read().strip().splitlines()[-1]); print(d['roofline']['traffic'], d['roofline']['kernel'])"
-GWT_SMALL_GRP=1 timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/b2.log 2>&1; python tools/show_bench.py gpurun_out/b2.log 2>/dev/null | head -4
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "leading" 2>&1 | tail -3
