@@ -644,11 +644,12 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     const char* path0 = std::getenv("GWT_SINR_PATH");
     const bool fused0 = scope == GWT_SCOPE_PAPER && t.users() <= 128 && path0 && std::strcmp(path0, "fused") == 0;
     const char* pl = std::getenv("GWT_SINR_PIPELINE");
-    const int64_t nch = std::min<int64_t>(ngroups, pl ? std::max(1, std::atoi(pl)) : 8);
+    const int64_t nch = std::min<int64_t>(ngroups, pl ? std::max(1, std::atoi(pl)) : 4);
     if (mem == GWT_MEM_HOST && !fused0 && nch > 1) {
-        // host buffers: group chunks round-robin over 3 stream lanes, each chunk H2D -> device
+        // host buffers: 4 group chunks on 4 stream lanes (GWT_SINR_PIPELINE / GWT_SINR_LANES), each chunk H2D -> device
         // pipeline -> D2H on its lane, so copies in both directions overlap the other chunks' kernels
-        const int NS = (int)std::min<int64_t>(3, nch);
+        const char* nl = std::getenv("GWT_SINR_LANES");
+        const int NS = (int)std::min<int64_t>(nl ? std::max(1, std::atoi(nl)) : 4, nch);
         while ((int)ctx->lanes.size() < NS - 1) {
             gwt_ctx::Lane ln;
             ck(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking), "cudaStreamCreate");

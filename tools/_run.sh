@@ -1,1 +1,1 @@
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "leading" 2>&1 | tail -3
+timeout 120 python tools/e2e_probe.py
