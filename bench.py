@@ -339,6 +339,8 @@ def main():
         t1 = time.perf_counter()
         if it >= max(args.warmup, 1):
             e2e_ms.append((t1 - t0) * 1e3)
+    if os.environ.get("GWT_BENCH_DEBUG"):
+        print("e2e_ms", [round(x, 3) for x in e2e_ms], file=sys.stderr)
     e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)

@@ -345,19 +345,21 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
     __syncthreads();
     const int rounds = s_rounds;
     GWT_CLK(t_ph2);
-    // 3b. inverse iteration, thread t = eigenvalue t
+    // 3b. inverse iteration, thread t = eigenvalue t; the iterate lives in XR[i][t] (shared memory,
+    // conflict free across t) so the thread keeps no D-long register array
     {
         const int t = tid;
 #define LU_(arr, i) arr[(i) * count + t]
+#define XV(i) XR[(i) * count + t]
         const R tiny = (R)fmax(eps * tnorm, sizeof(R) == 4 ? 1e-30 : 1e-290);
-    // solves from the fp32 bisection shift (~2e-7 rel): 2 reach fp32 accuracy, 3 binary64
-    constexpr int kSolves = sizeof(R) == 4 ? 2 : 3;
+        // solves from the fp32 bisection shift (~2e-7 rel): 2 reach fp32 accuracy, 3 binary64
+        constexpr int kSolves = sizeof(R) == 4 ? 2 : 3;
         for (int rd = 0; rd < rounds; ++rd) {
             if (t < count && scl[t] == rd) {
-                R x[DM];
                 const R lam = (R)lamv[t];
-                unsigned long long sw = 0ull;  // DM <= 64 bits used per word; DM = 128 uses the high word below
-                unsigned long long sw2 = 0ull;
+                uint32_t sw[DM / 32];
+#pragma unroll
+                for (int w2 = 0; w2 < DM / 32; ++w2) sw[w2] = 0u;
                 R dcur = sd[0] - lam, ucur = se[0];
                 for (int i = 0; i + 1 < D; ++i) {
                     const R sb = se[i], dn = sd[i + 1] - lam, en = (i + 2 < D) ? se[i + 1] : R(0);
@@ -371,8 +373,7 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                         ucur = en;
                     } else {
                         mult = dcur / sb;
-                        if (i < 64) sw |= 1ull << i;
-                        else sw2 |= 1ull << (i - 64);
+                        sw[i >> 5] |= 1u << (i & 31);
                         LU_(DDv, i) = sb;
                         LU_(DUv, i) = dn;
                         dcur = ucur - mult * dn;
@@ -386,78 +387,62 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                     if (fabs(di) < tiny) di = di < R(0) ? -tiny : tiny;
                     LU_(DDv, i) = R(1) / di;
                 }
-#pragma unroll
-                for (int i = 0; i < DM; ++i) x[i] = i < D ? R(1) + R(0.25) * (R)__sinf(0.7f * i + 1.3f * t) : R(0);
+                for (int i = 0; i < D; ++i) XV(i) = R(1) + R(0.25) * (R)__sinf(0.7f * i + 1.3f * t);
                 for (int it = 0; it <= kSolves; ++it) {
                     for (int s2 = t - rd; s2 < t; ++s2) {
                         R dot = R(0);
-#pragma unroll
-                        for (int i = 0; i < DM; ++i)
-                            if (i < D) dot += XR[i * count + s2] * x[i];
-#pragma unroll
-                        for (int i = 0; i < DM; ++i)
-                            if (i < D) x[i] -= dot * XR[i * count + s2];
+                        for (int i = 0; i < D; ++i) dot += XR[i * count + s2] * XV(i);
+                        for (int i = 0; i < D; ++i) XV(i) -= dot * XR[i * count + s2];
                     }
                     R nn = R(0);
-#pragma unroll
-                    for (int i = 0; i < DM; ++i) nn += x[i] * x[i];
+                    for (int i = 0; i < D; ++i) nn += XV(i) * XV(i);
                     const R inv = nn > R(0) ? R(1) / sqrt(nn) : R(1);
-#pragma unroll
-                    for (int i = 0; i < DM; ++i) x[i] *= inv;
+                    for (int i = 0; i < D; ++i) XV(i) *= inv;
                     if (it == kSolves) break;
-#pragma unroll
-                    for (int i = 0; i + 1 < DM; ++i) {
-                        if (i + 1 < D) {
-                            const R ml = LU_(MLv, i);
-                            const bool swp = i < 64 ? ((sw >> i) & 1ull) : ((sw2 >> (i - 64)) & 1ull);
-                            if (swp) {
-                                const R t0 = x[i];
-                                x[i] = x[i + 1];
-                                x[i + 1] = t0 - ml * x[i + 1];
-                            } else {
-                                x[i + 1] -= ml * x[i];
-                            }
+                    R xi = XV(0);  // forward: row interchanges and multipliers, carried in registers
+                    for (int i = 0; i + 1 < D; ++i) {
+                        const R ml = LU_(MLv, i), xn = XV(i + 1);
+                        if ((sw[i >> 5] >> (i & 31)) & 1u) {
+                            XV(i) = xn;
+                            xi = xi - ml * xn;
+                        } else {
+                            XV(i) = xi;
+                            xi = xn - ml * xi;
                         }
                     }
-#pragma unroll
-                    for (int i = DM - 1; i >= 0; --i) {
-                        if (i < D) {
-                            R acc = x[i];
-                            if (i + 1 < DM && i + 1 < D) acc -= LU_(DUv, i) * x[i + 1];
-                            const bool swp = i < 64 ? ((sw >> i) & 1ull) : ((sw2 >> (i - 64)) & 1ull);
-                            if (i + 2 < DM && i + 2 < D && swp) acc -= se[i + 1] * x[i + 2];
-                            x[i] = acc * LU_(DDv, i);
-                        }
+                    XV(D - 1) = xi;
+                    R x1 = R(0), x2 = R(0);  // back substitution with U, x[i+1], x[i+2] in registers
+                    for (int i = D - 1; i >= 0; --i) {
+                        R acc = XV(i);
+                        if (i + 1 < D) acc -= LU_(DUv, i) * x1;
+                        if (i + 2 < D && ((sw[i >> 5] >> (i & 31)) & 1u)) acc -= se[i + 1] * x2;
+                        const R v = acc * LU_(DDv, i);
+                        XV(i) = v;
+                        x2 = x1;
+                        x1 = v;
                     }
                     R mx = R(0);
-#pragma unroll
-                    for (int i = 0; i < DM; ++i) mx = fmax(mx, fabs(x[i]));
+                    for (int i = 0; i < D; ++i) mx = fmax(mx, fabs(XV(i)));
                     if (!(mx > R(0)) || !isfinite(mx)) {
                         if (fail) atomicExch(fail, 1);
                         break;
                     }
                     const R sc = R(1) / mx;
-#pragma unroll
-                    for (int i = 0; i < DM; ++i) x[i] *= sc;
+                    for (int i = 0; i < D; ++i) XV(i) *= sc;
                 }
-#pragma unroll
-                for (int i = 0; i < DM; ++i)
-                    if (i < D) XR[i * count + t] = x[i];
                 double rq = 0.0;
-#pragma unroll
-                for (int i = 0; i < DM; ++i) {
-                    if (i < D) {
-                        double tz = (double)sd[i] * x[i];
-                        if (i > 0) tz += (double)se[i - 1] * x[i - 1];
-                        if (i + 1 < DM && i + 1 < D) tz += (double)se[i] * x[i + 1];
-                        rq += (double)x[i] * tz;
-                    }
+                for (int i = 0; i < D; ++i) {
+                    double tz = (double)sd[i] * XV(i);
+                    if (i > 0) tz += (double)se[i - 1] * XV(i - 1);
+                    if (i + 1 < D) tz += (double)se[i] * XV(i + 1);
+                    rq += (double)XV(i) * tz;
                 }
                 lamv[t] = rq;
             }
             __syncthreads();
         }
 #undef LU_
+#undef XV
     }
     GWT_CLK(t_ph3);
     // 4. back-transform, 4 threads per eigenvector (rows i = qb mod 4)
