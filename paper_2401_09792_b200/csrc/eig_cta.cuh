@@ -82,6 +82,98 @@ __device__ __forceinline__ void reflector(double2 x0, double t2, double2& al, do
     tk = 2.0 / (t2 + v0.x * v0.x + v0.y * v0.y);
 }
 
+// back-transform y = H_0 ... H_{D-3} diag(delta) z with QB threads per eigenvector (rows i = qb mod QB),
+// phase normalisation, store (shared by k_heev_cr's two thread-per-vector configurations)
+template <class R, int DM, int QB>
+__device__ __forceinline__ void cta_backtransform(int D, int count, int LD, int64_t b, const cplx_t<R>* A,
+                                                  const R* XR, const cplx_t<R>* dlt, const R* tau, const double* lamv,
+                                                  double* evals, cplx_t<R>* out) {
+    using C = cplx_t<R>;
+    const int tid = threadIdx.x, lane = tid % 32;
+{
+        constexpr int RPT = DM / QB;
+        const int t = tid / QB, qb = tid % QB;
+        const bool on = t < count;  // count <= 64 (host-checked)
+        if (on && qb == 0 && evals) evals[b * count + t] = lamv[t];
+        C y[RPT];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int i = qb + QB * u;
+            y[u] = czero<C>();
+            if (on && i < D) {
+                const R z = XR[i * count + t];
+                const C dl = dlt[i];
+                y[u] = mk(dl.x * z, dl.y * z);
+            }
+        }
+        for (int k = D - 3; k >= 0; --k) {
+            const R tk = tau[k];
+            if (tk == R(0)) continue;
+            C dot = czero<C>();
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i > k && i < D) cfmaconj(dot, A[i + LD * k], y[u]);
+            }
+#pragma unroll
+            for (int o = 1; o < QB; o <<= 1) {
+                dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
+                dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
+            }
+            dot = mk(dot.x * tk, dot.y * tk);
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i > k && i < D) {
+                    const C pr = cmul(A[i + LD * k], dot);
+                    y[u].x -= pr.x;
+                    y[u].y -= pr.y;
+                }
+            }
+        }
+        R best = R(-1);
+        int bi = 0;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int i = qb + QB * u;
+            const R mag = y[u].x * y[u].x + y[u].y * y[u].y;
+            if (i < D && mag > best) {
+                best = mag;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < QB; o <<= 1) {
+            const R ob2 = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob2 > best || (ob2 == best && oi < bi)) {
+                best = ob2;
+                bi = oi;
+            }
+        }
+        // the owner of row bi broadcasts y[bi]
+        C yb = czero<C>();
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+            if (qb + QB * u == bi) yb = y[u];
+        const int owner = (lane & ~(QB - 1)) | (bi % QB);
+        yb = shfl_c(yb, owner);
+        if (on) {
+            C fac = mk(R(1), R(0));
+            if (best > R(0)) {
+                const R im = R(1) / sqrt(best);
+                fac = mk(yb.x * im, -yb.y * im);
+            }
+            C* ob = out + (b * count + t) * (int64_t)D;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = qb + QB * u;
+                if (i < D) ob[i] = cmul(y[u], fac);
+            }
+        }
+    }
+}
+
 template <class R, int DM, int NT>
 __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, const cplx_t<R>* __restrict__ in,
                                                           cplx_t<R>* __restrict__ out, double* __restrict__ evals,
@@ -445,89 +537,9 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
 #undef XV
     }
     GWT_CLK(t_ph3);
-    // 4. back-transform, 4 threads per eigenvector (rows i = qb mod 4)
-    {
-        constexpr int QB = 4, RPT = DM / QB;
-        const int t = tid / QB, qb = tid % QB;
-        const bool on = t < count;  // count <= 64 (host-checked)
-        if (on && qb == 0 && evals) evals[b * count + t] = lamv[t];
-        C y[RPT];
-#pragma unroll
-        for (int u = 0; u < RPT; ++u) {
-            const int i = qb + QB * u;
-            y[u] = czero<C>();
-            if (on && i < D) {
-                const R z = XR[i * count + t];
-                const C dl = dlt[i];
-                y[u] = mk(dl.x * z, dl.y * z);
-            }
-        }
-        for (int k = D - 3; k >= 0; --k) {
-            const R tk = tau[k];
-            if (tk == R(0)) continue;
-            C dot = czero<C>();
-#pragma unroll
-            for (int u = 0; u < RPT; ++u) {
-                const int i = qb + QB * u;
-                if (i > k && i < D) cfmaconj(dot, A[i + LD * k], y[u]);
-            }
-#pragma unroll
-            for (int o = 1; o < QB; o <<= 1) {
-                dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
-                dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
-            }
-            dot = mk(dot.x * tk, dot.y * tk);
-#pragma unroll
-            for (int u = 0; u < RPT; ++u) {
-                const int i = qb + QB * u;
-                if (i > k && i < D) {
-                    const C pr = cmul(A[i + LD * k], dot);
-                    y[u].x -= pr.x;
-                    y[u].y -= pr.y;
-                }
-            }
-        }
-        R best = R(-1);
-        int bi = 0;
-#pragma unroll
-        for (int u = 0; u < RPT; ++u) {
-            const int i = qb + QB * u;
-            const R mag = y[u].x * y[u].x + y[u].y * y[u].y;
-            if (i < D && mag > best) {
-                best = mag;
-                bi = i;
-            }
-        }
-#pragma unroll
-        for (int o = 1; o < QB; o <<= 1) {
-            const R ob2 = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ob2 > best || (ob2 == best && oi < bi)) {
-                best = ob2;
-                bi = oi;
-            }
-        }
-        // the owner of row bi broadcasts y[bi]
-        C yb = czero<C>();
-#pragma unroll
-        for (int u = 0; u < RPT; ++u)
-            if (qb + QB * u == bi) yb = y[u];
-        const int owner = (lane & ~(QB - 1)) | (bi % QB);
-        yb = shfl_c(yb, owner);
-        if (on) {
-            C fac = mk(R(1), R(0));
-            if (best > R(0)) {
-                const R im = R(1) / sqrt(best);
-                fac = mk(yb.x * im, -yb.y * im);
-            }
-            C* ob = out + (b * count + t) * (int64_t)D;
-#pragma unroll
-            for (int u = 0; u < RPT; ++u) {
-                const int i = qb + QB * u;
-                if (i < D) ob[i] = cmul(y[u], fac);
-            }
-        }
-    }
+    // 4. back-transform: 8 threads per eigenvector when count <= NT/8, else 4
+    if (count * 8 <= NT) cta_backtransform<R, DM, 8>(D, count, LD, b, A, XR, dlt, tau, lamv, evals, out);
+    else cta_backtransform<R, DM, 4>(D, count, LD, b, A, XR, dlt, tau, lamv, evals, out);
 #ifdef GWT_PHASE_TIMERS
     if (b == 0 && tid == 0) {
         const long long t_ph4 = clock64();

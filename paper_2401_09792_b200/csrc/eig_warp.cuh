@@ -375,8 +375,84 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
     }
 #undef LU_
     GWT_CLK(t_ph3);
-    // 4. back-transform y = H_0 ... H_{D-3} diag(delta) z, lane = eigenvector
-    if (t < count) {
+    // 4. back-transform y = H_0 ... H_{D-3} diag(delta) z. count <= 16: 2 lanes per eigenvector (rows
+    // i = h mod 2, z read from XR, dots combined by one shuffle); else lane = eigenvector.
+    if (count <= 16) {
+        constexpr int RPT = DM / 2;
+        const int tv = lane >> 1, h = lane & 1;
+        const bool on = tv < count;
+        if (on && h == 0 && evals) evals[b * count + tv] = lamv[tv];
+        C y[RPT];
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int i = h + 2 * u;
+            y[u] = czero<C>();
+            if (on && i < D) {
+                const R z = XR[i * count + tv];
+                const C dl = dlt[i];
+                y[u] = mk(dl.x * z, dl.y * z);
+            }
+        }
+        for (int k = D - 3; k >= 0; --k) {
+            const R tk = tau[k];
+            if (tk == R(0)) continue;
+            C dot = czero<C>();
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = h + 2 * u;
+                if (i > k && i < D) cfmaconj(dot, A[i + D * k], y[u]);
+            }
+            dot.x += __shfl_xor_sync(0xffffffffu, dot.x, 1);
+            dot.y += __shfl_xor_sync(0xffffffffu, dot.y, 1);
+            dot = mk(dot.x * tk, dot.y * tk);
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = h + 2 * u;
+                if (i > k && i < D) {
+                    const C pr = cmul(A[i + D * k], dot);
+                    y[u].x -= pr.x;
+                    y[u].y -= pr.y;
+                }
+            }
+        }
+        R best = R(-1);
+        int bi = 0;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int i = h + 2 * u;
+            const R mag = y[u].x * y[u].x + y[u].y * y[u].y;
+            if (i < D && mag > best) {
+                best = mag;
+                bi = i;
+            }
+        }
+        {
+            const R ob2 = __shfl_xor_sync(0xffffffffu, best, 1);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, 1);
+            if (ob2 > best || (ob2 == best && oi < bi)) {
+                best = ob2;
+                bi = oi;
+            }
+        }
+        C yb = czero<C>();
+#pragma unroll
+        for (int u = 0; u < RPT; ++u)
+            if (h + 2 * u == bi) yb = y[u];
+        yb = shfl_c(yb, (lane & ~1) | (bi & 1));
+        if (on) {
+            C fac = mk(R(1), R(0));
+            if (best > R(0)) {
+                const R im = R(1) / sqrt(best);
+                fac = mk(yb.x * im, -yb.y * im);
+            }
+            C* ob = out + (b * count + tv) * (int64_t)D;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int i = h + 2 * u;
+                if (i < D) ob[i] = cmul(y[u], fac);
+            }
+        }
+    } else if (t < count) {
         if (evals) evals[b * count + t] = lamv[t];
         C y[DM];
 #pragma unroll
