@@ -550,13 +550,32 @@ void validate_sinr(const gwt_topology& tp, const gwt_ranks& r, int scope) {
     if (r.m > 8) invalid("sinr: compressed receive rank m > 8 is not supported by the B200 small-matrix kernel");
 }
 
+// Per-stage CUDA events recorded by sinr_device without a host wait (lanes stay asynchronous);
+// resolved after the caller's final synchronisation.
+struct StageEvents {
+    std::vector<cudaEvent_t> evs;  // per lane call: boundaries
+    std::vector<int> kind;         // interval i between evs[i] and evs[i+1] (within one call), -1 = call break
+    void resolve(double& ms_r, double& ms_p, double& ms_s) {
+        for (size_t i = 0; i < kind.size(); ++i) {
+            if (kind[i] < 0) continue;
+            float a = 0;
+            cudaEventElapsedTime(&a, evs[i], evs[i + 1]);
+            (kind[i] == 0 ? ms_r : kind[i] == 1 ? ms_p : ms_s) += a;
+        }
+        for (auto& ev : evs) cudaEventDestroy(ev);
+        evs.clear();
+        kind.clear();
+    }
+};
+
 // Generic device pipeline (any scope) for ngroups groups on device pointers, on solver/SINR lane
 // `lane` (stream st + its workspace): rebuild -> pair Grams per subcarrier chunk, then ONE eig+MMSE
 // launch per pair-Gram block. timing: per-stage CUDA events (host waits at the end).
 template <class T>
 void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const gwt_topology* topo, int64_t ngroups,
                  const void* Cd, const void* Gd, const double* taud, const double* fd, const void* cod, int64_t F,
-                 int scope, double* sd, double* sgd, int* std_, bool timing, double& ms_r, double& ms_p, double& ms_s) {
+                 int scope, double* sd, double* sgd, int* std_, bool timing, double& ms_r, double& ms_p, double& ms_s,
+                 StageEvents* deferred = nullptr) {
     using Cx = cplx_t<T>;
     const size_t cs = sizeof(Cx);
     const int links = t.links(), users = t.users();
@@ -577,15 +596,18 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
         const int64_t Fs = std::max<int64_t>(Fc, std::min<int64_t>(F, (int64_t)(2ll << 30) / std::max<int64_t>(per_f_pg, 1)) / Fc * Fc);
         double2* PG = (double2*)ctx->lws(lane, WS_PG, 16 * ngroups * std::min(Fs, F) * users * S * t.m * t.m);
         double* EG = (double*)ctx->lws(lane, WS_EG, 8 * ngroups * std::min(Fs, F) * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
-        std::vector<cudaEvent_t> evs;
+        std::vector<cudaEvent_t> evs_local;
+        std::vector<int> kind_local;  // 0 rebuild, 1 pair gram, 2 small, per interval
+        std::vector<cudaEvent_t>& evs = deferred ? deferred->evs : evs_local;
+        std::vector<int>& kind = deferred ? deferred->kind : kind_local;
+        if (deferred && !evs.empty()) kind.push_back(-1);  // break between two calls' event chains
         auto rec = [&]() {
-            if (!timing) return;
+            if (!timing && !deferred) return;
             cudaEvent_t ev;
             ck(cudaEventCreate(&ev), "cudaEventCreate");
             ck(cudaEventRecord(ev, st), "event");
             evs.push_back(ev);
         };
-        std::vector<int> kind;  // 0 rebuild, 1 pair gram, 2 small, per interval
         // rg: paper scope with small groups -> rebuild + pair Grams fused in shared memory (H~ never in HBM)
         rec();
         for (int64_t F0 = 0; F0 < F; F0 += Fs) {
@@ -610,7 +632,7 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
             rec();
             kind.push_back(2);
         }
-        if (timing) {
+        if (timing && !deferred) {
             ck(cudaEventSynchronize(evs.back()), "sync");
             for (size_t i = 0; i < kind.size(); ++i) {
                 float a = 0;
@@ -618,7 +640,8 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
                 (kind[i] == 0 ? ms_r : kind[i] == 1 ? ms_p : ms_s) += a;
             }
         }
-        for (auto& ev : evs) cudaEventDestroy(ev);
+        if (!deferred)
+            for (auto& ev : evs) cudaEventDestroy(ev);
     }
 }
 
@@ -645,6 +668,45 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     const bool fused0 = scope == GWT_SCOPE_PAPER && t.users() <= 128 && path0 && std::strcmp(path0, "fused") == 0;
     const char* pl = std::getenv("GWT_SINR_PIPELINE");
     const int64_t nch = std::min<int64_t>(ngroups, pl ? std::max(1, std::atoi(pl)) : 4);
+    const char* dl = std::getenv("GWT_SINR_DEV_LANES");
+    const int64_t ndev = std::min<int64_t>(ngroups, dl ? std::max(1, std::atoi(dl)) : 2);
+    if (mem == GWT_MEM_DEVICE && !fused0 && ndev > 1 && !coeffs) {
+        // device-resident: group chunks on ndev stream lanes so the FP32-issue-bound rebuild of one
+        // chunk overlaps the memory/fp64-bound Gram and small-matrix stages of the others
+        while ((int)ctx->lanes.size() < ndev - 1) {
+            gwt_ctx::Lane ln;
+            ck(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking), "cudaStreamCreate");
+            ck(cudaEventCreateWithFlags(&ln.ev, cudaEventDisableTiming), "cudaEventCreate");
+            ctx->lanes.push_back(ln);
+        }
+        auto lane_st = [&](int l) { return l == 0 ? ctx->stream : ctx->lanes[l - 1].st; };
+        ck(cudaEventRecord(ctx->ev[10], ctx->stream), "cudaEventRecord");
+        for (int l = 1; l < ndev; ++l) ck(cudaStreamWaitEvent(lane_st(l), ctx->ev[10], 0), "cudaStreamWaitEvent");
+        const int64_t cg = (ngroups + ndev - 1) / ndev;
+        double dr = 0, dp = 0, ds = 0;
+        StageEvents sev;
+        for (int64_t c = 0, g0 = 0; g0 < ngroups; ++c, g0 += cg) {
+            const int l = (int)c;
+            const int64_t G = std::min(cg, ngroups - g0);
+            sinr_device<T>(ctx, l, lane_st(l), t, topo, G, (const char*)Cf + cs * g0 * c_g, (const char*)Gc + cs * g0 * g_g,
+                           tau + g0 * links * t.P, freqs, nullptr, F, scope, sinr + g0 * F * users * t.L,
+                           signal + g0 * F * users * t.L, status + g0 * F * users, false, dr, dp, ds, &sev);
+        }
+        for (int l = 1; l < ndev; ++l) {
+            ck(cudaEventRecord(ctx->lanes[l - 1].ev, lane_st(l)), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(ctx->stream, ctx->lanes[l - 1].ev, 0), "cudaStreamWaitEvent");
+        }
+        tm.mark(6);
+        ck(cudaStreamSynchronize(ctx->stream), "sync");
+        sev.resolve(dr, dp, ds);
+        std::fill(ctx->stage_ms, ctx->stage_ms + 8, 0.0);
+        ctx->stage_ms[0] = tm.between(0, 6);
+        // per-stage kernel time summed over the lanes (the lanes overlap, so the sum exceeds stage_ms[0])
+        ctx->stage_ms[4] = dr;
+        ctx->stage_ms[5] = dp;
+        ctx->stage_ms[6] = ds;
+        return;
+    }
     if (mem == GWT_MEM_HOST && !fused0 && nch > 1) {
         // host buffers: 4 group chunks on 4 stream lanes (GWT_SINR_PIPELINE / GWT_SINR_LANES), each chunk H2D -> device
         // pipeline -> D2H on its lane, so copies in both directions overlap the other chunks' kernels
