@@ -594,10 +594,8 @@ template cudaError_t launch_rebuild_pg<double>(const Topo&, int, int, int64_t, i
 // top-L eigenpairs (descending). EG layout per item: lambda[L] (padded to even) then U[M][L]
 // column-major (M x L), fp64.
 template <int M>
-__global__ void __launch_bounds__(128) k_precoder_eig(Topo t, int scope, int S, int64_t items,
-                                                      const double2* __restrict__ PG, double* __restrict__ EG) {
-    const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (item >= items) return;
+__device__ __forceinline__ void precoder_item(const Topo& t, int scope, int S, int64_t item, const double2* PG,
+                                              double* EG, int64_t eg_item) {
     const int L = t.L;
     const int u = (int)(item % t.users());
     const int i = u / t.K, j = u % t.K;
@@ -632,7 +630,7 @@ __global__ void __launch_bounds__(128) k_precoder_eig(Topo t, int scope, int S, 
         rank[r] = rk;
     }
     const int Lp = (L + 1) & ~1;  // keep the U block 16-byte aligned
-    double* dst = EG + item * (int64_t)(Lp + 2 * M * L);
+    double* dst = EG + eg_item * (int64_t)(Lp + 2 * M * L);
     double2* du = reinterpret_cast<double2*>(dst + Lp);
 #pragma unroll
     for (int r = 0; r < M; ++r) {
@@ -644,17 +642,21 @@ __global__ void __launch_bounds__(128) k_precoder_eig(Topo t, int scope, int S, 
     }
 }
 
+template <int M>
+__global__ void __launch_bounds__(128) k_precoder_eig(Topo t, int scope, int S, int64_t items,
+                                                      const double2* __restrict__ PG, double* __restrict__ EG) {
+    const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= items) return;
+    precoder_item<M>(t, scope, S, item, PG, EG, item);
+}
+
 // ---------------------------------------------------------------------------
 // K3b: covariance, Cholesky (with the reference's PD and condition checks),
 // filter and per-stream SINR; one thread per (group, subcarrier, user).
 template <int M>
-__global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t items, double sigma, int fc,
-                                              int64_t Ftot, int64_t f0, const double2* __restrict__ PG,
-                                              const double* __restrict__ EG,
-                                              double* __restrict__ sinr, double* __restrict__ signal,
-                                              int* __restrict__ status) {
-    const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (item >= items) return;
+__device__ __forceinline__ void mmse_item(const Topo& t, int scope, int S, int64_t item, double sigma, int fc,
+                                          int64_t Ftot, int64_t f0, const double2* PG, const double* EG,
+                                          int64_t eg_item, double* sinr, double* signal, int* status) {
     const int L = t.L;
     const int users = t.users();
     const int u = (int)(item % users);
@@ -662,7 +664,7 @@ __global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t 
     const int i = u / t.K, j = u % t.K;
     const int Lp = (L + 1) & ~1;
     const int64_t eg_stride = Lp + 2 * M * L;
-    const double* own = EG + item * eg_stride;
+    const double* own = EG + eg_item * eg_stride;
     const double2* ownU = reinterpret_cast<const double2*>(own + Lp);
     int st = 0;
     double2 Q[M][M];
@@ -693,7 +695,7 @@ __global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t 
         if (s == ss) continue;
         int k, l;
         scope_slot(t, scope, i, j, s, k, l);
-        const int64_t pidx = gf * users + (k * t.K + l);
+        const int64_t pidx = (eg_item / users) * users + (k * t.K + l);
         const double* pe = EG + pidx * eg_stride;
         const double2* pU = reinterpret_cast<const double2*>(pe + Lp);
         const double2* X = PG + (item * S + s) * M * M;
@@ -794,6 +796,33 @@ __global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t 
         sg[r] = sp;
     }
     status[orow] = st;
+}
+
+template <int M>
+__global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t items, double sigma, int fc,
+                                              int64_t Ftot, int64_t f0, const double2* __restrict__ PG,
+                                              const double* __restrict__ EG,
+                                              double* __restrict__ sinr, double* __restrict__ signal,
+                                              int* __restrict__ status) {
+    const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= items) return;
+    mmse_item<M>(t, scope, S, item, sigma, fc, Ftot, f0, PG, EG, item, sinr, signal, status);
+}
+
+// K3 fused: a CTA holds whole (group, subcarrier) slices (users x SL threads); the precoders go to
+// shared memory and the MMSE phase reads its partners' from there (no EG round trip through HBM).
+template <int M>
+__global__ void __launch_bounds__(128) k_small_fused(Topo t, int scope, int S, int64_t items, double sigma, int fc,
+                                                     int64_t Ftot, int64_t f0, const double2* __restrict__ PG,
+                                                     double* __restrict__ sinr, double* __restrict__ signal,
+                                                     int* __restrict__ status) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* eg = reinterpret_cast<double*>(smem_raw);
+    const int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool on = item < items;
+    if (on) precoder_item<M>(t, scope, S, item, PG, eg, threadIdx.x);
+    __syncthreads();
+    if (on) mmse_item<M>(t, scope, S, item, sigma, fc, Ftot, f0, PG, eg, threadIdx.x, sinr, signal, status);
 }
 
 // ---------------------------------------------------------------------------
@@ -1834,6 +1863,17 @@ template <int M>
 static cudaError_t launch_small_m(const Topo& t, int scope, int S, int64_t items, double sigma, int fc, int64_t Ftot,
                                   int64_t f0, const double2* PG, double* EG, double* sinr, double* signal, int* status,
                                   cudaStream_t st) {
+    const int users = t.users();
+    if (users <= 128 && !std::getenv("GWT_SMALL_SPLIT")) {
+        const int thr = (128 / users) * users;  // whole (group, subcarrier) slices per CTA
+        const int Lp = (t.L + 1) & ~1;
+        const size_t sm = (size_t)thr * (Lp + 2 * M * t.L) * 8;
+        cudaError_t e = cudaFuncSetAttribute(k_small_fused<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        k_small_fused<M><<<(unsigned)((items + thr - 1) / thr), thr, sm, st>>>(t, scope, S, items, sigma, fc, Ftot, f0,
+                                                                                PG, sinr, signal, status);
+        return cudaGetLastError();
+    }
     const unsigned blocks = (unsigned)((items + 127) / 128);
     k_precoder_eig<M><<<blocks, 128, 0, st>>>(t, scope, S, items, PG, EG);
     cudaError_t e = cudaGetLastError();

@@ -1,1 +1,2 @@
-timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/b.log 2>&1; python tools/show_bench.py gpurun_out/b.log 2>/dev/null | head -4; tail -1 gpurun_out/b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(r['ms_per_step_single_lane'], r['kernel'], r['frac'], d['gpu_launches'], d['e2e']['value'])"
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "sinr or pipeline or end_to_end or large or device" 2>&1 | tail -2
+for v in 0 1; do if [ $v = 1 ]; then export GWT_SMALL_SPLIT=1; fi; GWT_SINR_DEV_LANES=1 timeout 120 python tools/sinr_time.py C2 40 2>&1 | tail -1; done
