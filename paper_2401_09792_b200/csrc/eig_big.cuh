@@ -11,7 +11,8 @@
 //  2. fp32 multisection on Sturm counts (8 lanes per wanted eigenvalue).
 //  3. Inverse iteration, thread per eigenvalue, iterate in shared memory ([i][t], conflict free),
 //     pivoted LU in the global workspace (L1-resident per thread column).
-//  4. Back-transform with 8 threads per eigenvector (32 rows each in registers).
+//  4. Back-transform with 8 threads per eigenvector (32 rows each in registers), vectors in
+//     batches of 64 (counts up to 128: the C5 rank sweep n = 96).
 #pragma once
 
 constexpr int kBigNT = 512;
@@ -376,11 +377,11 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, const 
 #undef XV
     }
     GWT_CLK(t_ph3);
-    // 4. back-transform, 8 threads per eigenvector (rows i = qb mod 8)
-    {
+    // 4. back-transform, 8 threads per eigenvector (rows i = qb mod 8), vectors in batches of NT/8
+    for (int tb = 0; tb < count; tb += NT / 8) {
         constexpr int QB = 8, RPT = DM / QB;
-        const int t = tid / QB, qb = tid % QB;
-        const bool on = t < count;  // count <= 64
+        const int t = tb + tid / QB, qb = tid % QB;
+        const bool on = t < count;
         if (on && qb == 0 && evals) evals[b * count + t] = lamv[t];
         C y[RPT];
 #pragma unroll

@@ -1072,8 +1072,8 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
         }
     }
     const bool cr_fits = D <= 128 && count <= 64 && eig_cta_layout(D, count, sizeof(T)).total <= 227 * 1024;
-    if (sizeof(T) == 4 && !force_cta && !force_warp && !legacy_warp && D > 64 && D <= 256 && count <= 64 &&
-        !(D <= 128 && cr_fits)) {
+    if (sizeof(T) == 4 && !force_cta && !force_warp && !legacy_warp && D > 64 && D <= 256 && count <= 128 &&
+        eig_big_smem(D, count) <= 227 * 1024 && !(D <= 128 && cr_fits)) {
         // fp32, matrix in the (L2-resident) global workspace (eig_big.cuh)
         const size_t sm = eig_big_smem(D, count);
         cudaError_t e = cudaFuncSetAttribute(k_heev_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

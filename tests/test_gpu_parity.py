@@ -335,6 +335,18 @@ def test_large_configs_parity(ctx, name, ngroups, sweeps, F):
     assert rel_err(rep.sinr, want).max() <= 1e-4
 
 
+@pytest.mark.parametrize("n,p", [(16, 8), (96, 32)])
+def test_c5_rank_sweep_corners(ctx, n, p):
+    """BASELINE C5 rank sweep corners (Nt-mode n in {16..96}, K-mode p in {8..32}) on the C5 shape:
+    NMSE trace vs the oracle (exercises the count > 64 eigensolver route for n = 96)."""
+    import dataclasses
+    cfg = dataclasses.replace(gw.CONFIGS["C5"], n=n, p=p)
+    X, X128, tau = baseline_inputs(cfg, 1)
+    fo = O.alternating_solve(dims_of(cfg), X128, 2, early_stop=False, nthreads=8)
+    res = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), 2, early_stop=False)
+    assert np.max(np.abs(res.trace / res.energy[:, None] - fo["trace"] / fo["energy"][:, None])) <= 1e-6
+
+
 @pytest.mark.parametrize("name,ngroups", [("C1", None), ("C2", 2), ("C2d", 2)])
 def test_full_pipeline_parity(ctx, name, ngroups):
     """run_full_pipeline (the e_c / R_t comparator) on the uncompressed channels vs the oracle."""
