@@ -137,6 +137,32 @@ def binding_roofline(flops, pipe, nbytes, ms, hbm, peaks_t):
     return {"bound": pipe, "achieved": ach, "peak": peaks_t[pipe], "unit": "TFLOP/s", "frac": ach / peaks_t[pipe]}
 
 
+def cublas_peaks(dev):
+    """Measured FP32 (SGEMM, TF32 off) and FP64 (DGEMM) cuBLAS throughput on this GPU, best of a few
+    square GEMMs timed with CUDA events: the achievable CUDA-core ceilings SURVEY.md §8(d) asks for
+    beside the derived 148 SM x clock peaks (cuBLAS is a measuring tool here, not on the hot path)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    out = {}
+    for name, dt, n, reps in (("sgemm_tflops", torch.float32, 8192, 5), ("dgemm_tflops", torch.float64, 4096, 3)):
+        a = torch.randn(n, n, dtype=dt, device=dev)
+        b = torch.randn(n, n, dtype=dt, device=dev)
+        torch.matmul(a, b)
+        best = 1e30
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = 2.0 * n ** 3 / (best * 1e-3) / 1e12
+        del a, b
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    return out
+
+
 def tucker_flops(cfg):
     """Canonical-order flops of one groupwise_solve (init + S sweeps) per SURVEY.md §8(d)."""
     M, N, P, m, n, p, S = cfg.M, cfg.N, cfg.P, cfg.m, cfg.n, cfg.p, cfg.sweeps
@@ -271,6 +297,21 @@ def main():
         e1.synchronize()
         tt.append(e0.elapsed_time(e1))
     tucker_stage = ctx.stage_ms()
+    # reference stop rule (decompose.cpp:363-368: stop once decrease < 1e-10 * energy), timed the same way
+    es_ms, es_iters = [], None
+    for it in range(4):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fes = ctx.groupwise_solve(topo, X, ranks, cfg.sweeps, early_stop=True)
+        e1.record(stream)
+        e1.synchronize()
+        if it > 0:
+            es_ms.append(e0.elapsed_time(e1))
+        if os.environ.get("GWT_BENCH_DEBUG"):
+            print("early-stop solve ms", e0.elapsed_time(e1), ctx.stage_ms()[:3], file=sys.stderr)
+        it_ = fes.iterations_run
+        es_iters = np.asarray(it_.cpu() if hasattr(it_, "cpu") else it_)
     barrier()
 
     # ---------------- SINR stage (the step), device-resident inputs
@@ -383,6 +424,7 @@ def main():
     # ---------------- roofline of the dominant SINR kernel (binding resource), all stages listed
     hbm, peak_kind, pk = peaks()
     clk_max = pk.get("sm_max_mhz", 1965.0)
+    cublas = cublas_peaks(dev)
     peaks_t = {"fp32": 148 * 128 * 2 * clk_max * 1e6 / 1e12, "fp64": 148 * 64 * 2 * clk_max * 1e6 / 1e12}
     costs = sinr_costs(cfg, cs)
     stage = {"rebuild": st_acc[4], "pair_gram": st_acc[5], "small": st_acc[6]}
@@ -418,8 +460,13 @@ def main():
               "algorithmic_tflops": tfl / (tk * 1e-3) / 1e12,
               "roofline": {"bound": "fp32-cuda-core", "achieved": tfl / (tk * 1e-3) / 1e12, "peak": fp32_peak,
                            "unit": "TFLOP/s", "frac": tfl / (tk * 1e-3) / 1e12 / fp32_peak,
+                           "frac_vs_cublas": tfl / (tk * 1e-3) / 1e12 / cublas["sgemm_tflops" if cs == 8 else "dgemm_tflops"],
                            "peak_source": "derived 148 SMs x 128 FFMA x 2 x max clock (not measured)"},
               "stage_ms": {"init_obj": tucker_stage[1], "sweeps": tucker_stage[2]},
+              "early_stop": {"mode": "reference stop rule (decrease < 1e-10 * energy)",
+                             "ms_per_solve": float(np.mean(es_ms)),
+                             "value": cfg.links * world / (float(np.mean(es_ms)) * 1e-3),
+                             "iterations_mean": float(es_iters.mean()), "iterations_max": int(es_iters.max())},
               "e2e_ms": tuck_e2e_ms, "e2e_h2d_bytes": Xh.nbytes,
               "e2e_d2h_bytes": sum(int(np.prod(a.shape)) * cs for a in (fac_h.rx, fac_h.tx, fac_h.delay, fac_h.cores))}
     cpu = None
@@ -443,6 +490,7 @@ def main():
             "tucker": tucker,
             "paper_metrics": paper,
             "clocks": clk.summary(),
+            "cublas_peaks": cublas,
             "status_nonzero": int(bad),
             "wall_s_timed": t_wall,
         }

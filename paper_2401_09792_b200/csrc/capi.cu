@@ -43,14 +43,19 @@ struct gwt_ctx {
         void* p = nullptr;
         size_t bytes = 0;
     };
-    std::vector<Slot> slots = std::vector<Slot>(32);
+    std::vector<Slot> slots = std::vector<Slot>(40);
     cudaEvent_t ev[16] = {};
+    int* pinned[8] = {};  // per solver lane: early-stop count read back without a blocking copy
+    int* pin(int lane) {
+        if (!pinned[lane]) ck(cudaMallocHost(&pinned[lane], 64), "cudaMallocHost");
+        return pinned[lane];
+    }
     double stage_ms[8] = {};
     // extra solver lanes (stream + workspace) that run group sub-chunks concurrently with lane 0 (ctx->stream)
     struct Lane {
         cudaStream_t st = nullptr;
         cudaEvent_t ev = nullptr;
-        std::vector<Slot> slots = std::vector<Slot>(32);
+        std::vector<Slot> slots = std::vector<Slot>(40);
     };
     std::vector<Lane> lanes;
 
@@ -80,7 +85,7 @@ namespace {
 enum {
     WS_X = 0, WS_A, WS_B, WS_C, WS_G, WS_Y1, WS_W, WS_W2, WS_Z, WS_Z2, WS_GRAM, WS_EIGA, WS_EIGZ, WS_EIGX, WS_POOL,
     WS_ENERGY, WS_CAPT, WS_TRACE, WS_FAIL, WS_FROZEN, WS_TAU, WS_FREQ, WS_COEF, WS_H, WS_PG, WS_EG, WS_SINR, WS_SIG,
-    WS_STATUS, WS_MISC, WS_PART, WS_GPART
+    WS_STATUS, WS_MISC, WS_PART, WS_GPART, WS_STOP
 };
 
 size_t ws_budget() {
@@ -179,14 +184,15 @@ struct SolveLane {
     int hfail = 0;
     GemmDesc dZ{}, dZ2{}, dG{}, dY1{}, dW{}, dW2{};
     int rx_kind = 0, tx_kind = 0, rx_copies = 0, tx_copies = 0;
-    // early stop (decompose.cpp:363-368)
+    // early stop (decompose.cpp:363-368), decided on the device (k_stop_freeze)
     bool early = false;
-    std::vector<char> stopped;
     std::vector<int> iters;
-    std::vector<double> trace_h, energy_h;
     char* frozen = nullptr;
+    int* stopd = nullptr;  // [G flags][G iterations_run][count]
+    int* hcount = nullptr;  // pinned copy of the stopped count
+    cudaEvent_t sev[3] = {};
+    bool done = false;
     size_t a_sz = 0, b_sz = 0, c_sz = 0, g_sz = 0;
-    int64_t active = 0;
 
     void* ws(int slot, size_t bytes) { return ctx->lws(lane, slot, bytes); }
     void gemm(const GemmDesc& d, const void* in, const void* U, void* out) {
@@ -279,19 +285,20 @@ struct SolveLane {
             gram_eig(g3, X, t.P, t.p, Cf, 0);
         }
         objective(0);
-        stopped.assign(G, 0);
         a_sz = cs * users * t.M * t.m;
         b_sz = cs * t.J * t.N * t.n;
         c_sz = cs * links * t.P * t.p;
         g_sz = cs * links * t.m * t.n * t.p;
         if (early) {
             frozen = (char*)ws(WS_FROZEN, (a_sz + b_sz + c_sz + g_sz) * G);
-            energy_h.resize(G);
-            ck(cudaMemcpyAsync(energy_h.data(), energy, 8 * G, cudaMemcpyDeviceToHost, st), "D2H");
+            stopd = (int*)ws(WS_STOP, 4 * (2 * G + 1));
+            ck(cudaMemsetAsync(stopd, 0, 4 * (2 * G + 1), st), "memset");
+            hcount = ctx->pin(lane);
+            *hcount = 0;
+            for (auto& e : sev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
         }
-        trace_h.assign((size_t)G * (sweeps + 1), 0.0);
         iters.assign(G, sweeps);
-        active = G;
+        done = false;
     }
 
     // enqueue one alternating sweep (decompose.cpp:330-370): rx, tx, delay factors, then cores + objective
@@ -310,39 +317,29 @@ struct SolveLane {
         gemm(dG, Z2, Cf, Gc);
         ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)t.links() * t.m * t.n * t.p, G, capt, part, st));
         ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, s + 1, st));
-        if (early) ck(cudaMemcpyAsync(trace_h.data(), trace_d, 8 * trace_h.size(), cudaMemcpyDeviceToHost, st), "D2H");
+        if (early) {
+            ctx->launched(launch_stop_freeze(G, trace_d, energy, sweeps + 1, s, stopd, A, B, Cf, Gc, frozen, a_sz, b_sz,
+                                             c_sz, g_sz, st));
+            ck(cudaMemcpyAsync(hcount, stopd + 2 * G, 4, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaEventRecord(sev[s % 3], st), "cudaEventRecord");
+        }
     }
 
-    // host side, after the lane's stream has completed sweep s: freeze converged groups
-    void check(int s) {
-        for (int64_t g = 0; g < G; ++g) {
-            if (stopped[g]) continue;
-            const double dec = trace_h[g * (sweeps + 1) + s] - trace_h[g * (sweeps + 1) + s + 1];
-            if (dec < 1e-10 * energy_h[g]) {
-                stopped[g] = 1;
-                --active;
-                iters[g] = s + 1;
-                char* fz = frozen + g * (a_sz + b_sz + c_sz + g_sz);
-                ck(cudaMemcpyAsync(fz, (char*)A + g * a_sz, a_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                ck(cudaMemcpyAsync(fz + a_sz, (char*)B + g * b_sz, b_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                ck(cudaMemcpyAsync(fz + a_sz + b_sz, (char*)Cf + g * c_sz, c_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                ck(cudaMemcpyAsync(fz + a_sz + b_sz + c_sz, (char*)Gc + g * g_sz, g_sz, cudaMemcpyDeviceToDevice, st),
-                   "D2D");
-            }
-        }
+    // host side, early-stop mode: wait for sweep s to finish (the lane keeps the next sweep queued)
+    // and retire the lane once every group in it has stopped
+    void poll(int s) {
+        ck(cudaEventSynchronize(sev[s % 3]), "cudaEventSynchronize");
+        if (*hcount >= G) done = true;
     }
 
     void end() {
         if (early) {
-            for (int64_t g = 0; g < G; ++g) {
-                if (!stopped[g]) continue;
-                char* fz = frozen + g * (a_sz + b_sz + c_sz + g_sz);
-                ck(cudaMemcpyAsync((char*)A + g * a_sz, fz, a_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                ck(cudaMemcpyAsync((char*)B + g * b_sz, fz + a_sz, b_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                ck(cudaMemcpyAsync((char*)Cf + g * c_sz, fz + a_sz + b_sz, c_sz, cudaMemcpyDeviceToDevice, st), "D2D");
-                ck(cudaMemcpyAsync((char*)Gc + g * g_sz, fz + a_sz + b_sz + c_sz, g_sz, cudaMemcpyDeviceToDevice, st),
-                   "D2D");
-            }
+            ctx->launched(launch_unfreeze(G, stopd, A, B, Cf, Gc, frozen, a_sz, b_sz, c_sz, g_sz, st));
+            std::vector<int> h(2 * G);
+            ck(cudaMemcpyAsync(h.data(), stopd, 8 * G, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "sync");
+            for (int64_t g = 0; g < G; ++g) iters[g] = h[g] ? h[G + g] : sweeps;
+            for (auto& e : sev) cudaEventDestroy(e);
         }
         ck(cudaMemcpyAsync(&hfail, failp, 4, cudaMemcpyDeviceToHost, st), "D2H");
     }
@@ -400,20 +397,19 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
     }
     tm.mark(2);
     const bool early = flags & GWT_SOLVE_EARLY_STOP;
+    // early stop is decided on the device; the host stays one sweep ahead of each lane (so the GPU
+    // never idles on it) and stops enqueuing a lane once all its groups have stopped
     for (int s = 0; s < sweeps; ++s) {
         bool any = false;
         for (auto& ln : lanes)
-            if (ln.active > 0) {
+            if (!ln.done) {
                 ln.sweep(s);
                 any = true;
             }
         if (!any) break;
-        if (early)
+        if (early && s >= 1 && !std::getenv("GWT_NO_POLL"))
             for (auto& ln : lanes)
-                if (ln.active > 0) {
-                    ck(cudaStreamSynchronize(ln.st), "sync");
-                    ln.check(s);
-                }
+                if (!ln.done) ln.poll(s - 1);
     }
     for (auto& ln : lanes) ln.end();
     for (int l = 1; l < L; ++l) {  // ctx->stream waits for the other lanes
@@ -900,6 +896,8 @@ void gwt_ctx_destroy(gwt_ctx* ctx) {
     }
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto* p : ctx->pinned)
+        if (p) cudaFreeHost(p);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }

@@ -203,6 +203,178 @@ __global__ void __launch_bounds__(128) k_rebuild_link(Topo t, int Fc, int64_t f0
     }
 }
 
+// K1 v2 (register-blocked; the default for c64/c128 when p <= 32): ncu showed k_rebuild_link
+// limited by the L1/shared-memory pipe (l1tex 83 %, FMA pipe 49 %): every cMAC of H~ = G E re-read
+// one G entry and half an E pair. Here each thread keeps an RB x 8 block of H~ (RB rows 32 apart,
+// 8 subcarriers) in registers, so one q step costs RB conflict-free G loads + 4 broadcast 16-byte E
+// loads for 32*RB FFMA; E = C^T ph is blocked as (subcarrier, half of the q range) with two q per
+// 16-byte broadcast load of the transposed C. Phasors are formed once per (tap, subcarrier) tile
+// entry (binary64 argument reduction, conj_coeff). One CTA per (subcarrier tile range, link, group).
+template <class T, int FT, int RB, int PH, bool GS>
+__global__ void __launch_bounds__(128) k_rebuild_rb(Topo t, int Fc, int64_t f0, int tpc,
+                                                    const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
+                                                    const double* __restrict__ tau, const double* __restrict__ freqs,
+                                                    cplx_t<T>* __restrict__ H) {
+    using C = cplx_t<T>;
+    constexpr int NT = 128, QG = NT / FT;  // q groups in the E phase
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int P = t.P, p = t.p, mn = t.m * t.n, links = t.links();
+    const int pp = QG * PH;  // padded q extent (C^T row length, E rows)
+    C* ph = reinterpret_cast<C*>(smem_raw);  // [P][FT]
+    C* E = ph + (size_t)P * FT;              // [pp][FT]
+    C* sG = E + (size_t)pp * FT;             // [p][mn]
+    C* sCt = sG + (GS ? (size_t)p * mn : 0);  // [P][pp]  (transposed C_l, zero padded)
+    double* st = reinterpret_cast<double*>(sCt + (size_t)P * pp);  // [P]
+    const int l = blockIdx.y;
+    const int64_t g = blockIdx.z;
+    const int64_t gl = g * links + l;
+    const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+    const C* Gl = G + gl * (int64_t)mn * p;
+    const C* Cl = Cd + gl * (int64_t)P * p;
+    if constexpr (GS)
+        for (int e = tid; e < mn * p; e += NT) sG[e] = Gl[e];
+    for (int e = tid; e < P * pp; e += NT) {
+        const int r = e / pp, q = e % pp;
+        sCt[e] = q < p ? Cl[r + (size_t)P * q] : czero<C>();
+    }
+    for (int e = tid; e < P; e += NT) st[e] = tau[gl * P + e];
+    const int ntile = (Fc + FT - 1) / FT;
+    const int tbeg = blockIdx.x * tpc, tend = min(ntile, tbeg + tpc);
+    const int64_t fstride = (int64_t)links * mn;  // H~ stride between subcarriers
+    const int nrb = (mn + 32 * RB - 1) / (32 * RB);
+    for (int tile = tbeg; tile < tend; ++tile) {
+        const int ft0 = tile * FT, nf = min(FT, Fc - ft0);
+        __syncthreads();  // previous tile's ph/E consumed (and staging done on the first pass)
+        {
+            const int f = tid % FT;
+            const double fr = f < nf ? freqs[f0 + ft0 + f] : 0.0;
+            for (int r = tid / FT; r < P; r += QG) ph[r * FT + f] = f < nf ? conj_coeff<T>(fr, st[r]) : czero<C>();
+        }
+        __syncthreads();
+        {
+            const int f = tid % FT, q0 = (tid / FT) * PH;
+            C acc[PH];
+#pragma unroll
+            for (int i = 0; i < PH; ++i) acc[i] = czero<C>();
+            for (int r = 0; r < P; ++r) {
+                const C x = ph[r * FT + f];
+                const C* cr = sCt + (size_t)r * pp + q0;
+                if constexpr (sizeof(C) == 8 && PH % 2 == 0) {
+                    const float4* c4 = reinterpret_cast<const float4*>(cr);  // pp, q0 even: 16-byte aligned
+#pragma unroll
+                    for (int i = 0; i < PH / 2; ++i) {
+                        const float4 cv = c4[i];
+                        cfma(acc[2 * i], C{cv.x, cv.y}, x);
+                        cfma(acc[2 * i + 1], C{cv.z, cv.w}, x);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < PH; ++i) cfma(acc[i], cr[i], x);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < PH; ++i) E[(q0 + i) * FT + f] = acc[i];
+        }
+        __syncthreads();
+        for (int item = warp; item < nrb * (FT / 8); item += NT / 32) {
+            const int rb = item % nrb, fb = (item / nrb) * 8;
+            if (fb >= nf) continue;
+            const int row0 = rb * 32 * RB + lane;
+            C acc[RB][8];
+#pragma unroll
+            for (int u = 0; u < RB; ++u)
+#pragma unroll
+                for (int f = 0; f < 8; ++f) acc[u][f] = czero<C>();
+            for (int q = 0; q < p; ++q) {
+                C gv[RB];
+#pragma unroll
+                for (int u = 0; u < RB; ++u) {
+                    const int row = row0 + 32 * u;
+                    if constexpr (GS) gv[u] = row < mn ? sG[(size_t)q * mn + row] : czero<C>();
+                    else gv[u] = row < mn ? __ldg(Gl + (size_t)q * mn + row) : czero<C>();
+                }
+                const C* eq = E + q * FT + fb;
+                if constexpr (sizeof(C) == 8) {
+                    const float4* e4 = reinterpret_cast<const float4*>(eq);
+#pragma unroll
+                    for (int f2 = 0; f2 < 4; ++f2) {
+                        const float4 ev = e4[f2];
+#pragma unroll
+                        for (int u = 0; u < RB; ++u) {
+                            cfma(acc[u][2 * f2], gv[u], C{ev.x, ev.y});
+                            cfma(acc[u][2 * f2 + 1], gv[u], C{ev.z, ev.w});
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int f = 0; f < 8; ++f) {
+                        const C ev = eq[f];
+#pragma unroll
+                        for (int u = 0; u < RB; ++u) cfma(acc[u][f], gv[u], ev);
+                    }
+                }
+            }
+            C* hp = H + ((g * Fc + ft0 + fb) * links + l) * (int64_t)mn;
+#pragma unroll
+            for (int f = 0; f < 8; ++f, hp += fstride)
+                if (fb + f < nf)
+#pragma unroll
+                    for (int u = 0; u < RB; ++u) {
+                        const int row = row0 + 32 * u;
+                        if (row < mn) hp[row] = acc[u][f];
+                    }
+        }
+    }
+}
+
+template <class T, int FT, int RB, int PH, bool GS>
+static cudaError_t launch_rebuild_rb_t(const Topo& t, int ngroups, int Fc, int64_t f0, const void* Cd, const void* G,
+                                       const double* tau, const double* freqs, void* H, cudaStream_t st) {
+    using C = cplx_t<T>;
+    const int pp = (128 / FT) * PH, mn = t.m * t.n;
+    const size_t sm = sizeof(C) * ((size_t)t.P * FT + (size_t)pp * FT + (GS ? (size_t)t.p * mn : 0) + (size_t)t.P * pp) +
+                      8 * (size_t)t.P;
+    if (sm > 200 * 1024) return cudaErrorNotSupported;
+    cudaError_t e = cudaFuncSetAttribute(k_rebuild_rb<T, FT, RB, PH, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+    const int ntile = (Fc + FT - 1) / FT;
+    const int64_t base = (int64_t)ngroups * t.links();
+    // tiles per CTA: as many as keeps >= ~6 CTAs per SM in the grid (amortises the C/G staging),
+    // then evened out so no CTA gets a short remainder
+    int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(ntile, (base * ntile) / (148 * 6)));
+    const int nz = (ntile + tpc - 1) / tpc;
+    tpc = (ntile + nz - 1) / nz;
+    dim3 grid((ntile + tpc - 1) / tpc, t.links(), ngroups);
+    k_rebuild_rb<T, FT, RB, PH, GS><<<grid, 128, sm, st>>>(t, Fc, f0, tpc, (const C*)Cd, (const C*)G, tau, freqs, (C*)H);
+    return cudaGetLastError();
+}
+
+// dispatch: RB by the row count (mn a multiple of 96 -> 3, of 64 -> 2, else 1), PH by p; G staged in
+// shared memory when it is small (<= 32 KB), else read through L1/L2 (C3/C4: 60-200 KB per link)
+template <class T, int FT>
+static cudaError_t launch_rebuild_rb(const Topo& t, int ngroups, int Fc, int64_t f0, const void* Cd, const void* G,
+                                     const double* tau, const double* freqs, void* H, cudaStream_t st) {
+    constexpr int QG = 128 / FT;
+    const int mn = t.m * t.n;
+    const int ph = (t.p + QG - 1) / QG;
+    const int rb = (sizeof(T) == 4 && mn % 96 == 0) ? 3 : (mn % 64 == 0 ? 2 : 1);
+    const char* gse = std::getenv("GWT_REBUILD_GSMEM");
+    const bool gs = gse ? std::atoi(gse) != 0 : (size_t)mn * t.p * sizeof(cplx_t<T>) <= 32 * 1024;
+#define GWT_RB(RBV, PHV)                                                                                        \
+    if (rb == RBV && ph <= PHV)                                                                                 \
+        return gs ? launch_rebuild_rb_t<T, FT, RBV, PHV, true>(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st)   \
+                  : launch_rebuild_rb_t<T, FT, RBV, PHV, false>(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st);
+    if (QG == 2) {
+        GWT_RB(3, 6) GWT_RB(3, 8) GWT_RB(3, 12) GWT_RB(3, 16) GWT_RB(2, 6) GWT_RB(2, 8) GWT_RB(2, 12) GWT_RB(2, 16)
+        GWT_RB(1, 8) GWT_RB(1, 16)
+    } else {
+        GWT_RB(3, 4) GWT_RB(3, 6) GWT_RB(3, 8) GWT_RB(2, 4) GWT_RB(2, 6) GWT_RB(2, 8) GWT_RB(1, 4) GWT_RB(1, 8)
+    }
+#undef GWT_RB
+    return cudaErrorNotSupported;
+}
+
 // scope slot s of user (i,j) -> (k,l), mirroring scope_pairs (sinr.cpp:47-62)
 __device__ __forceinline__ void scope_slot(const Topo& t, int scope, int i, int j, int s, int& k, int& l) {
     if (scope == 0) {  // full: all (k,l) k-major
@@ -1765,6 +1937,17 @@ cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64
     if (sizeof(T) == 4 && !coeffs && rtc && std::atoi(rtc) != 0) {
         // tensor-core rebuild (k_tc.cu, opt-in) when the shape fits; else the CUDA-core kernels below
         cudaError_t e = launch_rebuild_tc(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
+    if (!coeffs && !std::getenv("GWT_REBUILD_V1")) {
+        // subcarrier tile: 64 while the phasor tile (P x 64) stays <= 16 KB (C1/C2), else 32 (C3-C5:
+        // P = 48/64, where FT = 64 halves the resident CTAs); GWT_REBUILD_FT overrides
+        const char* ftv = std::getenv("GWT_REBUILD_FT");
+        const int ft = ftv ? std::atoi(ftv) : (t.P * 64 * (int)sizeof(C) <= 16 * 1024 ? 64 : 32);
+        cudaError_t e = (ft == 32)
+                            ? launch_rebuild_rb<T, 32>(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st)
+                            : launch_rebuild_rb<T, 64>(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st);
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();
     }

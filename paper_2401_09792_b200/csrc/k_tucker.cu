@@ -421,6 +421,73 @@ __global__ void k_objective(int64_t ngroups, const double* __restrict__ energy, 
     if (g < ngroups) trace[g * stride + slot] = energy[g] - captured[g];
 }
 
+// Early stop on the device (decompose.cpp:363-368): after sweep s, group g stops when
+// trace[s] - trace[s+1] < 1e-10 * energy (NaN never stops, as on the host); its factors and core
+// are copied to `frozen` at that point and restored by k_unfreeze after the last sweep, so the
+// host never synchronises per sweep. stop = [G flags][G iterations_run][1 stopped count].
+__global__ void k_stop_freeze(int64_t ngroups, const double* __restrict__ trace, const double* __restrict__ energy,
+                              int stride, int s, int* __restrict__ stop, const char* __restrict__ A,
+                              const char* __restrict__ B, const char* __restrict__ Cf, const char* __restrict__ Gc,
+                              char* __restrict__ frozen, int64_t a_sz, int64_t b_sz, int64_t c_sz, int64_t g_sz) {
+    const int64_t g = blockIdx.x;
+    if (stop[g]) return;
+    const double dec = trace[g * stride + s] - trace[g * stride + s + 1];
+    if (!(dec < 1e-10 * energy[g])) return;
+    // byte sizes are multiples of 8 (complex64 and up)
+    const int64_t tot = a_sz + b_sz + c_sz + g_sz;
+    unsigned long long* fz = reinterpret_cast<unsigned long long*>(frozen + g * tot);
+    const int64_t na = a_sz / 8, nb = b_sz / 8, nc = c_sz / 8, ng = g_sz / 8;
+    const unsigned long long* sa = reinterpret_cast<const unsigned long long*>(A + g * a_sz);
+    const unsigned long long* sb = reinterpret_cast<const unsigned long long*>(B + g * b_sz);
+    const unsigned long long* sc = reinterpret_cast<const unsigned long long*>(Cf + g * c_sz);
+    const unsigned long long* sg = reinterpret_cast<const unsigned long long*>(Gc + g * g_sz);
+    for (int64_t e = threadIdx.x; e < na + nb + nc + ng; e += blockDim.x)
+        fz[e] = e < na ? sa[e] : e < na + nb ? sb[e - na] : e < na + nb + nc ? sc[e - na - nb] : sg[e - na - nb - nc];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        stop[g] = 1;
+        stop[ngroups + g] = s + 1;
+        atomicAdd(stop + 2 * ngroups, 1);
+    }
+}
+
+__global__ void k_unfreeze(int64_t ngroups, const int* __restrict__ stop, char* __restrict__ A, char* __restrict__ B,
+                           char* __restrict__ Cf, char* __restrict__ Gc, const char* __restrict__ frozen, int64_t a_sz,
+                           int64_t b_sz, int64_t c_sz, int64_t g_sz) {
+    const int64_t g = blockIdx.x;
+    if (!stop[g]) return;
+    const int64_t tot = a_sz + b_sz + c_sz + g_sz;
+    const unsigned long long* fz = reinterpret_cast<const unsigned long long*>(frozen + g * tot);
+    const int64_t na = a_sz / 8, nb = b_sz / 8, nc = c_sz / 8, ng = g_sz / 8;
+    unsigned long long* da = reinterpret_cast<unsigned long long*>(A + g * a_sz);
+    unsigned long long* db = reinterpret_cast<unsigned long long*>(B + g * b_sz);
+    unsigned long long* dc = reinterpret_cast<unsigned long long*>(Cf + g * c_sz);
+    unsigned long long* dg = reinterpret_cast<unsigned long long*>(Gc + g * g_sz);
+    for (int64_t e = threadIdx.x; e < na + nb + nc + ng; e += blockDim.x) {
+        const unsigned long long v = fz[e];
+        if (e < na) da[e] = v;
+        else if (e < na + nb) db[e - na] = v;
+        else if (e < na + nb + nc) dc[e - na - nb] = v;
+        else dg[e - na - nb - nc] = v;
+    }
+}
+
+cudaError_t launch_stop_freeze(int64_t ngroups, const double* trace, const double* energy, int stride, int s, int* stop,
+                               const void* A, const void* B, const void* Cf, const void* Gc, void* frozen, int64_t a_sz,
+                               int64_t b_sz, int64_t c_sz, int64_t g_sz, cudaStream_t st) {
+    k_stop_freeze<<<(unsigned)ngroups, 256, 0, st>>>(ngroups, trace, energy, stride, s, stop, (const char*)A,
+                                                      (const char*)B, (const char*)Cf, (const char*)Gc, (char*)frozen,
+                                                      a_sz, b_sz, c_sz, g_sz);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unfreeze(int64_t ngroups, const int* stop, void* A, void* B, void* Cf, void* Gc, const void* frozen,
+                            int64_t a_sz, int64_t b_sz, int64_t c_sz, int64_t g_sz, cudaStream_t st) {
+    k_unfreeze<<<(unsigned)ngroups, 256, 0, st>>>(ngroups, stop, (char*)A, (char*)B, (char*)Cf, (char*)Gc,
+                                                   (const char*)frozen, a_sz, b_sz, c_sz, g_sz);
+    return cudaGetLastError();
+}
+
 // Broadcast one factor per group to `copies` slots per group (shared model).
 template <class T>
 __global__ void k_broadcast(const cplx_t<T>* __restrict__ src, cplx_t<T>* __restrict__ dst, int64_t elems, int copies,

@@ -55,6 +55,11 @@ template <class T> cudaError_t launch_gram(const Topo& t, const GramDesc& d, int
 constexpr int kSqnormMaxBlocks = 128;
 template <class T> cudaError_t launch_group_sqnorm(const void* v, int64_t per_group, int64_t ngroups, double* out,
                                                    double* partial, cudaStream_t st);
+cudaError_t launch_stop_freeze(int64_t ngroups, const double* trace, const double* energy, int stride, int s, int* stop,
+                               const void* A, const void* B, const void* Cf, const void* Gc, void* frozen, int64_t a_sz,
+                               int64_t b_sz, int64_t c_sz, int64_t g_sz, cudaStream_t st);
+cudaError_t launch_unfreeze(int64_t ngroups, const int* stop, void* A, void* B, void* Cf, void* Gc, const void* frozen,
+                            int64_t a_sz, int64_t b_sz, int64_t c_sz, int64_t g_sz, cudaStream_t st);
 cudaError_t launch_objective(int64_t ngroups, const double* energy, const double* captured, double* trace, int stride,
                              int slot, cudaStream_t st);
 template <class T> cudaError_t launch_broadcast(const void* src, void* dst, int64_t elems, int copies, int64_t ngroups,

@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "rank_sweep or leading or large" 2>&1 | tail -3
+GWT_BENCH_DEBUG=1 timeout 400 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -5 gpurun_out/bench.err
