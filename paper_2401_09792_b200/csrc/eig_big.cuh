@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, const 
             if (__all_sync(0xffffffffu, done)) break;
             const float step = (hi - lo) / (float)(S + 1);
             const float pt = lo + (float)(s + 1) * step;
-            const bool le = !done && sturm_count_f32(D, fd, fe2, pt, 1e-30f) <= want;
+            const bool le = !done && sturm_count_r<float>(D, fd, fe2, pt) <= want;
             const unsigned bits = __ballot_sync(0xffffffffu, le);
             if (!done) {
                 const int j = __popc((bits >> (gl * S)) & ((1u << S) - 1u));
@@ -300,13 +300,13 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, const 
                     R mult;
                     if (fabsf(dcur) >= fabsf(sb)) {
                         const R di = dcur == 0.f ? tiny : dcur;
-                        mult = sb / di;
+                        mult = ii_div(sb, di);
                         LU_(DDv, i) = di;
                         LU_(DUv, i) = ucur;
                         dcur = dn - mult * ucur;
                         ucur = en;
                     } else {
-                        mult = dcur / sb;
+                        mult = ii_div(dcur, sb);
                         sw[i >> 5] |= 1u << (i & 31);
                         LU_(DDv, i) = sb;
                         LU_(DUv, i) = dn;

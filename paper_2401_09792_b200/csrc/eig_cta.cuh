@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
             if (__all_sync(0xffffffffu, done)) break;
             const float step = (hi - lo) / (float)(S + 1);
             const float pt = lo + (float)(s + 1) * step;
-            const bool le = !done && sturm_count_f32(D, fd, fe2, pt, 1e-30f) <= want;
+            const bool le = !done && sturm_count_r<R>(D, fd, fe2, pt) <= want;
             const unsigned bits = __ballot_sync(0xffffffffu, le);
             if (!done) {
                 const int j = __popc((bits >> (gl * S)) & ((S == 32 ? 0u : (1u << S)) - 1u));
@@ -458,13 +458,13 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                     R mult;
                     if (fabs(dcur) >= fabs(sb)) {
                         const R di = dcur == R(0) ? tiny : dcur;
-                        mult = sb / di;
+                        mult = ii_div(sb, di);
                         LU_(DDv, i) = di;
                         LU_(DUv, i) = ucur;
                         dcur = dn - mult * ucur;
                         ucur = en;
                     } else {
-                        mult = dcur / sb;
+                        mult = ii_div(dcur, sb);
                         sw[i >> 5] |= 1u << (i & 31);
                         LU_(DDv, i) = sb;
                         LU_(DUv, i) = dn;
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                 for (int i = 0; i < D; ++i) {
                     R di = LU_(DDv, i);
                     if (fabs(di) < tiny) di = di < R(0) ? -tiny : tiny;
-                    LU_(DDv, i) = R(1) / di;
+                    LU_(DDv, i) = ii_div(R(1), di);
                 }
                 for (int i = 0; i < D; ++i) XV(i) = R(1) + R(0.25) * (R)__sinf(0.7f * i + 1.3f * t);
                 for (int it = 0; it <= kSolves; ++it) {
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                         if (fail) atomicExch(fail, 1);
                         break;
                     }
-                    const R sc = R(1) / mx;
+                    const R sc = ii_div(R(1), mx);
                     for (int i = 0; i < D; ++i) XV(i) *= sc;
                 }
                 double rq = 0.0;

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
             if (__all_sync(0xffffffffu, done)) break;
             const float step = (hi - lo) / (float)(S + 1);
             const float pt = lo + (float)(s + 1) * step;
-            const bool le = !done && sturm_count_f32(D, fd, fe2, pt, 1e-30f) <= want;
+            const bool le = !done && sturm_count_r<R>(D, fd, fe2, pt) <= want;
             const unsigned bits = __ballot_sync(0xffffffffu, le);
             if (!done) {
                 const int j = __popc((bits >> (t * S)) & ((1u << S) - 1u));
@@ -281,13 +281,13 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
                 R mult;
                 if (fabs(dcur) >= fabs(sb)) {
                     const R di = dcur == R(0) ? tiny : dcur;
-                    mult = sb / di;
+                    mult = ii_div(sb, di);
                     LU_(DDv, i) = di;
                     LU_(DUv, i) = ucur;
                     dcur = dn - mult * ucur;
                     ucur = en;
                 } else {
-                    mult = dcur / sb;
+                    mult = ii_div(dcur, sb);
                     sw |= 1u << i;
                     LU_(DDv, i) = sb;
                     LU_(DUv, i) = dn;
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
             for (int i = 0; i < D; ++i) {  // reciprocal pivots (tiny-guarded)
                 R di = LU_(DDv, i);
                 if (fabs(di) < tiny) di = di < R(0) ? -tiny : tiny;
-                LU_(DDv, i) = R(1) / di;
+                LU_(DDv, i) = ii_div(R(1), di);
             }
 #pragma unroll
             for (int i = 0; i < DM; ++i) x[i] = i < D ? R(1) + R(0.25) * (R)__sinf(0.7f * i + 1.3f * t) : R(0);
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
                     if (fail) atomicExch(fail, 1);
                     break;
                 }
-                const R sc = R(1) / mx;
+                const R sc = ii_div(R(1), mx);
 #pragma unroll
                 for (int i = 0; i < DM; ++i) x[i] *= sc;
             }

@@ -95,6 +95,45 @@ __device__ __forceinline__ int sturm_count_fast(int D, const double* d, const do
 
 // fp32 Sturm count on a scaled tridiagonal: bisection only has to deliver an inverse-iteration
 // shift (~1e-7 relative); the reported eigenvalue is the binary64 Rayleigh quotient.
+// Division-free form: the count of sign changes of the leading-minor sequence
+// p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2} (p_0 = 1) equals the count of negative pivots
+// q_i = p_i / p_{i-1}, so the serial chain is one FFMA per row (the e^2 p_{i-2} product is off the
+// chain) instead of a reciprocal + multiply + add; the pair (p_{i-1}, p_i) is rescaled by a power
+// of two every 8 rows (|d - x| <= 2 on the normalised T keeps 8 rows far from overflow). An exact
+// zero p_i (+0) counts like the q = -pivmin convention: the sign change moves to the next row.
+// Used for the fp32-storage (c64) solvers; the c128 solvers keep the pivot recurrence below, whose
+// count is monotone in x (Kahan), so their fp32 shifts resolve small eigenvalues reproducibly.
+__device__ __forceinline__ int sturm_count_p32(int D, const float* d, const float* e2, float x) {
+    float pm = 1.0f, p = d[0] - x;
+    int cnt = (int)(__float_as_uint(p) >> 31);
+    int i = 1;
+    for (; i + 8 <= D; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float pn = fmaf(d[i + u] - x, p, -e2[i + u - 1] * pm);
+            cnt += (int)((__float_as_uint(pn) ^ __float_as_uint(p)) >> 31);
+            pm = p;
+            p = pn;
+        }
+        const float mx = fmaxf(fabsf(p), fabsf(pm));
+        const float sc = __int_as_float(0x7f000000 - (__float_as_int(mx) & 0x7f800000));  // ~1/mx, power of 2
+        p *= sc;
+        pm *= sc;
+    }
+    for (; i < D; ++i) {
+        const float pn = fmaf(d[i] - x, p, -e2[i - 1] * pm);
+        cnt += (int)((__float_as_uint(pn) ^ __float_as_uint(p)) >> 31);
+        pm = p;
+        p = pn;
+    }
+    return cnt;
+}
+
+// inverse-iteration arithmetic in the storage precision: fp32 uses the fast reciprocal (the LU of
+// T - lambda I only has to be backward stable; the eigenvalue is the binary64 Rayleigh quotient)
+__device__ __forceinline__ float ii_div(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double ii_div(double a, double b) { return a / b; }
+
 __device__ __forceinline__ int sturm_count_f32(int D, const float* d, const float* e2, float x, float pivmin) {
     int cnt = 0;
     float q = d[0] - x;
@@ -106,6 +145,11 @@ __device__ __forceinline__ int sturm_count_f32(int D, const float* d, const floa
         cnt += q < 0.0f;
     }
     return cnt;
+}
+template <class R>
+__device__ __forceinline__ int sturm_count_r(int D, const float* d, const float* e2, float x) {
+    if constexpr (sizeof(R) == 4) return sturm_count_p32(D, d, e2, x);
+    else return sturm_count_f32(D, d, e2, x, 1e-30f);
 }
 
 #include "eig_warp.cuh"
