@@ -57,31 +57,6 @@ __device__ __forceinline__ R rows_sum(R v) {
     return v;
 }
 
-// Householder reflector of x = (x0, tail) with ||tail||^2 = t2 (t2 > 0): alpha = -phase(x0) ||x||,
-// v0 = x0 - alpha, tau = 2 / ||v||^2. fp32: one rsqrt + one reciprocal on the step's critical path.
-__device__ __forceinline__ void reflector(float2 x0, float t2, float2& al, float2& v0, float& tk) {
-    const float s2 = x0.x * x0.x + x0.y * x0.y;
-    const float xn = sqrtf(t2 + s2);
-    if (s2 > 0.f) {
-        const float f = xn * rsqrtf(s2);  // ||x|| / |x0|
-        al = make_float2(-x0.x * f, -x0.y * f);
-        v0 = make_float2(x0.x * (1.f + f), x0.y * (1.f + f));
-        tk = __frcp_rn(0.5f * (t2 + s2 * (1.f + f) * (1.f + f)));
-    } else {
-        al = make_float2(-xn, 0.f);
-        v0 = make_float2(xn, 0.f);
-        tk = __frcp_rn(0.5f * (t2 + xn * xn));
-    }
-}
-__device__ __forceinline__ void reflector(double2 x0, double t2, double2& al, double2& v0, double& tk) {
-    const double ax0 = hypot(x0.x, x0.y);
-    const double xnorm = sqrt(t2 + ax0 * ax0);
-    const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
-    al = make_double2(-ph.x * xnorm, -ph.y * xnorm);
-    v0 = make_double2(x0.x - al.x, x0.y - al.y);
-    tk = 2.0 / (t2 + v0.x * v0.x + v0.y * v0.y);
-}
-
 // back-transform y = H_0 ... H_{D-3} diag(delta) z with QB threads per eigenvector (rows i = qb mod QB),
 // phase normalisation, store (shared by k_heev_cr's two thread-per-vector configurations)
 template <class R, int DM, int QB>

@@ -29,8 +29,8 @@ __host__ __device__ inline EigWarpLayout eig_warp_layout(int D, int count, int r
     L.field = o;                        \
     o = (o + (bytes) + 15) & ~size_t(15);
     GWT_TAKE(oA, (size_t)D * D * cs)
-    GWT_TAKE(ov, D * cs)
-    GWT_TAKE(ow, D * cs)
+    GWT_TAKE(ov, ((D + 31) / 32 * 32) * cs)  // a full warp's worth: hh_reg32 reads v/w pairs up to column 31
+    GWT_TAKE(ow, ((D + 31) / 32 * 32) * cs)
     GWT_TAKE(otau, D * (size_t)rs)
     GWT_TAKE(osub, D * cs)
     GWT_TAKE(odl, D * cs)
@@ -60,6 +60,115 @@ __device__ __forceinline__ float2 shfl_c(float2 v, int src) {
 }
 __device__ __forceinline__ double2 shfl_c(double2 v, int src) {
     return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// Householder reflector of x = (x0, tail) with ||tail||^2 = t2 (t2 > 0): alpha = -phase(x0) ||x||,
+// v0 = x0 - alpha, tau = 2 / ||v||^2. fp32: one rsqrt + one reciprocal on the step's critical path.
+__device__ __forceinline__ void reflector(float2 x0, float t2, float2& al, float2& v0, float& tk) {
+    const float s2 = x0.x * x0.x + x0.y * x0.y;
+    const float xn = sqrtf(t2 + s2);
+    if (s2 > 0.f) {
+        const float f = xn * rsqrtf(s2);  // ||x|| / |x0|
+        al = make_float2(-x0.x * f, -x0.y * f);
+        v0 = make_float2(x0.x * (1.f + f), x0.y * (1.f + f));
+        tk = __frcp_rn(0.5f * (t2 + s2 * (1.f + f) * (1.f + f)));
+    } else {
+        al = make_float2(-xn, 0.f);
+        v0 = make_float2(xn, 0.f);
+        tk = __frcp_rn(0.5f * (t2 + xn * xn));
+    }
+}
+__device__ __forceinline__ void reflector(double2 x0, double t2, double2& al, double2& v0, double& tk) {
+    const double ax0 = hypot(x0.x, x0.y);
+    const double xnorm = sqrt(t2 + ax0 * ax0);
+    const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
+    al = make_double2(-ph.x * xnorm, -ph.y * xnorm);
+    v0 = make_double2(x0.x - al.x, x0.y - al.y);
+    tk = 2.0 / (t2 + v0.x * v0.x + v0.y * v0.y);
+}
+
+// Register-resident Householder for fp32 storage and 16 < D <= 32 (phase 1 of k_heev_wr): lane r
+// keeps row r of the matrix in registers, so a reflector step costs two broadcast 16-byte shared
+// loads per column pair (v and w) instead of a shared-memory read-modify-write of the whole trailing
+// matrix (the old form was shared-pipe bound with ~12 warps per SM). v_c = w_c = 0 for c <= k, so
+// the mat-vec and the rank-2 update run unpredicated over a static column range [CB, 32): the k
+// loop is split into 4 blocks of 8 steps, each starting at column CB = 8 b.
+template <int CB>
+__device__ __forceinline__ void hh_reg_block(int k0, int k1, int D, int r, float2 (&a)[32], float2& x, float2* A,
+                                             float2* vv, float2* ww, float* tau, float2* sub) {
+    for (int k = k0; k < k1 && k + 2 < D; ++k) {
+        const bool act = r > k && r < D;
+        const float t2 = warp_sum_r<float>((r > k + 1 && r < D) ? x.x * x.x + x.y * x.y : 0.f);
+        const float2 x0 = shfl_c(x, k + 1);
+        if (t2 == 0.f) {  // warp-uniform: column already reduced
+            if (r == 0) {
+                tau[k] = 0.f;
+                sub[k] = x0;
+            }
+#pragma unroll
+            for (int c = CB; c < 32; ++c)
+                if (c == k + 1) x = a[c];
+            continue;
+        }
+        float2 al, v0;
+        float tk;
+        reflector(x0, t2, al, v0, tk);
+        const float2 v = act ? (r == k + 1 ? v0 : x) : make_float2(0.f, 0.f);
+        if (act) A[r + D * k] = v;  // reflector column k (read by the back-transform)
+        if (r == 0) {
+            tau[k] = tk;
+            sub[k] = al;
+        }
+        vv[r] = v;
+        __syncwarp();
+        float2 p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = CB; c < 32; c += 2) {
+            const float4 vc = *reinterpret_cast<const float4*>(vv + c);
+            cfma(p0, a[c], make_float2(vc.x, vc.y));
+            cfma(p1, a[c + 1], make_float2(vc.z, vc.w));
+        }
+        const float2 p = make_float2(tk * (p0.x + p1.x), tk * (p0.y + p1.y));
+        const float kk = 0.5f * tk * warp_sum_r<float>(act ? v.x * p.x + v.y * p.y : 0.f);
+        const float2 w = act ? make_float2(p.x - kk * v.x, p.y - kk * v.y) : make_float2(0.f, 0.f);
+        ww[r] = w;
+        __syncwarp();
+#pragma unroll
+        for (int c = CB; c < 32; c += 2) {
+            const float4 vc = *reinterpret_cast<const float4*>(vv + c);
+            const float4 wc = *reinterpret_cast<const float4*>(ww + c);
+            // a[r][c] -= v_r conj(w_c) + w_r conj(v_c)
+            a[c].x -= v.x * wc.x + v.y * wc.y + w.x * vc.x + w.y * vc.y;
+            a[c].y -= v.y * wc.x - v.x * wc.y + w.y * vc.x - w.x * vc.y;
+            a[c + 1].x -= v.x * wc.z + v.y * wc.w + w.x * vc.z + w.y * vc.w;
+            a[c + 1].y -= v.y * wc.z - v.x * wc.w + w.y * vc.z - w.x * vc.w;
+        }
+#pragma unroll
+        for (int c = CB; c < 32; ++c)
+            if (c == k + 1) x = a[c];
+        __syncwarp();  // v/w of this step consumed before the next step rewrites them
+    }
+}
+
+__device__ __forceinline__ void hh_reg32(int D, int r, float2* A, float2* vv, float2* ww, float* tau, float2* sub) {
+    float2 a[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a[c] = (r < D && c < D) ? A[r + D * c] : make_float2(0.f, 0.f);
+    float2 x = a[0];
+    hh_reg_block<0>(0, 8, D, r, a, x, A, vv, ww, tau, sub);
+    hh_reg_block<8>(8, 16, D, r, a, x, A, vv, ww, tau, sub);
+    hh_reg_block<16>(16, 24, D, r, a, x, A, vv, ww, tau, sub);
+    hh_reg_block<24>(24, 32, D, r, a, x, A, vv, ww, tau, sub);
+    // diagonal and the last subdiagonal entry back to shared memory (phase 2 reads them there)
+    float2 dg = make_float2(0.f, 0.f), ls = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+        if (c == r) dg = a[c];
+        if (c == D - 2) ls = a[c];
+    }
+    if (r < D) A[r + D * r] = dg;
+    if (r == D - 1 && D >= 2) A[(D - 1) + D * (D - 2)] = ls;
+    __syncwarp();
 }
 
 template <class R, int DM>
@@ -104,7 +213,13 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
     GWT_CLK(t_ph0);
     const int r = lane;
     // 1. Householder: A22 <- H A22 H, reflector of step k stored in column k below the diagonal
-    for (int k = 0; k + 2 < D; ++k) {
+    bool hh_done = false;
+    if constexpr (sizeof(R) == 4 && DM == 32) {
+        hh_reg32(D, r, reinterpret_cast<float2*>(A), reinterpret_cast<float2*>(vv), reinterpret_cast<float2*>(ww),
+                 reinterpret_cast<float*>(tau), reinterpret_cast<float2*>(sub));
+        hh_done = true;
+    }
+    for (int k = 0; !hh_done && k + 2 < D; ++k) {
         const bool act = r > k && r < D;
         C x = czero<C>();
         if (act) x = A[r + D * k];
