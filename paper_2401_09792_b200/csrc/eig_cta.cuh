@@ -149,7 +149,128 @@ __device__ __forceinline__ void cta_backtransform(int D, int count, int LD, int6
     }
 }
 
-template <class R, int DM, int NT>
+// Register-resident Householder for fp32 storage, 32 < D <= 64, 256 threads (phase 1 of k_heev_cr
+// with HREG, used for small batches where the per-matrix latency is the critical path: C2's tx
+// Grams, 193k -> 177k cycles; its 134 registers cost occupancy on the large delay batches of C3/C5):
+// thread (r, q) keeps A[r][q + 4u] (u < 16) in registers. The shared-memory matrix only receives
+// the column that becomes the next reflector (written by its owners during the update) plus the
+// diagonal at the end, so a step reads the reflector column and p by broadcast instead of
+// reading and writing the whole trailing matrix (the old form was shared-pipe bound).
+__device__ __forceinline__ void hh_cta_reg64(int D, int LD, float2* A, float2* pp, float* tau, float2* sub,
+                                             float* rt2, float* rkp) {
+    constexpr int Q = 4, NW = 8, U = 16;
+    const int tid = threadIdx.x, lane = tid % 32, wid = tid / 32;
+    const int r = tid / Q, q = tid % Q;
+    float2 a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int c = q + Q * u;
+        a[u] = (r < D && c < D) ? A[r + LD * c] : make_float2(0.f, 0.f);
+    }
+    {
+        float part = 0.f;
+        if (q == 0 && r > 1 && r < D) {
+            const float2 x = A[r];
+            part = x.x * x.x + x.y * x.y;
+        }
+        part = rows_sum<Q>(part);
+        if (lane == 0) rt2[wid] = part;
+    }
+    for (int k = 0; k + 2 < D; ++k) {
+        const bool act = r > k && r < D;
+        __syncthreads();  // [A] column k and its norm partials are in shared memory
+        float t2 = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) t2 += rt2[w];
+        const float2* colk = A + LD * k;
+        const float2 x0 = colk[k + 1];
+        const int kn = k + 1, qn = kn % Q, un = kn / Q;  // owner of column k+1
+        if (t2 == 0.f) {  // uniform: column already reduced
+            if (tid == 0) {
+                tau[k] = 0.f;
+                sub[k] = x0;
+            }
+            __syncthreads();  // rt2 reads done
+            float2 xn = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (u == un) xn = a[u];
+            float part = 0.f;
+            if (q == qn && r < D) {
+                A[r + LD * kn] = xn;
+                if (r > kn + 1) part = xn.x * xn.x + xn.y * xn.y;
+            }
+            part = __shfl_sync(0xffffffffu, rows_sum<Q>(part), qn);  // the owner lanes hold the partials
+            if (lane == 0) rt2[wid] = part;
+            continue;
+        }
+        float2 al, v0;
+        float tk;
+        reflector(x0, t2, al, v0, tk);
+        const float2 v = act ? (r == k + 1 ? v0 : colk[r]) : make_float2(0.f, 0.f);
+        float2 vc[U];
+        float2 p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = q + Q * u;
+            vc[u] = (c > k && c < D) ? (c == k + 1 ? v0 : colk[c]) : make_float2(0.f, 0.f);
+            if (u & 1) cfma(p1, a[u], vc[u]);
+            else cfma(p0, a[u], vc[u]);
+        }
+        float2 p = make_float2(p0.x + p1.x, p0.y + p1.y);
+#pragma unroll
+        for (int o = 1; o < Q; o <<= 1) {
+            p.x += __shfl_xor_sync(0xffffffffu, p.x, o);
+            p.y += __shfl_xor_sync(0xffffffffu, p.y, o);
+        }
+        p = make_float2(p.x * tk, p.y * tk);
+        float kp = (q == 0 && act) ? v.x * p.x + v.y * p.y : 0.f;
+        kp = rows_sum<Q>(kp);
+        if (lane == 0) rkp[wid] = kp;
+        if (act && q == 0) pp[r] = p;
+        __syncthreads();  // [B]
+        float ks = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) ks += rkp[w];
+        const float kk = 0.5f * tk * ks;
+        const float2 w = act ? make_float2(p.x - kk * v.x, p.y - kk * v.y) : make_float2(0.f, 0.f);
+        if (tid == 0) {
+            tau[k] = tk;
+            sub[k] = al;
+        }
+        float2 xn = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = q + Q * u;
+            float2 wc = make_float2(0.f, 0.f);
+            if (c > k && c < D) {
+                const float2 pc = pp[c];
+                wc = make_float2(pc.x - kk * vc[u].x, pc.y - kk * vc[u].y);
+            }
+            // a[r][c] -= v_r conj(w_c) + w_r conj(v_c)
+            a[u].x -= v.x * wc.x + v.y * wc.y + w.x * vc[u].x + w.y * vc[u].y;
+            a[u].y -= v.y * wc.x - v.x * wc.y + w.y * vc[u].x - w.x * vc[u].y;
+            if (u == un) xn = a[u];
+        }
+        float part = 0.f;
+        if (q == qn && r < D) {  // next column to shared memory (next reflector) + its norm partials
+            A[r + LD * kn] = xn;
+            if (r > kn + 1) part = xn.x * xn.x + xn.y * xn.y;
+        }
+        if (r == k + 1 && q == 0) A[r + LD * k] = v0;  // store the reflector (x0 no longer read)
+        part = __shfl_sync(0xffffffffu, rows_sum<Q>(part), qn);  // the owner lanes hold the partials
+        if (lane == 0) rt2[wid] = part;  // rt2 of step k was consumed before [B]
+    }
+    // diagonal back to shared memory (phase 2 reads it there)
+    float2 dg = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (q + Q * u == r) dg = a[u];
+    if (r < D && (r % Q) == q) A[r + LD * r] = dg;
+    __syncthreads();
+}
+
+template <class R, int DM, int NT, bool HREG = false>
 __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, const cplx_t<R>* __restrict__ in,
                                                           cplx_t<R>* __restrict__ out, double* __restrict__ evals,
                                                           int* __restrict__ fail) {
@@ -200,7 +321,13 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
     R* rt2 = reinterpret_cast<R*>(red);       // [NW] norm partials of the current column
     R* rkp = rt2 + NW;                        // [NW] v^H p partials
     C* pp = vv;              // p of the current step
-    {
+    bool hh_done = false;
+    if constexpr (HREG && sizeof(R) == 4 && DM == 64 && NT == 256) {
+        hh_cta_reg64(D, LD, reinterpret_cast<float2*>(A), reinterpret_cast<float2*>(pp), reinterpret_cast<float*>(tau),
+                     reinterpret_cast<float2*>(sub), reinterpret_cast<float*>(rt2), reinterpret_cast<float*>(rkp));
+        hh_done = true;
+    }
+    if (!hh_done) {
         R part = R(0);
         if (q == 0 && r > 1 && r < D) {
             const C a = A[r];
@@ -209,7 +336,7 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
         part = rows_sum<Q>(part);
         if (lane == 0) rt2[wid] = part;
     }
-    for (int k = 0; k + 2 < D; ++k) {
+    for (int k = 0; !hh_done && k + 2 < D; ++k) {
         const bool act = r > k && r < D;
         __syncthreads();  // [A]
         R t2 = R(0);

@@ -1101,7 +1101,14 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
         if (L.total <= 227 * 1024) {
             const size_t sm = L.total;
             cudaError_t e;
-            if (D <= 64) {
+            if (D <= 64 && sizeof(T) == 4 && batch <= 64) {
+                // small batch (C2 tx Grams): latency-bound, register-resident Householder
+                e = cudaFuncSetAttribute(k_heev_cr<T, 64, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+                if (e != cudaSuccess) return e;
+                k_heev_cr<T, 64, 256, true><<<(unsigned)batch, 256, sm, st>>>(D, count, (const cplx_t<T>*)in,
+                                                                              (cplx_t<T>*)out, evals, fail);
+            } else if (D <= 64) {
                 e = cudaFuncSetAttribute(k_heev_cr<T, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 if (e != cudaSuccess) return e;
                 k_heev_cr<T, 64, 256><<<(unsigned)batch, 256, sm, st>>>(D, count, (const cplx_t<T>*)in, (cplx_t<T>*)out,
