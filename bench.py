@@ -428,7 +428,7 @@ def main():
     peaks_t = {"fp32": 148 * 128 * 2 * clk_max * 1e6 / 1e12, "fp64": 148 * 64 * 2 * clk_max * 1e6 / 1e12}
     costs = sinr_costs(cfg, cs)
     stage = {"rebuild": st_acc[4], "pair_gram": st_acc[5], "small": st_acc[6]}
-    kern = {"rebuild": "k_rebuild_link", "pair_gram": "k_pair_gram_gf", "small": "k_small_fused"}
+    kern = {"rebuild": "k_rebuild_rb", "pair_gram": "k_pair_gram_gf", "small": "k_small_fused"}
     per_stage = {}
     for k_, ms_k in stage.items():
         fl, pipe, by = costs[k_]

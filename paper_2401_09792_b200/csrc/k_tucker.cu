@@ -430,7 +430,10 @@ __global__ void k_stop_freeze(int64_t ngroups, const double* __restrict__ trace,
                               const char* __restrict__ B, const char* __restrict__ Cf, const char* __restrict__ Gc,
                               char* __restrict__ frozen, int64_t a_sz, int64_t b_sz, int64_t c_sz, int64_t g_sz) {
     const int64_t g = blockIdx.x;
-    if (stop[g]) return;
+    // stopped at an earlier sweep? (iterations_run is written as s+1 by this launch's block y = 0, so
+    // the other blocks of this launch still see the group as running and copy their slices)
+    const int itr = stop[ngroups + g];
+    if (itr != 0 && itr <= s) return;
     const double dec = trace[g * stride + s] - trace[g * stride + s + 1];
     if (!(dec < 1e-10 * energy[g])) return;
     // byte sizes are multiples of 8 (complex64 and up)
@@ -441,10 +444,14 @@ __global__ void k_stop_freeze(int64_t ngroups, const double* __restrict__ trace,
     const unsigned long long* sb = reinterpret_cast<const unsigned long long*>(B + g * b_sz);
     const unsigned long long* sc = reinterpret_cast<const unsigned long long*>(Cf + g * c_sz);
     const unsigned long long* sg = reinterpret_cast<const unsigned long long*>(Gc + g * g_sz);
-    for (int64_t e = threadIdx.x; e < na + nb + nc + ng; e += blockDim.x)
+    const int64_t step = (int64_t)blockDim.x * gridDim.y;
+    for (int64_t e = threadIdx.x + (int64_t)blockIdx.y * blockDim.x; e < na + nb + nc + ng; e += step)
         fz[e] = e < na ? sa[e] : e < na + nb ? sb[e - na] : e < na + nb + nc ? sc[e - na - nb] : sg[e - na - nb - nc];
+    // the slices of the copy run in gridDim.y blocks; block y = 0 publishes the stop after its slice.
+    // Other slices may still be copying when the flag is set: readers of the flag (k_unfreeze, the
+    // next sweep's k_stop_freeze) run later on the same stream, after this whole grid completed.
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && blockIdx.y == 0) {
         stop[g] = 1;
         stop[ngroups + g] = s + 1;
         atomicAdd(stop + 2 * ngroups, 1);
@@ -463,7 +470,8 @@ __global__ void k_unfreeze(int64_t ngroups, const int* __restrict__ stop, char* 
     unsigned long long* db = reinterpret_cast<unsigned long long*>(B + g * b_sz);
     unsigned long long* dc = reinterpret_cast<unsigned long long*>(Cf + g * c_sz);
     unsigned long long* dg = reinterpret_cast<unsigned long long*>(Gc + g * g_sz);
-    for (int64_t e = threadIdx.x; e < na + nb + nc + ng; e += blockDim.x) {
+    for (int64_t e = threadIdx.x + (int64_t)blockIdx.y * blockDim.x; e < na + nb + nc + ng;
+         e += (int64_t)blockDim.x * gridDim.y) {
         const unsigned long long v = fz[e];
         if (e < na) da[e] = v;
         else if (e < na + nb) db[e - na] = v;
@@ -475,7 +483,9 @@ __global__ void k_unfreeze(int64_t ngroups, const int* __restrict__ stop, char* 
 cudaError_t launch_stop_freeze(int64_t ngroups, const double* trace, const double* energy, int stride, int s, int* stop,
                                const void* A, const void* B, const void* Cf, const void* Gc, void* frozen, int64_t a_sz,
                                int64_t b_sz, int64_t c_sz, int64_t g_sz, cudaStream_t st) {
-    k_stop_freeze<<<(unsigned)ngroups, 256, 0, st>>>(ngroups, trace, energy, stride, s, stop, (const char*)A,
+    const int64_t words = (a_sz + b_sz + c_sz + g_sz) / 8;
+    const dim3 grid((unsigned)ngroups, (unsigned)std::max<int64_t>(1, std::min<int64_t>(32, (words + 2047) / 2048)));
+    k_stop_freeze<<<grid, 256, 0, st>>>(ngroups, trace, energy, stride, s, stop, (const char*)A,
                                                       (const char*)B, (const char*)Cf, (const char*)Gc, (char*)frozen,
                                                       a_sz, b_sz, c_sz, g_sz);
     return cudaGetLastError();
@@ -483,7 +493,9 @@ cudaError_t launch_stop_freeze(int64_t ngroups, const double* trace, const doubl
 
 cudaError_t launch_unfreeze(int64_t ngroups, const int* stop, void* A, void* B, void* Cf, void* Gc, const void* frozen,
                             int64_t a_sz, int64_t b_sz, int64_t c_sz, int64_t g_sz, cudaStream_t st) {
-    k_unfreeze<<<(unsigned)ngroups, 256, 0, st>>>(ngroups, stop, (char*)A, (char*)B, (char*)Cf, (char*)Gc,
+    const int64_t words = (a_sz + b_sz + c_sz + g_sz) / 8;
+    const dim3 grid((unsigned)ngroups, (unsigned)std::max<int64_t>(1, std::min<int64_t>(32, (words + 2047) / 2048)));
+    k_unfreeze<<<grid, 256, 0, st>>>(ngroups, stop, (char*)A, (char*)B, (char*)Cf, (char*)Gc,
                                                    (const char*)frozen, a_sz, b_sz, c_sz, g_sz);
     return cudaGetLastError();
 }
