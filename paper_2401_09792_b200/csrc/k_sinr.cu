@@ -984,7 +984,7 @@ __global__ void __launch_bounds__(128) k_mmse(Topo t, int scope, int S, int64_t 
 // K3 fused: a CTA holds whole (group, subcarrier) slices (users x SL threads); the precoders go to
 // shared memory and the MMSE phase reads its partners' from there (no EG round trip through HBM).
 template <int M>
-__global__ void __launch_bounds__(128) k_small_fused(Topo t, int scope, int S, int64_t items, double sigma, int fc,
+__global__ void __launch_bounds__(128, 3) k_small_fused(Topo t, int scope, int S, int64_t items, double sigma, int fc,
                                                      int64_t Ftot, int64_t f0, const double2* __restrict__ PG,
                                                      double* __restrict__ sinr, double* __restrict__ signal,
                                                      int* __restrict__ status) {
