@@ -567,13 +567,28 @@ __global__ void __launch_bounds__(256) k_pair_gram_gf(Topo t, int Fc, int64_t f0
     const C* Hf = H + ((g * Fc + f) * links) * (int64_t)mn;
     const int tot = links * mn;
     if (sizeof(C) == 8 && (mn % 2) == 0) {
+        // all of a thread's 16-byte loads are issued before the first conversion/store: the staging
+        // phase was HBM-latency bound with one load in flight per thread (ncu: long-scoreboard stalls
+        // on the store line)
+        constexpr int U = 4;
         const float4* h4 = reinterpret_cast<const float4*>(Hf);
         const int n4 = tot / 2;
-        for (int e = threadIdx.x; e < n4; e += blockDim.x) {
-            const float4 v = h4[e];
-            const int l = (2 * e) / mn, r = (2 * e) % mn;
-            sh[l * LS + r] = make_double2(v.x, v.y);
-            sh[l * LS + r + 1] = make_double2(v.z, v.w);
+        for (int e0 = threadIdx.x; e0 < n4; e0 += U * blockDim.x) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * blockDim.x;
+                if (e < n4) v[u] = __ldg(h4 + e);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * blockDim.x;
+                if (e < n4) {
+                    const int l = (2 * e) / mn, r = (2 * e) % mn;
+                    sh[l * LS + r] = make_double2(v[u].x, v[u].y);
+                    sh[l * LS + r + 1] = make_double2(v[u].z, v[u].w);
+                }
+            }
         }
     } else {
         for (int e = threadIdx.x; e < tot; e += blockDim.x) sh[(e / mn) * LS + e % mn] = to_d2(Hf[e]);

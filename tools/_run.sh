@@ -1,2 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 300 python tools/tucker_probe.py 2>&1 | tail -4
+for c in C2 C2d C1 C5; do echo "== $c $(GWT_SINR_DEV_LANES=1 timeout 120 python tools/sinr_time.py $c 30 | tail -1)"; done
+echo "== C2 2 lanes $(timeout 120 python tools/sinr_time.py C2 100 | tail -1)"
