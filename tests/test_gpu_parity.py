@@ -68,6 +68,27 @@ def test_leading_eigenvectors_c64(ctx, n, count):
         assert np.linalg.norm(vec[k].astype(np.complex128).conj().T @ vec[k] - np.eye(count)) < 1e-4
 
 
+@pytest.mark.parametrize("n,count,batch", [(17, 6, 8), (31, 16, 40), (33, 10, 8), (47, 16, 96), (64, 16, 8), (64, 16, 96)])
+def test_leading_eigenvectors_c64_paths_decaying_spectrum(ctx, n, count, batch):
+    """fp32 eigensolver code paths (register-resident warp Householder for 16 < n <= 32, the CTA kernel's
+    register (batch <= 64) and shared-memory (batch > 64) Householder for 32 < n <= 64, division-free
+    Sturm counts) on Gram-like spectra with exponential decay (clustered small eigenvalues, as the
+    channel Grams have): eigenvalues and the top-count subspace vs fp64 LAPACK."""
+    rng = np.random.default_rng(100 + n + batch)
+    Z = rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))
+    Qm, _ = np.linalg.qr(Z)
+    lam = np.exp(-0.2 * np.arange(n)) * (1.0 + 0.05 * rng.random((batch, n)))
+    H = ((Qm * lam[:, None, :]) @ np.conj(np.swapaxes(Qm, 1, 2))).astype(np.complex64)
+    vec, ev = ctx.leading_eigenvectors(H, count, with_values=True)
+    for k in range(0, batch, max(1, batch // 8)):
+        Hk = H[k].astype(np.complex128)
+        w, U = np.linalg.eigh(Hk)
+        w, U = w[::-1][:count], U[:, ::-1][:, :count]
+        assert np.max(np.abs(ev[k] - w)) <= 1e-5 * w[0]
+        assert _max_angle(vec[k].astype(np.complex128), U) < 1e-3
+        assert np.linalg.norm(vec[k].astype(np.complex128).conj().T @ vec[k] - np.eye(count)) < 1e-4
+
+
 def test_leading_eigenvectors_errors(ctx):
     H = np.eye(4, dtype=np.complex128)[None]
     with pytest.raises(gw.InvalidArgument, match="count 5 out of range for size 4"):

@@ -1,3 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for c in C2 C2d C1 C5; do echo "== $c $(GWT_SINR_DEV_LANES=1 timeout 120 python tools/sinr_time.py $c 30 | tail -1)"; done
-echo "== C2 2 lanes $(timeout 120 python tools/sinr_time.py C2 100 | tail -1)"
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "decaying" 2>&1 | tail -15
