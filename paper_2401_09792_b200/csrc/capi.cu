@@ -46,6 +46,16 @@ struct gwt_ctx {
     std::vector<Slot> slots = std::vector<Slot>(40);
     cudaEvent_t ev[16] = {};
     int* pinned[8] = {};  // per solver lane: early-stop count read back without a blocking copy
+    // per solver lane: side stream + events for the objective tail of a sweep (SolveLane::sweep)
+    cudaStream_t side[8] = {};
+    cudaEvent_t side_ev[8][2] = {};
+    cudaStream_t side_stream(int lane) {
+        if (!side[lane]) {
+            ck(cudaStreamCreateWithFlags(&side[lane], cudaStreamNonBlocking), "cudaStreamCreate");
+            for (auto& e : side_ev[lane]) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        }
+        return side[lane];
+    }
     int* pin(int lane) {
         if (!pinned[lane]) ck(cudaMallocHost(&pinned[lane], 64), "cudaMallocHost");
         return pinned[lane];
@@ -192,6 +202,12 @@ struct SolveLane {
     int* hcount = nullptr;  // pinned copy of the stopped count
     cudaEvent_t sev[3] = {};
     bool done = false;
+    // fixed-sweep mode: the objective tail (core, ||core||^2, trace entry) of sweep s runs on a side
+    // stream; nothing on the next sweep's rx -> tx path reads its inputs' successors, only that
+    // sweep's Z2 = Z x2 B^H rewrite (and the delay update after it) must wait for it
+    cudaStream_t side = nullptr;
+    cudaEvent_t evc = nullptr, evo = nullptr;
+    bool tail_pending = false;
     size_t a_sz = 0, b_sz = 0, c_sz = 0, g_sz = 0;
 
     void* ws(int slot, size_t bytes) { return ctx->lws(lane, slot, bytes); }
@@ -299,6 +315,13 @@ struct SolveLane {
         }
         iters.assign(G, sweeps);
         done = false;
+        tail_pending = false;
+        side = nullptr;
+        if (!early && sweeps > 0 && !std::getenv("GWT_SOLVE_NO_SIDE")) {
+            side = ctx->side_stream(lane);
+            evc = ctx->side_ev[lane][0];
+            evo = ctx->side_ev[lane][1];
+        }
     }
 
     // enqueue one alternating sweep (decompose.cpp:330-370): rx, tx, delay factors, then cores + objective
@@ -311,9 +334,23 @@ struct SolveLane {
         GramDesc gtx{t.N, t.m, t.p, (int64_t)t.m * t.N * t.p, t.m, 1, (int64_t)t.m * t.N, tx_kind};
         gram_eig(gtx, W2, t.N, t.n, B, tx_copies);
         gemm(dZ, X, A, Z);
+        if (tail_pending) {  // the previous sweep's tail still reads Z2 and C
+            ck(cudaStreamWaitEvent(st, evo, 0), "cudaStreamWaitEvent");
+            tail_pending = false;
+        }
         gemm(dZ2, Z, B, Z2);
         GramDesc gd{t.P, t.m * t.n, 1, (int64_t)t.m * t.n * t.P, (int64_t)t.m * t.n, 1, 0, FI_LINK};
         gram_eig(gd, Z2, t.P, t.p, Cf, 0);
+        if (side) {
+            ck(cudaEventRecord(evc, st), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(side, evc, 0), "cudaStreamWaitEvent");
+            ctx->launched(launch_cgemm<T>(t, dG, G, Z2, Cf, Gc, side));
+            ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)t.links() * t.m * t.n * t.p, G, capt, part, side));
+            ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, s + 1, side));
+            ck(cudaEventRecord(evo, side), "cudaEventRecord");
+            tail_pending = true;
+            return;
+        }
         gemm(dG, Z2, Cf, Gc);
         ctx->launched(launch_group_sqnorm<T>(Gc, (int64_t)t.links() * t.m * t.n * t.p, G, capt, part, st));
         ctx->launched(launch_objective(G, energy, capt, trace_d, sweeps + 1, s + 1, st));
@@ -333,6 +370,10 @@ struct SolveLane {
     }
 
     void end() {
+        if (tail_pending) {
+            ck(cudaStreamWaitEvent(st, evo, 0), "cudaStreamWaitEvent");
+            tail_pending = false;
+        }
         if (early) {
             ctx->launched(launch_unfreeze(G, stopd, A, B, Cf, Gc, frozen, a_sz, b_sz, c_sz, g_sz, st));
             std::vector<int> h(2 * G);
@@ -898,6 +939,12 @@ void gwt_ctx_destroy(gwt_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     for (auto* p : ctx->pinned)
         if (p) cudaFreeHost(p);
+    for (int l = 0; l < 8; ++l)
+        if (ctx->side[l]) {
+            cudaStreamSynchronize(ctx->side[l]);
+            cudaStreamDestroy(ctx->side[l]);
+            for (auto& e : ctx->side_ev[l]) cudaEventDestroy(e);
+        }
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }

@@ -1,1 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "decaying" 2>&1 | tail -15
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 300 python tools/tucker_probe.py 2>&1 | tail -4
+GWT_SOLVE_NO_SIDE=1 timeout 300 python tools/tucker_probe.py 2>&1 | tail -4
