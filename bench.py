@@ -434,6 +434,8 @@ def main():
         fl, pipe, by = costs[k_]
         r = binding_roofline(fl, pipe, by, ms_k, hbm, peaks_t)
         r.update(kernel=kern[k_], ms=round(ms_k, 4), alg_bytes=int(by), alg_flops=int(fl))
+        if r["bound"] in ("fp32", "fp64"):  # same achieved rate against the cuBLAS ceiling measured in this run
+            r["frac_vs_cublas"] = r["achieved"] / cublas["sgemm_tflops" if r["bound"] == "fp32" else "dgemm_tflops"]
         per_stage[k_] = r
     dom = max(stage, key=stage.get)
     roof = dict(per_stage[dom])
