@@ -1,3 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for c in C2 C1 C5 C3; do echo "== $c $(GWT_SINR_DEV_LANES=1 timeout 120 python tools/sinr_time.py $c 10 | tail -1)"; done
-echo "== C2 2 lanes $(timeout 120 python tools/sinr_time.py C2 100 | tail -1)"
+GWT_LIB_PATH=paper_2401_09792_b200/_build/phase/libgwt_b200.so timeout 300 python tools/eig_real_phases.py 2>&1 | tail -3
