@@ -22,7 +22,7 @@ so = torch.empty((cfg.groups, F, users, topo.num_streams), dtype=torch.float64).
 sg = torch.empty_like(so).pin_memory()
 stt = torch.empty((cfg.groups, F, users), dtype=torch.int32).pin_memory()
 led = api.L.Ledger() if hasattr(api, "L") else None
-for chunks, lanes in (("4", "2"), ("8", "2"), ("16", "2"), ("8", "3"), ("8", "4"), ("16", "4"), ("32", "2")):
+for chunks, lanes in (("4", "2"), ("5", "2"), ("6", "2"), ("3", "2"), ("4", "2")):
     os.environ["GWT_SINR_PIPELINE"] = chunks
     os.environ["GWT_SINR_LANES"] = lanes
     for _ in range(3):
