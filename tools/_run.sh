@@ -1,2 +1,3 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for e in 1.0 0.5 0.33; do echo "edge $e"; GWT_SINR_EDGE=$e timeout 300 python tools/e2e_probe.py 2>&1 | tail -5; done
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
+timeout 600 python bench.py --impl reference > gpurun_out/ref.json 2> gpurun_out/ref.err; tail -1 gpurun_out/ref.json | cut -c1-300
