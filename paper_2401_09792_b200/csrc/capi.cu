@@ -63,7 +63,7 @@ struct gwt_ctx {
     }
     // per solver lane: side stream + events for the objective tail of a sweep (SolveLane::sweep)
     cudaStream_t side[8] = {};
-    cudaEvent_t side_ev[8][2] = {};
+    cudaEvent_t side_ev[8][4] = {};
     cudaStream_t side_stream(int lane) {
         if (!side[lane]) {
             ck(cudaStreamCreateWithFlags(&side[lane], cudaStreamNonBlocking), "cudaStreamCreate");
@@ -221,7 +221,7 @@ struct SolveLane {
     // stream; nothing on the next sweep's rx -> tx path reads its inputs' successors, only that
     // sweep's Z2 = Z x2 B^H rewrite (and the delay update after it) must wait for it
     cudaStream_t side = nullptr;
-    cudaEvent_t evc = nullptr, evo = nullptr;
+    cudaEvent_t evc = nullptr, evo = nullptr, eva = nullptr, evz = nullptr;
     bool tail_pending = false;
     size_t a_sz = 0, b_sz = 0, c_sz = 0, g_sz = 0;
 
@@ -336,6 +336,8 @@ struct SolveLane {
             side = ctx->side_stream(lane);
             evc = ctx->side_ev[lane][0];
             evo = ctx->side_ev[lane][1];
+            eva = ctx->side_ev[lane][2];
+            evz = ctx->side_ev[lane][3];
         }
     }
 
@@ -345,10 +347,21 @@ struct SolveLane {
         gemm(dW, Y1, B, W);
         GramDesc grx{t.M, t.n * t.p, 1, (int64_t)t.M * t.n * t.p, 1, t.M, 0, rx_kind};
         gram_eig(grx, W, t.M, t.m, A, rx_copies);
+        if (side) {  // Z = X x1 A^H needs only the new A: computed beside the tx update, behind the tail
+            ck(cudaEventRecord(eva, st), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(side, eva, 0), "cudaStreamWaitEvent");
+            ctx->launched(launch_cgemm<T>(t, dZ, G, X, A, Z, side));
+            ck(cudaEventRecord(evz, side), "cudaEventRecord");
+        }
         gemm(dW2, Y1, A, W2);
         GramDesc gtx{t.N, t.m, t.p, (int64_t)t.m * t.N * t.p, t.m, 1, (int64_t)t.m * t.N, tx_kind};
         gram_eig(gtx, W2, t.N, t.n, B, tx_copies);
-        gemm(dZ, X, A, Z);
+        if (side) {  // Z ready, and the previous sweep's tail (which still read Z2 and C) done before it
+            ck(cudaStreamWaitEvent(st, evz, 0), "cudaStreamWaitEvent");
+            tail_pending = false;
+        } else {
+            gemm(dZ, X, A, Z);
+        }
         if (tail_pending) {  // the previous sweep's tail still reads Z2 and C
             ck(cudaStreamWaitEvent(st, evo, 0), "cudaStreamWaitEvent");
             tail_pending = false;
