@@ -1304,6 +1304,34 @@ int gwt_leading_eigenvectors(gwt_ctx* ctx, int32_t n, int32_t count, int64_t bat
     });
 }
 
+int gwt_woodbury_inverse(gwt_ctx* ctx, int32_t m, int64_t batch, gwt_mem mem, const void* Q, double sigma, void* T,
+                         int32_t* status) {
+    return guarded(ctx, [&] {
+        if (!(sigma > 0.0)) invalid("woodbury_inverse_apply: sigma must be > 0");  // sinr.cpp:206-207
+        if (m < 1 || batch < 0) invalid("woodbury_inverse_apply: bad covariance size");
+        if (batch == 0) return;
+        cudaStream_t st = ctx->stream;
+        const size_t bytes = 16 * (size_t)batch * m * m;
+        const void* Qd = Q;
+        void* Td = T;
+        int* Sd = (int*)status;
+        if (mem == GWT_MEM_HOST) {
+            void* q = ctx->ws(WS_GRAM, bytes);
+            ck(cudaMemcpyAsync(q, Q, bytes, cudaMemcpyHostToDevice, st), "H2D");
+            Qd = q;
+            Td = ctx->ws(WS_POOL, bytes);
+            Sd = (int*)ctx->ws(WS_STATUS, 4 * batch);
+        }
+        void* Lw = ctx->ws(WS_EIGA, bytes);
+        ctx->launched(launch_woodbury(m, batch, Qd, sigma, Lw, Td, Sd, st));
+        if (mem == GWT_MEM_HOST) {
+            ck(cudaMemcpyAsync(T, Td, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(status, Sd, 4 * batch, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        ck(cudaStreamSynchronize(st), "sync");
+    });
+}
+
 int gwt_reconstruct(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, int64_t ngroups, gwt_dtype dtype,
                     gwt_mem mem, const void* A, const void* B, const void* C, const void* G, void* X) {
     return guarded(ctx, [&] {

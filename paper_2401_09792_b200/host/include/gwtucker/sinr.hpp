@@ -1,6 +1,7 @@
 // gwt:: drop-in API (B200 backend) — mirrors proj/include/gwtucker/sinr.hpp (pipeline level).
 #pragma once
 
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -19,6 +20,24 @@ struct CompressedChannels {
     }
 };
 
+/// Top-L SVD of a serving channel (sinr.hpp:14-20): V (n x L), singular values, U (m x L).
+struct Precoder {
+    Matrix v;
+    std::vector<double> singular_values;
+    Matrix u;
+};
+
+struct StreamSinr {
+    double signal_power = 0.0;
+    double sinr = 0.0;  // linear scale
+};
+
+/// Small-form representation of the full covariance inverse (sinr.hpp:116-119).
+struct WoodburyInverse {
+    Matrix t;  // m x m, Qs^-1 (Qs - sigma^2 I)
+    double inv_sigma_sq = 0.0;
+};
+
 struct SinrReport {
     int num_cells = 0;
     int users_per_cell = 0;
@@ -35,6 +54,21 @@ std::vector<std::pair<int, int>> scope_pairs(const SystemTopology& topology, Int
 
 CompressedChannels assemble_all_compressed(const SystemTopology& topology, const GroupwiseFactorSet& factors,
                                            const std::vector<Vector>& coeffs, FlopLedger* ledger = nullptr);
+
+// Single-system stage API of the compressed path (sinr.hpp:99-124). The batched pipeline below runs
+// these stages fused on the device; the stage functions keep the reference's building blocks for
+// callers that compose them: the SVD and the Cholesky run on the device (truncated_svd ->
+// batched eigensolver, woodbury_inverse_apply -> gwt_woodbury_inverse), the m x n products and the
+// per-stream formula use the Matrix type like the Eigen expressions they replace.
+Precoder precoder_compressed(const Matrix& h_small, int streams, FlopLedger* ledger = nullptr);
+std::vector<Precoder> precoders_compressed(const CompressedChannels& compressed, FlopLedger* ledger = nullptr);
+Matrix covariance_compressed(const CompressedChannels& compressed, const std::vector<Precoder>& precoders,
+                             InterferenceScope scope, int i, int j, FlopLedger* ledger = nullptr);
+WoodburyInverse woodbury_inverse_apply(const Matrix& q_small, double sigma, FlopLedger* ledger = nullptr);
+Matrix filter_compressed(const WoodburyInverse& inverse, const Matrix& h_serving, const Matrix& v_serving,
+                         FlopLedger* ledger = nullptr);
+std::vector<StreamSinr> sinr_compressed(const Matrix& w_small, const Matrix& q_small, const Matrix& h_serving,
+                                        const Matrix& v_serving, FlopLedger* ledger = nullptr);
 
 /// B200: rebuild + precoder + covariance + Woodbury/Cholesky + filter + SINR in batched kernels.
 SinrReport run_compressed_pipeline(const SystemTopology& topology, const GroupwiseFactorSet& factors,

@@ -8,6 +8,7 @@
 // without a CUDA device every GPU-backed call throws.
 #include <chrono>
 #include <cmath>
+#include <limits>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -582,6 +583,106 @@ std::vector<std::pair<int, int>> scope_pairs(const SystemTopology& topology, Int
     for (int k = 0; k < topology.num_cells; ++k)
         if (k != i) pairs.emplace_back(k, 0);
     return pairs;
+}
+
+// ---- single-system stages of the compressed path (sinr.cpp:162-254)
+Precoder precoder_compressed(const Matrix& h_small, int streams, FlopLedger* ledger) {
+    if (streams > std::min(h_small.rows(), h_small.cols()))
+        throw std::invalid_argument("precoder: stream count " + std::to_string(streams) +
+                                    " exceeds compressed channel size " + std::to_string(h_small.rows()) + "x" +
+                                    std::to_string(h_small.cols()) + " (ranks chosen below stream count)");
+    TruncatedSvd svd = truncated_svd(h_small, streams);  // device eigensolver on the Gram
+    if (ledger) ledger->precoder += i64(h_small.rows()) * h_small.cols() * streams;
+    return {std::move(svd.v), std::move(svd.singular_values), std::move(svd.u)};
+}
+
+std::vector<Precoder> precoders_compressed(const CompressedChannels& compressed, FlopLedger* ledger) {
+    const SystemTopology& topo = compressed.topology;
+    std::vector<Precoder> out;
+    out.reserve(static_cast<std::size_t>(topo.num_users()));
+    for (int i = 0; i < topo.num_cells; ++i)
+        for (int j = 0; j < topo.users_per_cell; ++j)
+            out.push_back(precoder_compressed(compressed.at(i, i, j), topo.num_streams, ledger));
+    return out;
+}
+
+Matrix covariance_compressed(const CompressedChannels& compressed, const std::vector<Precoder>& precoders,
+                             InterferenceScope scope, int i, int j, FlopLedger* ledger) {
+    const SystemTopology& topo = compressed.topology;
+    const double sigma = topo.noise_std;
+    const int m = compressed.ranks.m;
+    Matrix q = (sigma * sigma) * Matrix::Identity(m, m);
+    for (const auto& kl : scope_pairs(topo, scope, i, j)) {
+        const std::size_t user = static_cast<std::size_t>(kl.first) * topo.users_per_cell + kl.second;
+        if (user >= precoders.size()) throw std::invalid_argument("covariance: scope references missing precoder");
+        const Matrix term = compressed.at(kl.first, i, j) * precoders[user].v;
+        q += term * term.adjoint();
+    }
+    if (ledger) {
+        const std::int64_t mm = m, n = compressed.ranks.n, L = topo.num_streams;
+        ledger->covariance += i64(topo.num_users()) * (mm * n * L + mm * mm * L);
+    }
+    return q;
+}
+
+WoodburyInverse woodbury_inverse_apply(const Matrix& q_small, double sigma, FlopLedger* ledger) {
+    if (!(sigma > 0.0)) throw std::invalid_argument("woodbury_inverse_apply: sigma must be > 0");
+    if (!q_small.allFinite()) throw std::invalid_argument("woodbury_inverse_apply: non-finite input");
+    const Index m = q_small.rows();
+    WoodburyInverse out;
+    out.t = Matrix(m, m);
+    int32_t status = 0;
+    check(gwt_woodbury_inverse(ctx(), static_cast<int32_t>(m), 1, GWT_MEM_HOST, q_small.data(), sigma, out.t.data(),
+                               &status));
+    if (status == 1) throw std::runtime_error("woodbury_inverse_apply: covariance is numerically singular");
+    if (status == 2)
+        throw std::runtime_error("woodbury_inverse_apply: covariance is numerically singular "
+                                 "(condition estimate above 1e14)");
+    if (status == 4) throw std::invalid_argument("woodbury_inverse_apply: non-finite input");
+    out.inv_sigma_sq = 1.0 / (sigma * sigma);
+    if (ledger) ledger->inverse += 2 * i64(m) * m * m;
+    return out;
+}
+
+Matrix filter_compressed(const WoodburyInverse& inverse, const Matrix& h_serving, const Matrix& v_serving,
+                         FlopLedger* ledger) {
+    if (!h_serving.allFinite() || !v_serving.allFinite())
+        throw std::invalid_argument("filter_compressed: non-finite input");
+    const Matrix hv = h_serving * v_serving;
+    Matrix w = inverse.inv_sigma_sq * (hv - inverse.t * hv);
+    if (ledger) {
+        const std::int64_t m = inverse.t.rows(), L = v_serving.cols();
+        ledger->filter += m * m * L + m * L;
+    }
+    return w;
+}
+
+std::vector<StreamSinr> sinr_compressed(const Matrix& w_small, const Matrix& q_small, const Matrix& h_serving,
+                                        const Matrix& v_serving, FlopLedger* ledger) {
+    const Matrix hv = h_serving * v_serving;
+    if (ledger) {
+        const std::int64_t m = q_small.rows(), L = w_small.cols();
+        ledger->sinr += L * (m * m + 2 * m);
+    }
+    const int streams = static_cast<int>(w_small.cols());  // stream_sinrs (sinr.cpp:28-43)
+    std::vector<StreamSinr> out(static_cast<std::size_t>(streams));
+    const Matrix qw = q_small * w_small;
+    for (int r = 0; r < streams; ++r) {
+        Cplx amp(0, 0), wqw(0, 0);
+        for (Index a = 0; a < w_small.rows(); ++a) {
+            amp += std::conj(w_small(a, r)) * hv(a, r);
+            wqw += std::conj(w_small(a, r)) * qw(a, r);
+        }
+        const double sp = std::norm(amp);
+        double denom = std::real(wqw) - sp;
+        if (denom <= -1e-12)
+            throw std::runtime_error("sinr: interference-plus-noise power is negative for stream " + std::to_string(r) +
+                                     " (numerically invalid configuration)");
+        denom = std::max(denom, std::numeric_limits<double>::min());
+        out[static_cast<std::size_t>(r)].signal_power = sp;
+        out[static_cast<std::size_t>(r)].sinr = sp / denom;
+    }
+    return out;
 }
 
 namespace {

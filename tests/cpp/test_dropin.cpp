@@ -140,6 +140,37 @@ int main() {
         CHECK(rep.ledger.total() == want.total());
         CHECK(throws_with<std::invalid_argument>([&] { groupwise_solve(set, {7, 4, 3}, 1); },
                                                  "rank m = 7 out of range for mode-1 size 6"));
+        // stage API (sinr.cpp:162-254) composed per user == the fused batched pipeline; Woodbury lift
+        // Q * (1/s^2)(I - T) = I (test_sinr.cpp:293-314)
+        for (InterferenceScope sc : {InterferenceScope::paper_experiment, InterferenceScope::full}) {
+            CompressedChannels cc = assemble_all_compressed(set.topology, fs, set.coeffs);
+            FlopLedger led;
+            std::vector<Precoder> pre = precoders_compressed(cc, &led);
+            SinrReport want = run_compressed_pipeline(set.topology, fs, set.coeffs, sc);
+            double worst = 0.0, lift = 0.0;
+            for (int i = 0; i < set.topology.num_cells; ++i)
+                for (int j = 0; j < set.topology.users_per_cell; ++j) {
+                    const Matrix q = covariance_compressed(cc, pre, sc, i, j, &led);
+                    const WoodburyInverse inv = woodbury_inverse_apply(q, set.topology.noise_std, &led);
+                    const Matrix qi = inv.inv_sigma_sq * (Matrix::Identity(q.rows()) - inv.t);
+                    lift = std::max(lift, (q * qi - Matrix::Identity(q.rows())).norm());
+                    const Precoder& own = pre[static_cast<std::size_t>(i * set.topology.users_per_cell + j)];
+                    const Matrix w = filter_compressed(inv, cc.at(i, i, j), own.v, &led);
+                    const std::vector<StreamSinr> ss = sinr_compressed(w, q, cc.at(i, i, j), own.v, &led);
+                    for (int r = 0; r < set.topology.num_streams; ++r) {
+                        const double a = ss[static_cast<std::size_t>(r)].sinr, b = want.sinr_at(i, j, r);
+                        worst = std::max(worst, std::abs(a - b) / std::max(std::abs(b), 1e-300));
+                    }
+                }
+            CHECK(worst <= 1e-9);
+            CHECK(lift <= 1e-8);
+        }
+        CHECK(throws_with<std::invalid_argument>([&] { woodbury_inverse_apply(Matrix::Identity(3), 0.0); },
+                                                 "woodbury_inverse_apply: sigma must be > 0"));
+        CHECK(throws_with<std::runtime_error>([&] { woodbury_inverse_apply(Matrix(3, 3), 0.1); },
+                                              "covariance is numerically singular"));
+        CHECK(throws_with<std::invalid_argument>(
+            [&] { precoder_compressed(rng.matrix(3, 4), 4); }, "precoder: stream count 4 exceeds compressed channel size 3x4"));
     }
     // test_sinr.cpp:391-399: single user, single stream at full ranks -> sigma_1^2 / sigma^2
     {

@@ -99,7 +99,9 @@ def test_cpp_dropin_library_exports_gwt_api():
     out = subprocess.run(["nm", "-DC", lib], capture_output=True, text=True).stdout
     for sym in ("gwt::groupwise_solve(", "gwt::run_compressed_pipeline(", "gwt::mode_product(", "gwt::hosvd(",
                 "gwt::leading_eigenvectors(", "gwt::assemble_channel_compressed(", "gwt::reconstruct(",
-                "gwt::flop_estimate(", "gwt::shared_solve(", "gwt::truncated_svd("):
+                "gwt::flop_estimate(", "gwt::shared_solve(", "gwt::truncated_svd(", "gwt::precoder_compressed(",
+                "gwt::covariance_compressed(", "gwt::woodbury_inverse_apply(", "gwt::filter_compressed(",
+                "gwt::sinr_compressed("):
         assert sym in out, sym
 
 

@@ -1,3 +1,2 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 300 python tools/tucker_probe.py 2>&1 | tail -4
-timeout 300 python tools/tucker_probe.py 2>&1 | tail -4 | head -1
+./paper_2401_09792_b200/_build/test_dropin 2>&1 | tail -5
