@@ -396,6 +396,31 @@ class Context:
         vec = out.transpose(-1, -2) if _is_torch(out) else np.swapaxes(out, -1, -2)
         return (vec, ev) if with_values else vec
 
+    def woodbury_inverse_apply(self, Q, sigma: float):
+        """Batched gwt::woodbury_inverse_apply (sinr.hpp:121-122, sinr.cpp:205-227): Q [batch, m, m] Hermitian
+        covariances (complex128, natural indexing). Returns (T [batch, m, m] = Q^-1 (Q - sigma^2 I),
+        inv_sigma_sq). Device Cholesky with the reference's checks; raises the reference's errors for the
+        first failing matrix."""
+        b, m = Q.shape[0], Q.shape[-1]
+        if _is_torch(Q):
+            Qc = Q.to(dtype=torch.complex128).transpose(-1, -2).contiguous()
+        else:
+            Qc = np.ascontiguousarray(np.swapaxes(np.asarray(Q, dtype=np.complex128), -1, -2))
+        T = _like(Qc, (b, m, m), "c")
+        st = _like(Qc, (b,), "i32")
+        rc = self.lib.gwt_woodbury_inverse(self.h, m, b, _mem(Qc), _ptr(Qc), float(sigma), _ptr(T), _ptr(st))
+        self.check(rc)
+        sth = st.cpu().numpy() if _is_torch(st) else st
+        bad = np.nonzero(sth)[0]
+        if bad.size:
+            code = int(sth[bad[0]])
+            if code == 4:
+                raise InvalidArgument("woodbury_inverse_apply: non-finite input")
+            raise NumericalError("woodbury_inverse_apply: covariance is numerically singular" +
+                                  (" (condition estimate above 1e14)" if code == 2 else ""))
+        T = T.transpose(-1, -2) if _is_torch(T) else np.swapaxes(T, -1, -2)
+        return T, 1.0 / (sigma * sigma)
+
     def mode_product(self, X, U, mode: int):
         """Batched gwt::mode_product (tensor.hpp:68-70): X [batch, d3, d2, d1] (mode-1 fastest), U natural
         [rows, dim(mode)] shared by the batch. Returns Y with dim(mode) replaced by rows."""

@@ -89,6 +89,32 @@ def test_leading_eigenvectors_c64_paths_decaying_spectrum(ctx, n, count, batch):
         assert np.linalg.norm(vec[k].astype(np.complex128).conj().T @ vec[k] - np.eye(count)) < 1e-4
 
 
+def test_woodbury_inverse_apply_matches_dense_inverse(ctx):
+    """woodbury_inverse_apply on the device (sinr.cpp:205-227): T = Q^-1 (Q - s^2 I) vs a dense inverse, the
+    lift Q (1/s^2)(I - T) = I (test_sinr.cpp:269-314), and the reference's error texts."""
+    rng = np.random.default_rng(11)
+    for m, b in ((4, 7), (8, 3), (24, 2)):
+        A = rng.standard_normal((b, m, 2 * m)) + 1j * rng.standard_normal((b, m, 2 * m))
+        sigma = 0.3
+        Q = A @ np.conj(np.swapaxes(A, 1, 2)) + sigma ** 2 * np.eye(m)
+        T, iss = ctx.woodbury_inverse_apply(Q, sigma)
+        want = np.linalg.solve(Q, Q - sigma ** 2 * np.eye(m))
+        assert np.max(np.abs(T - want)) <= 1e-10 * max(1.0, np.abs(want).max())
+        lift = Q @ (iss * (np.eye(m) - T)) - np.eye(m)
+        assert np.max(np.abs(lift)) <= 1e-8
+    with pytest.raises(gw.InvalidArgument, match="sigma must be > 0"):
+        ctx.woodbury_inverse_apply(np.eye(3, dtype=np.complex128)[None], 0.0)
+    with pytest.raises(gw.NumericalError, match="covariance is numerically singular"):
+        ctx.woodbury_inverse_apply(np.zeros((1, 3, 3), np.complex128), 0.1)
+    ill = np.diag([1.0, 1e-15, 1.0]).astype(np.complex128)[None]
+    with pytest.raises(gw.NumericalError, match="condition estimate above 1e14"):
+        ctx.woodbury_inverse_apply(ill, 0.1)
+    bad = np.eye(3, dtype=np.complex128)[None].copy()
+    bad[0, 1, 1] = np.nan
+    with pytest.raises(gw.InvalidArgument, match="non-finite input"):
+        ctx.woodbury_inverse_apply(bad, 0.1)
+
+
 def test_leading_eigenvectors_errors(ctx):
     H = np.eye(4, dtype=np.complex128)[None]
     with pytest.raises(gw.InvalidArgument, match="count 5 out of range for size 4"):
