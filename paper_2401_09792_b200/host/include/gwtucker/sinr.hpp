@@ -80,6 +80,10 @@ std::vector<SinrReport> run_compressed_pipeline_batched(const SystemTopology& to
                                                         const std::vector<std::vector<Vector>>& coeffs_per_grid,
                                                         InterferenceScope scope);
 
+/// Full-size comparator (sinr.hpp:134): H(f) = X x3 c^* per link, SVD precoders, MMSE SINR — batched
+/// kernels on the device (gwt_sinr_full; M <= 8).
+SinrReport run_full_pipeline(const ChannelSet& channels, InterferenceScope scope);
+
 enum class PipelinePath { full, compressed };
 FlopLedger flop_estimate(const SystemTopology& topology, const CompressionRanks& ranks, PipelinePath path);
 

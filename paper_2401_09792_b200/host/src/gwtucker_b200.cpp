@@ -814,6 +814,50 @@ SinrReport run_compressed_pipeline(const SystemTopology& topology, const Groupwi
     return run_compressed_pipeline_batched(topology, factors, {coeffs}, scope).front();
 }
 
+SinrReport run_full_pipeline(const ChannelSet& channels, InterferenceScope scope) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const SystemTopology& topology = channels.topology;
+    check_channel_dims(channels);
+    const int links = topology.num_links(), M = topology.rx_antennas, N = topology.tx_antennas,
+              P = topology.num_taps;
+    if (static_cast<int>(channels.coeffs.size()) != links)
+        throw std::invalid_argument("assemble_all_full: coefficient count does not match links");
+    std::vector<Cplx> X(static_cast<std::size_t>(links) * M * N * P), co(static_cast<std::size_t>(links) * P);
+    for (int l = 0; l < links; ++l) {
+        std::copy(channels.tensors[l].data(), channels.tensors[l].data() + static_cast<std::size_t>(M) * N * P,
+                  X.begin() + static_cast<std::size_t>(l) * M * N * P);
+        if (channels.coeffs[l].size() != P)
+            throw std::invalid_argument("assemble_channel_full: coefficient length " +
+                                        std::to_string(channels.coeffs[l].size()) + " does not match mode-3 size " +
+                                        std::to_string(P));
+        std::copy(channels.coeffs[l].data(), channels.coeffs[l].data() + P, co.begin() + static_cast<std::size_t>(l) * P);
+    }
+    gwt_topology t = ctopo(topology);
+    const int users = topology.num_users(), L = topology.num_streams;
+    std::vector<double> sinr(static_cast<std::size_t>(users) * L), sig(static_cast<std::size_t>(users) * L);
+    std::vector<int32_t> st(static_cast<std::size_t>(users));
+    gwt_ledger led{};
+    check(gwt_sinr_full(ctx(), &t, 1, GWT_C128, GWT_MEM_HOST, X.data(), nullptr, nullptr, co.data(), 1,
+                        scope == InterferenceScope::full ? GWT_SCOPE_FULL : GWT_SCOPE_PAPER, sinr.data(), sig.data(),
+                        st.data(), &led));
+    for (std::size_t i = 0; i < st.size(); ++i) {
+        bool runtime = false;
+        if (const char* msg = item_error(st[i], runtime)) {
+            if (runtime) throw std::runtime_error(msg);
+            throw std::invalid_argument(msg);
+        }
+    }
+    SinrReport rep;
+    rep.num_cells = topology.num_cells;
+    rep.users_per_cell = topology.users_per_cell;
+    rep.num_streams = L;
+    rep.sinr = std::move(sinr);
+    rep.signal_power = std::move(sig);
+    rep.ledger = FlopLedger{led.reconstruct, led.precoder, led.covariance, led.inverse, led.filter, led.sinr};
+    rep.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rep;
+}
+
 FlopLedger flop_estimate(const SystemTopology& topology, const CompressionRanks& ranks, PipelinePath path) {
     topology.validate();
     ranks.validate_against(topology.rx_antennas, topology.tx_antennas, topology.num_taps);

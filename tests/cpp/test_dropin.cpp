@@ -172,6 +172,27 @@ int main() {
         CHECK(throws_with<std::invalid_argument>(
             [&] { precoder_compressed(rng.matrix(3, 4), 4); }, "precoder: stream count 4 exceeds compressed channel size 3x4"));
     }
+    // test_sinr.cpp:337-365: lossless ranks -> compressed == full pipeline within 1e-8, both scopes
+    {
+        ChannelSet set;
+        set.topology = SystemTopology{2, 2, 6, 8, 5, 2, 0.1};
+        for (int l = 0; l < 8; ++l) {
+            set.tensors.push_back(rng.tensor(6, 8, 5));
+            Vector c(5);
+            for (int q = 0; q < 5; ++q) c(q) = rng.c();
+            set.coeffs.push_back(c);
+        }
+        auto [fs, tr] = groupwise_solve(set, {6, 8, 5}, 2);
+        for (InterferenceScope sc : {InterferenceScope::paper_experiment, InterferenceScope::full}) {
+            const SinrReport comp = run_compressed_pipeline(set.topology, fs, set.coeffs, sc);
+            const SinrReport full = run_full_pipeline(set, sc);
+            double worst = 0.0;
+            for (std::size_t e = 0; e < full.sinr.size(); ++e)
+                worst = std::max(worst, std::abs(comp.sinr[e] - full.sinr[e]) / std::abs(full.sinr[e]));
+            CHECK(worst <= 1e-8);
+            CHECK(full.ledger.total() == flop_estimate(set.topology, {6, 8, 5}, PipelinePath::full).total());
+        }
+    }
     // test_sinr.cpp:391-399: single user, single stream at full ranks -> sigma_1^2 / sigma^2
     {
         ChannelSet set;
