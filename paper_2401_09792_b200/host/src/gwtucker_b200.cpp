@@ -571,6 +571,51 @@ double projection_energy(const ChannelSet& channels, const GroupwiseFactorSet& f
     return channels.total_squared_norm() - objective_value(channels, factors);
 }
 
+// ---- single Gauss-Seidel factor updates (decompose.cpp:146-193)
+Matrix rx_update_gram(const ChannelSet& channels, const GroupwiseFactorSet& factors, int i, int j) {
+    const int dim = channels.topology.rx_antennas;
+    Matrix gram(dim, dim);
+    for (int k = 0; k < channels.topology.num_cells; ++k) {
+        const Tensor3 t = mode_product(mode_product(channels.tensor(k, i, j), factors.tx(k).adjoint(), 2),
+                                       factors.delay(k, i, j).adjoint(), 3);
+        const Matrix w = matricize(t, 1);
+        gram += w * w.adjoint();
+    }
+    return gram;
+}
+
+Matrix update_rx_factor(const ChannelSet& channels, const GroupwiseFactorSet& factors, int i, int j) {
+    return leading_eigenvectors(rx_update_gram(channels, factors, i, j), factors.ranks.m);
+}
+
+Matrix tx_update_gram(const ChannelSet& channels, const GroupwiseFactorSet& factors, int k) {
+    const int dim = channels.topology.tx_antennas;
+    Matrix gram(dim, dim);
+    for (int i = 0; i < channels.topology.num_cells; ++i)
+        for (int j = 0; j < channels.topology.users_per_cell; ++j) {
+            const Tensor3 t = mode_product(mode_product(channels.tensor(k, i, j), factors.rx(i, j).adjoint(), 1),
+                                           factors.delay(k, i, j).adjoint(), 3);
+            const Matrix w = matricize(t, 2);
+            gram += w * w.adjoint();
+        }
+    return gram;
+}
+
+Matrix update_tx_factor(const ChannelSet& channels, const GroupwiseFactorSet& factors, int k) {
+    return leading_eigenvectors(tx_update_gram(channels, factors, k), factors.ranks.n);
+}
+
+Matrix delay_update_gram(const ChannelSet& channels, const GroupwiseFactorSet& factors, int k, int i, int j) {
+    const Tensor3 t = mode_product(mode_product(channels.tensor(k, i, j), factors.rx(i, j).adjoint(), 1),
+                                   factors.tx(k).adjoint(), 2);
+    const Matrix w = matricize(t, 3);
+    return w * w.adjoint();
+}
+
+Matrix update_delay_factor(const ChannelSet& channels, const GroupwiseFactorSet& factors, int k, int i, int j) {
+    return leading_eigenvectors(delay_update_gram(channels, factors, k, i, j), factors.ranks.p);
+}
+
 // ---------------------------------------------------------------- sinr
 std::vector<std::pair<int, int>> scope_pairs(const SystemTopology& topology, InterferenceScope scope, int i, int j) {
     std::vector<std::pair<int, int>> pairs;  // sinr.cpp:47-62

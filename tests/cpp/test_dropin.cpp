@@ -172,6 +172,36 @@ int main() {
         CHECK(throws_with<std::invalid_argument>(
             [&] { precoder_compressed(rng.matrix(3, 4), 4); }, "precoder: stream count 4 exceeds compressed channel size 3x4"));
     }
+    // single Gauss-Seidel updates (decompose.cpp:146-193) replayed from the initial factors reproduce one
+    // sweep of groupwise_solve: rx from the old factors, tx with the new rx, delay with both
+    {
+        ChannelSet set;
+        set.topology = SystemTopology{2, 2, 6, 8, 5, 2, 0.1};
+        for (int l = 0; l < 8; ++l) {
+            set.tensors.push_back(rng.tensor(6, 8, 5));
+            Vector c(5);
+            for (int q = 0; q < 5; ++q) c(q) = rng.c();
+            set.coeffs.push_back(c);
+        }
+        const CompressionRanks rk{3, 4, 3};
+        GroupwiseFactorSet f = groupwise_solve(set, rk, 0).first;
+        const GroupwiseFactorSet one = groupwise_solve(set, rk, 1).first;
+        const GroupwiseFactorSet old = f;
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) f.rx_factors[f.user_index(i, j)] = update_rx_factor(set, old, i, j);
+        for (int k = 0; k < 2; ++k) f.tx_factors[k] = update_tx_factor(set, f, k);
+        for (int k = 0; k < 2; ++k)
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 2; ++j) f.delay_factors[f.link_index(k, i, j)] = update_delay_factor(set, f, k, i, j);
+        double d = 0.0;
+        for (std::size_t u = 0; u < f.rx_factors.size(); ++u) d = std::max(d, (f.rx_factors[u] - one.rx_factors[u]).norm());
+        for (std::size_t u = 0; u < f.tx_factors.size(); ++u) d = std::max(d, (f.tx_factors[u] - one.tx_factors[u]).norm());
+        for (std::size_t u = 0; u < f.delay_factors.size(); ++u)
+            d = std::max(d, (f.delay_factors[u] - one.delay_factors[u]).norm());
+        CHECK(d <= 1e-8);
+        const Matrix g = rx_update_gram(set, old, 1, 0);
+        CHECK((g - g.adjoint()).norm() <= 1e-12 * g.norm());
+    }
     // test_sinr.cpp:337-365: lossless ranks -> compressed == full pipeline within 1e-8, both scopes
     {
         ChannelSet set;
