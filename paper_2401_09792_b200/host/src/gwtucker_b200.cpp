@@ -525,6 +525,44 @@ std::vector<std::pair<GroupwiseFactorSet, SolveTrace>> groupwise_solve_batched(c
     return solve_groups(g, ranks, sweeps, nullptr, false, early_stop);
 }
 
+IndividualResult individual_solve(const ChannelSet& channels, const CompressionRanks& ranks, int sweeps,
+                                  const GroupwiseFactorSet* init) {
+    check_channel_dims(channels);
+    const SystemTopology& topo = channels.topology;
+    ranks.validate_against(topo.rx_antennas, topo.tx_antennas, topo.num_taps);
+    if (sweeps < 0) throw std::invalid_argument("solve: sweeps must be >= 0");
+    const int links = topo.num_links();
+    std::vector<ChannelSet> sets;
+    std::vector<GroupwiseFactorSet> warm;
+    sets.reserve(static_cast<std::size_t>(links));
+    for (int k = 0; k < topo.num_cells; ++k)
+        for (int i = 0; i < topo.num_cells; ++i)
+            for (int j = 0; j < topo.users_per_cell; ++j) {
+                sets.push_back(single(channels.tensor(k, i, j)));
+                if (init) warm.push_back(as_set(init->rx(i, j), init->tx(k), init->delay(k, i, j)));
+            }
+    std::vector<const ChannelSet*> g;
+    std::vector<const GroupwiseFactorSet*> in;
+    for (std::size_t l = 0; l < sets.size(); ++l) {
+        g.push_back(&sets[l]);
+        if (init) in.push_back(&warm[l]);
+    }
+    auto solved = solve_groups(g, ranks, sweeps, init ? &in : nullptr, false, true);
+    IndividualResult result;
+    std::size_t longest = 1;
+    for (auto& r : solved) {
+        result.links.push_back(TuckerFactors{r.first.rx_factors[0], r.first.tx_factors[0], r.first.delay_factors[0],
+                                             r.first.cores[0]});
+        longest = std::max(longest, r.second.objective.size());
+        result.trace.iterations_run = std::max(result.trace.iterations_run, r.second.iterations_run);
+    }
+    result.trace.objective.assign(longest, 0.0);
+    for (auto& r : solved)
+        for (std::size_t s2 = 0; s2 < longest; ++s2)
+            result.trace.objective[s2] += r.second.objective[std::min(s2, r.second.objective.size() - 1)];
+    return result;
+}
+
 TuckerFactors hosvd(const Tensor3& x, const CompressionRanks& ranks) {
     ranks.validate_against(x.dim1(), x.dim2(), x.dim3());
     auto r = groupwise_solve(single(x), ranks, 0);

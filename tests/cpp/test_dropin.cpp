@@ -202,6 +202,36 @@ int main() {
         const Matrix g = rx_update_gram(set, old, 1, 0);
         CHECK((g - g.adjoint()).norm() <= 1e-12 * g.norm());
     }
+    // individual_solve == per-link hooi (test_decompose.cpp:326-335), cold and warm-started
+    {
+        ChannelSet set;
+        set.topology = SystemTopology{2, 2, 6, 8, 5, 2, 0.1};
+        for (int l = 0; l < 8; ++l) {
+            set.tensors.push_back(rng.tensor(6, 8, 5));
+            Vector c(5);
+            for (int q = 0; q < 5; ++q) c(q) = rng.c();
+            set.coeffs.push_back(c);
+        }
+        const CompressionRanks rk{3, 4, 3};
+        const IndividualResult ind = individual_solve(set, rk, 3);
+        CHECK(ind.links.size() == 8u);
+        double sum0 = 0.0;
+        for (int l : {0, 5}) {
+            const auto h = hooi(set.tensors[static_cast<std::size_t>(l)], rk, 3);
+            CHECK(std::abs(h.second.final() - tucker_residual(set.tensors[static_cast<std::size_t>(l)],
+                                                              ind.links[static_cast<std::size_t>(l)].rx,
+                                                              ind.links[static_cast<std::size_t>(l)].tx,
+                                                              ind.links[static_cast<std::size_t>(l)].delay)) <=
+                  1e-9 * h.second.initial());
+        }
+        for (int l = 0; l < 8; ++l) sum0 += hooi(set.tensors[static_cast<std::size_t>(l)], rk, 0).second.initial();
+        CHECK(std::abs(ind.trace.initial() - sum0) <= 1e-9 * sum0);
+        auto [gs, gt] = groupwise_solve(set, rk, 2);
+        const IndividualResult warm = individual_solve(set, rk, 2, &gs);
+        CHECK(warm.trace.initial() <= gt.final() * (1 + 1e-9));
+        for (std::size_t s2 = 1; s2 < warm.trace.objective.size(); ++s2)
+            CHECK(warm.trace.objective[s2] <= warm.trace.objective[s2 - 1] * (1 + 1e-12) + 1e-12);
+    }
     // test_sinr.cpp:337-365: lossless ranks -> compressed == full pipeline within 1e-8, both scopes
     {
         ChannelSet set;

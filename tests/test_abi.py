@@ -102,7 +102,7 @@ def test_cpp_dropin_library_exports_gwt_api():
                 "gwt::flop_estimate(", "gwt::shared_solve(", "gwt::truncated_svd(", "gwt::precoder_compressed(",
                 "gwt::covariance_compressed(", "gwt::woodbury_inverse_apply(", "gwt::filter_compressed(",
                 "gwt::sinr_compressed(", "gwt::run_full_pipeline(", "gwt::update_rx_factor(",
-                "gwt::tx_update_gram(", "gwt::update_delay_factor("):
+                "gwt::tx_update_gram(", "gwt::update_delay_factor(", "gwt::individual_solve("):
         assert sym in out, sym
 
 
