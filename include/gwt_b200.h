@@ -154,12 +154,13 @@ int gwt_reconstruct(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ran
 int gwt_mode_product(gwt_ctx* ctx, gwt_dtype dtype, gwt_mem mem, int64_t batch, int32_t d1, int32_t d2, int32_t d3,
                      const void* X, int32_t rows, const void* U, int32_t mode, void* Y);
 
-/* woodbury_inverse_apply (sinr.cpp:205-227) for `batch` m x m Hermitian covariances Q (complex128,
- * column-major): T = Q^-1 (Q - sigma^2 I) through a binary64 Cholesky on the device. status[b]:
- * 0 ok, 1 not positive definite, 2 condition estimate above 1e14, 4 non-finite input (the C++
- * drop-in rethrows the reference's exception texts). sigma <= 0 -> GWT_INVALID_ARGUMENT. */
-int gwt_woodbury_inverse(gwt_ctx* ctx, int32_t m, int64_t batch, gwt_mem mem, const void* Q, double sigma, void* T,
-                         int32_t* status);
+/* X = Q^-1 B for `batch` m x m Hermitian positive-definite Q and m x nrhs B (complex128, column-major)
+ * through a binary64 Cholesky on the device: the LLT of woodbury_inverse_apply (sinr.cpp:205-227,
+ * B = Q - sigma^2 I, check_cond = 1) and filter_full (sinr.cpp:113-127, B = H V, check_cond = 0).
+ * status[b]: 0 ok, 1 not positive definite, 2 condition estimate above 1e14 (check_cond), 4
+ * non-finite input; the C++ drop-in rethrows the reference's exception texts. */
+int gwt_hpd_solve(gwt_ctx* ctx, int32_t m, int32_t nrhs, int64_t batch, gwt_mem mem, const void* Q, const void* B,
+                  int32_t check_cond, void* X, int32_t* status);
 
 /* Closed-form system ledger (sinr.cpp:353-382); path 0 = full, 1 = compressed. Host only. */
 int gwt_flop_estimate(const gwt_topology* topo, const gwt_ranks* ranks, int32_t path, gwt_ledger* out);

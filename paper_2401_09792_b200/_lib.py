@@ -24,7 +24,7 @@ EXPORTS = (
     "gwt_ctx_create", "gwt_ctx_destroy", "gwt_last_error", "gwt_ctx_set_stream", "gwt_ctx_launch_count",
     "gwt_ctx_stage_times", "gwt_groupwise_solve", "gwt_sinr_compressed", "gwt_sinr_compressed_coeffs",
     "gwt_assemble_compressed", "gwt_leading_eigenvectors", "gwt_reconstruct", "gwt_flop_estimate",
-    "gwt_generate_channels", "gwt_mode_product", "gwt_sinr_full", "gwt_woodbury_inverse",
+    "gwt_generate_channels", "gwt_mode_product", "gwt_sinr_full", "gwt_hpd_solve",
 )
 
 
@@ -80,7 +80,7 @@ def load():
         "gwt_flop_estimate": (C.c_int, [P_T, P_R, i32, P_L]),
         "gwt_sinr_full": (C.c_int, [vp, P_T, i64, C.c_int, C.c_int, vp, vp, vp, vp, i64, C.c_int, vp, vp, vp, P_L]),
         "gwt_mode_product": (C.c_int, [vp, C.c_int, C.c_int, i64, i32, i32, i32, vp, i32, vp, i32, vp]),
-        "gwt_woodbury_inverse": (C.c_int, [vp, i32, i64, C.c_int, vp, C.c_double, vp, vp]),
+        "gwt_hpd_solve": (C.c_int, [vp, i32, i32, i64, C.c_int, vp, vp, i32, vp, vp]),
         "gwt_generate_channels": (C.c_int, [P_T, i64, i64, C.c_uint64, C.c_double, C.c_double, C.c_int, vp, vp,
                                             i32]),
     }

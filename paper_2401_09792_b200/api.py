@@ -406,9 +406,14 @@ class Context:
             Qc = Q.to(dtype=torch.complex128).transpose(-1, -2).contiguous()
         else:
             Qc = np.ascontiguousarray(np.swapaxes(np.asarray(Q, dtype=np.complex128), -1, -2))
+        if not sigma > 0.0:
+            raise InvalidArgument("woodbury_inverse_apply: sigma must be > 0")
+        eye = (torch.eye(m, dtype=Qc.dtype, device=Qc.device) if _is_torch(Qc) else np.eye(m, dtype=Qc.dtype))
+        Bc = Qc - (sigma * sigma) * eye  # RHS Q - sigma^2 I (column-major like Qc; the shift is symmetric)
+        Bc = Bc.contiguous() if _is_torch(Bc) else np.ascontiguousarray(Bc)
         T = _like(Qc, (b, m, m), "c")
         st = _like(Qc, (b,), "i32")
-        rc = self.lib.gwt_woodbury_inverse(self.h, m, b, _mem(Qc), _ptr(Qc), float(sigma), _ptr(T), _ptr(st))
+        rc = self.lib.gwt_hpd_solve(self.h, m, m, b, _mem(Qc), _ptr(Qc), _ptr(Bc), 1, _ptr(T), _ptr(st))
         self.check(rc)
         sth = st.cpu().numpy() if _is_torch(st) else st
         bad = np.nonzero(sth)[0]

@@ -1304,28 +1304,31 @@ int gwt_leading_eigenvectors(gwt_ctx* ctx, int32_t n, int32_t count, int64_t bat
     });
 }
 
-int gwt_woodbury_inverse(gwt_ctx* ctx, int32_t m, int64_t batch, gwt_mem mem, const void* Q, double sigma, void* T,
-                         int32_t* status) {
+int gwt_hpd_solve(gwt_ctx* ctx, int32_t m, int32_t nrhs, int64_t batch, gwt_mem mem, const void* Q, const void* B,
+                  int32_t check_cond, void* X, int32_t* status) {
     return guarded(ctx, [&] {
-        if (!(sigma > 0.0)) invalid("woodbury_inverse_apply: sigma must be > 0");  // sinr.cpp:206-207
-        if (m < 1 || batch < 0) invalid("woodbury_inverse_apply: bad covariance size");
-        if (batch == 0) return;
+        if (m < 1 || nrhs < 0 || batch < 0) invalid("hpd_solve: bad covariance or right-hand-side size");
+        if (batch == 0 || nrhs == 0) return;
         cudaStream_t st = ctx->stream;
-        const size_t bytes = 16 * (size_t)batch * m * m;
+        const size_t qb = 16 * (size_t)batch * m * m, bb = 16 * (size_t)batch * m * nrhs;
         const void* Qd = Q;
-        void* Td = T;
+        const void* Bd = B;
+        void* Xd = X;
         int* Sd = (int*)status;
         if (mem == GWT_MEM_HOST) {
-            void* q = ctx->ws(WS_GRAM, bytes);
-            ck(cudaMemcpyAsync(q, Q, bytes, cudaMemcpyHostToDevice, st), "H2D");
+            void* q = ctx->ws(WS_GRAM, qb);
+            void* r = ctx->ws(WS_EIGX, bb);
+            ck(cudaMemcpyAsync(q, Q, qb, cudaMemcpyHostToDevice, st), "H2D");
+            ck(cudaMemcpyAsync(r, B, bb, cudaMemcpyHostToDevice, st), "H2D");
             Qd = q;
-            Td = ctx->ws(WS_POOL, bytes);
+            Bd = r;
+            Xd = ctx->ws(WS_POOL, bb);
             Sd = (int*)ctx->ws(WS_STATUS, 4 * batch);
         }
-        void* Lw = ctx->ws(WS_EIGA, bytes);
-        ctx->launched(launch_woodbury(m, batch, Qd, sigma, Lw, Td, Sd, st));
+        void* Lw = ctx->ws(WS_EIGA, qb);
+        ctx->launched(launch_hpd_solve(m, nrhs, batch, Qd, Bd, check_cond, Lw, Xd, Sd, st));
         if (mem == GWT_MEM_HOST) {
-            ck(cudaMemcpyAsync(T, Td, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(X, Xd, bb, cudaMemcpyDeviceToHost, st), "D2H");
             ck(cudaMemcpyAsync(status, Sd, 4 * batch, cudaMemcpyDeviceToHost, st), "D2H");
         }
         ck(cudaStreamSynchronize(st), "sync");

@@ -5,22 +5,30 @@
 
 namespace gwtk {
 
-// woodbury_inverse_apply (proj/src/sinr.cpp:205-227) for a batch of m x m Hermitian covariances
-// (column-major binary64 complex): finite check, Cholesky of the lower triangle (Eigen::LLT
-// semantics: a non-positive pivot fails), condition estimate (max/min Cholesky diagonal)^2 > 1e14,
-// then T = Q^-1 (Q - sigma^2 I) by forward/back substitution, one column at a time. One thread per
-// matrix, L in a global workspace (single small systems: latency, not throughput, matters here).
+// Hermitian positive-definite solve X = Q^-1 B for a batch of m x m covariances and m x nrhs right-hand
+// sides (column-major binary64 complex), the Eigen::LLT use of woodbury_inverse_apply
+// (proj/src/sinr.cpp:205-227; B = Q - sigma^2 I) and filter_full (:113-127; B = H V): finite check,
+// Cholesky of the lower triangle (a non-positive pivot fails), optional condition estimate
+// (max/min Cholesky diagonal)^2 > 1e14, forward/back substitution per column. One thread per matrix,
+// L in a global workspace (single small systems: latency, not throughput, matters here).
 // status: 0 ok, 1 not positive definite, 2 condition estimate above 1e14, 4 non-finite input.
-__global__ void k_woodbury(int m, int64_t batch, const double2* __restrict__ Q, double sigma, double2* __restrict__ Lw,
-                           double2* __restrict__ T, int* __restrict__ status) {
+__global__ void k_hpd_solve(int m, int nrhs, int64_t batch, const double2* __restrict__ Q,
+                            const double2* __restrict__ B, int check_cond, double2* __restrict__ Lw,
+                            double2* __restrict__ T, int* __restrict__ status) {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch) return;
     const int64_t mm = (int64_t)m * m;
     const double2* q = Q + b * mm;
+    const double2* rhs = B + b * (int64_t)m * nrhs;
     double2* l = Lw + b * mm;
-    double2* t = T + b * mm;
+    double2* t = T + b * (int64_t)m * nrhs;
     for (int64_t e = 0; e < mm; ++e)
         if (!isfinite(q[e].x) || !isfinite(q[e].y)) {
+            status[b] = 4;
+            return;
+        }
+    for (int64_t e = 0; e < (int64_t)m * nrhs; ++e)
+        if (!isfinite(rhs[e].x) || !isfinite(rhs[e].y)) {
             status[b] = 4;
             return;
         }
@@ -49,16 +57,14 @@ __global__ void k_woodbury(int m, int64_t batch, const double2* __restrict__ Q, 
             l[r + (int64_t)m * c] = make_double2(s.x / lcc, s.y / lcc);
         }
     }
-    if ((dmax / dmin) * (dmax / dmin) > 1e14) {
+    if (check_cond && (dmax / dmin) * (dmax / dmin) > 1e14) {
         status[b] = 2;
         return;
     }
-    const double s2 = sigma * sigma;
-    for (int j = 0; j < m; ++j) {
+    for (int j = 0; j < nrhs; ++j) {
         double2* x = t + (int64_t)m * j;
-        for (int i = 0; i < m; ++i) {  // forward: L y = q_j - sigma^2 e_j
-            double2 acc = q[i + (int64_t)m * j];
-            if (i == j) acc.x -= s2;
+        for (int i = 0; i < m; ++i) {  // forward: L y = b_j
+            double2 acc = rhs[i + (int64_t)m * j];
             for (int k = 0; k < i; ++k) {
                 const double2 a = l[i + (int64_t)m * k], y = x[k];
                 acc.x -= a.x * y.x - a.y * y.y;
@@ -81,10 +87,10 @@ __global__ void k_woodbury(int m, int64_t batch, const double2* __restrict__ Q, 
     status[b] = 0;
 }
 
-cudaError_t launch_woodbury(int m, int64_t batch, const void* Q, double sigma, void* Lw, void* T, int* status,
-                            cudaStream_t st) {
-    k_woodbury<<<(unsigned)((batch + 63) / 64), 64, 0, st>>>(m, batch, (const double2*)Q, sigma, (double2*)Lw,
-                                                              (double2*)T, status);
+cudaError_t launch_hpd_solve(int m, int nrhs, int64_t batch, const void* Q, const void* B, int check_cond, void* Lw,
+                             void* X, int* status, cudaStream_t st) {
+    k_hpd_solve<<<(unsigned)((batch + 63) / 64), 64, 0, st>>>(m, nrhs, batch, (const double2*)Q, (const double2*)B,
+                                                               check_cond, (double2*)Lw, (double2*)X, status);
     return cudaGetLastError();
 }
 

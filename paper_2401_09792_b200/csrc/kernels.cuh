@@ -60,8 +60,8 @@ cudaError_t launch_stop_freeze(int64_t ngroups, const double* trace, const doubl
                                int64_t b_sz, int64_t c_sz, int64_t g_sz, cudaStream_t st);
 cudaError_t launch_unfreeze(int64_t ngroups, const int* stop, void* A, void* B, void* Cf, void* Gc, const void* frozen,
                             int64_t a_sz, int64_t b_sz, int64_t c_sz, int64_t g_sz, cudaStream_t st);
-cudaError_t launch_woodbury(int m, int64_t batch, const void* Q, double sigma, void* Lw, void* T, int* status,
-                            cudaStream_t st);
+cudaError_t launch_hpd_solve(int m, int nrhs, int64_t batch, const void* Q, const void* B, int check_cond, void* Lw,
+                             void* X, int* status, cudaStream_t st);
 cudaError_t launch_objective(int64_t ngroups, const double* energy, const double* captured, double* trace, int stride,
                              int slot, cudaStream_t st);
 template <class T> cudaError_t launch_broadcast(const void* src, void* dst, int64_t elems, int copies, int64_t ngroups,

@@ -55,10 +55,35 @@ std::vector<std::pair<int, int>> scope_pairs(const SystemTopology& topology, Int
 CompressedChannels assemble_all_compressed(const SystemTopology& topology, const GroupwiseFactorSet& factors,
                                            const std::vector<Vector>& coeffs, FlopLedger* ledger = nullptr);
 
+struct AssembledChannels {
+    SystemTopology topology;
+    std::vector<Matrix> h;  // num_links(), each M x N
+    const Matrix& at(int k, int i, int j) const {
+        return h[(k * topology.num_cells + i) * topology.users_per_cell + j];
+    }
+};
+
+// Single-system stage API of the full-size path (sinr.hpp:69-89) and the whole-system evaluation on
+// assembled channels (sinr.hpp:128-129), the reference's literal per-user route: device SVD
+// (truncated_svd) and device Cholesky solve (gwt_hpd_solve), Matrix products on the host side.
+// run_full_pipeline below is the batched device path of the same computation.
+AssembledChannels assemble_all_full(const ChannelSet& channels, FlopLedger* ledger = nullptr);
+Precoder precoder_full(const Matrix& h, int streams, FlopLedger* ledger = nullptr);
+std::vector<Precoder> precoders_full(const AssembledChannels& assembled, FlopLedger* ledger = nullptr);
+Matrix covariance_full(const AssembledChannels& assembled, const std::vector<Precoder>& precoders,
+                       InterferenceScope scope, int i, int j, FlopLedger* ledger = nullptr);
+Matrix filter_full(const Matrix& q, const Matrix& h_serving, const Matrix& v_serving, FlopLedger* ledger = nullptr);
+std::vector<StreamSinr> sinr_full(const Matrix& w, const Matrix& q, const Matrix& h_serving, const Matrix& v_serving,
+                                  FlopLedger* ledger = nullptr);
+SinrReport evaluate_assembled(const AssembledChannels& assembled, InterferenceScope scope, FlopLedger initial = {});
+/// Individual-model evaluation (sinr.hpp:141-143): per-link factors rebuilt at full size, then the full path.
+SinrReport run_reconstructed_pipeline(const SystemTopology& topology, const std::vector<TuckerFactors>& links,
+                                      const std::vector<Vector>& coeffs, InterferenceScope scope);
+
 // Single-system stage API of the compressed path (sinr.hpp:99-124). The batched pipeline below runs
 // these stages fused on the device; the stage functions keep the reference's building blocks for
 // callers that compose them: the SVD and the Cholesky run on the device (truncated_svd ->
-// batched eigensolver, woodbury_inverse_apply -> gwt_woodbury_inverse), the m x n products and the
+// batched eigensolver, woodbury_inverse_apply -> gwt_hpd_solve), the m x n products and the
 // per-stream formula use the Matrix type like the Eigen expressions they replace.
 Precoder precoder_compressed(const Matrix& h_small, int streams, FlopLedger* ledger = nullptr);
 std::vector<Precoder> precoders_compressed(const CompressedChannels& compressed, FlopLedger* ledger = nullptr);

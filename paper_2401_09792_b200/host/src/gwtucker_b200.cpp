@@ -668,6 +668,127 @@ std::vector<std::pair<int, int>> scope_pairs(const SystemTopology& topology, Int
     return pairs;
 }
 
+// ---- single-system stages of the full-size path (sinr.cpp:67-138)
+AssembledChannels assemble_all_full(const ChannelSet& channels, FlopLedger* ledger) {
+    AssembledChannels out;
+    out.topology = channels.topology;
+    out.h.reserve(channels.tensors.size());
+    for (std::size_t l = 0; l < channels.tensors.size(); ++l)
+        out.h.push_back(assemble_channel_full(channels.tensors[l], channels.coeffs[l], ledger));
+    return out;
+}
+
+Precoder precoder_full(const Matrix& h, int streams, FlopLedger* ledger) {
+    if (streams > std::min(h.rows(), h.cols()))
+        throw std::invalid_argument("precoder: stream count " + std::to_string(streams) + " exceeds min dimension of " +
+                                    std::to_string(h.rows()) + "x" + std::to_string(h.cols()) + " channel");
+    TruncatedSvd svd = truncated_svd(h, streams);
+    if (ledger) ledger->precoder += i64(h.rows()) * h.cols() * streams;
+    return {std::move(svd.v), std::move(svd.singular_values), std::move(svd.u)};
+}
+
+std::vector<Precoder> precoders_full(const AssembledChannels& assembled, FlopLedger* ledger) {
+    const SystemTopology& topo = assembled.topology;
+    std::vector<Precoder> out;
+    out.reserve(static_cast<std::size_t>(topo.num_users()));
+    for (int i = 0; i < topo.num_cells; ++i)
+        for (int j = 0; j < topo.users_per_cell; ++j)
+            out.push_back(precoder_full(assembled.at(i, i, j), topo.num_streams, ledger));
+    return out;
+}
+
+Matrix covariance_full(const AssembledChannels& assembled, const std::vector<Precoder>& precoders,
+                       InterferenceScope scope, int i, int j, FlopLedger* ledger) {
+    const SystemTopology& topo = assembled.topology;
+    const double sigma = topo.noise_std;
+    Matrix q = (sigma * sigma) * Matrix::Identity(topo.rx_antennas, topo.rx_antennas);
+    for (const auto& kl : scope_pairs(topo, scope, i, j)) {
+        const std::size_t user = static_cast<std::size_t>(kl.first) * topo.users_per_cell + kl.second;
+        if (user >= precoders.size()) throw std::invalid_argument("covariance: scope references missing precoder");
+        const Matrix term = assembled.at(kl.first, i, j) * precoders[user].v;
+        q += term * term.adjoint();
+    }
+    if (ledger) {
+        const std::int64_t M = topo.rx_antennas, N = topo.tx_antennas, L = topo.num_streams;
+        ledger->covariance += i64(topo.num_users()) * (M * N * L + M * M * L);
+    }
+    return q;
+}
+
+Matrix filter_full(const Matrix& q, const Matrix& h_serving, const Matrix& v_serving, FlopLedger* ledger) {
+    if (!q.allFinite() || !h_serving.allFinite() || !v_serving.allFinite())
+        throw std::invalid_argument("filter: non-finite input");
+    const Matrix hv = h_serving * v_serving;
+    Matrix w(q.rows(), hv.cols());
+    int32_t status = 0;
+    check(gwt_hpd_solve(ctx(), static_cast<int32_t>(q.rows()), static_cast<int32_t>(hv.cols()), 1, GWT_MEM_HOST,
+                        q.data(), hv.data(), 0, w.data(), &status));
+    if (status == 4) throw std::invalid_argument("filter: non-finite input");
+    if (status != 0) throw std::runtime_error("filter: covariance is not positive definite");
+    if (ledger) {
+        const std::int64_t M = q.rows(), L = v_serving.cols();
+        ledger->inverse += M * M * M;
+        ledger->filter += M * M * L;
+    }
+    return w;
+}
+
+std::vector<StreamSinr> sinr_full(const Matrix& w, const Matrix& q, const Matrix& h_serving, const Matrix& v_serving,
+                                  FlopLedger* ledger) {
+    if (ledger) {
+        const std::int64_t M = q.rows(), L = w.cols();
+        ledger->sinr += L * (M * M + 2 * M);
+    }
+    return sinr_compressed(w, q, h_serving, v_serving, nullptr);  // same stream formula (stream_sinrs)
+}
+
+SinrReport evaluate_assembled(const AssembledChannels& assembled, InterferenceScope scope, FlopLedger initial) {
+    const SystemTopology& topo = assembled.topology;
+    SinrReport report;
+    report.num_cells = topo.num_cells;
+    report.users_per_cell = topo.users_per_cell;
+    report.num_streams = topo.num_streams;
+    report.ledger = initial;
+    report.signal_power.resize(static_cast<std::size_t>(topo.num_users()) * topo.num_streams);
+    report.sinr.resize(report.signal_power.size());
+    const std::vector<Precoder> precoders = precoders_full(assembled, &report.ledger);
+    for (int i = 0; i < topo.num_cells; ++i)
+        for (int j = 0; j < topo.users_per_cell; ++j) {
+            const Matrix& h = assembled.at(i, i, j);
+            const Precoder& pre = precoders[static_cast<std::size_t>(report.user_index(i, j))];
+            const Matrix q = covariance_full(assembled, precoders, scope, i, j, &report.ledger);
+            const Matrix w = filter_full(q, h, pre.v, &report.ledger);
+            const std::vector<StreamSinr> ss = sinr_full(w, q, h, pre.v, &report.ledger);
+            for (int r = 0; r < topo.num_streams; ++r) {
+                const std::size_t at = static_cast<std::size_t>(report.user_index(i, j)) * topo.num_streams + r;
+                report.signal_power[at] = ss[static_cast<std::size_t>(r)].signal_power;
+                report.sinr[at] = ss[static_cast<std::size_t>(r)].sinr;
+            }
+        }
+    return report;
+}
+
+SinrReport run_reconstructed_pipeline(const SystemTopology& topology, const std::vector<TuckerFactors>& links,
+                                      const std::vector<Vector>& coeffs, InterferenceScope scope) {
+    if (links.size() != coeffs.size() || static_cast<int>(links.size()) != topology.num_links())
+        throw std::invalid_argument("run_reconstructed_pipeline: grid sizes do not match topology");
+    const auto t0 = std::chrono::steady_clock::now();
+    FlopLedger ledger;
+    AssembledChannels assembled;
+    assembled.topology = topology;
+    assembled.h.reserve(links.size());
+    for (std::size_t l = 0; l < links.size(); ++l) {
+        const TuckerFactors& f = links[l];
+        const Matrix h_small = assemble_channel_compressed(f.core, f.delay, coeffs[l], &ledger);
+        assembled.h.push_back(f.rx * h_small * f.tx.transpose());  // Tucker mode-2 convention: B^T
+        const std::int64_t M = f.rx.rows(), m = f.rx.cols(), n = f.tx.cols(), N = f.tx.rows();
+        ledger.reconstruct += M * m * n + M * n * N;
+    }
+    SinrReport report = evaluate_assembled(assembled, scope, ledger);
+    report.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return report;
+}
+
 // ---- single-system stages of the compressed path (sinr.cpp:162-254)
 Precoder precoder_compressed(const Matrix& h_small, int streams, FlopLedger* ledger) {
     if (streams > std::min(h_small.rows(), h_small.cols()))
@@ -715,8 +836,9 @@ WoodburyInverse woodbury_inverse_apply(const Matrix& q_small, double sigma, Flop
     WoodburyInverse out;
     out.t = Matrix(m, m);
     int32_t status = 0;
-    check(gwt_woodbury_inverse(ctx(), static_cast<int32_t>(m), 1, GWT_MEM_HOST, q_small.data(), sigma, out.t.data(),
-                               &status));
+    const Matrix rhs = q_small - (sigma * sigma) * Matrix::Identity(m, m);
+    check(gwt_hpd_solve(ctx(), static_cast<int32_t>(m), static_cast<int32_t>(m), 1, GWT_MEM_HOST, q_small.data(),
+                        rhs.data(), 1, out.t.data(), &status));
     if (status == 1) throw std::runtime_error("woodbury_inverse_apply: covariance is numerically singular");
     if (status == 2)
         throw std::runtime_error("woodbury_inverse_apply: covariance is numerically singular "

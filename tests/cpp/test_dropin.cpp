@@ -251,7 +251,24 @@ int main() {
                 worst = std::max(worst, std::abs(comp.sinr[e] - full.sinr[e]) / std::abs(full.sinr[e]));
             CHECK(worst <= 1e-8);
             CHECK(full.ledger.total() == flop_estimate(set.topology, {6, 8, 5}, PipelinePath::full).total());
+            // the reference's literal per-user route (assemble_all_full -> evaluate_assembled) == batched path
+            FlopLedger led;
+            const SinrReport lit = evaluate_assembled(assemble_all_full(set, &led), sc, led);
+            double w2 = 0.0;
+            for (std::size_t e = 0; e < full.sinr.size(); ++e)
+                w2 = std::max(w2, std::abs(lit.sinr[e] - full.sinr[e]) / std::abs(full.sinr[e]));
+            CHECK(w2 <= 1e-9);
+            CHECK(lit.ledger.total() == full.ledger.total());
+            // individual model at lossless ranks: rebuilt channels reproduce the full path
+            const IndividualResult ind = individual_solve(set, {6, 8, 5}, 1);
+            const SinrReport rec = run_reconstructed_pipeline(set.topology, ind.links, set.coeffs, sc);
+            double w3 = 0.0;
+            for (std::size_t e = 0; e < full.sinr.size(); ++e)
+                w3 = std::max(w3, std::abs(rec.sinr[e] - full.sinr[e]) / std::abs(full.sinr[e]));
+            CHECK(w3 <= 1e-8);
         }
+        CHECK(throws_with<std::runtime_error>([&] { filter_full(Matrix(3, 3), rng.matrix(3, 4), rng.matrix(4, 2)); },
+                                              "filter: covariance is not positive definite"));
     }
     // test_sinr.cpp:391-399: single user, single stream at full ranks -> sigma_1^2 / sigma^2
     {

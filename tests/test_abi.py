@@ -102,7 +102,8 @@ def test_cpp_dropin_library_exports_gwt_api():
                 "gwt::flop_estimate(", "gwt::shared_solve(", "gwt::truncated_svd(", "gwt::precoder_compressed(",
                 "gwt::covariance_compressed(", "gwt::woodbury_inverse_apply(", "gwt::filter_compressed(",
                 "gwt::sinr_compressed(", "gwt::run_full_pipeline(", "gwt::update_rx_factor(",
-                "gwt::tx_update_gram(", "gwt::update_delay_factor(", "gwt::individual_solve("):
+                "gwt::tx_update_gram(", "gwt::update_delay_factor(", "gwt::individual_solve(",
+                "gwt::evaluate_assembled(", "gwt::run_reconstructed_pipeline(", "gwt::filter_full("):
         assert sym in out, sym
 
 
