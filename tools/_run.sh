@@ -1,2 +1,5 @@
-./paper_2401_09792_b200/_build/test_dropin 2>&1 | tail -5
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
+python tools/ncu_summary.py launches gpurun_out/launches.csv > gpurun_out/r01_launches.txt
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
