@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, const 
     const double inv_n = tnorm > 0.0 ? 1.0 / tnorm : 1.0;
     for (int i = tid; i < D; i += NT) {
         fd[i] = (float)((double)sd[i] * inv_n);
-        fe2[i] = (float)((double)se2[i] * inv_n * inv_n);
+        fe2[i] = i > 0 ? (float)((double)se2[i - 1] * inv_n * inv_n) : 0.f;  // shifted (sturm_count_p32)
     }
     __syncthreads();
     {

@@ -492,7 +492,9 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
     const double inv_n = tnorm > 0.0 ? 1.0 / tnorm : 1.0;
     for (int i = tid; i < D; i += NT) {
         fd[i] = (float)((double)sd[i] * inv_n);
-        fe2[i] = (float)((double)se2[i] * inv_n * inv_n);
+        // fp32 storage: shifted (fe2[i] = e_{i-1}^2) for sturm_count_p32; binary64: as is
+        if constexpr (sizeof(R) == 4) fe2[i] = i > 0 ? (float)((double)se2[i - 1] * inv_n * inv_n) : 0.f;
+        else fe2[i] = (float)((double)se2[i] * inv_n * inv_n);
     }
     __syncthreads();
     // 3a. multisection, S lanes (power of two, within one warp) per wanted eigenvalue
@@ -547,7 +549,7 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
 #define XV(i) XR[(i) * count + t]
         const R tiny = (R)fmax(eps * tnorm, sizeof(R) == 4 ? 1e-30 : 1e-290);
         // solves from the fp32 bisection shift (~2e-7 rel): 2 reach fp32 accuracy, 3 binary64
-        constexpr int kSolves = sizeof(R) == 4 ? 2 : 3;
+        constexpr int kSolves = sizeof(R) == 4 ? GWT_FP32_SOLVES : 3;
         for (int rd = 0; rd < rounds; ++rd) {
             if (t < count && scl[t] == rd) {
                 const R lam = (R)lamv[t];

@@ -332,7 +332,9 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
     const double inv_n = tnorm > 0.0 ? 1.0 / tnorm : 1.0;
     for (int i = lane; i < D; i += 32) {
         fd[i] = (float)((double)sd[i] * inv_n);
-        fe2[i] = (float)((double)se2[i] * inv_n * inv_n);
+        // fp32 storage: shifted (fe2[i] = e_{i-1}^2) for sturm_count_p32; binary64: as is
+        if constexpr (sizeof(R) == 4) fe2[i] = i > 0 ? (float)((double)se2[i - 1] * inv_n * inv_n) : 0.f;
+        else fe2[i] = (float)((double)se2[i] * inv_n * inv_n);
     }
     __syncwarp();
     // 3a. multisection: S lanes per wanted eigenvalue (t-th largest = ascending index D-1-t)
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
 #define LU_(arr, i) arr[(i) * count + t]
     const R tiny = (R)fmax(eps * tnorm, sizeof(R) == 4 ? 1e-30 : 1e-290);
     // solves from the fp32 bisection shift (~2e-7 rel): 2 reach fp32 accuracy, 3 binary64
-    constexpr int kSolves = sizeof(R) == 4 ? 2 : 3;
+    constexpr int kSolves = sizeof(R) == 4 ? GWT_FP32_SOLVES : 3;
     R x[DM];
 #pragma unroll
     for (int i = 0; i < DM; ++i) x[i] = R(0);

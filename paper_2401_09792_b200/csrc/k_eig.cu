@@ -103,14 +103,21 @@ __device__ __forceinline__ int sturm_count_fast(int D, const double* d, const do
 // zero p_i (+0) counts like the q = -pivmin convention: the sign change moves to the next row.
 // Used for the fp32-storage (c64) solvers; the c128 solvers keep the pivot recurrence below, whose
 // count is monotone in x (Kahan), so their fp32 shifts resolve small eigenvalues reproducibly.
-__device__ __forceinline__ int sturm_count_p32(int D, const float* d, const float* e2, float x) {
-    float pm = 1.0f, p = d[0] - x;
-    int cnt = (int)(__float_as_uint(p) >> 31);
-    int i = 1;
+__device__ __forceinline__ int sturm_count_p32(int D, const float* d, const float* e2s, float x) {
+    // e2s is the SHIFTED squared off-diagonal (e2s[0] = 0, e2s[i] = e_{i-1}^2, written so by the fp32
+    // callers) and d, e2s are 16-byte aligned: p_{i+1} = (d_i - x) p_i - e2s[i] p_{i-1}, p_0 = 1,
+    // p_{-1} = 0; blocks of 8 rows read both arrays with 16-byte loads
+    float pm = 0.0f, p = 1.0f;
+    int cnt = 0;
+    int i = 0;
     for (; i + 8 <= D; i += 8) {
+        const float4 da = *reinterpret_cast<const float4*>(d + i), db = *reinterpret_cast<const float4*>(d + i + 4);
+        const float4 ea = *reinterpret_cast<const float4*>(e2s + i), eb = *reinterpret_cast<const float4*>(e2s + i + 4);
+        const float dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+        const float ev[8] = {ea.x, ea.y, ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const float pn = fmaf(d[i + u] - x, p, -e2[i + u - 1] * pm);
+            const float pn = fmaf(dv[u] - x, p, -ev[u] * pm);
             cnt += (int)((__float_as_uint(pn) ^ __float_as_uint(p)) >> 31);
             pm = p;
             p = pn;
@@ -121,7 +128,7 @@ __device__ __forceinline__ int sturm_count_p32(int D, const float* d, const floa
         pm *= sc;
     }
     for (; i < D; ++i) {
-        const float pn = fmaf(d[i] - x, p, -e2[i - 1] * pm);
+        const float pn = fmaf(d[i] - x, p, -e2s[i] * pm);
         cnt += (int)((__float_as_uint(pn) ^ __float_as_uint(p)) >> 31);
         pm = p;
         p = pn;
@@ -152,6 +159,9 @@ __device__ __forceinline__ int sturm_count_r(int D, const float* d, const float*
     else return sturm_count_f32(D, d, e2, x, 1e-30f);
 }
 
+#ifndef GWT_FP32_SOLVES
+#define GWT_FP32_SOLVES 2  // inverse-iteration solves for fp32 storage (eig_warp.cuh / eig_cta.cuh)
+#endif
 #include "eig_warp.cuh"
 #include "eig_cta.cuh"
 #include "eig_big.cuh"

@@ -1,5 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
-python tools/ncu_summary.py launches gpurun_out/launches.csv > gpurun_out/r01_launches.txt
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -E "FAILED|passed|failed" | head -10
+GWT_LIB_PATH=paper_2401_09792_b200/_build/phase/libgwt_b200.so timeout 300 python tools/eig_real_phases.py 2>&1 | tail -2
+for i in 1 2; do timeout 300 python tools/tucker_probe.py 2>&1 | head -1; done
