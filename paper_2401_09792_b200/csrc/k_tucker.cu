@@ -536,6 +536,17 @@ cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, cons
         dim3 grid((rows + TR_ - 1) / TR_, (d.Cols + TC_ - 1) / TC_, (unsigned)std::min<int64_t>(65535, items - i0)); \
         k_cgemm_conjU<T, TR_, TC_, RT_, CT_><<<grid, 256, 0, st>>>(t, d, t.links(), i0, a, u, o);          \
     }
+    // short items (rows <= 64, e.g. W = Y1 x2 B^H with M*p = 48 rows at C2): 64-row tiles instead of
+    // 128-row tiles that would run 60 % empty
+    static const bool tr64 = !(std::getenv("GWT_GEMM_TR64") && std::atoi(std::getenv("GWT_GEMM_TR64")) == 0);
+    if (tr64 && rows <= 64 && d.Cols <= 32) {
+        if (d.Cols <= 8) GWT_GEMM(64, 8, 1, 2)
+        else if (d.Cols <= 12) GWT_GEMM(64, 12, 1, 3)
+        else if (d.Cols <= 16) GWT_GEMM(64, 16, 1, 4)
+        else if (d.Cols <= 24) GWT_GEMM(64, 24, 2, 3)
+        else GWT_GEMM(64, 32, 2, 4)
+        return cudaGetLastError();
+    }
     if (d.Cols <= 8) GWT_GEMM(128, 8, 2, 2)
     else if (d.Cols <= 12) GWT_GEMM(128, 12, 2, 3)
     else if (d.Cols <= 16) GWT_GEMM(128, 16, 2, 4)
