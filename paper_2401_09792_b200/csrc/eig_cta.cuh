@@ -213,7 +213,10 @@ __device__ __forceinline__ void hh_cta_reg64(int D, int LD, float2* A, float2* p
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int c = q + Q * u;
-            vc[u] = (c > k && c < D) ? (c == k + 1 ? v0 : colk[c]) : make_float2(0.f, 0.f);
+            // unconditional load (c < 64 stays inside the shared matrix: LD*(D-3) + 63 < LD*D), then
+            // selects: the predicated load compiled to per-column branches (ncu: branch_resolving stalls)
+            const float2 ck = colk[c];
+            vc[u] = (c > k && c < D) ? (c == k + 1 ? v0 : ck) : make_float2(0.f, 0.f);
             if (u & 1) cfma(p1, a[u], vc[u]);
             else cfma(p0, a[u], vc[u]);
         }
@@ -242,11 +245,9 @@ __device__ __forceinline__ void hh_cta_reg64(int D, int LD, float2* A, float2* p
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int c = q + Q * u;
-            float2 wc = make_float2(0.f, 0.f);
-            if (c > k && c < D) {
-                const float2 pc = pp[c];
-                wc = make_float2(pc.x - kk * vc[u].x, pc.y - kk * vc[u].y);
-            }
+            const float2 pc = pp[c];  // unconditional (inside the shared-memory layout), masked below
+            const float2 wc = (c > k && c < D) ? make_float2(pc.x - kk * vc[u].x, pc.y - kk * vc[u].y)
+                                                : make_float2(0.f, 0.f);
             // a[r][c] -= v_r conj(w_c) + w_r conj(v_c)
             a[u].x -= v.x * wc.x + v.y * wc.y + w.x * vc[u].x + w.y * vc[u].y;
             a[u].y -= v.y * wc.x - v.x * wc.y + w.y * vc[u].x - w.x * vc[u].y;
