@@ -560,22 +560,17 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                 R dcur = sd[0] - lam, ucur = se[0];
                 for (int i = 0; i + 1 < D; ++i) {
                     const R sb = se[i], dn = sd[i + 1] - lam, en = (i + 2 < D) ? se[i + 1] : R(0);
-                    R mult;
-                    if (fabs(dcur) >= fabs(sb)) {
-                        const R di = dcur == R(0) ? tiny : dcur;
-                        mult = ii_div(sb, di);
-                        LU_(DDv, i) = di;
-                        LU_(DUv, i) = ucur;
-                        dcur = dn - mult * ucur;
-                        ucur = en;
-                    } else {
-                        mult = ii_div(dcur, sb);
-                        sw[i >> 5] |= 1u << (i & 31);
-                        LU_(DDv, i) = sb;
-                        LU_(DUv, i) = dn;
-                        dcur = ucur - mult * dn;
-                        ucur = -mult * en;
-                    }
+                    // branch-free partial pivoting (the threads of a warp pivot differently: the
+                    // if/else form serialised both paths)
+                    const bool piv = !(fabs(dcur) >= fabs(sb));
+                    const R di = piv ? sb : (dcur == R(0) ? tiny : dcur);
+                    const R mult = ii_div(piv ? dcur : sb, di);
+                    if (piv) sw[i >> 5] |= 1u << (i & 31);
+                    LU_(DDv, i) = di;
+                    LU_(DUv, i) = piv ? dn : ucur;
+                    const R ndc = piv ? ucur - mult * dn : dn - mult * ucur;
+                    ucur = piv ? -mult * en : en;
+                    dcur = ndc;
                     LU_(MLv, i) = mult;
                 }
                 LU_(DDv, D - 1) = dcur;
@@ -599,20 +594,17 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                     R xi = XV(0);  // forward: row interchanges and multipliers, carried in registers
                     for (int i = 0; i + 1 < D; ++i) {
                         const R ml = LU_(MLv, i), xn = XV(i + 1);
-                        if ((sw[i >> 5] >> (i & 31)) & 1u) {
-                            XV(i) = xn;
-                            xi = xi - ml * xn;
-                        } else {
-                            XV(i) = xi;
-                            xi = xn - ml * xi;
-                        }
+                        const bool swp = (sw[i >> 5] >> (i & 31)) & 1u;
+                        XV(i) = swp ? xn : xi;
+                        xi = swp ? xi - ml * xn : xn - ml * xi;
                     }
                     XV(D - 1) = xi;
                     R x1 = R(0), x2 = R(0);  // back substitution with U, x[i+1], x[i+2] in registers
                     for (int i = D - 1; i >= 0; --i) {
                         R acc = XV(i);
                         if (i + 1 < D) acc -= LU_(DUv, i) * x1;
-                        if (i + 2 < D && ((sw[i >> 5] >> (i & 31)) & 1u)) acc -= se[i + 1] * x2;
+                        const R u2 = (i + 2 < D && ((sw[i >> 5] >> (i & 31)) & 1u)) ? se[i + 1] : R(0);
+                        acc -= u2 * x2;
                         const R v = acc * LU_(DDv, i);
                         XV(i) = v;
                         x2 = x1;

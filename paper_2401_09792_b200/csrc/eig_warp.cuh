@@ -395,22 +395,16 @@ __global__ void __launch_bounds__(128) k_heev_wr(int D, int count, int64_t batch
             R dcur = sd[0] - lam, ucur = se[0];
             for (int i = 0; i + 1 < D; ++i) {
                 const R sb = se[i], dn = sd[i + 1] - lam, en = (i + 2 < D) ? se[i + 1] : R(0);
-                R mult;
-                if (fabs(dcur) >= fabs(sb)) {
-                    const R di = dcur == R(0) ? tiny : dcur;
-                    mult = ii_div(sb, di);
-                    LU_(DDv, i) = di;
-                    LU_(DUv, i) = ucur;
-                    dcur = dn - mult * ucur;
-                    ucur = en;
-                } else {
-                    mult = ii_div(dcur, sb);
-                    sw |= 1u << i;
-                    LU_(DDv, i) = sb;
-                    LU_(DUv, i) = dn;
-                    dcur = ucur - mult * dn;
-                    ucur = -mult * en;
-                }
+                // branch-free partial pivoting (lanes pivot differently; if/else serialised both paths)
+                const bool piv = !(fabs(dcur) >= fabs(sb));
+                const R di = piv ? sb : (dcur == R(0) ? tiny : dcur);
+                const R mult = ii_div(piv ? dcur : sb, di);
+                if (piv) sw |= 1u << i;
+                LU_(DDv, i) = di;
+                LU_(DUv, i) = piv ? dn : ucur;
+                const R ndc = piv ? ucur - mult * dn : dn - mult * ucur;
+                ucur = piv ? -mult * en : en;
+                dcur = ndc;
                 LU_(MLv, i) = mult;
             }
             LU_(DDv, D - 1) = dcur;
