@@ -22,6 +22,8 @@
  *   gwt_flop_estimate        <- gwt::flop_estimate  include/gwtucker/sinr.hpp:148-149
  *   gwt_mode_product         <- gwt::mode_product  include/gwtucker/tensor.hpp:70 (batched)
  *   gwt_sinr_full            <- gwt::run_full_pipeline  include/gwtucker/sinr.hpp:134 (batched over F grids)
+ *   gwt_hpd_solve            <- the Eigen::LLT solves of woodbury_inverse_apply (sinr.cpp:205-227) and
+ *                               filter_full (sinr.cpp:113-127), batched
  *
  * Layouts. Complex = interleaved (re, im) pairs: float2 for
  * GWT_C64, double2 for GWT_C128 — layout-compatible with std::complex.
