@@ -1,2 +1,3 @@
-for v in "GWT_REBUILD_GSMEM=1" "GWT_REBUILD_GSMEM=0" "GWT_REBUILD_GSMEM=1" "GWT_REBUILD_GSMEM=0"; do echo "$v $(env GWT_SINR_DEV_LANES=1 $v timeout 120 python tools/sinr_time.py C2 100 | tail -1) | 2L $(env $v timeout 120 python tools/sinr_time.py C2 100 | tail -1 | cut -c1-40)"; done
-for c in C3 C5; do echo "$c $(GWT_SINR_DEV_LANES=1 timeout 200 python tools/sinr_time.py $c 3 | tail -1)"; done
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -E "FAILED|passed|failed" | head -5
+./paper_2401_09792_b200/_build/test_dropin 2>&1 | tail -1
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
