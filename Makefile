@@ -3,7 +3,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v
-CXXFLAGS := -O3 -std=c++17 -fPIC -Wall
+CXXFLAGS := -O3 -std=c++17 -fPIC -Wall -ffp-contract=off
 PKG := paper_2401_09792_b200
 SRC := $(PKG)/csrc
 OBJ := $(PKG)/_build/obj

@@ -1,29 +1,45 @@
 #!/usr/bin/env python
 """Benchmark of the B200 hot path (BASELINE.json metric) — one JSON line on rank 0.
 
-Workload: BASELINE.json configs[1] (C2): Nr=4, Nt=64, K=32 submatrices, G=16
-channels/group, 64 groups, 272 subcarriers, ranks (4,24,12), complex64, MMSE
-SINR at 10 dB, 4 streams (J=2, K=G/4 mapping, paper_experiment scope;
-DESIGN.md §2). A "step" is one pass of the compressed-form SINR stage
-(rebuild + precoder + MMSE over all groups x subcarriers) — the headline
-metric "SINR evals/sec" (one eval = one user x one subcarrier, all streams).
-The Tucker stage (groupwise_solve, 20 fixed sweeps, all groups) is timed in
-the same run and reported under "tucker" (Tucker channels/sec).
+Headline workload: BASELINE.json configs[3] (C4), the largest single-GPU
+config: Nr=8, Nt=256, K=64 submatrices, G=64 channels/group, 512 groups, 3276
+subcarriers, ranks (8,64,24), complex64, MMSE SINR at 8 streams (10 dB; C4
+names no SNR), J=2 / K=G/4 mapping, paper_experiment scope.
 
-Multi-GPU (torchrun): weak scaling — each rank compresses and evaluates its
-own C2-sized block of groups (group offset rank*64); no data-path collective;
-one NCCL all_reduce of a small stats vector at the end; times are max over ranks.
+* A "step" is one pass of the compressed-form SINR stage over every group x
+  subcarrier (rebuild + precoder + MMSE): the headline metric "SINR evals/sec"
+  (one eval = one user x one subcarrier, all streams). Factors are resident in
+  HBM (from a device groupwise_solve in the same run); L2 is flushed between
+  steps (256 MB write, > 126 MB L2).
+* The Tucker stage (groupwise_solve, init + 20 fixed sweeps, then the reference
+  stop rule) is timed in the same run: "tucker" (Tucker channels/sec).
+* `e2e`: the same SINR step through the public API with pinned HOST buffers
+  (factors + delays in, sinr/signal/status out, copies inside the timed region).
+* `configs`: every other BASELINE config (C1, C2, C2d = C2 in complex128, C3,
+  C5) measured the same way at N=1 with fewer steps.
+* `parity`: each rank checks a sample of its own timed output against the CPU
+  oracle (SINR relative error, NMSE) — the numbers are only reported if they
+  match (BASELINE tolerance 1e-4 c64 / 1e-9 c128, NMSE 1e-6).
 
---impl reference: times the reference algorithm's CPU implementation (the
-oracle restatement — the reference itself needs Eigen, absent here) on this
-host's cores for the same metric/config.
+Multi-GPU (torchrun, one rank per GPU): STRONG scaling — the 512 C4 groups are
+split into contiguous blocks by shard.group_range; no
+data-path collective; one NCCL reduction of the stats (shard.reduce_stats:
+evals, NMSE numerator/denominator, status counts; max step times and max SINR
+error). value = all groups' evals / max-over-ranks step time.
+
+--impl reference: the reference algorithm's CPU implementation (the oracle
+restatement; the reference itself needs Eigen, absent — DESIGN.md §1) on this
+host's cores, same metric and config, on a bounded sample. It loads nothing
+from the product package.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -31,27 +47,64 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, ROOT)
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+HEADLINE = "C4"
+EXTRA = ("C1", "C2", "C2d", "C3", "C5")
+SINR_TOL = {"c64": 1e-4, "c128": 1e-9}
 
 
-def parse():
+def load_configs():
+    """BASELINE configs without importing the product package (configs.py is dependency-free)."""
+    spec = importlib.util.spec_from_file_location("gwt_bench_configs",
+                                                  os.path.join(ROOT, "paper_2401_09792_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # dataclasses resolve the module by name
+    spec.loader.exec_module(mod)
+    return mod.CONFIGS
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default=HEADLINE)
+    ap.add_argument("--extra", default=",".join(EXTRA), help="secondary configs at N=1 ('' = none)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def lscpu_summary():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+    except Exception:
+        return None
+    keep = ("Model name", "CPU(s)", "Thread(s) per core", "Core(s) per socket", "Socket(s)", "CPU max MHz")
+    return {k.strip(): v.strip() for k, v in (ln.split(":", 1) for ln in out.splitlines() if ":" in ln)
+            if k.strip() in keep}
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return d["hbm_gbs"], "measured", d
+        return d["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)", d
     except Exception:
-        return 6650.0, "fallback", {}
+        return 6650.0, "fallback (B200_PROFILING.md)", {}
+
+
+def dims_of(cfg):
+    return dict(J=cfg.J, K=cfg.K, M=cfg.M, N=cfg.N, P=cfg.P, m=cfg.m, n=cfg.n, p=cfg.p)
 
 
 class ClockSampler:
@@ -64,6 +117,7 @@ class ClockSampler:
         self.device = device
         self.sm, self.mx, self.reasons = [], [], set()
         self.stop = threading.Event()
+        self.N = None
 
     def __enter__(self):
         try:
@@ -104,48 +158,48 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# algorithmic cost model (DESIGN.md §5)
+# algorithmic cost model (SURVEY.md §8(d); DESIGN.md §5)
 
-def sinr_costs(cfg, cs):
-    """Per-kernel algorithmic (flops, flop pipe, bytes) for one SINR step over the whole batch."""
+def sinr_costs(cfg):
+    """Per-kernel algorithmic (flops, pipe, bytes) of one SINR step over all of cfg's groups.
+
+    rebuild (stage R, per (link, subcarrier)): 8(mnp + Pp) flops; bytes = the H~ write m n b_c.
+    solve (stage S, per (user, subcarrier)): bytes = the user's J H~ reads J m n b_c + L binary64 SINR out
+    (§8(d)); flops = serving Gram (fp64, Hermitian half) + interference products H~_kij V'_k (n m L per
+    interferer) + the m x m eig / covariance / Cholesky / solves (counted as a Householder + QL eig,
+    ~(16/3 + 6 + 4) m^3 real flops, and 8(2 m^2 L + m^3/3 + L m^2 / 2))."""
     J, m, n, p, P, L = cfg.J, cfg.m, cfg.n, cfg.p, cfg.P, cfg.L
+    bc = 8 if cfg.dtype == "c64" else 16
     links, users, F, g = cfg.G, cfg.G // 2, cfg.F, cfg.groups
-    S = J
-    wp = "fp32" if cs == 8 else "fp64"
-    rebuild = (8 * (m * n * p + P * p) * links * F * g, wp,
-               (cs * m * n * links * F + cs * (m * n * p + P * p) * links + 8 * P * links) * g)
-    pair_gram = (8 * S * m * m * n * users * F * g, "fp64",
-                 (cs * m * n * (2 * J - 1) * users * F + 16 * S * m * m * users * F) * g)
-    # eig (cyclic Jacobi, ~6 sweeps) + covariance/Cholesky/solves, estimated fp64 flops per (user, subcarrier)
-    jac = 6 * (m * (m - 1) // 2) * 48 * m
-    mmse = 8 * (L * m * m + (S - 1) * 2 * m ** 3 + m ** 3 // 3 + L * m * m // 2)
-    Lp = (L + 1) // 2 * 2
-    small = ((jac + mmse) * users * F * g, "fp64",
-             (16 * S * m * m + 8 * (Lp + 2 * m * L) * (1 + (S - 1)) + 16 * L + 4) * users * F * g)
-    return dict(rebuild=rebuild, pair_gram=pair_gram, small=small)
+    rebuild = (8 * (m * n * p + P * p) * links * F * g, "fp32" if bc == 8 else "fp64", bc * m * n * links * F * g)
+    per_eval = (8 * (m * (m + 1) // 2) * n + 8 * (J - 1) * n * m * L + int((16 / 3 + 6 + 4) * m ** 3)
+                + 8 * (2 * m * m * L + m ** 3 // 3 + L * m * m // 2))
+    solve = (per_eval * users * F * g, "fp64", (J * m * n * bc + 8 * L) * users * F * g)
+    return dict(rebuild=rebuild, solve=solve)
 
 
 def binding_roofline(flops, pipe, nbytes, ms, hbm, peaks_t):
-    """t_roof = max(bytes/BW, flops/peak); report the binding resource's achieved rate vs its peak."""
+    """t_roof = max(bytes/BW, flops/peak); the binding resource's achieved rate vs its measured peak."""
     t = ms * 1e-3
     t_b = nbytes / (hbm * 1e9)
     t_f = flops / (peaks_t[pipe] * 1e12) if flops else 0.0
     if t_b >= t_f:
         ach = nbytes / t / 1e9
-        return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+        return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "t_roof_ms": t_b * 1e3}
     ach = flops / t / 1e12
-    return {"bound": pipe, "achieved": ach, "peak": peaks_t[pipe], "unit": "TFLOP/s", "frac": ach / peaks_t[pipe]}
+    return {"bound": pipe, "achieved": ach, "peak": peaks_t[pipe], "unit": "TFLOP/s", "frac": ach / peaks_t[pipe],
+            "t_roof_ms": t_f * 1e3}
 
 
 def cublas_peaks(dev):
-    """Measured FP32 (SGEMM, TF32 off) and FP64 (DGEMM) cuBLAS throughput on this GPU, best of a few
-    square GEMMs timed with CUDA events: the achievable CUDA-core ceilings SURVEY.md §8(d) asks for
-    beside the derived 148 SM x clock peaks (cuBLAS is a measuring tool here, not on the hot path)."""
+    """Measured FP32 (SGEMM, TF32 off) and FP64 (DGEMM) cuBLAS throughput on this GPU: the CUDA-core
+    roofline denominators (cuBLAS is a measuring tool here, never on the hot path)."""
     import torch
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
     out = {}
-    for name, dt, n, reps in (("sgemm_tflops", torch.float32, 8192, 5), ("dgemm_tflops", torch.float64, 4096, 3)):
+    for name, dt, n, reps in (("fp32", torch.float32, 8192, 5), ("fp64", torch.float64, 4096, 3)):
         a = torch.randn(n, n, dtype=dt, device=dev)
         b = torch.randn(n, n, dtype=dt, device=dev)
         torch.matmul(a, b)
@@ -163,7 +217,7 @@ def cublas_peaks(dev):
     return out
 
 
-def tucker_flops(cfg):
+def tucker_flops(cfg, links):
     """Canonical-order flops of one groupwise_solve (init + S sweeps) per SURVEY.md §8(d)."""
     M, N, P, m, n, p, S = cfg.M, cfg.N, cfg.P, cfg.m, cfg.n, cfg.p, cfg.sweeps
     init = M * M * N * P + N * N * M * P + P * P * M * N
@@ -171,330 +225,398 @@ def tucker_flops(cfg):
     tx = min(m * M * N * P + m * N * P * p, M * N * P * p + m * M * N * p) + N * N * m * p
     de = min(m * M * N * P + m * n * N * P, M * N * P * n + m * M * n * P) + P * P * m * n
     obj = m * n * P * p
-    return 8 * (init + S * (rx + tx + de + obj)) * cfg.links
+    return 8 * (init + S * (rx + tx + de + obj)) * links
 
 
 # ---------------------------------------------------------------------------
+# sharding and the stats reduction (exercised by tests/test_multigpu.py with gloo)
+
+def shard_plan(cfg, rank, world):
+    """This rank's contiguous block of the config's groups (shard.group_range), strong scaling."""
+    from paper_2401_09792_b200 import shard
+    return shard.group_range(rank, world, cfg.groups)
+
+
+def reduce_run_stats(local, device=None):
+    """One all_reduce of the per-rank stats (sums: evals, NMSE num/den, links, bad items; maxima: step ms,
+    Tucker ms, SINR relative error). Returns the reduced dict (identity at world 1)."""
+    from paper_2401_09792_b200 import shard
+    return shard.reduce_stats(local, device=device)
+
+
+def whole_job_value(cfg, reduced):
+    """value = all ranks' evals / max-over-ranks step time; Tucker channels/s likewise."""
+    return {"value": reduced["evals"] / (reduced["max_ms"] * 1e-3),
+            "tucker": reduced["links"] / (reduced["max_tucker_ms"] * 1e-3) if reduced["max_tucker_ms"] > 0 else None,
+            "nmse": reduced["nmse_num"] / reduced["nmse_den"] if reduced["nmse_den"] > 0 else None}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU): no product import
+
+def oracle_sample(cfg, cores, O, sinr_groups, sinr_freqs):
+    """Oracle (reference algorithm restated in C++, fp64) on a bounded sample of cfg: Tucker init + 0 and 1
+    sweeps on `cores` groups (one per thread; 20-sweep time extrapolated from the per-sweep difference), then
+    the SINR stage on those factors for `sinr_freqs` strided subcarriers."""
+    dims = dims_of(cfg)
+    gs = min(cfg.groups, sinr_groups)
+    X, tau = O.generate_baseline(cfg.J, cfg.K, cfg.M, cfg.N, cfg.P, gs, seed=0,
+                                 dtype=np.complex64 if cfg.dtype == "c64" else np.complex128, nthreads=cores)
+    X = X.astype(np.complex128)
+    t0 = time.perf_counter()
+    O.alternating_solve(dims, X, 0, early_stop=False, nthreads=cores)
+    t_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    fo = O.alternating_solve(dims, X, 1, early_stop=False, nthreads=cores)
+    t_one = time.perf_counter() - t0
+    t20 = t_init + cfg.sweeps * max(t_one - t_init, 0.0)
+    fidx = np.linspace(0, cfg.F - 1, min(cfg.F, sinr_freqs)).astype(np.int64)
+    co = O.coeffs_from_tau(tau, cfg.freqs()[fidx])
+    return dict(X=X, fo=fo, co=co, gs=gs, fs=len(fidx), tucker_cps=gs * cfg.G / t20, t_init=t_init,
+                t_sweep=t_one - t_init)
+
 
 def run_reference(args, cfg):
-    import paper_2401_09792_b200 as gw
-    from oracle import oracle as O
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    cores = os.cpu_count() or 1
-    topo = cfg.topology()
-    dims = dict(J=cfg.J, K=cfg.K, M=cfg.M, N=cfg.N, P=cfg.P, m=cfg.m, n=cfg.n, p=cfg.p)
-    # bounded sample of the same workload: 2*cores groups x 64 subcarriers per step
-    gs = min(cfg.groups, 2 * cores)
-    fs = min(cfg.F, 64)
-    X, tau = gw.generate_channels(topo, gs, seed=0, dtype=np.complex128)
-    if cfg.dtype == "c64":
-        X = X.astype(np.complex64).astype(np.complex128)
-    fo = O.alternating_solve(dims, X, 2, early_stop=False, nthreads=cores)
-    co = O.coeffs_from_tau(tau, cfg.freqs()[:fs])
+    from oracle import oracle as O
+    cores = host_cores()
+    s = oracle_sample(cfg, cores, O, sinr_groups=cores, sinr_freqs=16)
+    dims = dims_of(cfg)
     times = []
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        O.sinr_compressed(dims, fo["C"], fo["G"], co, cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=cores)
-        dt = time.perf_counter() - t0
+        O.sinr_compressed(dims, s["fo"]["C"], s["fo"]["G"], s["co"], cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=cores)
         if it >= args.warmup:
-            times.append(dt)
-    evals = gs * fs * cfg.J * cfg.K
+            times.append(time.perf_counter() - t0)
+    evals = s["gs"] * s["fs"] * cfg.J * cfg.K
     v = evals / statistics.median(times)
-    t0 = time.perf_counter()
-    O.alternating_solve(dims, X[: min(gs, cores)], cfg.sweeps, early_stop=False, nthreads=cores)
-    tuck = min(gs, cores) * cfg.G / (time.perf_counter() - t0)
+    sample = (f"{s['gs']} groups x {s['fs']} strided subcarriers per step (of {cfg.groups} x {cfg.F}); factors from "
+              f"init + 1 sweep on the same groups; oracle C++ restatement in complex128, one group per std::thread")
     line = {
         "impl": "reference", "metric": "SINR evals/sec", "value": v, "unit": "evals/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (fp64)",
-        "data": "synthetic (BASELINE.json generator, seed 0)",
-        "config": {"workload": cfg.name, "groups": cfg.groups, "subcarriers": cfg.F, "ranks": [cfg.m, cfg.n, cfg.p],
-                   "streams": cfg.L, "snr_db": cfg.snr_db, "scope": "paper_experiment"},
-        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "port",
-                         "sample": f"{gs} groups x {fs} subcarriers per step (of {cfg.groups} x {cfg.F}); "
-                                   "oracle C++ restatement, one group per std::thread"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128 (the reference computes in complex<double> only)",
+        "data": "synthetic (BASELINE.json generator, seed 0; c64-rounded inputs for c64 configs)",
+        "config": bench_config(cfg, 1),
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "tucker": {"value": tuck, "unit": "channels/s", "sample": f"{min(gs, cores)} groups x {cfg.sweeps} sweeps"},
+        "tucker": {"value": s["tucker_cps"], "unit": "channels/s",
+                   "sample": f"{s['gs']} groups: init {s['t_init']:.2f} s + 1 sweep {s['t_sweep']:.2f} s, "
+                             f"{cfg.sweeps}-sweep time extrapolated"},
+        "lscpu": lscpu_summary(),
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline_leg(cfg, cores):
-    """Oracle (port) on the host, bounded sample ~10 s; rank 0 at N=1 only."""
-    import paper_2401_09792_b200 as gw
-    from oracle import oracle as O
-    dims = dict(J=cfg.J, K=cfg.K, M=cfg.M, N=cfg.N, P=cfg.P, m=cfg.m, n=cfg.n, p=cfg.p)
-    gs = min(cfg.groups, 2 * cores)
-    fs = min(cfg.F, 64)
-    X, tau = gw.generate_channels(cfg.topology(), gs, seed=0, dtype=np.complex128)
-    if cfg.dtype == "c64":
-        X = X.astype(np.complex64).astype(np.complex128)
-    t0 = time.perf_counter()
-    fo = O.alternating_solve(dims, X, cfg.sweeps, early_stop=False, nthreads=cores)
-    t_tuck = time.perf_counter() - t0
-    co = O.coeffs_from_tau(tau, cfg.freqs()[:fs])
-    t0 = time.perf_counter()
-    O.sinr_compressed(dims, fo["C"], fo["G"], co, cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=cores)
-    t_s = time.perf_counter() - t0
-    return {"value": gs * fs * cfg.J * cfg.K / t_s, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": f"SINR: {gs} groups x {fs} subcarriers; Tucker: {gs} groups x {cfg.sweeps} sweeps "
-                      f"(oracle C++ restatement in fp64, one group per std::thread)",
-            "tucker_channels_per_s": gs * cfg.G / t_tuck}
+def bench_config(cfg, world):
+    return {"workload": cfg.name, "groups": cfg.groups, "subcarriers": cfg.F, "dims": [cfg.M, cfg.N, cfg.P],
+            "ranks": [cfg.m, cfg.n, cfg.p], "streams": cfg.L, "snr_db": cfg.snr_db, "scope": "paper_experiment",
+            "J": cfg.J, "K": cfg.K, "channels_per_group": cfg.G, "parallelism": f"group-sharded x{world}",
+            "l2": "flushed (256 MB write) between timed steps"}
 
 
-def main():
-    args = parse()
-    import paper_2401_09792_b200 as gw
-    cfg = gw.CONFIGS[args.config]
-    if args.impl == "reference":
-        return run_reference(args, cfg)
+# ---------------------------------------------------------------------------
+# GPU arm
 
-    import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    ctx = gw.Context(local)
-    stream = torch.cuda.current_stream(dev)
-    ctx.use_torch_stream()
-    topo, ranks = cfg.topology(), cfg.ranks()
+def upload_channels(gw, cfg, g0, g1, dev, torch):
+    """Generate groups [g0, g1) on the host in blocks and place X in HBM (not timed)."""
     npdt = np.complex64 if cfg.dtype == "c64" else np.complex128
-    cs = 8 if cfg.dtype == "c64" else 16
+    tdt = torch.complex64 if cfg.dtype == "c64" else torch.complex128
+    ng = g1 - g0
+    X = torch.empty((ng, cfg.G, cfg.P, cfg.N, cfg.M), dtype=tdt, device=dev)
+    tau = np.empty((ng, cfg.G, cfg.P), np.float64)
+    blk = max(1, int((2 << 30) // (cfg.G * cfg.P * cfg.N * cfg.M * np.dtype(npdt).itemsize)))
+    for b0 in range(0, ng, blk):
+        b1 = min(ng, b0 + blk)
+        Xh, th = gw.generate_channels(cfg.topology(), b1 - b0, seed=0, dtype=npdt, group0=g0 + b0,
+                                      nthreads=host_cores())
+        X[b0:b1].copy_(torch.from_numpy(Xh))
+        tau[b0:b1] = th
+    return X, tau
 
-    # inputs: this rank's block of groups, resident in HBM
-    Xh, tau_h = gw.generate_channels(topo, cfg.groups, seed=0, dtype=np.complex128, group0=rank * cfg.groups)
-    Xh = Xh.astype(npdt)
-    X = torch.from_numpy(Xh).to(dev)
+
+def timed(torch, stream, flush, fn, n):
+    """n calls of fn, each bracketed by CUDA events on `stream` after an L2 flush (synchronised)."""
+    out, ms = None, []
+    for _ in range(n):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = fn()
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    return out, ms
+
+
+def parity_sample(O, cfg, fac, X, tau, rep, groups, nfreq, nthreads):
+    """Compare a sample of the GPU's timed output with the oracle on the GPU's own factors: per-stream SINR
+    relative error on `groups` x `nfreq` strided subcarriers, and the NMSE of one group (oracle objective
+    on the GPU factors vs the GPU's trace / energy)."""
+    dims = dims_of(cfg)
+    gsel = list(range(min(groups, fac.cores.shape[0])))
+    fidx = np.linspace(0, cfg.F - 1, min(cfg.F, nfreq)).astype(np.int64)
+    Cd = fac.delay[gsel].cpu().numpy().astype(np.complex128)
+    G = fac.cores[gsel].cpu().numpy().astype(np.complex128)
+    co = O.coeffs_from_tau(tau[gsel], cfg.freqs()[fidx])
+    want, _ = O.sinr_compressed(dims, Cd, G, co, cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=nthreads)
+    got = rep.sinr[gsel].cpu().numpy()[:, fidx]
+    st = rep.status[gsel].cpu().numpy()[:, fidx]
+    ok = st == 0
+    rel = np.abs(got - want) / np.abs(want)
+    max_rel = float(rel[ok].max()) if ok.any() else None
+    # NMSE of group 0: oracle objective (explicit reconstruction, decompose.cpp:23-38) on the GPU factors
+    A = fac.rx[0].cpu().numpy().astype(np.complex128)
+    B = fac.tx[0].cpu().numpy().astype(np.complex128)
+    Cf = fac.delay[0].cpu().numpy().astype(np.complex128)
+    f_o, _ = O.objective(dims, X[0].cpu().numpy().astype(np.complex128), A, B, Cf)
+    e = float(fac.energy[0].cpu())
+    nm_gpu = float(fac.trace[0, -1].cpu()) / e
+    return {"sinr_max_rel_err": max_rel, "sinr_tol": SINR_TOL[cfg.dtype], "sinr_items": int(rel.size),
+            "status_nonzero_in_sample": int((~ok).sum()), "nmse_gpu": nm_gpu, "nmse_oracle": f_o / e,
+            "nmse_abs_diff": abs(nm_gpu - f_o / e), "nmse_tol": 1e-6,
+            "ok": bool(max_rel is not None and max_rel <= SINR_TOL[cfg.dtype] and abs(nm_gpu - f_o / e) <= 1e-6),
+            "sample": f"SINR: {len(gsel)} groups x {len(fidx)} strided subcarriers; NMSE: group 0"}
+
+
+def run_gpu_config(gw, O, torch, cfg, ctx, dev, stream, flush, rank, world, steps, warmup, hbm, peaks_t, headline):
+    """Compress (Tucker, fixed sweeps + reference stop rule) then time the SINR step for this rank's groups."""
+    g0, g1 = shard_plan(cfg, rank, world)
+    topo, ranks = cfg.topology(), cfg.ranks()
+    X, tau_h = upload_channels(gw, cfg, g0, g1, dev, torch)
     tau = torch.from_numpy(tau_h).to(dev)
     freqs = torch.from_numpy(cfg.freqs()).to(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    ng = g1 - g0
+    res = {"groups_this_rank": [g0, g1]}
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # ---------------- Tucker stage (device-resident), fixed 20 sweeps
-    fac = None
-    for _ in range(max(1, args.warmup // 2)):
-        fac = ctx.groupwise_solve(topo, X, ranks, cfg.sweeps, early_stop=False)
-    barrier()
-    tt = []
-    tucker_steps = max(2, min(args.steps, 5))
-    for _ in range(tucker_steps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        fac = ctx.groupwise_solve(topo, X, ranks, cfg.sweeps, early_stop=False)
-        e1.record(stream)
-        e1.synchronize()
-        tt.append(e0.elapsed_time(e1))
+    # ---------------- Tucker stage (device-resident), fixed sweeps
+    solve = lambda early: ctx.groupwise_solve(topo, X, ranks, cfg.sweeps, early_stop=early)  # noqa: E731
+    solve(False)
+    torch.cuda.synchronize()
+    fac, tt = timed(torch, stream, flush, lambda: solve(False), 2 if headline else 1)
     tucker_stage = ctx.stage_ms()
-    # reference stop rule (decompose.cpp:363-368: stop once decrease < 1e-10 * energy), timed the same way
-    es_ms, es_iters = [], None
-    for it in range(4):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        fes = ctx.groupwise_solve(topo, X, ranks, cfg.sweeps, early_stop=True)
-        e1.record(stream)
-        e1.synchronize()
-        if it > 0:
-            es_ms.append(e0.elapsed_time(e1))
-        if os.environ.get("GWT_BENCH_DEBUG"):
-            print("early-stop solve ms", e0.elapsed_time(e1), ctx.stage_ms()[:3], file=sys.stderr)
-        it_ = fes.iterations_run
-        es_iters = np.asarray(it_.cpu() if hasattr(it_, "cpu") else it_)
-    barrier()
+    fes, es_ms = timed(torch, stream, flush, lambda: solve(True), 1)
+    es_it = fes.iterations_run.cpu().numpy()
+    tk = float(np.mean(tt))
+    tfl = tucker_flops(cfg, ng * cfg.G)
+    res["tucker"] = {
+        "ms_per_solve": tk, "sweeps": cfg.sweeps, "mode": "fixed sweeps (no early stop)",
+        "stage_ms": {"init_obj": tucker_stage[1], "sweeps": tucker_stage[2]},
+        "roofline": {"bound": "fp32" if cfg.dtype == "c64" else "fp64",
+                     "achieved": tfl / (tk * 1e-3) / 1e12, "unit": "TFLOP/s",
+                     "peak": peaks_t["fp32" if cfg.dtype == "c64" else "fp64"],
+                     "frac": tfl / (tk * 1e-3) / 1e12 / peaks_t["fp32" if cfg.dtype == "c64" else "fp64"],
+                     "peak_source": "measured cuBLAS SGEMM (TF32 off) / DGEMM in this run",
+                     "alg_flops": tfl, "flops_basis": "canonical cheapest contraction order, SURVEY.md §8(d)"},
+        "early_stop": {"mode": "reference stop rule (decrease < 1e-10 * energy)", "ms_per_solve": float(es_ms[0]),
+                       "iterations_mean": float(es_it.mean()), "iterations_max": int(es_it.max())},
+    }
 
-    # ---------------- SINR stage (the step), device-resident inputs
-    for _ in range(args.warmup):
-        rep = ctx.run_compressed_pipeline(topo, fac, ranks, tau=tau, freqs=freqs)
-    barrier()
+    # ---------------- SINR stage (the step)
+    step = lambda: ctx.run_compressed_pipeline(topo, fac, ranks, tau=tau, freqs=freqs)  # noqa: E731
+    for _ in range(warmup):
+        rep = step()
+    torch.cuda.synchronize()
     launches0 = ctx.launches
-    step_ms, st_acc = [], np.zeros(8)
-    with ClockSampler(local) as clk:
-        t_wall = time.perf_counter()
-        for _ in range(args.steps):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            rep = ctx.run_compressed_pipeline(topo, fac, ranks, tau=tau, freqs=freqs)
-            e1.record(stream)
-            e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            st_acc += np.array(rep.stage_ms)
-        barrier()
-        t_wall = time.perf_counter() - t_wall
+    with ClockSampler(dev.index or 0) as clk:
+        rep, step_ms = timed(torch, stream, flush, step, steps)
     launches = ctx.launches - launches0
     ms = float(np.mean(step_ms))
-    st_acc /= args.steps
-    # The headline loop runs the groups on 2 overlapping stream lanes, so per-kernel durations there
-    # include inter-lane contention; the roofline is taken from a single-lane timed loop (same inputs,
-    # L2 flushed) whose per-stage kernel times sum to its step time.
-    prev = os.environ.get("GWT_SINR_DEV_LANES")
-    os.environ["GWT_SINR_DEV_LANES"] = "1"
-    st_acc = np.zeros(8)
-    rl_steps = max(10, min(args.steps, 50))
-    rl_ms = []
-    for _ in range(3):  # warm: the single-lane call sizes lane 0's workspaces for all groups
-        ctx.run_compressed_pipeline(topo, fac, ranks, tau=tau, freqs=freqs)
-    torch.cuda.synchronize()
-    for _ in range(rl_steps):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rep1 = ctx.run_compressed_pipeline(topo, fac, ranks, tau=tau, freqs=freqs)
-        e1.record(stream)
-        e1.synchronize()
-        rl_ms.append(e0.elapsed_time(e1))
-        st_acc += np.array(rep1.stage_ms)
-    st_acc /= rl_steps
-    if prev is None:
-        del os.environ["GWT_SINR_DEV_LANES"]
-    else:
-        os.environ["GWT_SINR_DEV_LANES"] = prev
-    tk = float(np.mean(tt))
-    stats = torch.tensor([ms, tk, float(rep.status.ne(0).sum())], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(stats, op=dist.ReduceOp.MAX)  # only collective: max-over-ranks times + status
-    ms, tk, bad = stats.tolist()
-    evals = cfg.groups * cfg.F * cfg.J * cfg.K * world
-    value = evals / (ms * 1e-3)
+    st = np.array(ctx.stage_ms())
+    evals = ng * cfg.F * cfg.J * cfg.K
+    bad = int(rep.status.ne(0).sum())
+    res.update(ms=ms, evals=evals, launches=launches, clocks=clk.summary(), status_nonzero=bad,
+               step_ms_all=[round(x, 4) for x in step_ms])
+    # per-stage kernel time of the last step (events on the launching stream(s))
+    costs = sinr_costs(cfg)
+    scale = ng / cfg.groups
+    stages = {}
+    for name, ms_k in (("rebuild", st[4]), ("solve", st[5] + st[6])):
+        fl, pipe, by = costs[name]
+        r = binding_roofline(fl * scale, pipe, by * scale, ms_k, hbm, peaks_t)
+        r.update(ms=round(float(ms_k), 4), alg_bytes=int(by * scale), alg_flops=int(fl * scale))
+        stages[name] = r
+    res["stages"] = stages
 
-    # ---------------- paper metrics on this workload (PAPER.md:477-489): full-size SINR on the raw
-    # channels (same kernels, cores = X, delay = I) vs the compressed step; R_t, e_c, R_s
-    from paper_2401_09792_b200 import metrics as pm
-    for _ in range(2):
-        full = ctx.run_full_pipeline(topo, X, tau=tau, freqs=freqs)
-    fms = []
-    for _ in range(max(3, min(args.steps, 10))):
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        full = ctx.run_full_pipeline(topo, X, tau=tau, freqs=freqs)
-        e1.record(stream)
-        e1.synchronize()
-        fms.append(e0.elapsed_time(e1))
-    paper = {"R_t_gpu": float(np.mean(fms)) / ms, "t_full_ms": float(np.mean(fms)), "t_compressed_ms": ms,
-             "e_c": pm.sinr_error(full.sinr.cpu().numpy(), rep.sinr.cpu().numpy()),
-             "R_s": pm.storage_ratio(topo, ranks),
-             "note": "paper Table 2 (groupwise, 3GPP J=21) reports R_t 6.19 / R_s 6.16 / e_c 9.4% on other data"}
+    # ---------------- parity of this rank's own timed output
+    if cfg.dtype in SINR_TOL:
+        res["parity"] = parity_sample(O, cfg, fac, X, tau_h, rep, groups=2, nfreq=16, nthreads=host_cores())
+    # NMSE over all of this rank's groups (trace / energy, fixed sweeps)
+    res["nmse_num"] = float(fac.trace[:, -1].sum().cpu())
+    res["nmse_den"] = float(fac.energy.sum().cpu())
+    res["_keep"] = (X, tau_h, fac, rep, tau, freqs)
+    return res
 
-    # ---------------- e2e through the public API with pinned host buffers
-    Ch = rep_in = None
+
+def e2e_sinr(gw, torch, cfg, fac, tau_h, local, warmup, steps):
+    """SINR step through the public API with pinned host buffers (copies inside the timed region)."""
+    topo, ranks = cfg.topology(), cfg.ranks()
     Ch = fac.delay.cpu().pin_memory()
     Gh = fac.cores.cpu().pin_memory()
     tauh = torch.from_numpy(tau_h).pin_memory()
     fh = torch.from_numpy(cfg.freqs()).pin_memory()
     ctx_h = gw.Context(local)
-    e2e_ms = []
-    for it in range(max(args.warmup, 1) + args.steps):
-        flush.zero_()
+    hf = gw.GroupwiseFactorSet(None, None, Ch, Gh)
+    ms = []
+    for it in range(max(warmup, 1) + steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        fh_fac = gw.GroupwiseFactorSet(None, None, Ch, Gh)
-        rep_h = ctx_h.run_compressed_pipeline(topo, fh_fac, ranks, tau=tauh, freqs=fh)
+        rep = ctx_h.run_compressed_pipeline(topo, hf, ranks, tau=tauh, freqs=fh)
         t1 = time.perf_counter()
-        if it >= max(args.warmup, 1):
-            e2e_ms.append((t1 - t0) * 1e3)
-    if os.environ.get("GWT_BENCH_DEBUG"):
-        print("e2e_ms", [round(x, 3) for x in e2e_ms], file=sys.stderr)
-    e2e_t = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    h2d = Ch.numel() * cs + Gh.numel() * cs + tauh.numel() * 8 + fh.numel() * 8
-    d2h = rep_h.sinr.numel() * 8 * 2 + rep_h.status.numel() * 4
-    # Tucker e2e: host X in, factors out
-    Xpin = torch.from_numpy(Xh).pin_memory()
-    fac_h = ctx_h.groupwise_solve(topo, Xpin, ranks, cfg.sweeps, early_stop=False)  # warm (workspaces, pinned outs)
-    t0 = time.perf_counter()
-    for _ in range(2):
-        fac_h = ctx_h.groupwise_solve(topo, Xpin, ranks, cfg.sweeps, early_stop=False)
-    tuck_e2e_ms = (time.perf_counter() - t0) * 1e3 / 2
+        if it >= max(warmup, 1):
+            ms.append((t1 - t0) * 1e3)
     ctx_h.close()
+    bc = Ch.element_size()
+    h2d = Ch.numel() * bc + Gh.numel() * bc + tauh.numel() * 8 + fh.numel() * 8
+    d2h = rep.sinr.numel() * 8 * 2 + rep.status.numel() * 4
+    return float(np.mean(ms)), int(h2d), int(d2h)
 
-    # ---------------- roofline of the dominant SINR kernel (binding resource), all stages listed
-    hbm, peak_kind, pk = peaks()
-    clk_max = pk.get("sm_max_mhz", 1965.0)
-    cublas = cublas_peaks(dev)
-    peaks_t = {"fp32": 148 * 128 * 2 * clk_max * 1e6 / 1e12, "fp64": 148 * 64 * 2 * clk_max * 1e6 / 1e12}
-    costs = sinr_costs(cfg, cs)
-    stage = {"rebuild": st_acc[4], "pair_gram": st_acc[5], "small": st_acc[6]}
-    kern = {"rebuild": "k_rebuild_rb", "pair_gram": "k_pair_gram_gf", "small": "k_small_fused"}
-    per_stage = {}
-    for k_, ms_k in stage.items():
-        fl, pipe, by = costs[k_]
-        r = binding_roofline(fl, pipe, by, ms_k, hbm, peaks_t)
-        r.update(kernel=kern[k_], ms=round(ms_k, 4), alg_bytes=int(by), alg_flops=int(fl))
-        if r["bound"] in ("fp32", "fp64"):  # same achieved rate against the cuBLAS ceiling measured in this run
-            r["frac_vs_cublas"] = r["achieved"] / cublas["sgemm_tflops" if r["bound"] == "fp32" else "dgemm_tflops"]
-        per_stage[k_] = r
-    dom = max(stage, key=stage.get)
-    roof = dict(per_stage[dom])
-    # measured DRAM traffic per launch of the dominant kernel from the committed ncu capture (same config)
+
+def cpu_baseline_leg(O, cfg):
+    """Oracle on this host, bounded sample (~10-30 s): single thread and all cores; rank 0 at N=1 only."""
+    cores = host_cores()
+    out = {"unit": "evals/s", "cores": cores, "kind": "port", "lscpu": lscpu_summary()}
+    s = oracle_sample(cfg, cores, O, sinr_groups=cores, sinr_freqs=8)
+    dims = dims_of(cfg)
+    evals = s["gs"] * s["fs"] * cfg.J * cfg.K
+    t0 = time.perf_counter()
+    O.sinr_compressed(dims, s["fo"]["C"], s["fo"]["G"], s["co"], cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=cores)
+    out["value"] = evals / (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    O.sinr_compressed(dims, s["fo"]["C"][:1], s["fo"]["G"][:1], s["co"][:1], cfg.sigma, cfg.L, O.SCOPE_PAPER,
+                      nthreads=1)
+    out["value_single_thread"] = s["fs"] * cfg.J * cfg.K / (time.perf_counter() - t0)
+    out["tucker_channels_per_s"] = s["tucker_cps"]
+    out["sample"] = (f"SINR: {s['gs']} groups x {s['fs']} strided subcarriers ({cores} threads) and 1 group "
+                     f"(1 thread); Tucker: {s['gs']} groups, init + 1 sweep timed, {cfg.sweeps} sweeps "
+                     f"extrapolated; oracle C++ restatement in complex128 (c64-rounded inputs)")
+    return out
+
+
+def main(argv=None):
+    args = parse(argv)
+    CONFIGS = load_configs()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_09792_b200 as gw
+    from oracle import oracle as O
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = gw.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.use_torch_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    hbm, hbm_src, _ = peaks()
+    cub = cublas_peaks(dev)
+    peaks_t = {"fp32": cub["fp32"], "fp64": cub["fp64"]}
+
+    # ---------------- headline config, sharded by group
+    r = run_gpu_config(gw, O, torch, cfg, ctx, dev, stream, flush, rank, world, args.steps, args.warmup, hbm,
+                       peaks_t, headline=True)
+    X, tau_h, fac, rep, tau, freqs = r.pop("_keep")
+    perr = (r.get("parity") or {}).get("sinr_max_rel_err") or 0.0
+    local_stats = {"evals": r["evals"], "links": (r["groups_this_rank"][1] - r["groups_this_rank"][0]) * cfg.G,
+                   "nmse_num": r["nmse_num"], "nmse_den": r["nmse_den"], "bad_items": r["status_nonzero"],
+                   "max_ms": r["ms"], "max_tucker_ms": r["tucker"]["ms_per_solve"], "max_sinr_rel_err": perr}
+    del X
+    # ---------------- e2e through the public API (host buffers)
+    e2e_ms, h2d, d2h = e2e_sinr(gw, torch, cfg, fac, tau_h, local, 1, max(2, min(args.steps, 5)))
+    local_stats_e2e = {"max_ms": e2e_ms}
+    del fac, rep, tau
+    torch.cuda.empty_cache()
+    red = reduce_run_stats(local_stats, device=dev)
+    red_e2e = reduce_run_stats(local_stats_e2e, device=dev)
+    whole = whole_job_value(cfg, red)
+
+    # ---------------- roofline of the dominant kernel (per-stage events; ncu traffic where captured)
+    stages = r["stages"]
+    dom = max(stages, key=lambda k: stages[k]["ms"])
+    roof = dict(stages[dom])
+    kern = {"rebuild": "k_rebuild*", "solve": "k_sinr_solve*/k_small*"}
     traffic = None
     try:
-        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")))
-        if tj.get("config") == args.config:
-            traffic = tj["bytes_per_launch"].get(kern[dom])
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+        if tj.get("config") == cfg.name:
+            traffic = tj["bytes_per_step"].get(dom)
     except (OSError, ValueError, KeyError):
         traffic = None
-    roof.update(traffic=traffic, traffic_source="profiles/r01_traffic.json" if traffic else None, peak_source={"hbm": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                                           "fp32": "derived: 148 SM x 128 FMA/clk x 2 x max clock (not measured)",
-                                           "fp64": "derived: 148 SM x 64 DFMA/clk x 2 x max clock (not measured)"}[roof["bound"]],
-                stage_share={k_: round(v / max(sum(stage.values()), 1e-9), 3) for k_, v in stage.items()},
-                timing="per-stage CUDA events of a single-lane timed loop (ms_per_step_single_lane); the headline "
-                       "value overlaps 2 group lanes",
-                ms_per_step_single_lane=round(float(np.mean(rl_ms)), 4),
-                stages=per_stage)
-    tfl = tucker_flops(cfg) * world
-    fp32_peak = peaks_t["fp32" if cs == 8 else "fp64"]
-    tucker = {"value": cfg.links * world / (tk * 1e-3), "unit": "channels/s", "ms_per_solve": tk,
-              "sweeps": cfg.sweeps, "mode": "fixed sweeps (no early stop)",
-              "algorithmic_tflops": tfl / (tk * 1e-3) / 1e12,
-              "roofline": {"bound": "fp32-cuda-core", "achieved": tfl / (tk * 1e-3) / 1e12, "peak": fp32_peak,
-                           "unit": "TFLOP/s", "frac": tfl / (tk * 1e-3) / 1e12 / fp32_peak,
-                           "frac_vs_cublas": tfl / (tk * 1e-3) / 1e12 / cublas["sgemm_tflops" if cs == 8 else "dgemm_tflops"],
-                           "peak_source": "derived 148 SMs x 128 FFMA x 2 x max clock (not measured)"},
-              "stage_ms": {"init_obj": tucker_stage[1], "sweeps": tucker_stage[2]},
-              "early_stop": {"mode": "reference stop rule (decrease < 1e-10 * energy)",
-                             "ms_per_solve": float(np.mean(es_ms)),
-                             "value": cfg.links * world / (float(np.mean(es_ms)) * 1e-3),
-                             "iterations_mean": float(es_iters.mean()), "iterations_max": int(es_iters.max())},
-              "e2e_ms": tuck_e2e_ms, "e2e_h2d_bytes": Xh.nbytes,
-              "e2e_d2h_bytes": sum(int(np.prod(a.shape)) * cs for a in (fac_h.rx, fac_h.tx, fac_h.delay, fac_h.cores))}
+    roof.update(kernel=kern[dom], traffic=traffic, traffic_source="profiles/r02_traffic.json" if traffic else None,
+                peak_source=hbm_src if roof["bound"] == "hbm" else "measured cuBLAS in this run",
+                stage_share={k: round(v["ms"] / max(sum(s["ms"] for s in stages.values()), 1e-9), 3)
+                             for k, v in stages.items()},
+                stages=stages, timing="per-stage CUDA events on the launching streams, last timed step")
+
+    # ---------------- secondary configs (N=1 only)
+    extra = {}
+    if world == 1 and args.extra:
+        for name in [c for c in args.extra.split(",") if c and c != cfg.name]:
+            c2 = CONFIGS[name]
+            try:
+                e = run_gpu_config(gw, O, torch, c2, ctx, dev, stream, flush, 0, 1, max(3, min(args.steps, 10)),
+                                   max(3, min(args.warmup, 3)), hbm, peaks_t, headline=False)
+                Xe, tau_e, fac_e, rep_e, _, _ = e.pop("_keep")
+                e["value"] = e["evals"] / (e["ms"] * 1e-3)
+                e["tucker"]["value"] = c2.links / (e["tucker"]["ms_per_solve"] * 1e-3)
+                e["dtype"] = c2.dtype
+                if name == "C2":  # paper metrics (PAPER.md:477-489) on the full-size comparator
+                    from paper_2401_09792_b200 import metrics as pm
+                    topo = c2.topology()
+                    ctx.run_full_pipeline(topo, Xe, tau=torch.from_numpy(tau_e).to(dev),
+                                          freqs=torch.from_numpy(c2.freqs()).to(dev))
+                    full, fms = timed(torch, stream, flush, lambda: ctx.run_full_pipeline(
+                        topo, Xe, tau=torch.from_numpy(tau_e).to(dev), freqs=torch.from_numpy(c2.freqs()).to(dev)), 3)
+                    e["paper_metrics"] = {
+                        "R_t_gpu": float(np.mean(fms)) / e["ms"], "t_full_ms": float(np.mean(fms)),
+                        "e_c": pm.sinr_error(full.sinr.cpu().numpy(), rep_e.sinr.cpu().numpy()),
+                        "R_s": pm.storage_ratio(topo, c2.ranks())}
+                for k in ("step_ms_all",):
+                    e.pop(k, None)
+                extra[name] = e
+                del Xe, fac_e, rep_e
+            except Exception as ex:  # a secondary config must not hide the headline line
+                extra[name] = {"error": f"{type(ex).__name__}: {ex}"}
+            torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_leg(cfg, os.cpu_count() or 1)
+        cpu = cpu_baseline_leg(O, cfg)
     if rank == 0:
         line = {
-            "metric": "SINR evals/sec", "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c64 (fp32 rebuild/products; fp64 Grams and m x m solves)",
+            "metric": "SINR evals/sec", "value": whole["value"], "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": red["max_ms"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "c64 (fp32 rebuild/products; fp64 Grams and m x m solves)" if cfg.dtype == "c64" else "c128",
             "data": "synthetic (BASELINE.json generator: 1 ray/tap ULA, exp PDP 0.3, tau U(0,1us), seed 0)",
-            "config": {"workload": cfg.name, "groups_per_gpu": cfg.groups, "subcarriers": cfg.F,
-                       "dims": [cfg.M, cfg.N, cfg.P], "ranks": [cfg.m, cfg.n, cfg.p], "streams": cfg.L,
-                       "snr_db": cfg.snr_db, "scope": "paper_experiment", "J": cfg.J, "K": cfg.K,
-                       "parallelism": f"group-sharded x{world}", "l2": "flushed (256 MB write) between steps"},
-            "e2e": {"value": evals / (e2e_t.item() * 1e-3), "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
-            "gpu_launches": int(launches),
+            "config": bench_config(cfg, world),
+            "e2e": {"value": red["evals"] / (red_e2e["max_ms"] * 1e-3), "unit": "evals/s",
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                    "ms_per_step": red_e2e["max_ms"], "path": "Context.run_compressed_pipeline, pinned host buffers"},
+            "gpu_launches": int(r["launches"]),
             "roofline": roof,
             "cpu_baseline": cpu,
-            "tucker": tucker,
-            "paper_metrics": paper,
-            "clocks": clk.summary(),
-            "cublas_peaks": cublas,
-            "status_nonzero": int(bad),
-            "wall_s_timed": t_wall,
+            "tucker": dict(r["tucker"], value=whole["tucker"], unit="channels/s", nmse=whole["nmse"]),
+            "parity": dict(r.get("parity") or {}, max_sinr_rel_err_all_ranks=red["max_sinr_rel_err"],
+                           status_nonzero_all_ranks=int(red["bad_items"])),
+            "clocks": r["clocks"],
+            "cublas_peaks_tflops": cub,
+            "hbm_peak_gbs": hbm,
+            "step_ms_all": r["step_ms_all"],
+            "configs": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

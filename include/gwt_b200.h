@@ -106,7 +106,9 @@ typedef struct {
 int gwt_ctx_create(gwt_ctx** out, int device);
 void gwt_ctx_destroy(gwt_ctx* ctx);
 const char* gwt_last_error(const gwt_ctx* ctx);
-/* Use an external CUDA stream (cudaStream_t passed as void*); NULL = the ctx's own. */
+/* Use an external CUDA stream (cudaStream_t passed as void*); NULL = the ctx's own non-blocking stream.
+   The legacy default stream is passed as cudaStreamLegacy ((void*)1), not NULL. Every call is ordered
+   after prior work on the bound stream and synchronises it before returning. */
 int gwt_ctx_set_stream(gwt_ctx* ctx, void* stream);
 /* Number of kernel launches issued through this ctx since creation. */
 int64_t gwt_ctx_launch_count(const gwt_ctx* ctx);

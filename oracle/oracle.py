@@ -69,6 +69,23 @@ def generate_reference(J, K, M, N, P, seed, rays=4, tap_decay=0.7, rician=10.0, 
     return X, c
 
 
+def generate_baseline(J, K, M, N, P, ngroups, seed=0, group0=0, dtype=np.complex128, pdp_decay=0.3,
+                      max_delay=1e-6, nthreads=None):
+    """BASELINE.json generator (oracle/gen_baseline.cpp), bit-identical to the product's.
+    Returns X [g, links, P, N, M] (complex128 or complex64) and tau [g, links, P]."""
+    links = J * J * K
+    X = np.empty((ngroups, links, P, N, M), dtype)
+    tau = np.empty((ngroups, links, P), np.float64)
+    rc = lib().orc_generate_baseline(C.c_int(J), C.c_int(K), C.c_int(M), C.c_int(N), C.c_int(P),
+                                     C.c_longlong(group0), C.c_longlong(ngroups), C.c_ulonglong(seed),
+                                     C.c_double(pdp_decay), C.c_double(max_delay),
+                                     C.c_int(1 if X.dtype == np.complex64 else 0), _p(X), _p(tau),
+                                     C.c_int(nthreads or os.cpu_count() or 1))
+    if rc != 0:
+        raise OracleError(1, "generate_baseline: invalid topology")
+    return X, tau
+
+
 def heev(a):
     a = _c128(a)
     n = a.shape[0]

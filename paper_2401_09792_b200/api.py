@@ -175,8 +175,13 @@ def _as_f64(ref, a):
     return np.ascontiguousarray(np.asarray(a.cpu().numpy() if _is_torch(a) else a, np.float64))
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy
+
+
 class Context:
     """Owns a gwt_ctx (CUDA stream, workspaces). One per host thread."""
+
+    _bound = None
 
     def __init__(self, device: int = 0):
         self.lib = L.load()
@@ -201,11 +206,28 @@ class Context:
             pass
 
     def use_stream(self, stream_handle: int | None):
-        self.lib.gwt_ctx_set_stream(self.h, C.c_void_p(stream_handle) if stream_handle else None)
+        """Bind the context to a CUDA stream handle; None restores the context's own stream. Handle 0 is the
+        legacy default stream and is passed as cudaStreamLegacy (the C ABI maps NULL to the own stream)."""
+        if stream_handle is None:
+            self.lib.gwt_ctx_set_stream(self.h, None)
+        else:
+            self.lib.gwt_ctx_set_stream(self.h, C.c_void_p(stream_handle if stream_handle else _CUDA_STREAM_LEGACY))
+        self._bound = stream_handle
 
     def use_torch_stream(self):
         """Run on torch's current CUDA stream so torch events bracket our kernels."""
         self.use_stream(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _bind(self, *arrays):
+        """Calls with torch CUDA tensors run on torch's current stream, so torch work queued before the call
+        (copies, transposes, allocator reuse) is ordered before our kernels; host-only calls keep the
+        context's own stream."""
+        if any(_is_torch(a) and a.is_cuda for a in arrays if a is not None):
+            h = torch.cuda.current_stream(self.device).cuda_stream
+            if h != self._bound:
+                self.use_stream(h)
+        elif self._bound is not None:
+            self.use_stream(None)
 
     @property
     def launches(self) -> int:
@@ -255,6 +277,7 @@ class Context:
         trace = _like(X, (g, max(sweeps, 0) + 1), "f64")
         iters = _like(X, (g,), "i32")
         energy = _like(X, (g,), "f64")
+        self._bind(X, A, B, Cd)
         rc = self.lib.gwt_groupwise_solve(self.h, C.byref(topo.c()), C.byref(ranks.c()), g, _dtype_code(X), _mem(X),
                                           _ptr(X), sweeps, flags, _ptr(A), _ptr(B), _ptr(Cd), _ptr(G), _ptr(trace),
                                           _ptr(iters), _ptr(energy))
@@ -319,6 +342,7 @@ class Context:
             sinr = _like(G, (g, F, users, topo.num_streams), "f64")
             sig = _like(G, (g, F, users, topo.num_streams), "f64")
             st = _like(G, (g, F, users), "i32")
+            self._bind(G, Cd, coeffs)
             rc = self.lib.gwt_sinr_compressed_coeffs(self.h, C.byref(topo.c()), C.byref(ranks.c()), g,
                                                      _dtype_code(G), _mem(G), _ptr(Cd), _ptr(G), _ptr(coeffs), F,
                                                      SCOPE[scope], _ptr(sinr), _ptr(sig), _ptr(st), C.byref(ledger))
@@ -329,6 +353,7 @@ class Context:
             sinr = _like(G, (g, F, users, topo.num_streams), "f64")
             sig = _like(G, (g, F, users, topo.num_streams), "f64")
             st = _like(G, (g, F, users), "i32")
+            self._bind(G, Cd, tau, freqs)
             rc = self.lib.gwt_sinr_compressed(self.h, C.byref(topo.c()), C.byref(ranks.c()), g, _dtype_code(G),
                                               _mem(G), _ptr(Cd), _ptr(G), _ptr(tau), _ptr(freqs), F, SCOPE[scope],
                                               _ptr(sinr), _ptr(sig), _ptr(st), C.byref(ledger))
@@ -357,6 +382,7 @@ class Context:
         sinr = _like(X, (g, F, users, L_), "f64")
         sig = _like(X, (g, F, users, L_), "f64")
         st = _like(X, (g, F, users), "i32")
+        self._bind(X, coeffs, tau, freqs)
         rc = self.lib.gwt_sinr_full(self.h, C.byref(topo.c()), g, _dtype_code(X), _mem(X), _ptr(X), tau_p, freqs_p,
                                     _ptr(coeffs), F, SCOPE[scope], _ptr(sinr), _ptr(sig), _ptr(st), C.byref(ledger))
         self.check(rc)
@@ -376,6 +402,7 @@ class Context:
             F = freqs.shape[0]
             tau_p, freqs_p = _ptr(tau), _ptr(freqs)
         H = _like(cores, (g, F, topo.num_links, ranks.n, ranks.m), "c")
+        self._bind(cores, delay, coeffs, tau, freqs)
         rc = self.lib.gwt_assemble_compressed(self.h, C.byref(topo.c()), C.byref(ranks.c()), g, _dtype_code(cores),
                                               _mem(cores), _ptr(delay), _ptr(cores), tau_p, freqs_p, _ptr(coeffs), F,
                                               _ptr(H))
@@ -390,6 +417,7 @@ class Context:
         Hc = H.transpose(-1, -2).contiguous() if _is_torch(H) else np.ascontiguousarray(np.swapaxes(H, -1, -2))
         out = _like(H, (b, count, n), "c")
         ev = _like(H, (b, count), "f64") if with_values else None
+        self._bind(Hc)
         rc = self.lib.gwt_leading_eigenvectors(self.h, n, count, b, _dtype_code(H), _mem(H), _ptr(Hc), _ptr(out),
                                                _ptr(ev))
         self.check(rc)
@@ -413,6 +441,7 @@ class Context:
         Bc = Bc.contiguous() if _is_torch(Bc) else np.ascontiguousarray(Bc)
         T = _like(Qc, (b, m, m), "c")
         st = _like(Qc, (b,), "i32")
+        self._bind(Qc, Bc)
         rc = self.lib.gwt_hpd_solve(self.h, m, m, b, _mem(Qc), _ptr(Qc), _ptr(Bc), 1, _ptr(T), _ptr(st))
         self.check(rc)
         sth = st.cpu().numpy() if _is_torch(st) else st
@@ -440,6 +469,7 @@ class Context:
         o = [d1, d2, d3]
         o[mode - 1] = rows
         Y = _like(X, (b, o[2], o[1], o[0]), "c")
+        self._bind(X, Uc)
         rc = self.lib.gwt_mode_product(self.h, _dtype_code(X), _mem(X), b, d1, d2, d3, _ptr(X), rows, _ptr(Uc), mode,
                                        _ptr(Y))
         self.check(rc)
@@ -450,6 +480,7 @@ class Context:
         G = factors.cores
         g = G.shape[0]
         X = _like(G, (g, topo.num_links, topo.num_taps, topo.tx_antennas, topo.rx_antennas), "c")
+        self._bind(G, factors.rx, factors.tx, factors.delay)
         rc = self.lib.gwt_reconstruct(self.h, C.byref(topo.c()), C.byref(ranks.c()), g, _dtype_code(G), _mem(G),
                                       _ptr(factors.rx), _ptr(factors.tx), _ptr(factors.delay), _ptr(G), _ptr(X))
         self.check(rc)

@@ -9,7 +9,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .api import CompressionRanks, SystemTopology
+# Dependency-free on purpose: bench.py's CPU reference arm loads this file by path so that it never
+# imports the product package (the topology()/ranks() helpers import the API lazily).
 
 SUBCARRIER_SPACING_HZ = 30e3
 MAX_DELAY_S = 1e-6
@@ -45,10 +46,12 @@ class BaselineConfig:
     def sigma(self):
         return 10.0 ** (-self.snr_db / 20.0)
 
-    def topology(self) -> SystemTopology:
+    def topology(self):
+        from .api import SystemTopology
         return SystemTopology(self.J, self.K, self.M, self.N, self.P, self.L, self.sigma)
 
-    def ranks(self) -> CompressionRanks:
+    def ranks(self):
+        from .api import CompressionRanks
         return CompressionRanks(self.m, self.n, self.p)
 
     def freqs(self):

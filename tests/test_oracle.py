@@ -226,3 +226,16 @@ def test_reference_generator_rank_one_and_determinism():  # test_channel.cpp:28-
     assert s[1] <= 1e-12 * s[0]
     with pytest.raises(O.OracleError, match="rays_per_slice"):
         O.generate_reference(1, 1, 2, 2, 2, 0, rays=0)
+
+
+@pytest.mark.parametrize("name,ngroups,group0", [("C1", 4, 0), ("C2", 2, 5), ("C4", 1, 300)])
+def test_baseline_generator_bit_identical(name, ngroups, group0):
+    """The oracle's generator (used by bench.py's reference arm, which loads no product code) and the
+    product's gwt_generate_channels produce bit-identical X and tau, in both precisions."""
+    cfg = gw.CONFIGS[name]
+    t = cfg.topology()
+    for dt in (np.complex128, np.complex64):
+        Xp, tp = gw.generate_channels(t, ngroups, seed=0, dtype=dt, group0=group0)
+        Xo, to = O.generate_baseline(cfg.J, cfg.K, cfg.M, cfg.N, cfg.P, ngroups, seed=0, group0=group0, dtype=dt)
+        assert Xp.tobytes() == Xo.tobytes()
+        assert tp.tobytes() == to.tobytes()
