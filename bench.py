@@ -500,16 +500,16 @@ def cpu_baseline_leg(O, cfg):
 
 def main(argv=None):
     args = parse(argv)
-    CONFIGS = load_configs()
-    cfg = CONFIGS[args.config]
     if args.impl == "reference":
-        return run_reference(args, cfg)
+        return run_reference(args, load_configs()[args.config])
 
     import torch
     import torch.distributed as dist
 
     import paper_2401_09792_b200 as gw
     from oracle import oracle as O
+    CONFIGS = gw.CONFIGS
+    cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

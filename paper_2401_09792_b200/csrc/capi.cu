@@ -654,13 +654,14 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
         // (measured on C2: L2-sized chunks are slower - fewer CTAs per launch - so default to 2 GiB)
         const int64_t chunk_bytes = cb ? std::atoll(cb) : (int64_t)(2ll << 30);
         const int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f_h, 1)));
-        const bool rg = scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
+        const bool users_path = scope == GWT_SCOPE_PAPER && sinr_users_fits(t, cs) && !(path && std::strcmp(path, "pg") == 0);
+        const bool rg = !users_path && scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
         void* H = rg ? nullptr : ctx->lws(lane, WS_H, cs * ngroups * Fc * links * t.m * t.n);
         // pair Grams for a block of Fs subcarriers: [g][Fs][users][S][m*m] (fp64), Fs bounded by ~2 GB
         const int64_t per_f_pg = (int64_t)ngroups * users * (16LL * S * t.m * t.m + 8LL * (((t.L + 1) & ~1) + 2 * t.m * t.L));
         const int64_t Fs = std::max<int64_t>(Fc, std::min<int64_t>(F, (int64_t)(2ll << 30) / std::max<int64_t>(per_f_pg, 1)) / Fc * Fc);
-        double2* PG = (double2*)ctx->lws(lane, WS_PG, 16 * ngroups * std::min(Fs, F) * users * S * t.m * t.m);
-        double* EG = (double*)ctx->lws(lane, WS_EG, 8 * ngroups * std::min(Fs, F) * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
+        double2* PG = users_path ? nullptr : (double2*)ctx->lws(lane, WS_PG, 16 * ngroups * std::min(Fs, F) * users * S * t.m * t.m);
+        double* EG = users_path ? nullptr : (double*)ctx->lws(lane, WS_EG, 8 * ngroups * std::min(Fs, F) * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
         std::vector<cudaEvent_t> evs_local;
         std::vector<int> kind_local;  // 0 rebuild, 1 pair gram, 2 small, per interval
         std::vector<cudaEvent_t>& evs = deferred ? deferred->evs : evs_local;
@@ -673,9 +674,21 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
             ck(cudaEventRecord(ev, st), "event");
             evs.push_back(ev);
         };
-        // rg: paper scope with small groups -> rebuild + pair Grams fused in shared memory (H~ never in HBM)
         rec();
-        for (int64_t F0 = 0; F0 < F; F0 += Fs) {
+        if (users_path) {
+            // paper scope: rebuild -> per-user solve (serving Gram, eig, anchor precoders, MMSE) per chunk
+            for (int64_t f0 = 0; f0 < F; f0 += Fc) {
+                const int fc = (int)std::min(Fc, F - f0);
+                ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
+                rec();
+                kind.push_back(0);
+                ctx->launched(launch_sinr_users<T>(t, ngroups * fc, fc, F, f0, topo->noise_std, H, sd, sgd, std_, st));
+                rec();
+                kind.push_back(2);
+            }
+        }
+        // rg: paper scope with small groups -> rebuild + pair Grams fused in shared memory (H~ never in HBM)
+        for (int64_t F0 = 0; !users_path && F0 < F; F0 += Fs) {
             const int64_t fs = std::min(Fs, F - F0);
             if (rg) {
                 ctx->launched(launch_rebuild_pg<T>(t, (int)ngroups, (int)fs, F0, F, 0, fs, Cd, Gd, taud, fd, cod, PG, st));

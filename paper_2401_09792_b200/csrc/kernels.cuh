@@ -92,6 +92,11 @@ template <class T> cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int
                                                  const double* freqs, int uniform, double df, const void* coeffs,
                                                  double2* GU, double* sinr, double* signal, int* status,
                                                  cudaStream_t st);
+// k_users.cu: stage S for the paper scope (serving Gram, eig, anchor precoders, interference, MMSE)
+bool sinr_users_fits(const Topo& t, size_t csize);
+template <class T> cudaError_t launch_sinr_users(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0,
+                                                 double sigma, const void* H, double* sinr, double* signal,
+                                                 int* status, cudaStream_t st);
 cudaError_t launch_sinr_small(const Topo& t, int scope, int S, int64_t items, double sigma, int fc, int64_t Ftot,
                               int64_t f0, const double2* PG, double* EG, double* sinr, double* signal, int* status,
                               cudaStream_t st);
