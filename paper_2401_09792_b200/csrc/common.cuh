@@ -65,15 +65,14 @@ __device__ __forceinline__ double2 phasor_neg(double f, double tau) {
     return make_double2(c, -s);
 }
 
-// conj(c_r(f)) for subcarrier index fa: binary64 argument reduction, then sincospi in the
-// working precision (fp32 for c64: |error| ~1e-7 rad; fp64 for c128)
+// conj(c_r(f)): binary64 argument reduction and binary64 sincospi, rounded once to the working
+// precision. (An fp32 sincospif of the reduced argument rounded to fp32 carried ~2e-7 rad of phase
+// error into every tap; E = C^T c* sums P such terms with cancellation, which put ~1e-6 relative
+// error into H~ and, at near-degenerate serving singular pairs, ~1e-4 into the per-stream SINR of C4.)
 template <class T> __device__ __forceinline__ cplx_t<T> conj_coeff(double f, double tau);
 template <> __device__ __forceinline__ float2 conj_coeff<float>(double f, double tau) {
-    double x = f * tau;
-    x -= floor(x);
-    float s, c;
-    sincospif(2.0f * (float)x, &s, &c);
-    return make_float2(c, -s);
+    const double2 v = phasor_neg(f, tau);
+    return make_float2((float)v.x, (float)v.y);
 }
 template <> __device__ __forceinline__ double2 conj_coeff<double>(double f, double tau) { return phasor_neg(f, tau); }
 

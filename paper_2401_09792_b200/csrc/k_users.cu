@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
 #pragma unroll
     for (int d = 0; d < ND; ++d) acc[d] = make_double2(0.0, 0.0);
     if (active) {
+#pragma unroll 4
         for (int y = 0; y < n; ++y) {
             // the column is m contiguous entries shared by the user's lanes (L1 broadcast)
             const C* col = Hs + (int64_t)y * m;
@@ -225,17 +226,19 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
                 for (int i = MP - 2; i >= l; --i) {
                     if (i < mm && !brk) {
                         const double f = s * eo[i], b = c * eo[i];
-                        rr = sqrt(f * f + g * g);
+                        const double t2 = f * f + g * g;
+                        const double inv = rsqrt(t2);  // one MUFU-seeded reciprocal square root, no divisions
+                        rr = t2 * inv;
                         eo[i + 1] = rr;
-                        if (rr == 0.0) {
+                        if (t2 == 0.0) {
                             dg[i + 1] -= p;
 #pragma unroll
                             for (int k = l; k < MP; ++k)
                                 if (k == mm) eo[k] = 0.0;
                             brk = true;
                         } else {
-                            s = f / rr;
-                            c = g / rr;
+                            s = f * inv;
+                            c = g * inv;
                             g = dg[i + 1] - p;
                             rr = (dg[i] - g) * s + 2.0 * c * b;
                             p = s * rr;
@@ -369,12 +372,22 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
 #pragma unroll
         for (int l = 0; l < MP; ++l) yrow[l] = czero<C>();
         if (active && r < m) {
+#pragma unroll 2
             for (int y = 0; y < n; ++y) {
                 const C hv = Hx[(int64_t)y * m + r];
                 const C* vr = Vk + (size_t)y * L;
+                if (sizeof(C) == 8 && L == MP) {  // 16-byte broadcast loads of V'_k[y][:]
 #pragma unroll
-                for (int l = 0; l < MP; ++l)
-                    if (l < L) cfma(yrow[l], hv, vr[l]);
+                    for (int l = 0; l < MP; l += 2) {
+                        const float4 v4 = *reinterpret_cast<const float4*>(vr + l);
+                        cfma(yrow[l], hv, mk((decltype(hv.x))v4.x, (decltype(hv.x))v4.y));
+                        cfma(yrow[l + 1], hv, mk((decltype(hv.x))v4.z, (decltype(hv.x))v4.w));
+                    }
+                } else {
+#pragma unroll
+                    for (int l = 0; l < MP; ++l)
+                        if (l < L) cfma(yrow[l], hv, vr[l]);
+                }
             }
         }
         __syncwarp();
