@@ -265,3 +265,150 @@ def evaluate_assembled(J, K, L, sigma, H, scope=SCOPE_PAPER):
     _call(lib().orc_evaluate_assembled, C.c_int(J), C.c_int(K), C.c_int(M), C.c_int(N), C.c_int(L),
           C.c_double(sigma), C.c_int(scope), _p(H), _p(sinr), _p(sig))
     return sinr, sig
+
+
+# ---------------------------------------------------------------------------
+# parity metrics (checker side)
+def serving_singular_values(cfg, Cd, G, tau, fidx):
+    """Singular values of every user's serving compressed channel H~_iij(f) (binary64 rebuild of the given
+    factors), [g, F, users, min(m, n)] descending."""
+    J, K, m, n, p, P = cfg.J, cfg.K, cfg.m, cfg.n, cfg.p, cfg.P
+    g = Cd.shape[0]
+    links = J * J * K
+    co = coeffs_from_tau(tau, cfg.freqs()[fidx])
+    C128 = np.asarray(Cd, np.complex128).reshape(g, links, p, P)
+    G128 = np.asarray(G, np.complex128).reshape(g, links, p, n, m)
+    serving = [(i * J + i) * K + j for i in range(J) for j in range(K)]
+    d = np.einsum("glqP,gflP->gflq", C128[:, serving], np.conj(co[:, :, serving]))
+    H = np.einsum("glqnm,gflq->gflnm", G128[:, serving], d)
+    return np.linalg.svd(H, compute_uv=False)
+
+
+def sinr_cluster_err(got, want, sv, gap=2e-2):
+    """Parity of per-stream SINR with near-degenerate serving singular pairs handled as clusters.
+
+    Where two consecutive serving singular values are within `gap` (relative), the split of the
+    per-stream SINR between those streams is ill-conditioned (a relative perturbation e of H~ rotates
+    the singular pair by ~e sigma^2 / (sigma_r^2 - sigma_r+1^2)); there the cluster sum of
+    gamma = SINR / (1 + SINR) (rotation invariant) is compared instead. Returns (max relative error
+    over well-separated streams and cluster sums, max raw per-stream error, number of clustered items)."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    L = got.shape[-1]
+    s = np.asarray(sv)[..., :L]
+    close = np.zeros(got.shape, bool)
+    if L > 1:
+        c = (s[..., :-1] - s[..., 1:]) <= gap * s[..., :-1]
+        close[..., :-1] |= c
+        close[..., 1:] |= c
+    raw = np.abs(got - want) / np.abs(want)
+    err = np.where(close, 0.0, raw)
+    gg, gw_ = got / (1 + got), want / (1 + want)
+    # cluster label: runs of consecutive 'close' streams
+    lab = np.zeros(got.shape, np.int64)
+    for r in range(1, L):
+        lab[..., r] = lab[..., r - 1] + (~(close[..., r] & close[..., r - 1] & ((s[..., r - 1] - s[..., r]) <= gap * s[..., r - 1]))).astype(np.int64)
+    worst = err.max() if err.size else 0.0
+    idx = np.argwhere(close.any(-1))
+    for ix in map(tuple, idx):
+        for cl in np.unique(lab[ix][close[ix]]):
+            sel = (lab[ix] == cl) & close[ix]
+            a, b = gg[ix][sel].sum(), gw_[ix][sel].sum()
+            worst = max(worst, abs(a - b) / abs(b))
+    return float(worst), float(raw.max()), int(len(idx))
+
+
+# ---------------------------------------------------------------------------
+# oracle/_ref: the reference's own sources compiled against the Eigen-subset shim (oracle/Makefile `ref`)
+
+_REF_PATH = os.path.join(_HERE, "_ref", "libgwtref.so")
+_ref = None
+
+
+def ref_available() -> bool:
+    if os.path.exists(_REF_PATH):
+        return True
+    if os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-C", _HERE, "ref"], check=True)
+        return os.path.exists(_REF_PATH)
+    return False
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise OSError("oracle/_ref/libgwtref.so not built (needs /root/reference)")
+        _ref = C.CDLL(_REF_PATH)
+        _ref.ref_model_name.restype = C.c_char_p
+    return _ref
+
+
+def ref_groupwise_solve(dims, X, sweeps, pooled=False):
+    """The reference's gwt::groupwise_solve (its own stop rule) on each group of X [g, links, P, N, M]."""
+    d = dims
+    J, K, M, N, P, m, n, p = (d[k] for k in ("J", "K", "M", "N", "P", "m", "n", "p"))
+    X = _c128(X)
+    g = X.shape[0]
+    users, links = J * K, J * J * K
+    out = dict(A=np.zeros((g, users, m, M), np.complex128), B=np.zeros((g, J, n, N), np.complex128),
+               C=np.zeros((g, links, p, P), np.complex128), G=np.zeros((g, links, p, n, m), np.complex128),
+               trace=np.zeros((g, sweeps + 1)), iters=np.zeros(g, np.int32))
+    _call(ref_lib().ref_groupwise_solve, *(C.c_int(v) for v in (J, K, M, N, P, m, n, p)), C.c_longlong(g), _p(X),
+          C.c_int(sweeps), C.c_int(int(pooled)), _p(out["A"]), _p(out["B"]), _p(out["C"]), _p(out["G"]),
+          _p(out["trace"]), _p(out["iters"]))
+    return out
+
+
+def ref_sinr_compressed(dims, Cd, G, coeffs, sigma, L, scope=SCOPE_PAPER):
+    d = dims
+    J, K, P, m, n, p = (d[k] for k in ("J", "K", "P", "m", "n", "p"))
+    coeffs = _c128(coeffs)
+    g, F = coeffs.shape[:2]
+    sinr = np.zeros((g, F, J * K, L))
+    sig = np.zeros_like(sinr)
+    led = np.zeros(6, np.int64)
+    _call(ref_lib().ref_sinr_compressed, *(C.c_int(v) for v in (J, K, P, m, n, p, L)), C.c_double(sigma),
+          C.c_int(scope), C.c_longlong(g), _p(_c128(Cd)), _p(_c128(G)), _p(coeffs), C.c_longlong(F), _p(sinr), _p(sig),
+          _p(led))
+    return sinr, sig, led
+
+
+def ref_sinr_full(dims, X, coeffs, sigma, L, scope=SCOPE_PAPER):
+    d = dims
+    J, K, M, N, P = (d[k] for k in ("J", "K", "M", "N", "P"))
+    coeffs = _c128(coeffs)
+    g, F = coeffs.shape[:2]
+    sinr = np.zeros((g, F, J * K, L))
+    sig = np.zeros_like(sinr)
+    _call(ref_lib().ref_sinr_full, *(C.c_int(v) for v in (J, K, M, N, P, L)), C.c_double(sigma), C.c_int(scope),
+          C.c_longlong(g), _p(_c128(X)), _p(coeffs), C.c_longlong(F), _p(sinr), _p(sig))
+    return sinr, sig
+
+
+def ref_generate_channel_set(J, K, M, N, P, seed, rays=4, tap_decay=0.7, rician=10.0, coeff_decay=0.8):
+    links = J * J * K
+    X = np.zeros((links, P, N, M), np.complex128)
+    c = np.zeros((links, P), np.complex128)
+    _call(ref_lib().ref_generate_channel_set, *(C.c_int(v) for v in (J, K, M, N, P, rays)), C.c_double(tap_decay),
+          C.c_double(rician), C.c_double(coeff_decay), C.c_ulonglong(seed), _p(X), _p(c))
+    return X, c
+
+
+def ref_save_archive(path, model, dims, A, B, Cd, G, coeffs):
+    d = dims
+    _call(ref_lib().ref_save_archive, str(path).encode(), C.c_int(model),
+          *(C.c_int(d[k]) for k in ("J", "K", "M", "N", "P", "m", "n", "p")), _p(_c128(A)), _p(_c128(B)),
+          _p(_c128(Cd)), _p(_c128(G)), _p(_c128(coeffs)))
+
+
+def ref_model_name(kind):
+    return ref_lib().ref_model_name(C.c_int(kind)).decode()
+
+
+def ref_model_from_name(name):
+    err = C.create_string_buffer(256)
+    rc = ref_lib().ref_model_from_name(name.encode(), err, C.c_int(256))
+    if rc < 0:
+        raise OracleError(-1 - rc, err.value.decode())
+    return rc

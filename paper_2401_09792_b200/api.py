@@ -14,6 +14,7 @@ RuntimeError) with the reference's message text.
 from __future__ import annotations
 
 import ctypes as C
+import enum
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -47,6 +48,28 @@ ITEM_ERRORS = {
     3: (NumericalError, "sinr: interference-plus-noise power is negative (numerically invalid configuration)"),
     4: (InvalidArgument, "woodbury_inverse_apply: non-finite input"),
 }
+
+
+class ModelKind(enum.IntEnum):
+    """gwt::ModelKind (decompose.hpp:12): which factor-sharing model a solve / archive uses."""
+    individual = 0
+    shared = 1
+    groupwise = 2
+
+
+def model_name(model: ModelKind) -> str:
+    """gwt::model_name (decompose.cpp:42-49)."""
+    try:
+        return ModelKind(model).name
+    except ValueError:
+        return "unknown"
+
+
+def model_from_name(name: str) -> ModelKind:
+    """gwt::model_from_name (decompose.cpp:51-56); throws the reference's invalid_argument text."""
+    if name in ModelKind.__members__:
+        return ModelKind[name]
+    raise InvalidArgument(f"unknown model '{name}' (expected individual, shared or groupwise)")
 
 
 @dataclass

@@ -654,7 +654,10 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
         // (measured on C2: L2-sized chunks are slower - fewer CTAs per launch - so default to 2 GiB)
         const int64_t chunk_bytes = cb ? std::atoll(cb) : (int64_t)(2ll << 30);
         const int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f_h, 1)));
-        const bool users_path = scope == GWT_SCOPE_PAPER && sinr_users_fits(t, cs) && !(path && std::strcmp(path, "pg") == 0);
+        // stage S: the per-user kernel (k_users.cu) for m > 4; for m <= 4 the pair-Gram route
+        // (K2 + thread-per-user K3) measured faster (C2: 0.21 vs 0.31 ms). GWT_SINR_PATH=users|pg forces one.
+        const bool force_users = path && std::strcmp(path, "users") == 0, force_pg = path && std::strcmp(path, "pg") == 0;
+        const bool users_path = scope == GWT_SCOPE_PAPER && sinr_users_fits(t, cs) && !force_pg && (t.m > 4 || force_users);
         const bool rg = !users_path && scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
         void* H = rg ? nullptr : ctx->lws(lane, WS_H, cs * ngroups * Fc * links * t.m * t.n);
         // pair Grams for a block of Fs subcarriers: [g][Fs][users][S][m*m] (fp64), Fs bounded by ~2 GB

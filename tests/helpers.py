@@ -31,3 +31,7 @@ def rel_err(a, b, floor=0.0):
 
 def to_np(x):
     return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+serving_singular_values = O.serving_singular_values
+sinr_cluster_err = O.sinr_cluster_err
