@@ -65,14 +65,19 @@ __device__ __forceinline__ double2 phasor_neg(double f, double tau) {
     return make_double2(c, -s);
 }
 
-// conj(c_r(f)): binary64 argument reduction and binary64 sincospi, rounded once to the working
-// precision. (An fp32 sincospif of the reduced argument rounded to fp32 carried ~2e-7 rad of phase
-// error into every tap; E = C^T c* sums P such terms with cancellation, which put ~1e-6 relative
-// error into H~ and, at near-degenerate serving singular pairs, ~1e-4 into the per-stream SINR of C4.)
+// conj(c_r(f)) for the fp32 kernels: binary64 argument reduction x = frac(f tau), then sincospif of the
+// fp32 head xh = (float)x and a first-order rotation by the remainder 2 pi (x - xh) (|x - xh| <= 3e-8), so the
+// phase carries ~1 ulp of fp32 instead of the 2e-7 rad of rounding the argument (a full binary64 sincospi
+// measured no better on H~ at C4: the E / H~ accumulations dominate).
 template <class T> __device__ __forceinline__ cplx_t<T> conj_coeff(double f, double tau);
 template <> __device__ __forceinline__ float2 conj_coeff<float>(double f, double tau) {
-    const double2 v = phasor_neg(f, tau);
-    return make_float2((float)v.x, (float)v.y);
+    double x = f * tau;
+    x -= floor(x);
+    const float xh = (float)x;
+    const float d = (float)(6.283185307179586 * (x - (double)xh));
+    float s, c;
+    sincospif(2.0f * xh, &s, &c);
+    return make_float2(fmaf(-s, d, c), -fmaf(c, d, s));
 }
 template <> __device__ __forceinline__ double2 conj_coeff<double>(double f, double tau) { return phasor_neg(f, tau); }
 

@@ -1955,6 +1955,11 @@ cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();
     }
+    if (sizeof(T) == 4 && !coeffs && rebuild_mm_fits(t) && !std::getenv("GWT_REBUILD_RB")) {
+        cudaError_t e = launch_rebuild_mm(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
     if (!coeffs && !std::getenv("GWT_REBUILD_V1")) {
         // subcarrier tile: 64 while the phasor tile (P x 64) stays <= 16 KB (C1/C2), else 32 (C3-C5:
         // P = 48/64, where FT = 64 halves the resident CTAs); GWT_REBUILD_FT overrides

@@ -92,6 +92,10 @@ template <class T> cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int
                                                  const double* freqs, int uniform, double df, const void* coeffs,
                                                  double2* GU, double* sinr, double* signal, int* status,
                                                  cudaStream_t st);
+// k_rebuild.cu: SGEMM-tiled rebuild for large cores (c64, m n >= 256)
+bool rebuild_mm_fits(const Topo& t);
+cudaError_t launch_rebuild_mm(const Topo& t, int ngroups, int Fc, int64_t f0, const void* Cd, const void* G,
+                              const double* tau, const double* freqs, void* H, cudaStream_t st);
 // k_users.cu: stage S for the paper scope (serving Gram, eig, anchor precoders, interference, MMSE)
 bool sinr_users_fits(const Topo& t, size_t csize);
 template <class T> cudaError_t launch_sinr_users(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0,
