@@ -110,7 +110,7 @@ namespace {
 enum {
     WS_X = 0, WS_A, WS_B, WS_C, WS_G, WS_Y1, WS_W, WS_W2, WS_Z, WS_Z2, WS_GRAM, WS_EIGA, WS_EIGZ, WS_EIGX, WS_POOL,
     WS_ENERGY, WS_CAPT, WS_TRACE, WS_FAIL, WS_FROZEN, WS_TAU, WS_FREQ, WS_COEF, WS_H, WS_PG, WS_EG, WS_SINR, WS_SIG,
-    WS_STATUS, WS_MISC, WS_PART, WS_GPART, WS_STOP
+    WS_STATUS, WS_MISC, WS_PART, WS_GPART, WS_STOP, WS_EIG64
 };
 
 size_t ws_budget() {
@@ -226,16 +226,38 @@ struct SolveLane {
     size_t a_sz = 0, b_sz = 0, c_sz = 0, g_sz = 0;
 
     void* ws(int slot, size_t bytes) { return ctx->lws(lane, slot, bytes); }
+    static int eig64_min_d() {
+        static const int v = [] {
+            const char* e = std::getenv("GWT_EIG64_MIN_D");
+            return e ? std::atoi(e) : 1 << 30;
+        }();
+        return v;
+    }
     void gemm(const GemmDesc& d, const void* in, const void* U, void* out) {
         ctx->launched(launch_cgemm<T>(t, d, G, in, U, out, st));
     }
-    void gram_eig(const GramDesc& d, const void* V, int D, int count, void* out_factor, int copies) {
+    void gram_eig(const GramDesc& d, const void* V, int D, int count, void* out_factor, int copies, bool delay = false) {
         // copies > 0: pooled (one set per group) broadcast to `copies` factors
         const int users = t.users(), links = t.links();
         const int sets = d.set_kind == FI_USER ? users : d.set_kind == FI_BASE ? t.J : d.set_kind == FI_LINK ? links : 1;
         ctx->launched(launch_gram<T>(t, d, G, sets, V, gram, gpart, gpart_bytes, st));
         void* dst = copies > 0 ? pool : out_factor;
-        ctx->launched(launch_heev_topk<T>(D, count, G * sets, gram, dst, nullptr, eA, eZ, eX, failp, st));
+        const int64_t batch = G * sets;
+        if (sizeof(T) == 4 && D > 8 && (D >= eig64_min_d() || (delay && D >= 64))) {
+            // c64 Gram decomposed in binary64: the delay Gram carries the power-delay profile's graded
+            // spectrum (p_q ~ e^-0.3q: 1e-3 at the 24th of 64 taps), and the fp32 Householder's eps32 ||A||
+            // backward error moves its trailing kept eigenvectors (C4: NMSE +1.3e-6 vs the oracle; 6e-8 in
+            // binary64). GWT_EIG64_MIN_D forces binary64 for every mode with D >= the value.
+            double2* g64 = (double2*)ws(WS_EIG64, 16 * batch * ((int64_t)D * D + (int64_t)D * count));
+            double2* o64 = g64 + batch * D * D;
+            ctx->launched(launch_cplx_widen(gram, g64, batch * D * D, st));
+            ctx->launched(launch_heev_topk<double>(D, count, batch, g64, o64, nullptr, eA, eZ, eX, failp, st));
+            ctx->launched(launch_cplx_narrow(o64, dst, batch * D * count, st));
+        } else {
+            ctx->launched(launch_heev_topk<T>(D, count, batch, gram, dst, nullptr, eA, eZ, eX, failp, st));
+            // fp32 eigensolvers: restore orthonormality in binary64 (k_orth.cu); D <= 8 is solved in binary64
+            if (sizeof(T) == 4 && D > 8) ctx->launched(launch_orth_cholqr(D, count, batch, dst, st));
+        }
         if (copies > 0) ctx->launched(launch_broadcast<T>(pool, out_factor, (int64_t)D * count, copies, G, st));
     }
     void objective(int slot) {
@@ -313,7 +335,7 @@ struct SolveLane {
             GramDesc g2{t.N, t.M, t.P, MNP, t.M, 1, (int64_t)t.M * t.N, tx_kind};
             gram_eig(g2, X, t.N, t.n, B, tx_copies);
             GramDesc g3{t.P, t.M * t.N, 1, MNP, (int64_t)t.M * t.N, 1, 0, FI_LINK};
-            gram_eig(g3, X, t.P, t.p, Cf, 0);
+            gram_eig(g3, X, t.P, t.p, Cf, 0, true);
         }
         objective(0);
         a_sz = cs * users * t.M * t.m;
@@ -368,7 +390,7 @@ struct SolveLane {
         }
         gemm(dZ2, Z, B, Z2);
         GramDesc gd{t.P, t.m * t.n, 1, (int64_t)t.m * t.n * t.P, (int64_t)t.m * t.n, 1, 0, FI_LINK};
-        gram_eig(gd, Z2, t.P, t.p, Cf, 0);
+        gram_eig(gd, Z2, t.P, t.p, Cf, 0, true);
         if (side) {
             ck(cudaEventRecord(evc, st), "cudaEventRecord");
             ck(cudaStreamWaitEvent(side, evc, 0), "cudaStreamWaitEvent");

@@ -74,6 +74,10 @@ cudaError_t launch_rebuild_tc(const Topo& t, int ngroups, int Fc, int64_t f0, co
 template <class T> cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, void* out,
                                                 double* evals, double2* ws_a, double* ws_z, double2* ws_x, int* fail,
                                                 cudaStream_t st);
+// k_orth.cu: binary64 Cholesky-QR re-orthonormalisation of fp32 eigenvector blocks (+ phase convention)
+cudaError_t launch_orth_cholqr(int D, int count, int64_t batch, void* V, cudaStream_t st);
+cudaError_t launch_cplx_widen(const void* in, void* out, int64_t n, cudaStream_t st);   // c64 -> c128
+cudaError_t launch_cplx_narrow(const void* in, void* out, int64_t n, cudaStream_t st);  // c128 -> c64
 size_t heev_ws_a_elems(int D);
 size_t heev_ws_z_elems(int D, int count);
 // k_sinr.cu
