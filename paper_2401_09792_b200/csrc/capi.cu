@@ -110,7 +110,7 @@ namespace {
 enum {
     WS_X = 0, WS_A, WS_B, WS_C, WS_G, WS_Y1, WS_W, WS_W2, WS_Z, WS_Z2, WS_GRAM, WS_EIGA, WS_EIGZ, WS_EIGX, WS_POOL,
     WS_ENERGY, WS_CAPT, WS_TRACE, WS_FAIL, WS_FROZEN, WS_TAU, WS_FREQ, WS_COEF, WS_H, WS_PG, WS_EG, WS_SINR, WS_SIG,
-    WS_STATUS, WS_MISC, WS_PART, WS_GPART, WS_STOP, WS_EIG64
+    WS_STATUS, WS_MISC, WS_PART, WS_GPART, WS_STOP, WS_EIG64, WS_BREADY, WS_EREADY
 };
 
 size_t ws_budget() {
@@ -681,6 +681,54 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
         const bool force_users = path && std::strcmp(path, "users") == 0, force_pg = path && std::strcmp(path, "pg") == 0;
         const bool users_path = scope == GWT_SCOPE_PAPER && sinr_users_fits(t, cs) && !force_pg && (t.m > 4 || force_users);
         const bool rg = !users_path && scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
+        // c64 paper scope, m in {4, 8}: rebuild fused with the pair Grams on the tensor cores (k_rgram.cu)
+        const bool tc_path = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !cod && rgram_fits(t) &&
+                             !(path && (std::strcmp(path, "users") == 0 || std::strcmp(path, "pg") == 0 ||
+                                        std::strcmp(path, "rg") == 0));
+        if (tc_path) {
+            const int64_t Ft = std::min<int64_t>(F, 256);
+            double2* PGt = (double2*)ctx->lws(lane, WS_PG, 16 * ngroups * Ft * users * S * t.m * t.m);
+            double* EGt = (double*)ctx->lws(lane, WS_EG, 8 * ngroups * Ft * users * (((t.L + 1) & ~1) + 2 * t.m * t.L));
+            void* Bready = ctx->lws(lane, WS_BREADY, rgram_bready_bytes(t, ngroups));
+            void* Eready = ctx->lws(lane, WS_EREADY, rgram_eready_bytes(t, ngroups, (int)Ft));
+            std::vector<cudaEvent_t> evs_l;
+            std::vector<int> kind_l;
+            std::vector<cudaEvent_t>& evs = deferred ? deferred->evs : evs_l;
+            std::vector<int>& kind = deferred ? deferred->kind : kind_l;
+            if (deferred && !evs.empty()) kind.push_back(-1);
+            auto rec = [&]() {
+                if (!timing && !deferred) return;
+                cudaEvent_t ev;
+                ck(cudaEventCreate(&ev), "cudaEventCreate");
+                ck(cudaEventRecord(ev, st), "event");
+                evs.push_back(ev);
+            };
+            rec();
+            ctx->launched(launch_rgram_prep(t, ngroups, Gd, Bready, st));
+            rec();
+            kind.push_back(0);
+            for (int64_t f0 = 0; f0 < F; f0 += Ft) {
+                const int fc = (int)std::min(Ft, F - f0);
+                ctx->launched(launch_rgram(t, ngroups, fc, f0, 0, fc, Cd, taud, fd, Bready, Eready, PGt, st), 2);
+                rec();
+                kind.push_back(1);
+                ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PGt, EGt,
+                                                sd, sgd, std_, st));
+                rec();
+                kind.push_back(2);
+            }
+            if (timing && !deferred) {
+                ck(cudaEventSynchronize(evs.back()), "sync");
+                for (size_t q = 0; q < kind.size(); ++q) {
+                    float a = 0;
+                    cudaEventElapsedTime(&a, evs[q], evs[q + 1]);
+                    (kind[q] == 0 ? ms_r : kind[q] == 1 ? ms_p : ms_s) += a;
+                }
+            }
+            if (!deferred)
+                for (auto& ev : evs) cudaEventDestroy(ev);
+            return;
+        }
         void* H = rg ? nullptr : ctx->lws(lane, WS_H, cs * ngroups * Fc * links * t.m * t.n);
         // pair Grams for a block of Fs subcarriers: [g][Fs][users][S][m*m] (fp64), Fs bounded by ~2 GB
         const int64_t per_f_pg = (int64_t)ngroups * users * (16LL * S * t.m * t.m + 8LL * (((t.L + 1) & ~1) + 2 * t.m * t.L));

@@ -100,6 +100,16 @@ template <class T> cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int
 bool rebuild_mm_fits(const Topo& t);
 cudaError_t launch_rebuild_mm(const Topo& t, int ngroups, int Fc, int64_t f0, const void* Cd, const void* G,
                               const double* tau, const double* freqs, void* H, cudaStream_t st);
+// k_rgram.cu: stage R fused with the pair Grams on tcgen05 (c64, paper scope, m in {4, 8}): pre-split
+// B operands of the cores once per call (launch_rgram_prep), then per subcarrier chunk the E operands
+// and the Gram kernel writing PG[g][f - pf0][user][J][m*m]
+bool rgram_fits(const Topo& t);
+size_t rgram_bready_bytes(const Topo& t, int64_t ngroups);
+size_t rgram_eready_bytes(const Topo& t, int64_t ngroups, int Fc);
+cudaError_t launch_rgram_prep(const Topo& t, int64_t ngroups, const void* G, void* Bready, cudaStream_t st);
+cudaError_t launch_rgram(const Topo& t, int64_t ngroups, int Fc, int64_t f0, int64_t pf0, int64_t Fs, const void* Cd,
+                         const double* tau, const double* freqs, const void* Bready, void* Eready, double2* PG,
+                         cudaStream_t st);
 // k_users.cu: stage S for the paper scope (serving Gram, eig, anchor precoders, interference, MMSE)
 bool sinr_users_fits(const Topo& t, size_t csize);
 template <class T> cudaError_t launch_sinr_users(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0,
