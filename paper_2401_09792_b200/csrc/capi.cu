@@ -712,8 +712,12 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
                 ctx->launched(launch_rgram(t, ngroups, fc, f0, 0, fc, Cd, taud, fd, Bready, Eready, PGt, st), 2);
                 rec();
                 kind.push_back(1);
-                ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PGt, EGt,
-                                                sd, sgd, std_, st));
+                // m > 4: the per-user Householder/QL kernel in PG mode; m <= 4: the thread-per-user Jacobi kernel
+                if (t.m > 4 && sinr_users_pg_fits(t) && !std::getenv("GWT_PG_SMALL"))
+                    ctx->launched(launch_sinr_users_pg(t, ngroups * fc, fc, F, f0, topo->noise_std, PGt, sd, sgd, std_, st));
+                else
+                    ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PGt,
+                                                    EGt, sd, sgd, std_, st));
                 rec();
                 kind.push_back(2);
             }

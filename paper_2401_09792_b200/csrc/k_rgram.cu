@@ -27,6 +27,8 @@
 //                         tcgen05.ld -> binary64 -> DFMA accumulation of the entries of its rows
 // Binary64 accumulation of the exact products of the fp32 H~ values keeps the Gram route free of
 // the kappa^2 loss an fp32 Gram would add.
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "tc_sm100.cuh"
 
@@ -36,7 +38,8 @@ namespace {
 
 constexpr int kFT = 128;                          // subcarriers per tile = MMA M = TMEM lanes
 constexpr int kEpiWarps = 8;                      // two Gram threads per subcarrier
-constexpr int kRgThreads = (kEpiWarps + 2) * 32;  // + TMA warp + MMA warp
+constexpr int kRgThreads = kEpiWarps * 32;       // inline control: thread 0 also drives TMA and MMA (RgCtrl)
+constexpr int kRgThreadsWS = (kEpiWarps + 2) * 32;  // dedicated control: + MMA warp + TMA warp
 
 struct RgCfg {
     int m, n, p, mn, XC, nch, ks, tcols;
@@ -99,51 +102,63 @@ __global__ void __launch_bounds__(256) k_bsplit(Topo t, RgCfg c, const float2* _
 // A operands: Eready[g][l][tile][hi|lo] = [Er | Ei] rows = subcarriers of the tile, K-major canonical.
 // One thread per subcarrier: conj phasors (binary64 argument reduction) and E = C^T c* in fp32.
 template <int PQ>
-__global__ void __launch_bounds__(kFT) k_esplit(Topo t, RgCfg c, int Fc, int64_t f0, int ntiles,
-                                                const float2* __restrict__ Cd, const double* __restrict__ tau,
-                                                const double* __restrict__ freqs, unsigned char* __restrict__ Eready) {
+__global__ void __launch_bounds__(2 * kFT) k_esplit(Topo t, RgCfg c, int Fc, int64_t f0, int ntiles,
+                                                    const float2* __restrict__ Cd, const double* __restrict__ tau,
+                                                    const double* __restrict__ freqs, unsigned char* __restrict__ Eready) {
+    extern __shared__ __align__(16) unsigned char es_smem[];
+    float2* ph = reinterpret_cast<float2*>(es_smem);  // [P][kFT]
+    float2* sC = ph + (size_t)t.P * kFT;               // [PQ][P] (C_l column-major P x p)
     const int ti = blockIdx.x, l = blockIdx.y;
     const int64_t g = blockIdx.z, gl = g * t.links() + l;
-    const int P = t.P, fl = threadIdx.x, f = ti * kFT + fl;
+    const int P = t.P, tid = threadIdx.x;
     const float2* Cl = Cd + gl * (int64_t)P * PQ;
     const double* tl = tau + gl * P;
-    float2 e[PQ];
+    for (int e = tid; e < P * PQ; e += 2 * kFT) sC[e] = Cl[e];
+    for (int e = tid; e < P * kFT; e += 2 * kFT) {
+        const int r = e / kFT, f = ti * kFT + e % kFT;
+        ph[e] = f < Fc ? conj_coeff<float>(freqs[f0 + f], tl[r]) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    // thread (subcarrier fl, half qh): E(q, f) for q in [qh*PQ/2, (qh+1)*PQ/2)
+    constexpr int QH = PQ / 2;
+    const int fl = tid % kFT, qh = tid / kFT;
+    float2 e[QH];
 #pragma unroll
-    for (int q = 0; q < PQ; ++q) e[q] = make_float2(0.f, 0.f);
-    if (f < Fc) {
-        const double fr = freqs[f0 + f];
-#pragma unroll 2
-        for (int r = 0; r < P; ++r) {
-            const float2 ph = conj_coeff<float>(fr, tl[r]);
+    for (int q = 0; q < QH; ++q) e[q] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int r = 0; r < P; ++r) {
+        const float2 v = ph[r * kFT + fl];
 #pragma unroll
-            for (int q = 0; q < PQ; ++q) cfma(e[q], Cl[q * P + r], ph);
-        }
+        for (int q = 0; q < QH; ++q) cfma(e[q], sC[(qh * QH + q) * P + r], v);
     }
     unsigned char* hi = Eready + ((size_t)gl * ntiles + ti) * 2 * c.TA;
     unsigned char* lo = hi + c.TA;
+    // K columns: [0, p) Er, [p, 2p) Ei; this thread owns q in [qh*QH, qh*QH + QH)
 #pragma unroll
-    for (int k4 = 0; k4 < 2 * PQ; k4 += 4) {
-        float4 h, r;
-        float v[4];
-        if (k4 < PQ) {
+    for (int part = 0; part < 2; ++part) {
 #pragma unroll
-            for (int z = 0; z < 4; ++z) v[z] = e[(k4 + z) % PQ].x;
-        } else {
+        for (int z4 = 0; z4 < QH; z4 += 2) {
+            // two q -> write as float2 pairs (K-contiguous within a 16-byte core row when aligned)
 #pragma unroll
-            for (int z = 0; z < 4; ++z) v[z] = e[(k4 + z) % PQ].y;
+            for (int zz = 0; zz < 2; ++zz) {
+                const int q = qh * QH + z4 + zz;
+                if (z4 + zz < QH) {
+                    const float v = part == 0 ? e[z4 + zz].x : e[z4 + zz].y;
+                    float h, rr;
+                    tc::split_tf32_rn(v, h, rr);
+                    const uint32_t o = kmaj(fl, part * PQ + q, c.sbo_a);
+                    *reinterpret_cast<float*>(hi + o) = h;
+                    *reinterpret_cast<float*>(lo + o) = rr;
+                }
+            }
         }
-        tc::split_tf32_rn(v[0], h.x, r.x);
-        tc::split_tf32_rn(v[1], h.y, r.y);
-        tc::split_tf32_rn(v[2], h.z, r.z);
-        tc::split_tf32_rn(v[3], h.w, r.w);
-        const uint32_t o = kmaj(fl, k4, c.sbo_a);
-        *reinterpret_cast<float4*>(hi + o) = h;
-        *reinterpret_cast<float4*>(lo + o) = r;
     }
 }
 
 // ---------------------------------------------------------------------------------------------
 // Gram epilogue helpers (templated on the thread's half H so every accumulator index is static).
+struct RgCtrl;
+__device__ __forceinline__ void ctrl_step(const RgCtrl* ctl, int c);
 namespace {
 
 // serving-Gram rows of half H: MP = 8 -> {0,7,2,5} / {1,6,3,4}; MP = 4 -> {0,3} / {1,2} (balanced
@@ -171,12 +186,122 @@ template <> __device__ __forceinline__ void tmem_ldmp<8>(uint32_t taddr, uint32_
 template <> __device__ __forceinline__ void tmem_ldmp<4>(uint32_t taddr, uint32_t (&r)[4]) { tc::tmem_ld4_nw(taddr, r); }
 
 // one chunk of the serving Gram: acc(row, r') += H(row, c) conj(H(r', c)), r' <= row
+template <int MP, int H, int B>
+__device__ __forceinline__ void serving_step(uint32_t col0, int XC, int cl, int ncol, uint32_t (&hr)[2][MP],
+                                             uint32_t (&hi)[2][MP], double2 (&acc)[MP == 8 ? 18 : 5]) {
+    if (cl + 1 < ncol) {
+        tmem_ldmp<MP>(col0 + XC + MP * (cl + 1), hr[B ^ 1]);
+        tmem_ldmp<MP>(col0 + MP * (cl + 1), hi[B ^ 1]);
+    }
+    double2 v[MP];
+#pragma unroll
+    for (int r = 0; r < MP; ++r) v[r] = f2d(hr[B][r], hi[B][r]);
+#pragma unroll
+    for (int idx = 0; idx < srow_n<MP, H>(); ++idx) {
+        const int row = srow<MP, H>(idx);
+#pragma unroll
+        for (int r2 = 0; r2 < MP; ++r2)
+            if (r2 <= row) cfmac(acc[srow_off<MP, H>(idx) + r2], v[row], v[r2]);
+    }
+    tc::tmem_wait_ld();
+}
+
 template <int MP, int H>
-__device__ __forceinline__ void serving_chunk(uint32_t col0, int XC, double2 (&acc)[32]) {
+__device__ __forceinline__ void serving_chunk(uint32_t col0, int XC, double2 (&acc)[MP == 8 ? 18 : 5]) {
+    const int ncol = XC / MP;
+    uint32_t hr[2][MP], hi[2][MP];
+    tmem_ldmp<MP>(col0 + XC, hr[0]);  // Hr of slot 0
+    tmem_ldmp<MP>(col0, hi[0]);       // Hi of slot 0
+    tc::tmem_wait_ld();
+#pragma unroll 1
+    for (int cl = 0; cl < ncol; cl += 2) {
+        serving_step<MP, H, 0>(col0, XC, cl, ncol, hr, hi, acc);
+        serving_step<MP, H, 1>(col0, XC, cl + 1, ncol, hr, hi, acc);
+    }
+}
+
+// one chunk of the pair Gram: acc(row - H*MP/2, r') += Hx(row, c) conj(Ha(r', c)), rows of half H.
+// The TMEM loads of column cl+1 are issued before the DFMAs of column cl (one tcgen05.wait::ld per
+// column, after the math), so the load latency hides behind the arithmetic.
+template <int MP, int H>
+__device__ __forceinline__ void pair_load(uint32_t col0, int XC, int cl, uint32_t (&ar)[MP], uint32_t (&ai)[MP],
+                                          uint32_t (&xr)[4], uint32_t (&xi)[4]) {
+    constexpr int RH = MP / 2;
+    tmem_ldmp<MP>(col0 + 3 * XC + MP * cl, ar);  // Hr of slot 1 (anchor)
+    tmem_ldmp<MP>(col0 + 2 * XC + MP * cl, ai);  // Hi of slot 1
+    if constexpr (RH == 4) {
+        tc::tmem_ld4_nw(col0 + XC + MP * cl + H * RH, xr);
+        tc::tmem_ld4_nw(col0 + MP * cl + H * RH, xi);
+    } else {
+        tc::tmem_ld4_nw(col0 + XC + MP * cl, xr);
+        tc::tmem_ld4_nw(col0 + MP * cl, xi);
+    }
+}
+
+template <int MP, int H, int B>
+__device__ __forceinline__ void pair_step(uint32_t col0, int XC, int cl, int ncol, uint32_t (&ar)[2][MP],
+                                          uint32_t (&ai)[2][MP], uint32_t (&xr)[2][4], uint32_t (&xi)[2][4],
+                                          double2 (&acc)[32]) {
+    constexpr int RH = MP / 2;
+    if (cl + 1 < ncol) pair_load<MP, H>(col0, XC, cl + 1, ar[B ^ 1], ai[B ^ 1], xr[B ^ 1], xi[B ^ 1]);
+    double2 x[RH];
+#pragma unroll
+    for (int z = 0; z < RH; ++z) {
+        constexpr int off = RH == 4 ? 0 : H * RH;
+        x[z] = f2d(xr[B][off + z], xi[B][off + z]);
+    }
+#pragma unroll
+    for (int r2 = 0; r2 < MP; ++r2) {
+        const double2 a = f2d(ar[B][r2], ai[B][r2]);
+#pragma unroll
+        for (int z = 0; z < RH; ++z) cfmac(acc[z * MP + r2], x[z], a);
+    }
+    tc::tmem_wait_ld();
+}
+
+template <int MP, int H, int B>
+__device__ __forceinline__ void pair_step(uint32_t col0, int XC, int cl, int ncol, uint32_t (&ar)[2][MP],
+                                          uint32_t (&ai)[2][MP], uint32_t (&xr)[2][4], uint32_t (&xi)[2][4],
+                                          double2 (&acc)[MP * MP / 2]) {
+    constexpr int RH = MP / 2;
+    if (cl + 1 < ncol) pair_load<MP, H>(col0, XC, cl + 1, ar[B ^ 1], ai[B ^ 1], xr[B ^ 1], xi[B ^ 1]);
+    double2 x[RH];
+#pragma unroll
+    for (int z = 0; z < RH; ++z) {
+        constexpr int off = RH == 4 ? 0 : H * RH;
+        x[z] = f2d(xr[B][off + z], xi[B][off + z]);
+    }
+#pragma unroll
+    for (int r2 = 0; r2 < MP; ++r2) {
+        const double2 a = f2d(ar[B][r2], ai[B][r2]);
+#pragma unroll
+        for (int z = 0; z < RH; ++z) cfmac(acc[z * MP + r2], x[z], a);
+    }
+    tc::tmem_wait_ld();
+}
+
+// TMEM loads of column cl+1 are in flight while the DFMAs of column cl run (one wait::ld per column)
+template <int MP, int H>
+__device__ __forceinline__ void pair_chunk(uint32_t col0, int XC, double2 (&acc)[MP * MP / 2]) {
+    const int ncol = XC / MP;  // even (XC in {16, 32}, MP in {4, 8})
+    uint32_t ar[2][MP], ai[2][MP], xr[2][4], xi[2][4];
+    pair_load<MP, H>(col0, XC, 0, ar[0], ai[0], xr[0], xi[0]);
+    tc::tmem_wait_ld();
+#pragma unroll 1
+    for (int cl = 0; cl < ncol; cl += 2) {
+        pair_step<MP, H, 0>(col0, XC, cl, ncol, ar, ai, xr, xi, acc);
+        pair_step<MP, H, 1>(col0, XC, cl + 1, ncol, ar, ai, xr, xi, acc);
+    }
+}
+
+
+// single-buffered chunk bodies (dedicated-control-warp layout: 10 warps share the register file, 168 each)
+template <int MP, int H>
+__device__ __forceinline__ void serving_chunk_sb(uint32_t col0, int XC, double2 (&acc)[MP == 8 ? 18 : 5]) {
     for (int cl = 0; cl < XC / MP; ++cl) {
         uint32_t hr[MP], hi[MP];
-        tmem_ldmp<MP>(col0 + XC + MP * cl, hr);  // Hr of slot 0
-        tmem_ldmp<MP>(col0 + MP * cl, hi);       // Hi of slot 0
+        tmem_ldmp<MP>(col0 + XC + MP * cl, hr);
+        tmem_ldmp<MP>(col0 + MP * cl, hi);
         tc::tmem_wait_ld();
         double2 v[MP];
 #pragma unroll
@@ -190,34 +315,19 @@ __device__ __forceinline__ void serving_chunk(uint32_t col0, int XC, double2 (&a
         }
     }
 }
-
-// one chunk of the pair Gram: acc(row - H*MP/2, r') += Hx(row, c) conj(Ha(r', c)), rows of half H
 template <int MP, int H>
-__device__ __forceinline__ void pair_chunk(uint32_t col0, int XC, double2 (&acc)[32]) {
+__device__ __forceinline__ void pair_chunk_sb(uint32_t col0, int XC, double2 (&acc)[MP * MP / 2]) {
     constexpr int RH = MP / 2;
     for (int cl = 0; cl < XC / MP; ++cl) {
-        uint32_t ar[MP], ai[MP];
-        uint32_t xr[RH], xi[RH];
-        tmem_ldmp<MP>(col0 + 3 * XC + MP * cl, ar);  // Hr of slot 1 (anchor)
-        tmem_ldmp<MP>(col0 + 2 * XC + MP * cl, ai);  // Hi of slot 1
-        if constexpr (RH == 4) {
-            tc::tmem_ld4_nw(col0 + XC + MP * cl + H * RH, xr);
-            tc::tmem_ld4_nw(col0 + MP * cl + H * RH, xi);
-        } else {
-            uint32_t t4r[4], t4i[4];
-            tc::tmem_ld4_nw(col0 + XC + MP * cl, t4r);
-            tc::tmem_ld4_nw(col0 + MP * cl, t4i);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int z = 0; z < RH; ++z) {
-                xr[z] = t4r[H * RH + z];
-                xi[z] = t4i[H * RH + z];
-            }
-        }
+        uint32_t ar[MP], ai[MP], xr[4], xi[4];
+        pair_load<MP, H>(col0, XC, cl, ar, ai, xr, xi);
         tc::tmem_wait_ld();
         double2 x[RH];
 #pragma unroll
-        for (int z = 0; z < RH; ++z) x[z] = f2d(xr[z], xi[z]);
+        for (int z = 0; z < RH; ++z) {
+            constexpr int off = RH == 4 ? 0 : H * RH;
+            x[z] = f2d(xr[off + z], xi[off + z]);
+        }
 #pragma unroll
         for (int r2 = 0; r2 < MP; ++r2) {
             const double2 a = f2d(ar[r2], ai[r2]);
@@ -228,7 +338,7 @@ __device__ __forceinline__ void pair_chunk(uint32_t col0, int XC, double2 (&acc)
 }
 
 template <int MP, int H>
-__device__ __forceinline__ void write_serving(double2* __restrict__ out, int m, const double2 (&acc)[32]) {
+__device__ __forceinline__ void write_serving(double2* __restrict__ out, int m, const double2 (&acc)[MP == 8 ? 18 : 5]) {
 #pragma unroll
     for (int idx = 0; idx < srow_n<MP, H>(); ++idx) {
         const int row = srow<MP, H>(idx);
@@ -245,7 +355,7 @@ __device__ __forceinline__ void write_serving(double2* __restrict__ out, int m, 
 }
 
 template <int MP, int H>
-__device__ __forceinline__ void write_pair(double2* __restrict__ out, int m, const double2 (&acc)[32]) {
+__device__ __forceinline__ void write_pair(double2* __restrict__ out, int m, const double2 (&acc)[MP * MP / 2]) {
     constexpr int RH = MP / 2;
 #pragma unroll
     for (int z = 0; z < RH; ++z)
@@ -253,10 +363,148 @@ __device__ __forceinline__ void write_pair(double2* __restrict__ out, int m, con
         for (int r2 = 0; r2 < MP; ++r2) out[(H * RH + z) + m * r2] = acc[z * MP + r2];
 }
 
+
+// one whole job of the epilogue (all chunks + the PG write), so the serving (18 / 5) and pair (32 / 8)
+// accumulator sets never share live ranges
+struct EpiCtx {
+    uint64_t* t_full;
+    uint64_t* t_empty;
+    uint32_t tcol;  // tmem base + lane quarter
+    int XC, nch;
+    const RgCtrl* ctl;  // thread 0 only: the producer state machine
+};
+
+
+template <int MP, int H, bool PAIR, bool SB>
+__device__ __forceinline__ void epi_job(const EpiCtx& e, uint32_t& cnt, bool valid, double2* __restrict__ out, int m) {
+    constexpr int NA = PAIR ? MP * MP / 2 : (MP == 8 ? 18 : 5);
+    double2 acc[NA];
+#pragma unroll
+    for (int z = 0; z < NA; ++z) acc[z] = make_double2(0.0, 0.0);
+    for (int ch = 0; ch < e.nch; ++ch, ++cnt) {
+        const int st = cnt & 1;
+        const uint32_t use = cnt >> 1;
+        if (e.ctl) ctrl_step(e.ctl, (int)cnt);
+        __syncwarp();
+        tc::mbar_wait(&e.t_full[st], use & 1);
+        tc::fence_after_sync();
+        const uint32_t col0 = e.tcol + (uint32_t)(st * 4 * e.XC);
+        if constexpr (PAIR) {
+            if constexpr (SB) pair_chunk_sb<MP, H>(col0, e.XC, acc);
+            else pair_chunk<MP, H>(col0, e.XC, acc);
+        } else {
+            if constexpr (SB) serving_chunk_sb<MP, H>(col0, e.XC, acc);
+            else serving_chunk<MP, H>(col0, e.XC, acc);
+        }
+        tc::fence_before_sync();
+        tc::mbar_arrive(&e.t_empty[st]);
+    }
+    if (valid) {
+        if constexpr (PAIR) write_pair<MP, H>(out, m, acc);
+        else write_serving<MP, H>(out, m, acc);
+    }
+}
+
 }  // namespace
 
-template <int MP>
-__global__ void __launch_bounds__(kRgThreads, 1) k_rgram(Topo t, RgCfg c, int Fc, int ntiles, int64_t pf0, int64_t Fs,
+// Control state of the CTA's single producer thread (thread 0): TMA bulk loads and tcgen05.mma issue
+// for a flat sequence of chunks (tile, job, chunk). Thread 0 also computes Grams; before the epilogue
+// processes chunk c it keeps the MMAs one chunk ahead (c+1) and the B loads two ahead (c+2).
+struct RgCtrl {
+    const RgCfg* c;
+    unsigned char* sA;
+    unsigned char* sB;
+    const unsigned char* Bready;
+    const unsigned char* Eready;
+    uint64_t *a_full, *a_empty, *b_full, *b_empty, *t_full, *t_empty;
+    uint32_t tb;
+    int64_t g;
+    int links, ntiles, njobs, nch, total;
+    int i, j, J, K;
+    __device__ int job_link(int jb, int slot) const {
+        if (jb == 0) return (i * J + i) * K + j;
+        int k = jb - 1;
+        if (k >= i) ++k;
+        return slot == 0 ? (k * J + i) * K + j : (k * J + k) * K;
+    }
+    __device__ __forceinline__ void tma_b(int k) const {  // B operands of flat chunk k into stage k & 1
+        const int st = k & 1, use = k >> 1;
+        const int job = k / nch, ch = k % nch, jb = job % njobs;
+        const int ns = jb == 0 ? 1 : 2;
+        if (use > 0) tc::mbar_wait(&b_empty[st], (use - 1) & 1);
+        tc::mbar_arrive_expect_tx(&b_full[st], (uint32_t)ns * 2 * c->TB);
+        for (int sl = 0; sl < ns; ++sl) {
+            const int64_t gl = g * links + job_link(jb, sl);
+            tc::bulk_g2s(sB + ((size_t)st * 2 + sl) * 2 * c->TB, Bready + ((size_t)gl * nch + ch) * 2 * c->TB,
+                         2 * c->TB, &b_full[st]);
+        }
+    }
+    __device__ __forceinline__ void tma_a(int job, int sl, uint64_t* bar) const {
+        const int jb = job % njobs, ti = job / njobs;
+        const int64_t gl = g * links + job_link(jb, sl);
+        tc::bulk_g2s(sA + (size_t)sl * 2 * c->TA, Eready + ((size_t)gl * ntiles + ti) * 2 * c->TA, 2 * c->TA, bar);
+    }
+    __device__ __forceinline__ void mma(int k) const {  // all MMAs of flat chunk k (loads the job's A first)
+        const int st = k & 1, use = k >> 1;
+        const int job = k / nch, ch = k % nch, jb = job % njobs;
+        const int ns = jb == 0 ? 1 : 2;
+        const int XC = c->XC;
+        if (ch == 0) {
+            // A of this job. Job 0 uses slot 0 only, so the anchor A of job 1 (slot 1) is prefetched with it;
+            // job 1 then loads slot 0 alone. Any further job (J > 2) loads both slots.
+            if (job > 0) tc::mbar_wait(a_empty, (job - 1) & 1);  // previous job's MMAs done with A
+            const bool pre = jb == 0 && njobs > 1;
+            const int nload = jb == 1 ? 1 : (pre ? 2 : ns);
+            tc::mbar_arrive_expect_tx(a_full, (uint32_t)nload * 2 * c->TA);
+            if (jb == 0) {
+                tma_a(job, 0, a_full);
+                if (pre) tma_a(job + 1, 1, a_full);
+            } else if (jb == 1) {
+                tma_a(job, 0, a_full);
+            } else {
+                tma_a(job, 0, a_full);
+                tma_a(job, 1, a_full);
+            }
+            tc::mbar_wait(a_full, job & 1);
+        }
+        tc::mbar_wait(&b_full[st], use & 1);
+        if (use > 0) tc::mbar_wait(&t_empty[st], (use - 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t idesc = tc::idesc_tf32(kFT, XC);
+        const uint32_t roff = (uint32_t)(c->p / 4) * 128;  // B[:, p:3p] = [Gr | -Gi]
+        for (int sl = 0; sl < ns; ++sl) {
+            const uint32_t dI = tb + (uint32_t)(st * 4 * XC + sl * 2 * XC), dR = dI + XC;
+            const uint32_t ab = tc::smem_u32(sA + (size_t)sl * 2 * c->TA);
+            const uint32_t bb = tc::smem_u32(sB + ((size_t)st * 2 + sl) * 2 * c->TB);
+            // descriptor start-address field = addr >> 4 (14 bits, smem < 256 KB): k-step kk adds 16
+            const uint64_t dAh = tc::smem_desc(ab, 128, c->sbo_a), dAl = tc::smem_desc(ab + c->TA, 128, c->sbo_a);
+            const uint64_t dBh = tc::smem_desc(bb, 128, c->sbo_b), dBl = tc::smem_desc(bb + c->TB, 128, c->sbo_b);
+            const uint64_t rr = roff >> 4;
+#pragma unroll 1
+            for (int pass = 0; pass < 3; ++pass) {
+                const uint64_t da = pass == 2 ? dAl : dAh;
+                const uint64_t db = pass == 1 ? dBl : dBh;
+                for (int kk = 0; kk < c->ks; ++kk) {
+                    const uint32_t acc = (pass > 0 || kk > 0) ? 1u : 0u;
+                    const uint64_t o = (uint64_t)kk * 16;
+                    tc::mma_tf32(dI, da + o, db + o, idesc, acc);
+                    tc::mma_tf32(dR, da + o, db + rr + o, idesc, acc);
+                }
+            }
+        }
+        tc::commit(&b_empty[st]);
+        tc::commit(&t_full[st]);
+        if (ch == nch - 1) tc::commit(a_empty);
+    }
+};
+
+__device__ __forceinline__ void ctrl_step(const RgCtrl* ctl, int c) {
+    if (c + 1 < ctl->total) ctl->mma(c + 1);
+    if (c + 2 < ctl->total) ctl->tma_b(c + 2);
+}
+
+template <int MP, bool WS>
+__global__ void __launch_bounds__(WS ? kRgThreadsWS : kRgThreads, 1) k_rgram(Topo t, RgCfg c, int Fc, int ntiles, int64_t pf0, int64_t Fs,
                                                          const unsigned char* __restrict__ Bready,
                                                          const unsigned char* __restrict__ Eready,
                                                          double2* __restrict__ PG) {
@@ -264,12 +512,10 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_rgram(Topo t, RgCfg c, int Fc
     __shared__ uint64_t a_full, a_empty, b_full[2], b_empty[2], t_full[2], t_empty[2];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int u = blockIdx.x, users = t.users(), links = t.links();
+    const int u = blockIdx.x, users = t.users();
     const int64_t g = blockIdx.y;
-    const int J = t.J, K = t.K, i = u / K, j = u % K;
+    const int J = t.J, K = t.K;
     const int XC = c.XC, nch = c.nch;
-    unsigned char* sA = smem;                 // [slot][hi | lo]
-    unsigned char* sB = smem + 4 * c.TA;      // [stage][slot][hi | lo]
     if (warp == 0) tc::tmem_alloc(&tmem_base, c.tcols);
     if (tid == 32) {
         tc::mbar_init(&a_full, 1);
@@ -286,129 +532,47 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_rgram(Topo t, RgCfg c, int Fc
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tb = tmem_base;
-    // link of slot `slot` in job jb: job 0 = serving (i,i,j); job jb > 0: k = jb-th cell != i,
-    // slot 0 = receive link (k,i,j), slot 1 = anchor (k,k,0)
-    auto job_link = [&](int jb, int slot) -> int {
-        if (jb == 0) return (i * J + i) * K + j;
-        int k = jb - 1;
-        if (k >= i) ++k;
-        return slot == 0 ? (k * J + i) * K + j : (k * J + k) * K;
-    };
     const int njobs = J;
-
-    if (warp == kEpiWarps) {
-        // ---------------- TMA producer
-        if (lane == 0) {
-            uint32_t cnt = 0, nj = 0;
-            for (int ti = 0; ti < ntiles; ++ti) {
-                for (int jb = 0; jb < njobs; ++jb, ++nj) {
-                    const int ns = jb == 0 ? 1 : 2;
-                    if (nj > 0) tc::mbar_wait(&a_empty, (nj - 1) & 1);
-                    tc::mbar_arrive_expect_tx(&a_full, (uint32_t)ns * 2 * c.TA);
-                    for (int sl = 0; sl < ns; ++sl) {
-                        const int64_t gl = g * links + job_link(jb, sl);
-                        tc::bulk_g2s(sA + (size_t)sl * 2 * c.TA, Eready + ((size_t)gl * ntiles + ti) * 2 * c.TA,
-                                     2 * c.TA, &a_full);
-                    }
-                    for (int ch = 0; ch < nch; ++ch, ++cnt) {
-                        const int st = cnt & 1;
-                        const uint32_t use = cnt >> 1;
-                        if (use > 0) tc::mbar_wait(&b_empty[st], (use - 1) & 1);
-                        tc::mbar_arrive_expect_tx(&b_full[st], (uint32_t)ns * 2 * c.TB);
-                        for (int sl = 0; sl < ns; ++sl) {
-                            const int64_t gl = g * links + job_link(jb, sl);
-                            tc::bulk_g2s(sB + ((size_t)st * 2 + sl) * 2 * c.TB, Bready + ((size_t)gl * nch + ch) * 2 * c.TB,
-                                         2 * c.TB, &b_full[st]);
-                        }
-                    }
-                }
-            }
+    const int total = ntiles * njobs * nch;
+    RgCtrl ctl{&c, smem, smem + 4 * c.TA, Bready, Eready, &a_full, &a_empty, b_full, b_empty, t_full, t_empty, tb, g,
+               t.links(), ntiles, njobs, nch, total, u / K, u % K, J, K};
+    if constexpr (WS) {
+        if (warp == kEpiWarps) {  // MMA warp
+            if (lane == 0)
+                for (int k = 0; k < total; ++k) ctl.mma(k);
+            __syncwarp();
+        } else if (warp == kEpiWarps + 1) {  // TMA warp
+            if (lane == 0)
+                for (int k = 0; k < total; ++k) ctl.tma_b(k);
+            __syncwarp();
         }
-        __syncwarp();
-    } else if (warp == kEpiWarps + 1) {
-        // ---------------- MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc = tc::idesc_tf32(kFT, XC);
-            const uint32_t roff = (uint32_t)(c.p / 4) * 128;  // B[:, p:3p] = [Gr | -Gi]
-            uint32_t cnt = 0, nj = 0;
-            for (int ti = 0; ti < ntiles; ++ti) {
-                for (int jb = 0; jb < njobs; ++jb, ++nj) {
-                    const int ns = jb == 0 ? 1 : 2;
-                    tc::mbar_wait(&a_full, nj & 1);
-                    tc::fence_after_sync();
-                    for (int ch = 0; ch < nch; ++ch, ++cnt) {
-                        const int st = cnt & 1;
-                        const uint32_t use = cnt >> 1;
-                        tc::mbar_wait(&b_full[st], use & 1);
-                        if (use > 0) tc::mbar_wait(&t_empty[st], (use - 1) & 1);
-                        tc::fence_after_sync();
-                        for (int sl = 0; sl < ns; ++sl) {
-                            const uint32_t dI = tb + (uint32_t)(st * 4 * XC + sl * 2 * XC), dR = dI + XC;
-                            const uint32_t ab = tc::smem_u32(sA + (size_t)sl * 2 * c.TA);
-                            const uint32_t bb = tc::smem_u32(sB + ((size_t)st * 2 + sl) * 2 * c.TB);
-#pragma unroll 1
-                            for (int pass = 0; pass < 3; ++pass) {
-                                const uint32_t a0 = ab + (pass == 2 ? c.TA : 0u);
-                                const uint32_t b0 = bb + (pass == 1 ? c.TB : 0u);
-                                for (int kk = 0; kk < c.ks; ++kk) {
-                                    const uint64_t da = tc::smem_desc(a0 + kk * 256, 128, c.sbo_a);
-                                    const uint64_t dbi = tc::smem_desc(b0 + kk * 256, 128, c.sbo_b);
-                                    const uint64_t dbr = tc::smem_desc(b0 + roff + kk * 256, 128, c.sbo_b);
-                                    const uint32_t acc = (pass > 0 || kk > 0) ? 1u : 0u;
-                                    tc::mma_tf32(dI, da, dbi, idesc, acc);
-                                    tc::mma_tf32(dR, da, dbr, idesc, acc);
-                                }
-                            }
-                        }
-                        tc::commit(&b_empty[st]);
-                        tc::commit(&t_full[st]);
-                    }
-                    tc::commit(&a_empty);
-                }
-            }
-        }
-        __syncwarp();
     } else {
-        // ---------------- Gram epilogue: thread (subcarrier fl of the tile, half h)
-        const int q4 = warp & 3, h = warp >> 2;
-        const int fl = 32 * q4 + lane;
-        const uint32_t lanebase = (uint32_t)(32 * q4) << 16;
-        const int m = c.m, S = J;
-        uint32_t cnt = 0;
-        for (int ti = 0; ti < ntiles; ++ti) {
-            const int f = ti * kFT + fl;
-            const bool valid = f < Fc;
-            const int64_t row = ((int64_t)g * Fs + pf0 + f) * users + u;
-            for (int jb = 0; jb < njobs; ++jb) {
-                double2 acc[32];
-#pragma unroll
-                for (int z = 0; z < 32; ++z) acc[z] = make_double2(0.0, 0.0);
-                for (int ch = 0; ch < nch; ++ch, ++cnt) {
-                    const int st = cnt & 1;
-                    const uint32_t use = cnt >> 1;
-                    tc::mbar_wait(&t_full[st], use & 1);
-                    tc::fence_after_sync();
-                    const uint32_t col0 = tb + lanebase + (uint32_t)(st * 4 * XC);
-                    if (jb == 0) {
-                        if (h == 0) serving_chunk<MP, 0>(col0, XC, acc);
-                        else serving_chunk<MP, 1>(col0, XC, acc);
-                    } else {
-                        if (h == 0) pair_chunk<MP, 0>(col0, XC, acc);
-                        else pair_chunk<MP, 1>(col0, XC, acc);
-                    }
-                    tc::fence_before_sync();
-                    tc::mbar_arrive(&t_empty[st]);
-                }
-                if (valid) {
-                    double2* out = PG + (row * S + jb) * (int64_t)m * m;
-                    if (jb == 0) {
-                        if (h == 0) write_serving<MP, 0>(out, m, acc);
-                        else write_serving<MP, 1>(out, m, acc);
-                    } else {
-                        if (h == 0) write_pair<MP, 0>(out, m, acc);
-                        else write_pair<MP, 1>(out, m, acc);
-                    }
-                }
+        if (tid == 0) {
+            ctl.tma_b(0);
+            if (total > 1) ctl.tma_b(1);
+            ctl.mma(0);
+        }
+        __syncwarp();
+    }
+    // ---------------- Gram epilogue: thread (subcarrier fl of the tile, half h)
+    const int q4 = warp & 3, h = warp >> 2;
+    const int fl = 32 * q4 + lane;
+    const uint32_t lanebase = (uint32_t)(32 * q4) << 16;
+    const int m = c.m, S = J;
+    uint32_t cnt = 0;
+    const EpiCtx ec{t_full, t_empty, tb + lanebase, XC, nch, (!WS && tid == 0) ? &ctl : nullptr};
+    for (int ti = 0; warp < kEpiWarps && ti < ntiles; ++ti) {
+        const int f = ti * kFT + fl;
+        const bool valid = f < Fc;
+        const int64_t row = ((int64_t)g * Fs + pf0 + f) * users + u;
+        for (int jb = 0; jb < njobs; ++jb) {
+            double2* out = PG + (row * S + jb) * (int64_t)m * m;
+            if (jb == 0) {
+                if (h == 0) epi_job<MP, 0, false, WS>(ec, cnt, valid, out, m);
+                else epi_job<MP, 1, false, WS>(ec, cnt, valid, out, m);
+            } else {
+                if (h == 0) epi_job<MP, 0, true, WS>(ec, cnt, valid, out, m);
+                else epi_job<MP, 1, true, WS>(ec, cnt, valid, out, m);
             }
         }
     }
@@ -467,9 +631,15 @@ cudaError_t launch_rgram(const Topo& t, int64_t ngroups, int Fc, int64_t f0, int
     if (!rg_pick(t, c)) return cudaErrorNotSupported;
     const int ntiles = (Fc + kFT - 1) / kFT;
     dim3 ge(ntiles, t.links(), (unsigned)ngroups);
+    const size_t es_sm = sizeof(float2) * ((size_t)t.P * kFT + (size_t)t.P * t.p);
+    cudaError_t e0;
     switch (t.p) {
 #define GWT_ES(PQ) \
-    case PQ: k_esplit<PQ><<<ge, kFT, 0, st>>>(t, c, Fc, f0, ntiles, (const float2*)Cd, tau, freqs, (unsigned char*)Eready); break;
+    case PQ:                                                                                                         \
+        if ((e0 = cudaFuncSetAttribute(k_esplit<PQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)es_sm)) != cudaSuccess) \
+            return e0;                                                                                               \
+        k_esplit<PQ><<<ge, 2 * kFT, es_sm, st>>>(t, c, Fc, f0, ntiles, (const float2*)Cd, tau, freqs, (unsigned char*)Eready); \
+        break;
         GWT_ES(8) GWT_ES(12) GWT_ES(16) GWT_ES(24) GWT_ES(32)
 #undef GWT_ES
         default: return cudaErrorNotSupported;
@@ -477,17 +647,27 @@ cudaError_t launch_rgram(const Topo& t, int64_t ngroups, int Fc, int64_t f0, int
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 grid(t.users(), (unsigned)ngroups);
+    static const bool ws = [] {
+        // default: dedicated MMA / TMA warps (C4 single lane: 404 vs 650 ms for the inline-control layout,
+        // whose MMA issue serialises with thread 0's own Gram work); GWT_RGRAM_WS=0 selects the inline layout
+        const char* v = std::getenv("GWT_RGRAM_WS");
+        return !(v && std::atoi(v) == 0);
+    }();
+#define GWT_RG(MPV, WSV)                                                                                            \
+    do {                                                                                                            \
+        e = cudaFuncSetAttribute(k_rgram<MPV, WSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);      \
+        if (e != cudaSuccess) return e;                                                                             \
+        k_rgram<MPV, WSV><<<grid, WSV ? kRgThreadsWS : kRgThreads, c.smem, st>>>(                                   \
+            t, c, Fc, ntiles, pf0, Fs, (const unsigned char*)Bready, (const unsigned char*)Eready, PG);           \
+    } while (0)
     if (t.m == 8) {
-        e = cudaFuncSetAttribute(k_rgram<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-        if (e != cudaSuccess) return e;
-        k_rgram<8><<<grid, kRgThreads, c.smem, st>>>(t, c, Fc, ntiles, pf0, Fs, (const unsigned char*)Bready,
-                                                     (const unsigned char*)Eready, PG);
+        if (ws) GWT_RG(8, true);
+        else GWT_RG(8, false);
     } else {
-        e = cudaFuncSetAttribute(k_rgram<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-        if (e != cudaSuccess) return e;
-        k_rgram<4><<<grid, kRgThreads, c.smem, st>>>(t, c, Fc, ntiles, pf0, Fs, (const unsigned char*)Bready,
-                                                     (const unsigned char*)Eready, PG);
+        if (ws) GWT_RG(4, true);
+        else GWT_RG(4, false);
     }
+#undef GWT_RG
     return cudaGetLastError();
 }
 

@@ -24,6 +24,7 @@
 //  register indexing, rotations predicated), each lane rotating its own row of Z —
 //  then the back-transform with lane = eigenvector.
 #include <cfloat>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -64,14 +65,18 @@ struct SliceLayout {
 
 }  // namespace
 
-template <class T, int MP>
+// PGM = false: H~ in HBM ([g][f][link][n][m]); the serving Gram and the interference products are formed
+// here. PGM = true: the serving / pair Grams come precomputed in PG[item][user][J][m*m] (k_rgram.cu); the
+// interference of cell k is Y = X_{u,k} W'_k with W'_k = U'_L Lambda'^{-1/2} of the anchor (k,0)
+// (= H~_kij V'_k, the same product through the anchor's Gram eigenpairs), all in binary64.
+template <class T, int MP, bool PGM>
 __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t nslices, int fc, int64_t Ftot,
                                                     int64_t f0, double sigma, const cplx_t<T>* __restrict__ H,
-                                                    double* __restrict__ sinr, double* __restrict__ signal,
-                                                    int* __restrict__ status) {
-    using C = cplx_t<T>;
+                                                    const double2* __restrict__ PG, double* __restrict__ sinr,
+                                                    double* __restrict__ signal, int* __restrict__ status) {
+    using C = typename std::conditional<PGM, double2, cplx_t<T>>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int U = t.users(), L = t.L, m = t.m, n = t.n, J = t.J, K = t.K, links = t.links();
+    const int U = t.users(), L = t.L, m = t.m, n = PGM ? MP : t.n, J = t.J, K = t.K, links = t.links();
     SliceLayout lay;
     lay.init(U, MP, L, n, J, (int)sizeof(C));
     const int tid = threadIdx.x, lane = tid & 31;
@@ -90,8 +95,21 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     double2* stau = reinterpret_cast<double2*>(sbase + lay.tau_off) + u * MP;
     C* sV = reinterpret_cast<C*>(sbase + lay.v_off);
     const int i_cell = u / K, j_user = u % K;
+    const int MM = m * m;
+    // pair Grams of this (slice, user): slot 0 serving, then cells k != i ascending
+    const double2* Pu = PG + (sl_c * U + u) * (int64_t)J * MM;
+    if constexpr (PGM) {
+        // ---------------- phase 1a (PG): serving Gram row r
+#pragma unroll
+        for (int c = 0; c < MP; ++c) {
+            double2 a = (active && r < m && c < m) ? Pu[r + m * c] : make_double2(0.0, 0.0);
+            if (c == r) a.y = 0.0;
+            sA[r * (MP + 1) + c] = a;
+        }
+        __syncwarp();
+    } else {
     // H~ of this slice: item (g, f-in-chunk) = sl, links contiguous
-    const C* Hs = H + (sl_c * links + (int64_t)(i_cell * J + i_cell) * K + j_user) * (int64_t)m * n;
+    const cplx_t<T>* Hs = H + (sl_c * links + (int64_t)(i_cell * J + i_cell) * K + j_user) * (int64_t)m * t.n;
 
     // ---------------- phase 1a: serving Gram (binary64), balanced cyclic entries per lane
     constexpr int ND = MP / 2 + 1;
@@ -100,9 +118,9 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     for (int d = 0; d < ND; ++d) acc[d] = make_double2(0.0, 0.0);
     if (active) {
 #pragma unroll 4
-        for (int y = 0; y < n; ++y) {
+        for (int y = 0; y < t.n; ++y) {
             // the column is m contiguous entries shared by the user's lanes (L1 broadcast)
-            const C* col = Hs + (int64_t)y * m;
+            const cplx_t<T>* col = Hs + (int64_t)y * m;
             const double2 hr = r < m ? to_d2(col[r]) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int d = 0; d < ND; ++d) {
@@ -123,6 +141,7 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
         }
     }
     __syncwarp();
+    }
     // keep my row of A when the serving term of Q is A itself (L == m)
     double2 arow[MP];
 #pragma unroll
@@ -306,8 +325,21 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     }
     __syncthreads();
 
-    // ---------------- phase 2: anchor precoders V'_k = H~_kk0^H U'_L L'^-1/2 (all threads of the CTA)
-    {
+    // ---------------- phase 2: anchor precoders V'_k = H~_kk0^H U'_L L'^-1/2 (all threads of the CTA);
+    // PG mode: W'_k = U'_L L'^-1/2 (m x L) instead
+    if constexpr (PGM) {
+        const int per = J * MP * L;
+        for (int e = tid; e < spc * per; e += blockDim.x) {
+            const int s2 = e / per, rem = e % per, k = rem / (MP * L), a = (rem / L) % MP, l = rem % L;
+            unsigned char* sb2 = smem_raw + (size_t)s2 * lay.bytes;
+            const double2* U2 = reinterpret_cast<const double2*>(sb2 + lay.u_off) + (k * K) * L * MP;
+            const double* l2 = reinterpret_cast<const double*>(sb2 + lay.lam_off) + (k * K) * MP;
+            const double lam = l2[l];
+            const double sc = lam > 0.0 ? 1.0 / sqrt(lam) : 0.0;
+            const double2 v = U2[l * MP + a];
+            reinterpret_cast<double2*>(sb2 + lay.v_off)[(k * MP + a) * L + l] = make_double2(v.x * sc, v.y * sc);
+        }
+    } else {
         const int per = J * n;
         for (int e = tid; e < spc * per; e += blockDim.x) {
             const int s2 = e / per, rem = e % per, k = rem / n, y = rem % n;
@@ -317,7 +349,7 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
             const double2* U2 = reinterpret_cast<const double2*>(sb2 + lay.u_off) + (k * K) * L * MP;
             const double* l2 = reinterpret_cast<const double*>(sb2 + lay.lam_off) + (k * K) * MP;
             C* V2 = reinterpret_cast<C*>(sb2 + lay.v_off) + (k * n + y) * L;
-            const C* col = H + (sl2 * links + (int64_t)(k * J + k) * K) * (int64_t)m * n + (int64_t)y * m;
+            const cplx_t<T>* col = H + (sl2 * links + (int64_t)(k * J + k) * K) * (int64_t)m * t.n + (int64_t)y * m;
             double2 h[MP];
 #pragma unroll
             for (int a = 0; a < MP; ++a) h[a] = a < m ? to_d2(col[a]) : make_double2(0.0, 0.0);
@@ -366,14 +398,29 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
         const double* lk = slam + (k * K) * MP;
         for (int l = 0; l < L; ++l)
             if (!(lk[l] > 0.0)) st = st ? st : 5;
-        const C* Hx = H + (sl_c * links + (int64_t)(k * J + i_cell) * K + j_user) * (int64_t)m * n;
         const C* Vk = sV + (size_t)k * n * L;
         C yrow[MP];  // my row of Y (L <= MP entries)
 #pragma unroll
         for (int l = 0; l < MP; ++l) yrow[l] = czero<C>();
+        if constexpr (PGM) {
+            const double2* Xg = Pu + (int64_t)(1 + (k < i_cell ? k : k - 1)) * MM;  // slot of cell k
+            if (active && r < m) {
+#pragma unroll
+                for (int b = 0; b < MP; ++b) {
+                    if (b < m) {
+                        const double2 xv = Xg[r + m * b];
+                        const double2* wb = Vk + (size_t)b * L;
+#pragma unroll
+                        for (int l = 0; l < MP; ++l)
+                            if (l < L) cfma(yrow[l], xv, wb[l]);
+                    }
+                }
+            }
+        } else {
+        const cplx_t<T>* Hx = H + (sl_c * links + (int64_t)(k * J + i_cell) * K + j_user) * (int64_t)m * t.n;
         if (active && r < m) {
 #pragma unroll 2
-            for (int y = 0; y < n; ++y) {
+            for (int y = 0; y < t.n; ++y) {
                 const C hv = Hx[(int64_t)y * m + r];
                 const C* vr = Vk + (size_t)y * L;
                 if (sizeof(C) == 8 && L == MP) {  // 16-byte broadcast loads of V'_k[y][:]
@@ -389,6 +436,7 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
                         if (l < L) cfma(yrow[l], hv, vr[l]);
                 }
             }
+        }
         }
         __syncwarp();
 #pragma unroll
@@ -492,21 +540,22 @@ bool sinr_users_fits(const Topo& t, size_t csize) {
     return lay.bytes <= 200 * 1024;
 }
 
-template <class T, int MP>
+template <class T, int MP, bool PGM>
 static cudaError_t launch_users_mp(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0, double sigma,
-                                   const void* H, double* sinr, double* signal, int* status, cudaStream_t st) {
+                                   const void* H, const double2* PG, double* sinr, double* signal, int* status,
+                                   cudaStream_t st) {
     SliceLayout lay;
-    lay.init(t.users(), MP, t.L, t.n, t.J, (int)sizeof(cplx_t<T>));
+    lay.init(t.users(), MP, t.L, PGM ? MP : t.n, t.J, PGM ? 16 : (int)sizeof(cplx_t<T>));
     const int per = t.users() * MP;
     int spc = std::max(1, 256 / per);
     while (spc > 1 && (size_t)(spc + 1) * lay.bytes > 200 * 1024) --spc;
     const int threads = ((spc * per + 31) / 32) * 32;
     const size_t smem = (size_t)((threads + per - 1) / per) * lay.bytes;
-    cudaError_t e = cudaFuncSetAttribute(k_sinr_users<T, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_sinr_users<T, MP, PGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (nslices + spc - 1) / spc;
-    k_sinr_users<T, MP><<<(unsigned)blocks, threads, smem, st>>>(t, spc, nslices, fc, Ftot, f0, sigma,
-                                                                 (const cplx_t<T>*)H, sinr, signal, status);
+    k_sinr_users<T, MP, PGM><<<(unsigned)blocks, threads, smem, st>>>(t, spc, nslices, fc, Ftot, f0, sigma,
+                                                                      (const cplx_t<T>*)H, PG, sinr, signal, status);
     return cudaGetLastError();
 }
 
@@ -514,8 +563,23 @@ template <class T>
 cudaError_t launch_sinr_users(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0, double sigma,
                               const void* H, double* sinr, double* signal, int* status, cudaStream_t st) {
     if (!sinr_users_fits(t, sizeof(cplx_t<T>))) return cudaErrorNotSupported;
-    return t.m <= 4 ? launch_users_mp<T, 4>(t, nslices, fc, Ftot, f0, sigma, H, sinr, signal, status, st)
-                    : launch_users_mp<T, 8>(t, nslices, fc, Ftot, f0, sigma, H, sinr, signal, status, st);
+    return t.m <= 4 ? launch_users_mp<T, 4, false>(t, nslices, fc, Ftot, f0, sigma, H, nullptr, sinr, signal, status, st)
+                    : launch_users_mp<T, 8, false>(t, nslices, fc, Ftot, f0, sigma, H, nullptr, sinr, signal, status, st);
+}
+
+bool sinr_users_pg_fits(const Topo& t) {
+    const int MP = t.m <= 4 ? 4 : 8;
+    if (t.m > 8 || t.L > t.m || t.users() * MP > 256) return false;
+    SliceLayout lay;
+    lay.init(t.users(), MP, t.L, MP, t.J, 16);
+    return lay.bytes <= 200 * 1024;
+}
+
+cudaError_t launch_sinr_users_pg(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0, double sigma,
+                                 const double2* PG, double* sinr, double* signal, int* status, cudaStream_t st) {
+    if (!sinr_users_pg_fits(t)) return cudaErrorNotSupported;
+    return t.m <= 4 ? launch_users_mp<double, 4, true>(t, nslices, fc, Ftot, f0, sigma, nullptr, PG, sinr, signal, status, st)
+                    : launch_users_mp<double, 8, true>(t, nslices, fc, Ftot, f0, sigma, nullptr, PG, sinr, signal, status, st);
 }
 
 template cudaError_t launch_sinr_users<float>(const Topo&, int64_t, int, int64_t, int64_t, double, const void*, double*,

@@ -115,6 +115,10 @@ bool sinr_users_fits(const Topo& t, size_t csize);
 template <class T> cudaError_t launch_sinr_users(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0,
                                                  double sigma, const void* H, double* sinr, double* signal,
                                                  int* status, cudaStream_t st);
+// PG mode of the same kernel: Grams precomputed by k_rgram (PG[item][user][J][m*m]), binary64 throughout
+bool sinr_users_pg_fits(const Topo& t);
+cudaError_t launch_sinr_users_pg(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0, double sigma,
+                                 const double2* PG, double* sinr, double* signal, int* status, cudaStream_t st);
 cudaError_t launch_sinr_small(const Topo& t, int scope, int S, int64_t items, double sigma, int fc, int64_t Ftot,
                               int64_t f0, const double2* PG, double* EG, double* sinr, double* signal, int* status,
                               cudaStream_t st);

@@ -155,5 +155,11 @@ __device__ __forceinline__ void split_tf32_rn(float x, float& hi, float& lo) {
     lo = x - hi;
 }
 
+
+// warpgroup register reconfiguration (the whole warpgroup executes it): the Gram epilogue warps take the
+// registers the TMA / MMA warpgroup does not need
+template <int N> __device__ __forceinline__ void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N> __device__ __forceinline__ void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+
 }  // namespace tc
 }  // namespace gwtk
