@@ -38,8 +38,7 @@ namespace {
 
 constexpr int kFT = 128;                          // subcarriers per tile = MMA M = TMEM lanes
 constexpr int kEpiWarps = 8;                      // two Gram threads per subcarrier
-constexpr int kRgThreads = kEpiWarps * 32;       // inline control: thread 0 also drives TMA and MMA (RgCtrl)
-constexpr int kRgThreadsWS = (kEpiWarps + 2) * 32;  // dedicated control: + MMA warp + TMA warp
+constexpr int kRgThreads = (kEpiWarps + 2) * 32;  // + MMA warp + TMA warp
 
 struct RgCfg {
     int m, n, p, mn, XC, nch, ks, tcols;
@@ -157,15 +156,12 @@ __global__ void __launch_bounds__(2 * kFT) k_esplit(Topo t, RgCfg c, int Fc, int
 
 // ---------------------------------------------------------------------------------------------
 // Gram epilogue helpers (templated on the thread's half H so every accumulator index is static).
-struct RgCtrl;
-__device__ __forceinline__ void ctrl_step(const RgCtrl* ctl, int c);
 namespace {
 
 // serving-Gram rows of half H: MP = 8 -> {0,7,2,5} / {1,6,3,4}; MP = 4 -> {0,3} / {1,2} (balanced
 // lower-triangle entry counts: 18 / 18 and 5 / 5)
 template <int MP, int H> __host__ __device__ constexpr int srow_n() { return MP / 2; }
 template <int MP, int H> __host__ __device__ constexpr int srow(int idx) {
-    // MP = 8: h0 {0,7,2,5}, h1 {1,6,3,4};  MP = 4: h0 {0,3}, h1 {1,2}
     return MP == 8 ? (H == 0 ? (idx == 0 ? 0 : idx == 1 ? 7 : idx == 2 ? 2 : 5)
                              : (idx == 0 ? 1 : idx == 1 ? 6 : idx == 2 ? 3 : 4))
                    : (H == 0 ? (idx == 0 ? 0 : 3) : (idx == 0 ? 1 : 2));
@@ -175,6 +171,7 @@ template <int MP, int H> __host__ __device__ constexpr int srow_off(int idx) {
     for (int z = 0; z < idx; ++z) o += srow<MP, H>(z) + 1;
     return o;
 }
+template <int MP> constexpr int kServAcc = MP == 8 ? 18 : 5;
 
 __device__ __forceinline__ double2 f2d(uint32_t re, uint32_t im) {
     return make_double2((double)__uint_as_float(re), (double)__uint_as_float(im));
@@ -185,119 +182,14 @@ __device__ __forceinline__ void tmem_ldmp(uint32_t taddr, uint32_t (&r)[MP]);
 template <> __device__ __forceinline__ void tmem_ldmp<8>(uint32_t taddr, uint32_t (&r)[8]) { tc::tmem_ld8_nw(taddr, r); }
 template <> __device__ __forceinline__ void tmem_ldmp<4>(uint32_t taddr, uint32_t (&r)[4]) { tc::tmem_ld4_nw(taddr, r); }
 
-// one chunk of the serving Gram: acc(row, r') += H(row, c) conj(H(r', c)), r' <= row
-template <int MP, int H, int B>
-__device__ __forceinline__ void serving_step(uint32_t col0, int XC, int cl, int ncol, uint32_t (&hr)[2][MP],
-                                             uint32_t (&hi)[2][MP], double2 (&acc)[MP == 8 ? 18 : 5]) {
-    if (cl + 1 < ncol) {
-        tmem_ldmp<MP>(col0 + XC + MP * (cl + 1), hr[B ^ 1]);
-        tmem_ldmp<MP>(col0 + MP * (cl + 1), hi[B ^ 1]);
-    }
-    double2 v[MP];
-#pragma unroll
-    for (int r = 0; r < MP; ++r) v[r] = f2d(hr[B][r], hi[B][r]);
-#pragma unroll
-    for (int idx = 0; idx < srow_n<MP, H>(); ++idx) {
-        const int row = srow<MP, H>(idx);
-#pragma unroll
-        for (int r2 = 0; r2 < MP; ++r2)
-            if (r2 <= row) cfmac(acc[srow_off<MP, H>(idx) + r2], v[row], v[r2]);
-    }
-    tc::tmem_wait_ld();
-}
+// TMEM columns of stage base col0: slot 0 Hi [0, XC), Hr [XC, 2XC); slot 1 Hi [2XC, 3XC), Hr [3XC, 4XC);
+// within a slot, column x = r + MP c_local. Loads of column cl+1 are issued before the DFMAs of column cl
+// (one tcgen05.wait::ld per column, after the arithmetic), so the TMEM latency hides behind the math.
 
+// serving Gram: acc(row, r') += H(row, c) conj(H(r', c)), r' <= row, rows of half H
 template <int MP, int H>
-__device__ __forceinline__ void serving_chunk(uint32_t col0, int XC, double2 (&acc)[MP == 8 ? 18 : 5]) {
-    const int ncol = XC / MP;
-    uint32_t hr[2][MP], hi[2][MP];
-    tmem_ldmp<MP>(col0 + XC, hr[0]);  // Hr of slot 0
-    tmem_ldmp<MP>(col0, hi[0]);       // Hi of slot 0
-    tc::tmem_wait_ld();
-#pragma unroll 1
-    for (int cl = 0; cl < ncol; cl += 2) {
-        serving_step<MP, H, 0>(col0, XC, cl, ncol, hr, hi, acc);
-        serving_step<MP, H, 1>(col0, XC, cl + 1, ncol, hr, hi, acc);
-    }
-}
-
-// one chunk of the pair Gram: acc(row - H*MP/2, r') += Hx(row, c) conj(Ha(r', c)), rows of half H.
-// The TMEM loads of column cl+1 are issued before the DFMAs of column cl (one tcgen05.wait::ld per
-// column, after the math), so the load latency hides behind the arithmetic.
-template <int MP, int H>
-__device__ __forceinline__ void pair_load(uint32_t col0, int XC, int cl, uint32_t (&ar)[MP], uint32_t (&ai)[MP],
-                                          uint32_t (&xr)[4], uint32_t (&xi)[4]) {
-    constexpr int RH = MP / 2;
-    tmem_ldmp<MP>(col0 + 3 * XC + MP * cl, ar);  // Hr of slot 1 (anchor)
-    tmem_ldmp<MP>(col0 + 2 * XC + MP * cl, ai);  // Hi of slot 1
-    if constexpr (RH == 4) {
-        tc::tmem_ld4_nw(col0 + XC + MP * cl + H * RH, xr);
-        tc::tmem_ld4_nw(col0 + MP * cl + H * RH, xi);
-    } else {
-        tc::tmem_ld4_nw(col0 + XC + MP * cl, xr);
-        tc::tmem_ld4_nw(col0 + MP * cl, xi);
-    }
-}
-
-template <int MP, int H, int B>
-__device__ __forceinline__ void pair_step(uint32_t col0, int XC, int cl, int ncol, uint32_t (&ar)[2][MP],
-                                          uint32_t (&ai)[2][MP], uint32_t (&xr)[2][4], uint32_t (&xi)[2][4],
-                                          double2 (&acc)[32]) {
-    constexpr int RH = MP / 2;
-    if (cl + 1 < ncol) pair_load<MP, H>(col0, XC, cl + 1, ar[B ^ 1], ai[B ^ 1], xr[B ^ 1], xi[B ^ 1]);
-    double2 x[RH];
-#pragma unroll
-    for (int z = 0; z < RH; ++z) {
-        constexpr int off = RH == 4 ? 0 : H * RH;
-        x[z] = f2d(xr[B][off + z], xi[B][off + z]);
-    }
-#pragma unroll
-    for (int r2 = 0; r2 < MP; ++r2) {
-        const double2 a = f2d(ar[B][r2], ai[B][r2]);
-#pragma unroll
-        for (int z = 0; z < RH; ++z) cfmac(acc[z * MP + r2], x[z], a);
-    }
-    tc::tmem_wait_ld();
-}
-
-template <int MP, int H, int B>
-__device__ __forceinline__ void pair_step(uint32_t col0, int XC, int cl, int ncol, uint32_t (&ar)[2][MP],
-                                          uint32_t (&ai)[2][MP], uint32_t (&xr)[2][4], uint32_t (&xi)[2][4],
-                                          double2 (&acc)[MP * MP / 2]) {
-    constexpr int RH = MP / 2;
-    if (cl + 1 < ncol) pair_load<MP, H>(col0, XC, cl + 1, ar[B ^ 1], ai[B ^ 1], xr[B ^ 1], xi[B ^ 1]);
-    double2 x[RH];
-#pragma unroll
-    for (int z = 0; z < RH; ++z) {
-        constexpr int off = RH == 4 ? 0 : H * RH;
-        x[z] = f2d(xr[B][off + z], xi[B][off + z]);
-    }
-#pragma unroll
-    for (int r2 = 0; r2 < MP; ++r2) {
-        const double2 a = f2d(ar[B][r2], ai[B][r2]);
-#pragma unroll
-        for (int z = 0; z < RH; ++z) cfmac(acc[z * MP + r2], x[z], a);
-    }
-    tc::tmem_wait_ld();
-}
-
-// TMEM loads of column cl+1 are in flight while the DFMAs of column cl run (one wait::ld per column)
-template <int MP, int H>
-__device__ __forceinline__ void pair_chunk(uint32_t col0, int XC, double2 (&acc)[MP * MP / 2]) {
-    const int ncol = XC / MP;  // even (XC in {16, 32}, MP in {4, 8})
-    uint32_t ar[2][MP], ai[2][MP], xr[2][4], xi[2][4];
-    pair_load<MP, H>(col0, XC, 0, ar[0], ai[0], xr[0], xi[0]);
-    tc::tmem_wait_ld();
-#pragma unroll 1
-    for (int cl = 0; cl < ncol; cl += 2) {
-        pair_step<MP, H, 0>(col0, XC, cl, ncol, ar, ai, xr, xi, acc);
-        pair_step<MP, H, 1>(col0, XC, cl + 1, ncol, ar, ai, xr, xi, acc);
-    }
-}
-
-
-// single-buffered chunk bodies (dedicated-control-warp layout: 10 warps share the register file, 168 each)
-template <int MP, int H>
-__device__ __forceinline__ void serving_chunk_sb(uint32_t col0, int XC, double2 (&acc)[MP == 8 ? 18 : 5]) {
+__device__ __forceinline__ void serving_chunk(uint32_t col0, int XC, double2 (&acc)[kServAcc<MP>]) {
+    // single-buffered: 18 accumulators + the converted column leave no room for a second raw buffer
     for (int cl = 0; cl < XC / MP; ++cl) {
         uint32_t hr[MP], hi[MP];
         tmem_ldmp<MP>(col0 + XC + MP * cl, hr);
@@ -315,30 +207,65 @@ __device__ __forceinline__ void serving_chunk_sb(uint32_t col0, int XC, double2 
         }
     }
 }
-template <int MP, int H>
-__device__ __forceinline__ void pair_chunk_sb(uint32_t col0, int XC, double2 (&acc)[MP * MP / 2]) {
+
+// pair Gram, quarter (H, Q): acc(z, w) += Hx(H*RH + z, c) conj(Ha(Q*RH + w, c)), z, w < RH = MP / 2
+template <int MP, int H, int Q>
+__device__ __forceinline__ void pair_load(uint32_t col0, int XC, int cl, uint32_t (&xr)[4], uint32_t (&xi)[4],
+                                          uint32_t (&ar)[4], uint32_t (&ai)[4]) {
     constexpr int RH = MP / 2;
+    const uint32_t xo = MP * cl + (RH == 4 ? H * RH : 0), ao = MP * cl + (RH == 4 ? Q * RH : 0);
+    tc::tmem_ld4_nw(col0 + XC + xo, xr);      // Hr of slot 0 (receive link)
+    tc::tmem_ld4_nw(col0 + xo, xi);           // Hi of slot 0
+    tc::tmem_ld4_nw(col0 + 3 * XC + ao, ar);  // Hr of slot 1 (anchor)
+    tc::tmem_ld4_nw(col0 + 2 * XC + ao, ai);  // Hi of slot 1
+}
+template <int MP, int H, int Q>
+__device__ __forceinline__ void pair_chunk(uint32_t col0, int XC, double2 (&acc)[MP * MP / 4]) {
+    constexpr int RH = MP / 2;
+    constexpr int xoff = RH == 4 ? 0 : H * RH, aoff = RH == 4 ? 0 : Q * RH;
     for (int cl = 0; cl < XC / MP; ++cl) {
-        uint32_t ar[MP], ai[MP], xr[4], xi[4];
-        pair_load<MP, H>(col0, XC, cl, ar, ai, xr, xi);
+        uint32_t xr[4], xi[4], ar[4], ai[4];
+        pair_load<MP, H, Q>(col0, XC, cl, xr, xi, ar, ai);
         tc::tmem_wait_ld();
         double2 x[RH];
 #pragma unroll
-        for (int z = 0; z < RH; ++z) {
-            constexpr int off = RH == 4 ? 0 : H * RH;
-            x[z] = f2d(xr[off + z], xi[off + z]);
+        for (int z = 0; z < RH; ++z) x[z] = f2d(xr[xoff + z], xi[xoff + z]);
+#pragma unroll
+        for (int w = 0; w < RH; ++w) {
+            const double2 a = f2d(ar[aoff + w], ai[aoff + w]);
+#pragma unroll
+            for (int z = 0; z < RH; ++z) cfmac(acc[z * RH + w], x[z], a);
         }
+    }
+}
+
+// pair Gram, all columns of the thread's rows: acc(z, r') += Hx(H*RH + z, c) conj(Ha(r', c))
+template <int MP, int H>
+__device__ __forceinline__ void pair_chunk_full(uint32_t col0, int XC, double2 (&acc)[MP * MP / 2]) {
+    constexpr int RH = MP / 2;
+    constexpr int xoff = RH == 4 ? 0 : H * RH;
+    for (int cl = 0; cl < XC / MP; ++cl) {
+        uint32_t xr[4], xi[4], ar[MP], ai[MP];
+        const uint32_t xo = MP * cl + (RH == 4 ? H * RH : 0);
+        tc::tmem_ld4_nw(col0 + XC + xo, xr);
+        tc::tmem_ld4_nw(col0 + xo, xi);
+        tmem_ldmp<MP>(col0 + 3 * XC + MP * cl, ar);
+        tmem_ldmp<MP>(col0 + 2 * XC + MP * cl, ai);
+        tc::tmem_wait_ld();
+        double2 x[RH];
 #pragma unroll
-        for (int r2 = 0; r2 < MP; ++r2) {
-            const double2 a = f2d(ar[r2], ai[r2]);
+        for (int z = 0; z < RH; ++z) x[z] = f2d(xr[xoff + z], xi[xoff + z]);
 #pragma unroll
-            for (int z = 0; z < RH; ++z) cfmac(acc[z * MP + r2], x[z], a);
+        for (int w = 0; w < MP; ++w) {
+            const double2 a = f2d(ar[w], ai[w]);
+#pragma unroll
+            for (int z = 0; z < RH; ++z) cfmac(acc[z * MP + w], x[z], a);
         }
     }
 }
 
 template <int MP, int H>
-__device__ __forceinline__ void write_serving(double2* __restrict__ out, int m, const double2 (&acc)[MP == 8 ? 18 : 5]) {
+__device__ __forceinline__ void write_serving(double2* __restrict__ out, int m, const double2 (&acc)[kServAcc<MP>]) {
 #pragma unroll
     for (int idx = 0; idx < srow_n<MP, H>(); ++idx) {
         const int row = srow<MP, H>(idx);
@@ -353,63 +280,65 @@ __device__ __forceinline__ void write_serving(double2* __restrict__ out, int m, 
         }
     }
 }
-
 template <int MP, int H>
-__device__ __forceinline__ void write_pair(double2* __restrict__ out, int m, const double2 (&acc)[MP * MP / 2]) {
+__device__ __forceinline__ void write_pair_full(double2* __restrict__ out, int m, const double2 (&acc)[MP * MP / 2]) {
     constexpr int RH = MP / 2;
 #pragma unroll
     for (int z = 0; z < RH; ++z)
 #pragma unroll
-        for (int r2 = 0; r2 < MP; ++r2) out[(H * RH + z) + m * r2] = acc[z * MP + r2];
+        for (int w = 0; w < MP; ++w) out[(H * RH + z) + m * w] = acc[z * MP + w];
+}
+template <int MP, int H, int Q>
+__device__ __forceinline__ void write_pair(double2* __restrict__ out, int m, const double2 (&acc)[MP * MP / 4]) {
+    constexpr int RH = MP / 2;
+#pragma unroll
+    for (int z = 0; z < RH; ++z)
+#pragma unroll
+        for (int w = 0; w < RH; ++w) out[(H * RH + z) + m * (Q * RH + w)] = acc[z * RH + w];
 }
 
-
-// one whole job of the epilogue (all chunks + the PG write), so the serving (18 / 5) and pair (32 / 8)
-// accumulator sets never share live ranges
 struct EpiCtx {
     uint64_t* t_full;
     uint64_t* t_empty;
     uint32_t tcol;  // tmem base + lane quarter
     int XC, nch;
-    const RgCtrl* ctl;  // thread 0 only: the producer state machine
 };
 
-
-template <int MP, int H, bool PAIR, bool SB>
+// one whole job of the epilogue (all chunks + the PG write); KIND 0 = serving, 1 / 2 = pair quarter Q = 0 / 1,
+// 3 = whole pair rows of the thread's half
+template <int MP, int H, int KIND>
 __device__ __forceinline__ void epi_job(const EpiCtx& e, uint32_t& cnt, bool valid, double2* __restrict__ out, int m) {
-    constexpr int NA = PAIR ? MP * MP / 2 : (MP == 8 ? 18 : 5);
+    constexpr int NA = KIND == 0 ? kServAcc<MP> : (KIND == 3 ? MP * MP / 2 : MP * MP / 4);
     double2 acc[NA];
 #pragma unroll
     for (int z = 0; z < NA; ++z) acc[z] = make_double2(0.0, 0.0);
     for (int ch = 0; ch < e.nch; ++ch, ++cnt) {
         const int st = cnt & 1;
         const uint32_t use = cnt >> 1;
-        if (e.ctl) ctrl_step(e.ctl, (int)cnt);
-        __syncwarp();
         tc::mbar_wait(&e.t_full[st], use & 1);
         tc::fence_after_sync();
         const uint32_t col0 = e.tcol + (uint32_t)(st * 4 * e.XC);
-        if constexpr (PAIR) {
-            if constexpr (SB) pair_chunk_sb<MP, H>(col0, e.XC, acc);
-            else pair_chunk<MP, H>(col0, e.XC, acc);
-        } else {
-            if constexpr (SB) serving_chunk_sb<MP, H>(col0, e.XC, acc);
-            else serving_chunk<MP, H>(col0, e.XC, acc);
-        }
+        if constexpr (KIND == 0) serving_chunk<MP, H>(col0, e.XC, acc);
+        else if constexpr (KIND == 3) pair_chunk_full<MP, H>(col0, e.XC, acc);
+        else pair_chunk<MP, H, KIND - 1>(col0, e.XC, acc);
         tc::fence_before_sync();
         tc::mbar_arrive(&e.t_empty[st]);
     }
     if (valid) {
-        if constexpr (PAIR) write_pair<MP, H>(out, m, acc);
-        else write_serving<MP, H>(out, m, acc);
+        if constexpr (KIND == 0) write_serving<MP, H>(out, m, acc);
+        else if constexpr (KIND == 3) write_pair_full<MP, H>(out, m, acc);
+        else write_pair<MP, H, KIND - 1>(out, m, acc);
     }
 }
 
 }  // namespace
 
-// Control state of the CTA's single producer thread (thread 0): TMA bulk loads and tcgen05.mma issue
-// for a flat sequence of chunks (tile, job, chunk). Thread 0 also computes Grams; before the epilogue
-// processes chunk c it keeps the MMAs one chunk ahead (c+1) and the B loads two ahead (c+2).
+// Control state of the producer threads: TMA bulk loads (TMA warp) and tcgen05.mma issue (MMA warp) over
+// a flat sequence of chunks (tile, job, chunk). Jobs per tile: 0 = serving link; then for each cell k != i
+// two jobs (the two quarters Q of the pair Gram's columns, same links: receive (k,i,j) in slot 0, anchor
+// (k,k,0) in slot 1). Splitting the pair Gram into column halves keeps 16 binary64 accumulators per
+// thread, which leaves registers for double-buffered TMEM loads at 10 warps (the tensor cores recompute
+// the pair's H~ once more; they are not the binding pipe).
 struct RgCtrl {
     const RgCfg* c;
     unsigned char* sA;
@@ -420,10 +349,10 @@ struct RgCtrl {
     uint32_t tb;
     int64_t g;
     int links, ntiles, njobs, nch, total;
-    int i, j, J, K;
-    __device__ int job_link(int jb, int slot) const {
+    int i, j, J, K, split;  // split: 2 jobs (column quarters) per pair, else 1
+    __device__ __forceinline__ int job_link(int jb, int slot) const {
         if (jb == 0) return (i * J + i) * K + j;
-        int k = jb - 1;
+        int k = (jb - 1) / split;
         if (k >= i) ++k;
         return slot == 0 ? (k * J + i) * K + j : (k * J + k) * K;
     }
@@ -439,10 +368,10 @@ struct RgCtrl {
                          2 * c->TB, &b_full[st]);
         }
     }
-    __device__ __forceinline__ void tma_a(int job, int sl, uint64_t* bar) const {
+    __device__ __forceinline__ void tma_a(int job, int sl) const {
         const int jb = job % njobs, ti = job / njobs;
         const int64_t gl = g * links + job_link(jb, sl);
-        tc::bulk_g2s(sA + (size_t)sl * 2 * c->TA, Eready + ((size_t)gl * ntiles + ti) * 2 * c->TA, 2 * c->TA, bar);
+        tc::bulk_g2s(sA + (size_t)sl * 2 * c->TA, Eready + ((size_t)gl * ntiles + ti) * 2 * c->TA, 2 * c->TA, a_full);
     }
     __device__ __forceinline__ void mma(int k) const {  // all MMAs of flat chunk k (loads the job's A first)
         const int st = k & 1, use = k >> 1;
@@ -450,20 +379,18 @@ struct RgCtrl {
         const int ns = jb == 0 ? 1 : 2;
         const int XC = c->XC;
         if (ch == 0) {
-            // A of this job. Job 0 uses slot 0 only, so the anchor A of job 1 (slot 1) is prefetched with it;
-            // job 1 then loads slot 0 alone. Any further job (J > 2) loads both slots.
-            if (job > 0) tc::mbar_wait(a_empty, (job - 1) & 1);  // previous job's MMAs done with A
-            const bool pre = jb == 0 && njobs > 1;
-            const int nload = jb == 1 ? 1 : (pre ? 2 : ns);
+            // A of this job: job 0 uses slot 0 and prefetches the first pair's anchor into slot 1; the first
+            // pair's quarter 0 then loads slot 0 alone; quarter 1 reuses both slots; later pairs load both
+            if (job > 0) tc::mbar_wait(a_empty, (job - 1) & 1);
+            const int pk = (jb - 1) / split, q = (jb - 1) % split;
+            const int nload = jb == 0 ? (njobs > 1 ? 2 : 1) : (q == 1 ? 0 : (pk == 0 ? 1 : 2));
             tc::mbar_arrive_expect_tx(a_full, (uint32_t)nload * 2 * c->TA);
             if (jb == 0) {
-                tma_a(job, 0, a_full);
-                if (pre) tma_a(job + 1, 1, a_full);
-            } else if (jb == 1) {
-                tma_a(job, 0, a_full);
-            } else {
-                tma_a(job, 0, a_full);
-                tma_a(job, 1, a_full);
+                tma_a(job, 0);
+                if (njobs > 1) tma_a(job + 1, 1);
+            } else if (q == 0) {
+                tma_a(job, 0);
+                if (pk > 0) tma_a(job, 1);
             }
             tc::mbar_wait(a_full, job & 1);
         }
@@ -498,13 +425,8 @@ struct RgCtrl {
     }
 };
 
-__device__ __forceinline__ void ctrl_step(const RgCtrl* ctl, int c) {
-    if (c + 1 < ctl->total) ctl->mma(c + 1);
-    if (c + 2 < ctl->total) ctl->tma_b(c + 2);
-}
-
-template <int MP, bool WS>
-__global__ void __launch_bounds__(WS ? kRgThreadsWS : kRgThreads, 1) k_rgram(Topo t, RgCfg c, int Fc, int ntiles, int64_t pf0, int64_t Fs,
+template <int MP, bool SPLIT>
+__global__ void __launch_bounds__(kRgThreads, 1) k_rgram(Topo t, RgCfg c, int Fc, int ntiles, int64_t pf0, int64_t Fs,
                                                          const unsigned char* __restrict__ Bready,
                                                          const unsigned char* __restrict__ Eready,
                                                          double2* __restrict__ PG) {
@@ -532,47 +454,47 @@ __global__ void __launch_bounds__(WS ? kRgThreadsWS : kRgThreads, 1) k_rgram(Top
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tb = tmem_base;
-    const int njobs = J;
+    constexpr int SP = SPLIT ? 2 : 1;
+    const int njobs = 1 + SP * (J - 1);
     const int total = ntiles * njobs * nch;
-    RgCtrl ctl{&c, smem, smem + 4 * c.TA, Bready, Eready, &a_full, &a_empty, b_full, b_empty, t_full, t_empty, tb, g,
-               t.links(), ntiles, njobs, nch, total, u / K, u % K, J, K};
-    if constexpr (WS) {
-        if (warp == kEpiWarps) {  // MMA warp
-            if (lane == 0)
-                for (int k = 0; k < total; ++k) ctl.mma(k);
-            __syncwarp();
-        } else if (warp == kEpiWarps + 1) {  // TMA warp
-            if (lane == 0)
-                for (int k = 0; k < total; ++k) ctl.tma_b(k);
-            __syncwarp();
-        }
-    } else {
-        if (tid == 0) {
-            ctl.tma_b(0);
-            if (total > 1) ctl.tma_b(1);
-            ctl.mma(0);
-        }
+    const RgCtrl ctl{&c, smem, smem + 4 * c.TA, Bready, Eready, &a_full, &a_empty, b_full, b_empty, t_full, t_empty,
+                     tb, g, t.links(), ntiles, njobs, nch, total, u / K, u % K, J, K, SP};
+    if (warp == kEpiWarps) {  // MMA warp
+        if (lane == 0)
+            for (int k = 0; k < total; ++k) ctl.mma(k);
         __syncwarp();
-    }
-    // ---------------- Gram epilogue: thread (subcarrier fl of the tile, half h)
-    const int q4 = warp & 3, h = warp >> 2;
-    const int fl = 32 * q4 + lane;
-    const uint32_t lanebase = (uint32_t)(32 * q4) << 16;
-    const int m = c.m, S = J;
-    uint32_t cnt = 0;
-    const EpiCtx ec{t_full, t_empty, tb + lanebase, XC, nch, (!WS && tid == 0) ? &ctl : nullptr};
-    for (int ti = 0; warp < kEpiWarps && ti < ntiles; ++ti) {
-        const int f = ti * kFT + fl;
-        const bool valid = f < Fc;
-        const int64_t row = ((int64_t)g * Fs + pf0 + f) * users + u;
-        for (int jb = 0; jb < njobs; ++jb) {
-            double2* out = PG + (row * S + jb) * (int64_t)m * m;
-            if (jb == 0) {
-                if (h == 0) epi_job<MP, 0, false, WS>(ec, cnt, valid, out, m);
-                else epi_job<MP, 1, false, WS>(ec, cnt, valid, out, m);
-            } else {
-                if (h == 0) epi_job<MP, 0, true, WS>(ec, cnt, valid, out, m);
-                else epi_job<MP, 1, true, WS>(ec, cnt, valid, out, m);
+    } else if (warp == kEpiWarps + 1) {  // TMA warp
+        if (lane == 0)
+            for (int k = 0; k < total; ++k) ctl.tma_b(k);
+        __syncwarp();
+    } else {
+        // ---------------- Gram epilogue: thread (subcarrier fl of the tile, half h)
+        const int q4 = warp & 3, h = warp >> 2;
+        const int fl = 32 * q4 + lane;
+        const uint32_t lanebase = (uint32_t)(32 * q4) << 16;
+        const int m = c.m, S = J;
+        uint32_t cnt = 0;
+        const EpiCtx ec{t_full, t_empty, tb + lanebase, XC, nch};
+        for (int ti = 0; ti < ntiles; ++ti) {
+            const int f = ti * kFT + fl;
+            const bool valid = f < Fc;
+            const int64_t row = ((int64_t)g * Fs + pf0 + f) * users + u;
+            for (int jb = 0; jb < njobs; ++jb) {
+                const int slot = jb == 0 ? 0 : 1 + (jb - 1) / SP, q = jb == 0 ? 0 : (jb - 1) % SP;
+                double2* out = PG + (row * S + slot) * (int64_t)m * m;
+                if (jb == 0) {
+                    if (h == 0) epi_job<MP, 0, 0>(ec, cnt, valid, out, m);
+                    else epi_job<MP, 1, 0>(ec, cnt, valid, out, m);
+                } else if (!SPLIT) {
+                    if (h == 0) epi_job<MP, 0, 3>(ec, cnt, valid, out, m);
+                    else epi_job<MP, 1, 3>(ec, cnt, valid, out, m);
+                } else if (q == 0) {
+                    if (h == 0) epi_job<MP, 0, 1>(ec, cnt, valid, out, m);
+                    else epi_job<MP, 1, 1>(ec, cnt, valid, out, m);
+                } else {
+                    if (h == 0) epi_job<MP, 0, 2>(ec, cnt, valid, out, m);
+                    else epi_job<MP, 1, 2>(ec, cnt, valid, out, m);
+                }
             }
         }
     }
@@ -647,24 +569,22 @@ cudaError_t launch_rgram(const Topo& t, int64_t ngroups, int Fc, int64_t f0, int
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 grid(t.users(), (unsigned)ngroups);
-    static const bool ws = [] {
-        // default: dedicated MMA / TMA warps (C4 single lane: 404 vs 650 ms for the inline-control layout,
-        // whose MMA issue serialises with thread 0's own Gram work); GWT_RGRAM_WS=0 selects the inline layout
-        const char* v = std::getenv("GWT_RGRAM_WS");
-        return !(v && std::atoi(v) == 0);
+    static const bool split = [] {
+        const char* v = std::getenv("GWT_RGRAM_SPLIT");
+        return v && std::atoi(v) != 0;
     }();
-#define GWT_RG(MPV, WSV)                                                                                            \
+#define GWT_RG(MPV, SPV)                                                                                            \
     do {                                                                                                            \
-        e = cudaFuncSetAttribute(k_rgram<MPV, WSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);      \
+        e = cudaFuncSetAttribute(k_rgram<MPV, SPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);      \
         if (e != cudaSuccess) return e;                                                                             \
-        k_rgram<MPV, WSV><<<grid, WSV ? kRgThreadsWS : kRgThreads, c.smem, st>>>(                                   \
-            t, c, Fc, ntiles, pf0, Fs, (const unsigned char*)Bready, (const unsigned char*)Eready, PG);           \
+        k_rgram<MPV, SPV><<<grid, kRgThreads, c.smem, st>>>(t, c, Fc, ntiles, pf0, Fs, (const unsigned char*)Bready, \
+                                                            (const unsigned char*)Eready, PG);                       \
     } while (0)
     if (t.m == 8) {
-        if (ws) GWT_RG(8, true);
+        if (split) GWT_RG(8, true);
         else GWT_RG(8, false);
     } else {
-        if (ws) GWT_RG(4, true);
+        if (split) GWT_RG(4, true);
         else GWT_RG(4, false);
     }
 #undef GWT_RG
