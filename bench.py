@@ -160,20 +160,40 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # algorithmic cost model
 
-def sinr_costs(cfg):
-    """Per-kernel algorithmic (flops, pipe, bytes) of one SINR step over all of cfg's groups.
+def tc_path(cfg):
+    """Mirror of capi.cu:tc_sinr_shape — c64, m in {4, 8}, p % 4 == 0, m n >= 256 (C3, C4, C5) run stage R
+    fused with the pair Grams on the tensor cores (k_esplit + k_rgram), then k_sinr_users (PG mode) for
+    m > 4 or the thread-per-user kernel for m <= 4."""
+    return cfg.dtype == "c64" and cfg.m in (4, 8) and cfg.p % 4 == 0 and cfg.p <= 32 and cfg.m * cfg.n >= 256
 
-    rebuild (stage R, per (link, subcarrier)): 8(mnp + Pp) flops; bytes = the H~ write m n b_c.
-    solve (stage S, per (user, subcarrier)): bytes = the user's J H~ reads J m n b_c + L binary64 SINR out
-    (§8(d)); flops = serving Gram (fp64, Hermitian half) + interference products H~_kij V'_k (n m L per
-    interferer) + the m x m eig / covariance / Cholesky / solves (counted as a Householder + QL eig,
-    ~(16/3 + 6 + 4) m^3 real flops, and 8(2 m^2 L + m^3/3 + L m^2 / 2))."""
+
+def sinr_costs(cfg):
+    """Per-stage algorithmic (flops, pipe, bytes) of one SINR step over all of cfg's groups.
+
+    CUDA-core path (C1, C2):
+      rebuild (stage R, per (link, subcarrier)): 8(mnp + Pp) flops; bytes = the H~ write m n b_c.
+      solve (stage S, per (user, subcarrier)): bytes = the user's J H~ reads J m n b_c + L binary64 SINR out
+      (§8(d)); flops = serving Gram (fp64, Hermitian half) + interference products (n m L per interferer)
+      + the m x m eig / covariance / Cholesky / solves (a Householder + QL eig, ~(16/3 + 6 + 4) m^3 real
+      flops, and 8(2 m^2 L + m^3/3 + L m^2 / 2)).
+    Tensor-core path (C3-C5): H~ never reaches HBM.
+      rgram (k_esplit + k_rgram, per (user, subcarrier)): the binding work is the binary64 Gram epilogue,
+      8 [m(m+1)/2 n + (J-1) m^2 n] fp64 flops (serving Gram, Hermitian half, + the pair Grams); the user's
+      rebuild 8 J (mnp + Pp) runs on tcgen05 (3xTF32) beside it (reported as tensor_flops). Bytes: the
+      pair-Gram write J m^2 16 (the factors are read once per subcarrier tile, amortised).
+      solve (k_sinr_users PG mode): the same m x m work, bytes = the PG read J m^2 16 + L binary64 out."""
     J, m, n, p, P, L = cfg.J, cfg.m, cfg.n, cfg.p, cfg.P, cfg.L
     bc = 8 if cfg.dtype == "c64" else 16
     links, users, F, g = cfg.G, cfg.G // 2, cfg.F, cfg.groups
+    small = int((16 / 3 + 6 + 4) * m ** 3) + 8 * (2 * m * m * L + m ** 3 // 3 + L * m * m // 2)
+    if tc_path(cfg):
+        gram = 8 * ((m * (m + 1) // 2) * n + (J - 1) * m * m * n)
+        pgb = J * m * m * 16
+        rg = (gram * users * F * g, "fp64", pgb * users * F * g)
+        solve = ((small + 8 * (J - 1) * m * m * L) * users * F * g, "fp64", (pgb + 8 * L) * users * F * g)
+        return dict(rgram=rg, solve=solve, tensor_flops=8 * J * (m * n * p + P * p) * users * F * g)
     rebuild = (8 * (m * n * p + P * p) * links * F * g, "fp32" if bc == 8 else "fp64", bc * m * n * links * F * g)
-    per_eval = (8 * (m * (m + 1) // 2) * n + 8 * (J - 1) * n * m * L + int((16 / 3 + 6 + 4) * m ** 3)
-                + 8 * (2 * m * m * L + m ** 3 // 3 + L * m * m // 2))
+    per_eval = 8 * (m * (m + 1) // 2) * n + 8 * (J - 1) * n * m * L + small
     solve = (per_eval * users * F * g, "fp64", (J * m * n * bc + 8 * L) * users * F * g)
     return dict(rebuild=rebuild, solve=solve)
 
@@ -440,10 +460,15 @@ def run_gpu_config(gw, O, torch, cfg, ctx, dev, stream, flush, rank, world, step
     costs = sinr_costs(cfg)
     scale = ng / cfg.groups
     stages = {}
-    for name, ms_k in (("rebuild", st[4]), ("solve", st[5] + st[6])):
+    split = (("rgram", st[4] + st[5]), ("solve", st[6])) if tc_path(cfg) else (("rebuild", st[4]), ("solve", st[5] + st[6]))
+    for name, ms_k in split:
         fl, pipe, by = costs[name]
         r = binding_roofline(fl * scale, pipe, by * scale, ms_k, hbm, peaks_t)
         r.update(ms=round(float(ms_k), 4), alg_bytes=int(by * scale), alg_flops=int(fl * scale))
+        if name == "rgram":
+            tf = costs["tensor_flops"] * scale
+            r.update(tensor_flops=int(tf), tensor_tflops=tf / (ms_k * 1e-3) / 1e12 if ms_k > 0 else None,
+                     tensor_basis="stage R on tcgen05 kind::tf32 (3xTF32), 8 J (mnp + Pp) per (user, subcarrier)")
         stages[name] = r
     res["stages"] = stages
 
@@ -551,7 +576,8 @@ def main(argv=None):
     stages = r["stages"]
     dom = max(stages, key=lambda k: stages[k]["ms"])
     roof = dict(stages[dom])
-    kern = {"rebuild": "k_rebuild*", "solve": "k_sinr_solve*/k_small*"}
+    kern = {"rebuild": "k_rebuild*", "rgram": "k_rgram (+ k_esplit, k_bsplit)",
+            "solve": "k_sinr_users (PG mode)" if tc_path(cfg) else "k_pair_gram*/k_small*"}
     traffic = None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))

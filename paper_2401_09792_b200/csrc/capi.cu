@@ -655,6 +655,16 @@ struct StageEvents {
     }
 };
 
+// the tensor-core rebuild + pair-Gram path (k_rgram.cu) for large cores (m n >= 256: C3, C4, C5); the small
+// C2 cores (m n = 96) measured faster on the CUDA-core rebuild + pair-Gram kernels (0.54 vs 0.63 ms)
+bool tc_sinr_shape(const Topo& t) {
+    static const bool force = [] {
+        const char* p = std::getenv("GWT_SINR_PATH");
+        return p && std::strcmp(p, "tc") == 0;
+    }();
+    return rgram_fits(t) && (force || t.m * t.n >= 256);
+}
+
 // Generic device pipeline (any scope) for ngroups groups on device pointers, on solver/SINR lane
 // `lane` (stream st + its workspace): rebuild -> pair Grams per subcarrier chunk, then ONE eig+MMSE
 // launch per pair-Gram block. timing: per-stage CUDA events (host waits at the end).
@@ -682,7 +692,7 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
         const bool users_path = scope == GWT_SCOPE_PAPER && sinr_users_fits(t, cs) && !force_pg && (t.m > 4 || force_users);
         const bool rg = !users_path && scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
         // c64 paper scope, m in {4, 8}: rebuild fused with the pair Grams on the tensor cores (k_rgram.cu)
-        const bool tc_path = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !cod && rgram_fits(t) &&
+        const bool tc_path = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !cod && tc_sinr_shape(t) &&
                              !(path && (std::strcmp(path, "users") == 0 || std::strcmp(path, "pg") == 0 ||
                                         std::strcmp(path, "rg") == 0));
         if (tc_path) {
@@ -824,7 +834,10 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     const char* pl = std::getenv("GWT_SINR_PIPELINE");
     const int64_t nch = std::min<int64_t>(ngroups, pl ? std::max(1, std::atoi(pl)) : 4);
     const char* dl = std::getenv("GWT_SINR_DEV_LANES");
-    const int64_t ndev = std::min<int64_t>(ngroups, dl ? std::max(1, std::atoi(dl)) : 2);
+    // two stream lanes overlap the CUDA-core rebuild of one group half with the Gram / eig stages of the
+    // other; the tensor-core path keeps every SM busy with one lane (C4: 710 ms single lane vs 839 ms)
+    const bool tc_shape = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !coeffs && tc_sinr_shape(t);
+    const int64_t ndev = std::min<int64_t>(ngroups, dl ? std::max(1, std::atoi(dl)) : (tc_shape ? 1 : 2));
     if (mem == GWT_MEM_DEVICE && !fused0 && ndev > 1 && !coeffs) {
         // device-resident: group chunks on ndev stream lanes so the FP32-issue-bound rebuild of one
         // chunk overlaps the memory/fp64-bound Gram and small-matrix stages of the others
@@ -869,7 +882,7 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         // the kernels while the kernels keep the device-resident 2-lane concurrency (4 compute lanes of
         // the older scheme contended: 0.38 vs 0.36 ms device time on C2)
         const char* nl = std::getenv("GWT_SINR_LANES");
-        const int NS = (int)std::min<int64_t>(nl ? std::max(1, std::atoi(nl)) : 2, nch);
+        const int NS = (int)std::min<int64_t>(nl ? std::max(1, std::atoi(nl)) : (tc_shape ? 1 : 2), nch);
         while ((int)ctx->lanes.size() < NS - 1) {
             gwt_ctx::Lane ln;
             ck(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking), "cudaStreamCreate");
