@@ -106,50 +106,67 @@ __global__ void __launch_bounds__(2 * kFT) k_esplit(Topo t, RgCfg c, int Fc, int
                                                     const double* __restrict__ freqs, unsigned char* __restrict__ Eready) {
     extern __shared__ __align__(16) unsigned char es_smem[];
     float2* ph = reinterpret_cast<float2*>(es_smem);  // [P][kFT]
-    float2* sC = ph + (size_t)t.P * kFT;               // [PQ][P] (C_l column-major P x p)
+    float2* sC = ph + (size_t)t.P * kFT;               // [P][PQ] (C_l transposed: q contiguous per tap)
     const int ti = blockIdx.x, l = blockIdx.y;
     const int64_t g = blockIdx.z, gl = g * t.links() + l;
     const int P = t.P, tid = threadIdx.x;
     const float2* Cl = Cd + gl * (int64_t)P * PQ;
     const double* tl = tau + gl * P;
-    for (int e = tid; e < P * PQ; e += 2 * kFT) sC[e] = Cl[e];
+    for (int e = tid; e < P * PQ; e += 2 * kFT) {
+        const int q = e / P, r = e % P;  // coalesced read of the column-major P x p factor
+        sC[r * PQ + q] = Cl[e];
+    }
     for (int e = tid; e < P * kFT; e += 2 * kFT) {
         const int r = e / kFT, f = ti * kFT + e % kFT;
         ph[e] = f < Fc ? conj_coeff<float>(freqs[f0 + f], tl[r]) : make_float2(0.f, 0.f);
     }
     __syncthreads();
-    // thread (subcarrier fl, half qh): E(q, f) for q in [qh*PQ/2, (qh+1)*PQ/2)
-    constexpr int QH = PQ / 2;
-    const int fl = tid % kFT, qh = tid / kFT;
-    float2 e[QH];
+    // thread (subcarrier pair fp = (fl, fl + 64), q quarter qq): E(q, f) for q in [qq*QQ, qq*QQ + QQ);
+    // per tap: 2 phasor loads and QQ/2 16-byte broadcast loads of C feed 8 QQ FFMA
+    constexpr int QQ = PQ / 4;
+    const int fl = tid % (kFT / 2), qq = tid / (kFT / 2);
+    float2 e0[QQ], e1[QQ];
 #pragma unroll
-    for (int q = 0; q < QH; ++q) e[q] = make_float2(0.f, 0.f);
+    for (int q = 0; q < QQ; ++q) e0[q] = e1[q] = make_float2(0.f, 0.f);
 #pragma unroll 4
     for (int r = 0; r < P; ++r) {
-        const float2 v = ph[r * kFT + fl];
+        const float2 v0 = ph[r * kFT + fl], v1 = ph[r * kFT + fl + kFT / 2];
+        const float2* cr = sC + r * PQ + qq * QQ;
+        if constexpr (QQ % 2 == 0) {
 #pragma unroll
-        for (int q = 0; q < QH; ++q) cfma(e[q], sC[(qh * QH + q) * P + r], v);
+            for (int q = 0; q < QQ; q += 2) {
+                const float4 c2 = *reinterpret_cast<const float4*>(cr + q);
+                const float2 ca = make_float2(c2.x, c2.y), cb = make_float2(c2.z, c2.w);
+                cfma(e0[q], ca, v0);
+                cfma(e1[q], ca, v1);
+                cfma(e0[q + 1], cb, v0);
+                cfma(e1[q + 1], cb, v1);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < QQ; ++q) {
+                const float2 ca = cr[q];
+                cfma(e0[q], ca, v0);
+                cfma(e1[q], ca, v1);
+            }
+        }
     }
     unsigned char* hi = Eready + ((size_t)gl * ntiles + ti) * 2 * c.TA;
     unsigned char* lo = hi + c.TA;
-    // K columns: [0, p) Er, [p, 2p) Ei; this thread owns q in [qh*QH, qh*QH + QH)
+    // K columns: [0, p) Er, [p, 2p) Ei
 #pragma unroll
-    for (int part = 0; part < 2; ++part) {
+    for (int q = 0; q < QQ; ++q) {
+        const int k = qq * QQ + q;
+        const float v[4] = {e0[q].x, e0[q].y, e1[q].x, e1[q].y};
+        const int rows[4] = {fl, fl, fl + kFT / 2, fl + kFT / 2};
+        const int ks[4] = {k, PQ + k, k, PQ + k};
 #pragma unroll
-        for (int z4 = 0; z4 < QH; z4 += 2) {
-            // two q -> write as float2 pairs (K-contiguous within a 16-byte core row when aligned)
-#pragma unroll
-            for (int zz = 0; zz < 2; ++zz) {
-                const int q = qh * QH + z4 + zz;
-                if (z4 + zz < QH) {
-                    const float v = part == 0 ? e[z4 + zz].x : e[z4 + zz].y;
-                    float h, rr;
-                    tc::split_tf32_rn(v, h, rr);
-                    const uint32_t o = kmaj(fl, part * PQ + q, c.sbo_a);
-                    *reinterpret_cast<float*>(hi + o) = h;
-                    *reinterpret_cast<float*>(lo + o) = rr;
-                }
-            }
+        for (int z = 0; z < 4; ++z) {
+            float h, rr;
+            tc::split_tf32_rn(v[z], h, rr);
+            const uint32_t o = kmaj(rows[z], ks[z], c.sbo_a);
+            *reinterpret_cast<float*>(hi + o) = h;
+            *reinterpret_cast<float*>(lo + o) = rr;
         }
     }
 }

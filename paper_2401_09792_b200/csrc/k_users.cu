@@ -44,10 +44,87 @@ template <int MP> __device__ __forceinline__ double seg_sum(double v) {
 
 __device__ __forceinline__ double2 dmul(double2 a, double2 b) { return cmul(a, b); }
 
+// binary64 reciprocal: MUFU seed + two Newton steps (no division sequence on the QL's serial chain)
+__device__ __forceinline__ double frcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(y, fma(-x, y, 1.0), y);
+    return fma(y, fma(-x, y, 1.0), y);
+}
+
+// Implicit QL (tql2 with Wilkinson shift) on the real tridiagonal (d, e); this lane rotates RL rows of Z
+// (rows row0 .. row0 + RL - 1). `valid` lanes only; every lane of the warp must call it (warp votes).
+template <int MP, int RL>
+__device__ __forceinline__ void ql_rows(double (&dg)[MP], double (&eo)[MP], double (&z)[RL][MP], bool valid) {
+#pragma unroll
+    for (int l = 0; l < MP - 1; ++l) {
+        for (int iter = 0; iter < 40; ++iter) {
+            int mm = MP - 1;
+#pragma unroll
+            for (int k = MP - 2; k >= l; --k) {
+                const double dd = fabs(dg[k]) + fabs(dg[k + 1]);
+                if (fabs(eo[k]) <= DBL_EPSILON * dd) mm = k;
+            }
+            const bool go = valid && mm != l;
+            if (!__any_sync(0xffffffffu, go)) break;
+            if (go) {
+                double g = (dg[l + 1] - dg[l]) * (0.5 * frcp(eo[l]));
+                const double t1 = fma(g, g, 1.0);
+                double rr = t1 * rsqrt(t1);
+                double dm = dg[MP - 1];
+#pragma unroll
+                for (int k = l + 1; k < MP - 1; ++k)
+                    if (k == mm) dm = dg[k];
+                g = dm - dg[l] + eo[l] * frcp(g + (g >= 0.0 ? rr : -rr));
+                double s = 1.0, c = 1.0, p = 0.0;
+                bool brk = false;
+#pragma unroll
+                for (int i = MP - 2; i >= l; --i) {
+                    if (i < mm && !brk) {
+                        const double f = s * eo[i], b = c * eo[i];
+                        const double t2 = f * f + g * g;
+                        const double inv = rsqrt(t2);
+                        rr = t2 * inv;
+                        eo[i + 1] = rr;
+                        if (t2 == 0.0) {
+                            dg[i + 1] -= p;
+#pragma unroll
+                            for (int k = l; k < MP; ++k)
+                                if (k == mm) eo[k] = 0.0;
+                            brk = true;
+                        } else {
+                            s = f * inv;
+                            c = g * inv;
+                            g = dg[i + 1] - p;
+                            rr = (dg[i] - g) * s + 2.0 * c * b;
+                            p = s * rr;
+                            dg[i + 1] = g + p;
+                            g = c * rr - b;
+#pragma unroll
+                            for (int q = 0; q < RL; ++q) {
+                                const double zf = z[q][i + 1];
+                                z[q][i + 1] = s * z[q][i] + c * zf;
+                                z[q][i] = c * z[q][i] - s * zf;
+                            }
+                        }
+                    }
+                }
+                if (!brk) {
+                    dg[l] -= p;
+                    eo[l] = g;
+#pragma unroll
+                    for (int k = l + 1; k < MP; ++k)
+                        if (k == mm) eo[k] = 0.0;
+                }
+            }
+        }
+    }
+}
+
 // shared-memory layout of one slice (all offsets in bytes, 16-byte aligned)
 struct SliceLayout {
     int U, MP, L, n, J, tsz;  // tsz = sizeof(complex T)
-    int a_off, z_off, u_off, lam_off, tau_off, v_off, bytes;
+    int a_off, z_off, u_off, lam_off, tau_off, v_off, tri_off, bytes;
     __host__ __device__ void init(int U_, int MP_, int L_, int n_, int J_, int tsz_) {
         U = U_; MP = MP_; L = L_; n = n_; J = J_; tsz = tsz_;
         int o = 0;
@@ -59,6 +136,8 @@ struct SliceLayout {
         lam_off = o; o += U * MP * 8;                      // eigenvalues by rank
         tau_off = o; o += U * MP * 16;                     // Householder scalars
         v_off = o; o += J * n * L * tsz;                   // anchor precoders V'_k [k][y][l]
+        o = (o + 15) & ~15;
+        tri_off = o; o += U * 2 * MP * 8;                  // tridiagonal (d, e) -> eigenvalues (QL phase)
         bytes = (o + 15) & ~15;
     }
 };
@@ -143,9 +222,12 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     __syncwarp();
     }
     // keep my row of A when the serving term of Q is A itself (L == m)
-    double2 arow[MP];
+    // (PG mode re-reads it from PG in phase 3 instead of keeping it live through the eig)
+    double2 arow[PGM ? 1 : MP];
+    if constexpr (!PGM) {
 #pragma unroll
-    for (int c = 0; c < MP; ++c) arow[c] = sA[r * (MP + 1) + c];
+        for (int c = 0; c < MP; ++c) arow[c] = sA[r * (MP + 1) + c];
+    }
 
     // ---------------- phase 1b: Householder tridiagonalisation (zhetd2, lower), lane r owns row r
     double dg[MP], eo[MP];  // tridiagonal (replicated in every lane of the user)
@@ -216,73 +298,56 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     eo[MP - 1] = 0.0;
     // the last step (i = MP-2) may leave a complex phase only through tau (|1 - tau| = 1): e is real.
 
-    // ---------------- phase 1c: implicit QL (tql2 / tqli) on (dg, eo); lane r rotates row r of Z
-    double z[MP];
+    // ---------------- phase 1c: implicit QL (tql2) on (dg, eo). The scalar recurrence is serial, so it runs
+    // with 2 lanes per user (each rotating 4 rows of Z) on the first 2 U spc threads instead of being
+    // replicated over the user's 8 lanes: 4x fewer issued instructions for the same latency chain.
+    {
+        double* stri = reinterpret_cast<double*>(sbase + lay.tri_off) + u * 2 * MP;
+        if (r == 0) {
 #pragma unroll
-    for (int c = 0; c < MP; ++c) z[c] = c == r ? 1.0 : 0.0;
-#pragma unroll
-    for (int l = 0; l < MP - 1; ++l) {
-        for (int iter = 0; iter < 40; ++iter) {
-            int mm = MP - 1;
-#pragma unroll
-            for (int k = MP - 2; k >= l; --k) {
-                const double dd = fabs(dg[k]) + fabs(dg[k + 1]);
-                if (fabs(eo[k]) <= DBL_EPSILON * dd) mm = k;
-            }
-            const bool go = mm != l;
-            if (!__any_sync(0xffffffffu, go)) break;
-            if (go) {
-                double g = (dg[l + 1] - dg[l]) / (2.0 * eo[l]);
-                double rr = sqrt(g * g + 1.0);
-                double dm = dg[MP - 1];
-#pragma unroll
-                for (int k = l + 1; k < MP - 1; ++k)
-                    if (k == mm) dm = dg[k];
-                g = dm - dg[l] + eo[l] / (g + (g >= 0.0 ? rr : -rr));
-                double s = 1.0, c = 1.0, p = 0.0;
-                bool brk = false;
-#pragma unroll
-                for (int i = MP - 2; i >= l; --i) {
-                    if (i < mm && !brk) {
-                        const double f = s * eo[i], b = c * eo[i];
-                        const double t2 = f * f + g * g;
-                        const double inv = rsqrt(t2);  // one MUFU-seeded reciprocal square root, no divisions
-                        rr = t2 * inv;
-                        eo[i + 1] = rr;
-                        if (t2 == 0.0) {
-                            dg[i + 1] -= p;
-#pragma unroll
-                            for (int k = l; k < MP; ++k)
-                                if (k == mm) eo[k] = 0.0;
-                            brk = true;
-                        } else {
-                            s = f * inv;
-                            c = g * inv;
-                            g = dg[i + 1] - p;
-                            rr = (dg[i] - g) * s + 2.0 * c * b;
-                            p = s * rr;
-                            dg[i + 1] = g + p;
-                            g = c * rr - b;
-                            const double zf = z[i + 1];
-                            z[i + 1] = s * z[i] + c * zf;
-                            z[i] = c * z[i] - s * zf;
-                        }
-                    }
-                }
-                if (!brk) {
-                    dg[l] -= p;
-                    eo[l] = g;
-#pragma unroll
-                    for (int k = l + 1; k < MP; ++k)
-                        if (k == mm) eo[k] = 0.0;
-                }
+            for (int k = 0; k < MP; ++k) {
+                stri[k] = dg[k];
+                stri[MP + k] = eo[k];
             }
         }
+        __syncthreads();
+        constexpr int LQ = 2, RL = MP / LQ;
+        const int nql = spc * U * LQ;
+        if (tid < ((nql + 31) & ~31)) {
+            const bool qv = tid < nql;
+            const int qi = qv ? tid : 0;
+            const int qs = qi / (U * LQ), qu = (qi / LQ) % U, qh = qi % LQ;
+            unsigned char* qb = smem_raw + (size_t)qs * lay.bytes;
+            double* qt = reinterpret_cast<double*>(qb + lay.tri_off) + qu * 2 * MP;
+            double d[MP], e[MP];
+#pragma unroll
+            for (int k = 0; k < MP; ++k) {
+                d[k] = qt[k];
+                e[k] = qt[MP + k];
+            }
+            double zq[RL][MP];
+#pragma unroll
+            for (int q = 0; q < RL; ++q)
+#pragma unroll
+                for (int c = 0; c < MP; ++c) zq[q][c] = c == qh * RL + q ? 1.0 : 0.0;
+            ql_rows<MP, RL>(d, e, zq, qv);
+            __syncwarp();
+            if (qv) {
+                double* zs = reinterpret_cast<double*>(qb + lay.z_off) + qu * MP * (MP + 1);
+#pragma unroll
+                for (int q = 0; q < RL; ++q)
+#pragma unroll
+                    for (int c = 0; c < MP; ++c) zs[(qh * RL + q) * (MP + 1) + c] = zq[q][c];
+                if (qh == 0)
+#pragma unroll
+                    for (int k = 0; k < MP; ++k) qt[k] = d[k];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < MP; ++k) dg[k] = stri[k];
     }
     // ---------------- phase 1d: back-transform, lane j = eigenvector j: u = H_0 ... H_{MP-2} z_j
-#pragma unroll
-    for (int c = 0; c < MP; ++c) sZ[r * (MP + 1) + c] = z[c];
-    __syncwarp();
     double2 uv[MP];
 #pragma unroll
     for (int a = 0; a < MP; ++a) uv[a] = make_double2(sZ[a * (MP + 1) + r], 0.0);
@@ -371,7 +436,15 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     double2 q[MP];
     if (L == m) {
 #pragma unroll
-        for (int c = 0; c < MP; ++c) q[c] = arow[c];
+        for (int c = 0; c < MP; ++c) {
+            if constexpr (PGM) {
+                double2 a = (active && r < m && c < m) ? Pu[r + m * c] : make_double2(0.0, 0.0);
+                if (c == r) a.y = 0.0;
+                q[c] = a;
+            } else {
+                q[c] = arow[c];
+            }
+        }
     } else {
 #pragma unroll
         for (int c = 0; c < MP; ++c) q[c] = make_double2(0.0, 0.0);
