@@ -13,7 +13,7 @@ CUO := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU))
 HDR := $(wildcard $(SRC)/*.cuh) include/gwt_b200.h
 
 HOSTLIB := $(PKG)/_build/libgwtucker_b200.so
-HOSTSRC := $(PKG)/host/src/gwtucker_b200.cpp
+HOSTSRC := $(PKG)/host/src/gwtucker_b200.cpp $(PKG)/host/src/archive_b200.cpp
 HOSTHDR := $(wildcard $(PKG)/host/include/gwtucker/*.hpp)
 DROPIN := $(PKG)/_build/test_dropin
 

@@ -690,11 +690,9 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
         // (K2 + thread-per-user K3) measured faster (C2: 0.21 vs 0.31 ms). GWT_SINR_PATH=users|pg forces one.
         const bool force_users = path && std::strcmp(path, "users") == 0, force_pg = path && std::strcmp(path, "pg") == 0;
         const bool users_path = scope == GWT_SCOPE_PAPER && sinr_users_fits(t, cs) && !force_pg && (t.m > 4 || force_users);
-        const bool rg = !users_path && scope == GWT_SCOPE_PAPER && rebuild_pg_fits(t, cs) && path && std::strcmp(path, "rg") == 0;
         // c64 paper scope, m in {4, 8}: rebuild fused with the pair Grams on the tensor cores (k_rgram.cu)
         const bool tc_path = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !cod && tc_sinr_shape(t) &&
-                             !(path && (std::strcmp(path, "users") == 0 || std::strcmp(path, "pg") == 0 ||
-                                        std::strcmp(path, "rg") == 0));
+                             !(path && (std::strcmp(path, "users") == 0 || std::strcmp(path, "pg") == 0));
         if (tc_path) {
             const int64_t Ft = std::min<int64_t>(F, 256);
             double2* PGt = (double2*)ctx->lws(lane, WS_PG, 16 * ngroups * Ft * users * S * t.m * t.m);
@@ -743,7 +741,7 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
                 for (auto& ev : evs) cudaEventDestroy(ev);
             return;
         }
-        void* H = rg ? nullptr : ctx->lws(lane, WS_H, cs * ngroups * Fc * links * t.m * t.n);
+        void* H = ctx->lws(lane, WS_H, cs * ngroups * Fc * links * t.m * t.n);
         // pair Grams for a block of Fs subcarriers: [g][Fs][users][S][m*m] (fp64), Fs bounded by ~2 GB
         const int64_t per_f_pg = (int64_t)ngroups * users * (16LL * S * t.m * t.m + 8LL * (((t.L + 1) & ~1) + 2 * t.m * t.L));
         const int64_t Fs = std::max<int64_t>(Fc, std::min<int64_t>(F, (int64_t)(2ll << 30) / std::max<int64_t>(per_f_pg, 1)) / Fc * Fc);
@@ -774,15 +772,9 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
                 kind.push_back(2);
             }
         }
-        // rg: paper scope with small groups -> rebuild + pair Grams fused in shared memory (H~ never in HBM)
         for (int64_t F0 = 0; !users_path && F0 < F; F0 += Fs) {
             const int64_t fs = std::min(Fs, F - F0);
-            if (rg) {
-                ctx->launched(launch_rebuild_pg<T>(t, (int)ngroups, (int)fs, F0, F, 0, fs, Cd, Gd, taud, fd, cod, PG, st));
-                rec();
-                kind.push_back(1);
-            }
-            for (int64_t f0 = F0; !rg && f0 < F0 + fs; f0 += Fc) {
+            for (int64_t f0 = F0; f0 < F0 + fs; f0 += Fc) {
                 const int fc = (int)std::min(Fc, F0 + fs - f0);
                 ctx->launched(launch_rebuild<T>(t, (int)ngroups, fc, f0, F, Cd, Gd, taud, fd, cod, H, st));
                 rec();
@@ -829,8 +821,6 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     double *sd = sinr, *sgd = signal;
     int* std_ = (int*)status;
     const int64_t out_rows = ngroups * F * users;
-    const char* path0 = std::getenv("GWT_SINR_PATH");
-    const bool fused0 = scope == GWT_SCOPE_PAPER && t.users() <= 128 && path0 && std::strcmp(path0, "fused") == 0;
     const char* pl = std::getenv("GWT_SINR_PIPELINE");
     const int64_t nch = std::min<int64_t>(ngroups, pl ? std::max(1, std::atoi(pl)) : 4);
     const char* dl = std::getenv("GWT_SINR_DEV_LANES");
@@ -838,7 +828,7 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     // other; the tensor-core path keeps every SM busy with one lane (C4: 710 ms single lane vs 839 ms)
     const bool tc_shape = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !coeffs && tc_sinr_shape(t);
     const int64_t ndev = std::min<int64_t>(ngroups, dl ? std::max(1, std::atoi(dl)) : (tc_shape ? 1 : 2));
-    if (mem == GWT_MEM_DEVICE && !fused0 && ndev > 1 && !coeffs) {
+    if (mem == GWT_MEM_DEVICE && ndev > 1 && !coeffs) {
         // device-resident: group chunks on ndev stream lanes so the FP32-issue-bound rebuild of one
         // chunk overlaps the memory/fp64-bound Gram and small-matrix stages of the others
         while ((int)ctx->lanes.size() < ndev - 1) {
@@ -876,7 +866,7 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         return;
     }
     const char* cpp = std::getenv("GWT_SINR_COPY_STREAMS");
-    if (mem == GWT_MEM_HOST && !fused0 && nch > 1 && !(cpp && std::atoi(cpp) == 0)) {
+    if (mem == GWT_MEM_HOST && nch > 1 && !(cpp && std::atoi(cpp) == 0)) {
         // host buffers: group chunks flow through three engines — one H2D copy stream, NS compute lanes,
         // one D2H copy stream — chained by per-chunk events, so PCIe traffic in both directions overlaps
         // the kernels while the kernels keep the device-resident 2-lane concurrency (4 compute lanes of
@@ -953,7 +943,7 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         ctx->stage_ms[0] = tm.between(0, 6);
         return;
     }
-    if (mem == GWT_MEM_HOST && !fused0 && nch > 1) {
+    if (mem == GWT_MEM_HOST && nch > 1) {
         // host buffers: 4 group chunks on 4 stream lanes (GWT_SINR_PIPELINE / GWT_SINR_LANES), each chunk H2D -> device
         // pipeline -> D2H on its lane, so copies in both directions overlap the other chunks' kernels
         const char* nl = std::getenv("GWT_SINR_LANES");
@@ -1036,40 +1026,7 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         tm.mark(5);
     }
     double ms_r = 0, ms_p = 0, ms_s = 0;
-    const char* path = std::getenv("GWT_SINR_PATH");
-    // default: rebuild -> pair Grams -> eig/MMSE (fastest measured on C2);
-    // GWT_SINR_PATH=fused selects the shared-memory fused rebuild+Gram path (paper scope only)
-    // default: rebuild -> pair Grams -> eig/MMSE (fastest measured on C2);
-    // GWT_SINR_PATH=fused selects the shared-memory fused rebuild+Gram kernels (paper scope).
-    const bool fused = scope == GWT_SCOPE_PAPER && t.users() <= 128 && path && std::strcmp(path, "fused") == 0;
-    if (fused) {
-        // rebuild + Grams fused (H~ stays in shared memory), then the per-group small-matrix solve
-        std::vector<double> fh(coeffs ? 0 : F);
-        if (!coeffs) {
-            if (mem == GWT_MEM_HOST) std::memcpy(fh.data(), freqs, 8 * F);
-            else ck(cudaMemcpy(fh.data(), freqs, 8 * F, cudaMemcpyDeviceToHost), "freqs");
-        }
-        int uniform = coeffs ? 0 : 1;
-        const double df = (!coeffs && F > 1) ? fh[1] - fh[0] : 0.0;
-        for (int64_t f = 1; uniform && f < F; ++f)
-            if (std::fabs(fh[f] - fh[0] - df * f) > 1e-9 * std::max(std::fabs(df) * F, 1.0)) uniform = 0;
-        const int64_t per_f = 16LL * ngroups * users * t.J * t.m * t.m;
-        const int64_t Fc = std::max<int64_t>(16, std::min<int64_t>(F, (int64_t)(48ll << 20) / std::max<int64_t>(per_f, 1)));
-        double2* GU = (double2*)ctx->ws(WS_PG, 16 * ngroups * std::min(Fc, F) * users * t.J * t.m * t.m);
-        tm.mark(8);
-        for (int64_t f0 = 0; f0 < F; f0 += Fc) {
-            const int fc = (int)std::min(Fc, F - f0);
-            ctx->launched(launch_sinr_fused<T>(t, (int)ngroups, fc, f0, F, topo->noise_std, Cd, Gd, taud, fd, uniform,
-                                               df, cod, GU, sd, sgd, std_, st),
-                          2);
-        }
-        tm.mark(9);
-        ck(cudaEventSynchronize(ctx->ev[9]), "sync");
-        ms_r = tm.between(8, 9);
-    } else {
-        sinr_device<T>(ctx, 0, st, t, topo, ngroups, Cd, Gd, taud, fd, cod, F, scope, sd, sgd, std_, true, ms_r, ms_p,
-                       ms_s);
-    }
+    sinr_device<T>(ctx, 0, st, t, topo, ngroups, Cd, Gd, taud, fd, cod, F, scope, sd, sgd, std_, true, ms_r, ms_p, ms_s);
     if (mem == GWT_MEM_HOST) {
         tm.mark(12);
         ck(cudaMemcpyAsync(sinr, sd, 8 * out_rows * t.L, cudaMemcpyDeviceToHost, st), "D2H sinr");

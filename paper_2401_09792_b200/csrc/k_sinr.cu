@@ -490,64 +490,6 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// K2 (paper scope, c64), persistent and double-buffered: each CTA walks (group, subcarrier) slices
-// with stride gridDim.x; slice it+1's H~(f) block (contiguous links*m*n complex64) is fetched with
-// cp.async into a raw buffer while slice it is converted once to binary64 and reduced into the J
-// pair Grams of every user (one thread per Gram entry).
-template <int M>
-__global__ void __launch_bounds__(256) k_pair_gram_pipe(Topo t, int Fc, int64_t f0, int64_t Ftot, int64_t nslices,
-                                                        const float2* __restrict__ H, double2* __restrict__ PG) {
-    constexpr int MM = M * M;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int J = t.J, K = t.K, links = t.links(), users = t.users();
-    const int n = t.n, mn = M * n, tot = links * mn;  // complex elements per slice (tot % 2 == 0 checked)
-    float2* raw[2] = {reinterpret_cast<float2*>(smem_raw), reinterpret_cast<float2*>(smem_raw) + tot};
-    double2* sh = reinterpret_cast<double2*>(smem_raw + 2 * (size_t)tot * sizeof(float2));
-    const int nchunk = tot / 2;  // 16-byte chunks per slice
-    auto fetch = [&](int64_t sl, float2* dst) {
-        if (sl < nslices) {
-            const float2* src = H + sl * (int64_t)tot;  // slice = g * Fc + f (H~ layout [g][Fc][links][mn])
-            for (int c = threadIdx.x; c < nchunk; c += blockDim.x) cp_async16(dst + 2 * c, src + 2 * c);
-        }
-        cp_async_commit();
-    };
-    int64_t sl = blockIdx.x;
-    fetch(sl, raw[0]);
-    for (int it = 0; sl < nslices; ++it, sl += gridDim.x) {
-        fetch(sl + gridDim.x, raw[(it + 1) & 1]);
-        cp_async_wait1();
-        __syncthreads();
-        const float2* r = raw[it & 1];
-        for (int e = threadIdx.x; e < tot; e += blockDim.x) sh[e] = make_double2(r[e].x, r[e].y);
-        __syncthreads();
-        const int64_t g = sl / Fc, f = sl % Fc;
-        const int64_t orow0 = (g * Ftot + f0 + f) * users;
-        for (int e = threadIdx.x; e < users * J * MM; e += blockDim.x) {
-            const int u = e / (J * MM), s = (e / MM) % J, ab = e % MM, a = ab % M, b = ab / M;
-            const int i = u / K, j = u % K;
-            int lx, ly;
-            if (s == 0) {
-                lx = ly = (i * J + i) * K + j;
-            } else {
-                const int k = s - 1 < i ? s - 1 : s;
-                lx = (k * J + i) * K + j;
-                ly = (k * J + k) * K;
-            }
-            const double2* h1 = sh + (size_t)lx * mn + a;
-            const double2* h2 = sh + (size_t)ly * mn + b;
-            double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-            int c = 0;
-            for (; c + 1 < n; c += 2) {
-                cfmac(acc0, h1[M * c], h2[M * c]);
-                cfmac(acc1, h1[M * (c + 1)], h2[M * (c + 1)]);
-            }
-            if (c < n) cfmac(acc0, h1[M * c], h2[M * c]);
-            PG[((orow0 + u) * J + s) * MM + ab] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
-        }
-        __syncthreads();  // sh and raw[it&1] reused by the next iterations
-    }
-}
-
 // K2 (paper scope, whole subcarrier): one CTA per (group, subcarrier) stages every link of that
 // H~(f) (one contiguous links*m*n block, 16-byte vector loads, converted to binary64 once) and
 // computes all users' J pair Grams, one thread per Gram entry. No partner link is read twice.
@@ -618,163 +560,6 @@ __global__ void __launch_bounds__(256) k_pair_gram_gf(Topo t, int Fc, int64_t f0
         PG[((orow0 + u) * J + s) * MM + ab] = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
     }
 }
-
-// ---------------------------------------------------------------------------
-// K1+K2 fused (opt-in GWT_SINR_PATH=rg; measured slower than K1 -> K2 on C2): one CTA (512
-// threads) per (group, FT-subcarrier tile): phasors -> E -> every link's H~ for the tile (binary64
-// in shared memory) -> the J pair Grams of every user, 4 threads per (user, slot, subcarrier).
-template <int M>
-__host__ __device__ inline size_t rg_smem(const Topo& t, int FT, int csize) {
-    const size_t hd = (size_t)t.links() * M * t.n * FT * 16;
-    const size_t ph = (size_t)t.links() * t.P * FT * csize;
-    return (hd > ph ? hd : ph) + (size_t)t.links() * t.p * FT * csize;
-}
-
-template <class T, int M, int FT>
-__global__ void __launch_bounds__(512, 1) k_rebuild_pg(Topo t, int Fc, int64_t f0, int64_t Ftot, int64_t pf0, int64_t pfs,
-                                                     const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
-                                                     const double* __restrict__ tau, const double* __restrict__ freqs,
-                                                     const cplx_t<T>* __restrict__ coeffs, double2* __restrict__ PG) {
-    using C = cplx_t<T>;
-    constexpr int NT = 512, MM = M * M;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int J = t.J, K = t.K, links = t.links(), users = t.users();
-    const int n = t.n, mn = M * n, P = t.P, p = t.p;
-    double2* Hd = reinterpret_cast<double2*>(smem_raw);  // [links][mn][FT]   (phases 3-4)
-    C* Ph = reinterpret_cast<C*>(smem_raw);              // [links][P][FT]    (phases 1-2, aliases Hd)
-    const size_t hd_bytes = (size_t)links * mn * FT * 16, ph_bytes = (size_t)links * P * FT * sizeof(C);
-    C* E = reinterpret_cast<C*>(smem_raw + (hd_bytes > ph_bytes ? hd_bytes : ph_bytes));  // [links][p][FT]
-    const int64_t g = blockIdx.y;
-    const int ft0 = blockIdx.x * FT;
-    const int nf = min(FT, Fc - ft0);
-    const int tid = threadIdx.x;
-    for (int idx = tid; idx < links * P * FT; idx += NT) {
-        const int l = idx / (P * FT), r = (idx / FT) % P, f = idx % FT;
-        C v = czero<C>();
-        if (f < nf) {
-            const int64_t fa = f0 + ft0 + f;
-            v = coeffs ? cconj(coeffs[((g * Ftot + fa) * links + l) * P + r])
-                       : conj_coeff<T>(freqs[fa], tau[(g * links + l) * P + r]);
-        }
-        Ph[idx] = v;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < links * p * FT; idx += NT) {
-        const int l = idx / (p * FT), q = (idx / FT) % p, f = idx % FT;
-        const C* Cl = Cd + ((g * links + l) * P) * (int64_t)p + (int64_t)P * q;
-        const C* ph = Ph + (size_t)l * P * FT + f;
-        C acc = czero<C>();
-        for (int r = 0; r < P; ++r) cfma(acc, Cl[r], ph[r * FT]);
-        E[idx] = acc;
-    }
-    __syncthreads();
-    for (int rg = tid; rg < links * mn; rg += NT) {
-        const int l = rg / mn, row = rg % mn;
-        const C* Gl = G + (g * links + l) * (int64_t)mn * p + row;
-        const C* e = E + (size_t)l * p * FT;
-        C acc[FT];
-#pragma unroll
-        for (int f = 0; f < FT; ++f) acc[f] = czero<C>();
-        for (int q = 0; q < p; ++q) {
-            const C gv = Gl[(int64_t)mn * q];
-#pragma unroll
-            for (int f = 0; f < FT; ++f) cfma(acc[f], gv, e[q * FT + f]);
-        }
-        double2* h = Hd + (size_t)rg * FT;
-#pragma unroll
-        for (int f = 0; f < FT; ++f) h[f] = to_d2(acc[f]);
-    }
-    __syncthreads();
-    const int ntask = users * J * FT * 4;
-    for (int w = tid; w < ntask; w += NT) {
-        const int h = w & 3, f = (w >> 2) % FT, task = (w >> 2) / FT;
-        const int u = task / J, s = task % J;
-        const int i = u / K, j = u % K;
-        int lx, ly;
-        if (s == 0) {
-            lx = ly = (i * J + i) * K + j;
-        } else {
-            const int k = s - 1 < i ? s - 1 : s;
-            lx = (k * J + i) * K + j;
-            ly = (k * J + k) * K;
-        }
-        const double2* hx = Hd + (size_t)lx * mn * FT + f;
-        const double2* hy = Hd + (size_t)ly * mn * FT + f;
-        double2 acc[M][M];
-#pragma unroll
-        for (int a = 0; a < M; ++a)
-#pragma unroll
-            for (int b = 0; b < M; ++b) acc[a][b] = make_double2(0.0, 0.0);
-        for (int c = h; c < n; c += 4) {
-            double2 xa[M], yb[M];
-#pragma unroll
-            for (int a = 0; a < M; ++a) {
-                xa[a] = hx[(size_t)(a + M * c) * FT];
-                yb[a] = hy[(size_t)(a + M * c) * FT];
-            }
-#pragma unroll
-            for (int a = 0; a < M; ++a)
-#pragma unroll
-                for (int b = 0; b < M; ++b) cfmac(acc[a][b], xa[a], yb[b]);
-        }
-#pragma unroll
-        for (int a = 0; a < M; ++a)
-#pragma unroll
-            for (int b = 0; b < M; ++b)
-#pragma unroll
-                for (int o = 1; o < 4; o <<= 1) {
-                    acc[a][b].x += __shfl_xor_sync(0xffffffffu, acc[a][b].x, o);
-                    acc[a][b].y += __shfl_xor_sync(0xffffffffu, acc[a][b].y, o);
-                }
-        if (f < nf) {
-            double2* o = PG + (((g * pfs + pf0 + ft0 + f) * users + u) * J + s) * MM;
-#pragma unroll
-            for (int e = 0; e < MM; ++e)
-                if ((e & 3) == h) o[e] = acc[e % M][e / M];
-        }
-    }
-}
-
-template <class T>
-cudaError_t launch_rebuild_pg(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot, int64_t pf0, int64_t pfs,
-                              const void* Cd, const void* G, const double* tau, const double* freqs, const void* coeffs,
-                              double2* PG, cudaStream_t st) {
-    constexpr int FT = 8;
-    if (t.m > 4) return cudaErrorNotSupported;
-    const size_t cs = sizeof(cplx_t<T>);
-    dim3 grid((Fc + FT - 1) / FT, ngroups);
-    cudaError_t e = cudaErrorNotSupported;
-    switch (t.m) {
-#define GWT_RPG(MM)                                                                                                   \
-    case MM: {                                                                                                        \
-        const size_t sm = rg_smem<MM>(t, FT, (int)cs);                                                                \
-        if (sm > 227 * 1024) return cudaErrorNotSupported;                                                            \
-        e = cudaFuncSetAttribute(k_rebuild_pg<T, MM, FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
-        if (e != cudaSuccess) return e;                                                                               \
-        k_rebuild_pg<T, MM, FT><<<grid, 512, sm, st>>>(t, Fc, f0, Ftot, pf0, pfs, (const cplx_t<T>*)Cd,              \
-                                                       (const cplx_t<T>*)G, tau, freqs, (const cplx_t<T>*)coeffs, PG); \
-        return cudaGetLastError();                                                                                    \
-    }
-        GWT_RPG(1) GWT_RPG(2) GWT_RPG(3) GWT_RPG(4)
-#undef GWT_RPG
-    }
-    return e;
-}
-bool rebuild_pg_fits(const Topo& t, size_t csize) {
-    if (t.m > 4) return false;
-    switch (t.m) {
-        case 1: return rg_smem<1>(t, 8, (int)csize) <= 227 * 1024;
-        case 2: return rg_smem<2>(t, 8, (int)csize) <= 227 * 1024;
-        case 3: return rg_smem<3>(t, 8, (int)csize) <= 227 * 1024;
-        default: return rg_smem<4>(t, 8, (int)csize) <= 227 * 1024;
-    }
-}
-template cudaError_t launch_rebuild_pg<float>(const Topo&, int, int, int64_t, int64_t, int64_t, int64_t, const void*,
-                                              const void*, const double*, const double*, const void*, double2*,
-                                              cudaStream_t);
-template cudaError_t launch_rebuild_pg<double>(const Topo&, int, int, int64_t, int64_t, int64_t, int64_t, const void*,
-                                               const void*, const double*, const double*, const void*, double2*,
-                                               cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // K3a: precoder per (group, subcarrier, user): eig of the serving Gram ->
@@ -1312,632 +1097,7 @@ __global__ void __launch_bounds__(256) k_small_grp(Topo t, int scope, int S, int
     }
 }
 
-// ---------------------------------------------------------------------------
-// Fused compressed-SINR path (paper_experiment scope), two kernels:
-//  k_rebuild_gram: one CTA per (group, user batch, subcarrier tile). H~ is
-//    rebuilt tile by tile into shared memory and consumed there: per user the
-//    serving Gram A_u and one cross Gram X_{u,k} per other cell (fp64), so H~
-//    never touches HBM. Output: GU[g][f][user][J][m*m].
-//  k_sinr_solve: one CTA per (group, subcarrier tile), one thread per
-//    (user, subcarrier): eig of A_u (Jacobi), the partner projectors P_{k0}
-//    exchanged through shared memory, covariance, Cholesky, SINR.
-struct FusedShape {
-    int B, FT, fsplit;
-};
 
-// Shared-memory tile layouts (bank-conflict free for the access patterns below):
-//   Ph [nl][P][FT] conj(c_r(f)),  E [nl][p][FT],  H~ tile [m*n][FT+1] (subcarrier fastest, padded)
-// A CTA is split into NG independent groups of WG threads (named barriers), each group
-// rebuilding nl (<= 2) links at a time: phasors -> E -> H~ -> Grams, every phase fully parallel.
-
-__device__ __forceinline__ void group_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-template <class T, int M, int FT, int FPT>
-__device__ __forceinline__ void group_rebuild(const Topo& t, int lane, int WG, int bar_id, int nl, const int* lids,
-                                              int ft0, int Fc, int64_t f0, int64_t Ftot, int64_t gidx,
-                                              const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
-                                              const double* __restrict__ tau, const double* __restrict__ freqs,
-                                              const cplx_t<T>* __restrict__ coeffs, cplx_t<T>* Ph, cplx_t<T>* Es,
-                                              cplx_t<T>* const* dst) {
-    using C = cplx_t<T>;
-    constexpr int LD = FT + 1;
-    const int links = t.links();
-    const int PF = t.P * FT, pF = t.p * FT;
-    for (int idx = lane; idx < nl * PF; idx += WG) {
-        const int li = idx / PF, rem = idx % PF, r = rem / FT, f = rem % FT;
-        const int64_t gl = gidx * links + lids[li];
-        C v = czero<C>();
-        if (ft0 + f < Fc) {
-            const int64_t fa = f0 + ft0 + f;
-            v = coeffs ? cconj(coeffs[((gidx * Ftot + fa) * links + lids[li]) * t.P + r])
-                       : conj_coeff<T>(freqs[fa], tau[gl * t.P + r]);
-        }
-        Ph[idx] = v;
-    }
-    group_bar(bar_id, WG);
-    for (int idx = lane; idx < nl * pF; idx += WG) {
-        const int li = idx / pF, rem = idx % pF, q = rem / FT, f = rem % FT;
-        const C* Cl = Cd + (gidx * links + lids[li]) * t.P * t.p + (int64_t)t.P * q;
-        const C* ph = Ph + li * PF + f;
-        C acc = czero<C>();
-        for (int r = 0; r < t.P; ++r) cfma(acc, Cl[r], ph[r * FT]);
-        Es[idx] = acc;
-    }
-    group_bar(bar_id, WG);
-    const int mn = M * t.n;
-    constexpr int FS = FT / FPT;
-    for (int idx = lane; idx < nl * mn * FS; idx += WG) {
-        const int li = idx / (mn * FS), rem = idx % (mn * FS), row = rem % mn, fb = (rem / mn) * FPT;
-        const C* Gl = G + (gidx * links + lids[li]) * mn * t.p + row;
-        const C* e = Es + li * pF + fb;
-        C acc[FPT];
-#pragma unroll
-        for (int ff = 0; ff < FPT; ++ff) acc[ff] = czero<C>();
-        for (int q = 0; q < t.p; ++q) {
-            const C gv = Gl[(int64_t)mn * q];
-#pragma unroll
-            for (int ff = 0; ff < FPT; ++ff) cfma(acc[ff], gv, e[q * FT + ff]);
-        }
-        C* d = dst[li] + row * LD + fb;
-#pragma unroll
-        for (int ff = 0; ff < FPT; ++ff) d[ff] = acc[ff];
-    }
-    group_bar(bar_id, WG);
-}
-
-// Gram tasks of one user: serving (Hermitian, M(M+1)/2 entries) and `ncross` cross Grams (M*M each)
-// out[f*ostride + slot*MM + a + M b] = sum_c Hx[a + M c][f] conj(Hy[b + M c][f])  (fp64 accumulation)
-template <class T, int M, int FT>
-__device__ __forceinline__ void group_grams(int lane, int WG, int bar_id, int n, int Fvalid, const cplx_t<T>* Hs,
-                                            int ncross, const cplx_t<T>* const* Hc, const cplx_t<T>* const* Hp,
-                                            const int* slot, double2* out, int64_t ostride) {
-    constexpr int LD = FT + 1, MM = M * M, HS = M * (M + 1) / 2;
-    const int total = FT * (HS + ncross * MM);
-    for (int idx = lane; idx < total; idx += WG) {
-        const int f = idx % FT;
-        int e = idx / FT;
-        const cplx_t<T>*hx, *hy;
-        int a, b, sl;
-        bool herm = e < HS;
-        if (herm) {
-            a = 0;
-            while (e >= M - a) { e -= M - a; ++a; }
-            b = a + e;
-            hx = Hs;
-            hy = Hs;
-            sl = 0;
-        } else {
-            e -= HS;
-            const int c = e / MM;
-            e %= MM;
-            a = e % M;
-            b = e / M;
-            hx = Hc[c];
-            hy = Hp[c];
-            sl = slot[c];
-        }
-        if (f >= Fvalid) continue;
-        const cplx_t<T>* px = hx + a * LD + f;
-        const cplx_t<T>* py = hy + b * LD + f;
-        double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
-        for (int c = 0; c < n; ++c) cfmac(acc, to_d2(px[M * LD * c]), to_d2(py[M * LD * c]));
-        double2* o = out + f * ostride + sl * MM;
-        o[a + M * b] = acc;
-        if (herm && a != b) o[b + M * a] = make_double2(acc.x, -acc.y);
-    }
-    group_bar(bar_id, WG);
-}
-
-template <class T, int M, int FT, int FPT>
-__global__ void __launch_bounds__(256) k_rebuild_gram(Topo t, FusedShape fs, int Fc, int64_t f0, int64_t Ftot,
-                                                      const cplx_t<T>* __restrict__ Cd,
-                                                      const cplx_t<T>* __restrict__ G, const double* __restrict__ tau,
-                                                      const double* __restrict__ freqs, int uniform, double df,
-                                                      const cplx_t<T>* __restrict__ coeffs, double2* __restrict__ GU) {
-    using C = cplx_t<T>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int LD = FT + 1;
-    const int J = t.J, K = t.K, B = fs.B;
-    const int WG = fs.fsplit;  // threads per group
-    const int NG = blockDim.x / WG;
-    const int mn = M * t.n, MM = M * M;
-    const size_t tile = (size_t)mn * LD;
-    const size_t per_group = 2 * tile + (size_t)2 * FT * (t.P + t.p);
-    C* Hpart = reinterpret_cast<C*>(smem_raw);  // [J][mn][LD]
-    const int grp = threadIdx.x / WG, lane = threadIdx.x % WG, bar_id = 1 + grp;
-    C* gw = Hpart + (size_t)J * tile + grp * per_group;
-    C* Hw0 = gw;
-    C* Hw1 = gw + tile;
-    C* Ph = gw + 2 * tile;
-    C* Es = Ph + (size_t)2 * FT * t.P;
-    const int64_t gidx = blockIdx.z;
-    const int ft0 = blockIdx.x * FT;
-    const int Fvalid = min(FT, Fc - ft0);
-    const int u0 = blockIdx.y * B;
-    const int users = t.users();
-    auto link_id = [&](int k, int i, int j) { return (k * J + i) * K + j; };
-    const int64_t fstride = (int64_t)users * J * MM;
-    double2* gbase = GU + ((gidx * Fc + ft0) * users) * (int64_t)J * MM;
-    // partner links (k,k,0), round-robin over groups, into Hpart
-    for (int k = grp; k < J; k += NG) {
-        int lid[2] = {link_id(k, k, 0), 0};
-        C* dst[2] = {Hpart + (size_t)k * tile, nullptr};
-        group_rebuild<T, M, FT, FPT>(t, lane, WG, bar_id, 1, lid, ft0, Fc, f0, Ftot, gidx, Cd, G, tau, freqs, coeffs,
-                                     Ph, Es, dst);
-    }
-    __syncthreads();
-    const int ubeg = u0, uend = min(users, u0 + B);
-    for (int u = ubeg + grp; u < uend; u += NG) {
-        const int i = u / K, j = u % K;
-        // cross links (k,i,j), k != i, in slot order; the serving link rides along when j != 0
-        int kc = 0;
-        int cross_k[8];
-        for (int k = 0; k < J && kc < 8; ++k)
-            if (k != i) cross_k[kc++] = k;
-        const C* hs = Hpart + (size_t)i * tile;
-        int done = 0;
-        bool serving_pending = true;
-        while (serving_pending || done < kc) {
-            int lid[2];
-            C* dst[2];
-            int nl = 0;
-            const C* Hc[2];
-            const C* Hp[2];
-            int slot[2];
-            int ncross = 0;
-            bool with_serving = false;
-            if (serving_pending && j != 0) {
-                lid[nl] = link_id(i, i, j);
-                dst[nl] = Hw0;
-                ++nl;
-                hs = Hw0;
-                with_serving = true;
-            } else if (serving_pending) {
-                with_serving = true;  // serving link is the partner tile Hpart[i]
-            }
-            while (nl < 2 && done < kc) {
-                const int k = cross_k[done];
-                lid[nl] = link_id(k, i, j);
-                dst[nl] = nl == 0 ? Hw0 : Hw1;
-                Hc[ncross] = dst[nl];
-                Hp[ncross] = Hpart + (size_t)k * tile;
-                slot[ncross] = 1 + done;
-                ++ncross;
-                ++nl;
-                ++done;
-            }
-            if (nl > 0)
-                group_rebuild<T, M, FT, FPT>(t, lane, WG, bar_id, nl, lid, ft0, Fc, f0, Ftot, gidx, Cd, G, tau, freqs,
-                                             coeffs, Ph, Es, dst);
-            if (with_serving) {
-                group_grams<T, M, FT>(lane, WG, bar_id, t.n, Fvalid, hs, ncross, Hc, Hp, slot,
-                                      gbase + (int64_t)u * J * MM, fstride);
-            } else {
-                // cross-only round: reuse the Gram routine with a dummy serving slot skipped
-                constexpr int LDc = FT + 1;
-                const int total = FT * ncross * MM;
-                for (int idx = lane; idx < total; idx += WG) {
-                    const int f = idx % FT;
-                    int e = idx / FT;
-                    const int c = e / MM;
-                    e %= MM;
-                    const int a = e % M, b = e / M;
-                    if (f >= Fvalid) continue;
-                    const C* px = Hc[c] + a * LDc + f;
-                    const C* py = Hp[c] + b * LDc + f;
-                    double2 acc = make_double2(0.0, 0.0);
-                    for (int cc = 0; cc < t.n; ++cc) cfmac(acc, to_d2(px[M * LDc * cc]), to_d2(py[M * LDc * cc]));
-                    gbase[(int64_t)u * J * MM + f * fstride + slot[c] * MM + a + M * b] = acc;
-                }
-                group_bar(bar_id, WG);
-            }
-            serving_pending = false;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Whole-group rebuild + Grams (paper scope, small groups: all links of a group fit in shared
-// memory): one CTA per (group, FT subcarriers); every phase runs over ALL links at once, so
-// the CTA never serialises on per-link barriers. H~ stays in shared memory; output GU as above.
-template <class T, int M, int FT>
-__global__ void __launch_bounds__(256) k_sinr_group(Topo t, int Fc, int64_t f0, int64_t Ftot,
-                                                    const cplx_t<T>* __restrict__ Cd, const cplx_t<T>* __restrict__ G,
-                                                    const double* __restrict__ tau, const double* __restrict__ freqs,
-                                                    const cplx_t<T>* __restrict__ coeffs, double2* __restrict__ GU) {
-    using C = cplx_t<T>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int LD = FT + 1, MM = M * M, HS = M * (M + 1) / 2;
-    const int J = t.J, K = t.K, links = t.links(), users = t.users();
-    const int mn = M * t.n, P = t.P, p = t.p;
-    C* H = reinterpret_cast<C*>(smem_raw);      // [links][mn][LD]   (phases 3-4)
-    C* Ph = H;                                   // [links][P][FT]    (phases 1-2, aliases H)
-    C* E = H + (size_t)links * mn * LD;          // [links][p][FT]
-    const int64_t gidx = blockIdx.y;
-    const int ft0 = blockIdx.x * FT;
-    const int Fvalid = min(FT, Fc - ft0);
-    const int tid = threadIdx.x, nt = blockDim.x;
-    // 1. conj(c_r(f)) for every link
-    for (int idx = tid; idx < links * P * FT; idx += nt) {
-        const int l = idx / (P * FT), r = (idx / FT) % P, f = idx % FT;
-        C v = czero<C>();
-        if (f < Fvalid) {
-            const int64_t fa = f0 + ft0 + f;
-            v = coeffs ? cconj(coeffs[((gidx * Ftot + fa) * links + l) * P + r])
-                       : conj_coeff<T>(freqs[fa], tau[(gidx * links + l) * P + r]);
-        }
-        Ph[idx] = v;
-    }
-    __syncthreads();
-    // 2. E_l[q][f] = sum_r C_l(r,q) conj(c_r(f))
-    for (int idx = tid; idx < links * p * FT; idx += nt) {
-        const int l = idx / (p * FT), q = (idx / FT) % p, f = idx % FT;
-        const C* Cl = Cd + ((gidx * links + l) * P) * (int64_t)p + (int64_t)P * q;
-        const C* ph = Ph + (size_t)l * P * FT + f;
-        C acc = czero<C>();
-        for (int r = 0; r < P; ++r) cfma(acc, Cl[r], ph[r * FT]);
-        E[idx] = acc;
-    }
-    __syncthreads();
-    // 3. H~_l[row][f] = sum_q G_l[row + mn q] E_l[q][f], all links, one row x FT subcarriers per thread
-    for (int rg = tid; rg < links * mn; rg += nt) {
-        const int l = rg / mn, row = rg % mn;
-        const C* Gl = G + (gidx * links + l) * (int64_t)mn * p + row;
-        const C* e = E + (size_t)l * p * FT;
-        C acc[FT];
-#pragma unroll
-        for (int f = 0; f < FT; ++f) acc[f] = czero<C>();
-        for (int q = 0; q < p; ++q) {
-            const C gv = Gl[(int64_t)mn * q];
-#pragma unroll
-            for (int f = 0; f < FT; ++f) cfma(acc[f], gv, e[q * FT + f]);
-        }
-        C* h = H + (size_t)rg * LD;
-#pragma unroll
-        for (int f = 0; f < FT; ++f) h[f] = acc[f];
-    }
-    __syncthreads();
-    // 4. Grams per user: serving (Hermitian) + one cross Gram per other cell (fp64 accumulation)
-    const int per_user = HS + (J - 1) * MM;
-    const int64_t fstride = (int64_t)users * J * MM;
-    double2* gbase = GU + ((gidx * Fc + ft0) * users) * (int64_t)J * MM;
-    for (int idx = tid; idx < users * per_user * FT; idx += nt) {
-        const int f = idx % FT;
-        int e = (idx / FT) % per_user;
-        const int u = idx / (FT * per_user);
-        if (f >= Fvalid) continue;
-        const int i = u / K, j = u % K;
-        const C *hx, *hy;
-        int a, b, slot;
-        const bool herm = e < HS;
-        if (herm) {
-            a = 0;
-            while (e >= M - a) { e -= M - a; ++a; }
-            b = a + e;
-            hx = hy = H + (size_t)((i * J + i) * K + j) * mn * LD;
-            slot = 0;
-        } else {
-            e -= HS;
-            const int c = e / MM;
-            e %= MM;
-            a = e % M;
-            b = e / M;
-            const int k = c < i ? c : c + 1;  // c-th cell != i
-            hx = H + (size_t)((k * J + i) * K + j) * mn * LD;
-            hy = H + (size_t)((k * J + k) * K + 0) * mn * LD;
-            slot = 1 + c;
-        }
-        const C* px = hx + a * LD + f;
-        const C* py = hy + b * LD + f;
-        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-        int c = 0;
-        for (; c + 1 < t.n; c += 2) {
-            cfmac(acc0, to_d2(px[M * LD * c]), to_d2(py[M * LD * c]));
-            cfmac(acc1, to_d2(px[M * LD * (c + 1)]), to_d2(py[M * LD * (c + 1)]));
-        }
-        if (c < t.n) cfmac(acc0, to_d2(px[M * LD * c]), to_d2(py[M * LD * c]));
-        const double2 acc = make_double2(acc0.x + acc1.x, acc0.y + acc1.y);
-        double2* o = gbase + f * fstride + (int64_t)u * J * MM + slot * MM;
-        o[a + M * b] = acc;
-        if (herm && a != b) o[b + M * a] = make_double2(acc.x, -acc.y);
-    }
-}
-
-template <class T, int M>
-static size_t group_smem(const Topo& t, int FT) {
-    const size_t cs = sizeof(cplx_t<T>);
-    const size_t hbytes = cs * (size_t)t.links() * M * t.n * (FT + 1);
-    const size_t phbytes = cs * (size_t)t.links() * t.P * FT;
-    return std::max(hbytes, phbytes) + cs * (size_t)t.links() * t.p * FT;
-}
-
-template <int M>
-__device__ __forceinline__ void load_herm(const double2* src, double2 (&A)[M][M]) {
-#pragma unroll
-    for (int b = 0; b < M; ++b)
-#pragma unroll
-        for (int a = 0; a < M; ++a) A[a][b] = src[a + M * b];
-#pragma unroll
-    for (int a = 0; a < M; ++a) {
-        A[a][a].y = 0.0;
-#pragma unroll
-        for (int b = a + 1; b < M; ++b) {
-            const double2 v = make_double2(0.5 * (A[a][b].x + A[b][a].x), 0.5 * (A[a][b].y - A[b][a].y));
-            A[a][b] = v;
-            A[b][a] = make_double2(v.x, -v.y);
-        }
-    }
-}
-
-// one CTA per (group, subcarrier tile); thread = (f, user)
-template <int M>
-__global__ void __launch_bounds__(128) k_sinr_solve(Topo t, int FT, int Fc, int64_t f0, int64_t Ftot, double sigma,
-                                                    const double2* __restrict__ GU, double* __restrict__ sinr,
-                                                    double* __restrict__ signal, int* __restrict__ status) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int J = t.J, K = t.K, L = t.L, MM = M * M;
-    const int users = t.users();
-    double2* Pk = reinterpret_cast<double2*>(smem_raw);  // [FT][J][MM]
-    int* pbad = reinterpret_cast<int*>(Pk + (size_t)FT * J * MM);  // [FT][J]
-    const int64_t gidx = blockIdx.y;
-    const int ft0 = blockIdx.x * FT;
-    const int tid = threadIdx.x;
-    const int f = tid / users, u = tid % users;
-    const bool active = (f < FT) && (ft0 + f < Fc);
-    const int i = u / K, j = u % K;
-    double lam[M];
-    int rank[M];
-    double2 V[M][M];
-    const double2* g = GU + (((gidx * Fc + ft0 + f) * users + u) * (int64_t)J) * MM;
-    if (active) {
-        double2 A[M][M];
-        load_herm<M>(g, A);
-        jacobi_herm<M>(A, V);
-#pragma unroll
-        for (int r = 0; r < M; ++r) lam[r] = A[r][r].x;
-#pragma unroll
-        for (int r = 0; r < M; ++r) {
-            int rk = 0;
-#pragma unroll
-            for (int s2 = 0; s2 < M; ++s2) rk += (lam[s2] > lam[r] || (lam[s2] == lam[r] && s2 < r)) ? 1 : 0;
-            rank[r] = rk;
-        }
-        if (j == 0) {  // partner projector P = U_L Lambda_L^{-1} U_L^H for the other cells' users
-            double2* P = Pk + ((size_t)f * J + i) * MM;
-            int bad = 0;
-#pragma unroll
-            for (int a = 0; a < M; ++a)
-#pragma unroll
-                for (int b = 0; b < M; ++b) {
-                    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-                    for (int r = 0; r < M; ++r) {
-                        if (rank[r] < L && lam[r] > 0.0) {
-                            double2 v = make_double2(0, 0);
-                            cfmac(v, V[a][r], V[b][r]);
-                            const double il = 1.0 / lam[r];
-                            acc.x += il * v.x;
-                            acc.y += il * v.y;
-                        }
-                    }
-                    P[a + M * b] = acc;
-                }
-#pragma unroll
-            for (int r = 0; r < M; ++r) bad |= (rank[r] < L && !(lam[r] > 0.0));
-            pbad[f * J + i] = bad;
-        }
-    }
-    __syncthreads();
-    if (!active) return;
-    int st = 0;
-    double2 Q[M][M];
-    const double s2 = sigma * sigma;
-#pragma unroll
-    for (int a = 0; a < M; ++a)
-#pragma unroll
-        for (int b = 0; b < M; ++b) Q[a][b] = make_double2(a == b ? s2 : 0.0, 0.0);
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-        if (rank[r] < L) {
-            const double lr = fmax(lam[r], 0.0);
-#pragma unroll
-            for (int a = 0; a < M; ++a)
-#pragma unroll
-                for (int b = 0; b < M; ++b) {
-                    double2 v = make_double2(0, 0);
-                    cfmac(v, V[a][r], V[b][r]);
-                    Q[a][b].x += lr * v.x;
-                    Q[a][b].y += lr * v.y;
-                }
-        }
-    }
-    int s = 1;
-    for (int k = 0; k < J; ++k) {
-        if (k == i) continue;
-        const double2* X = g + (int64_t)s * MM;
-        const double2* P = Pk + ((size_t)f * J + k) * MM;
-        if (pbad[f * J + k]) st = 5;
-        double2 XP[M][M];
-#pragma unroll
-        for (int a = 0; a < M; ++a)
-#pragma unroll
-            for (int b = 0; b < M; ++b) {
-                double2 acc = make_double2(0, 0);
-#pragma unroll
-                for (int c = 0; c < M; ++c) cfma(acc, X[a + M * c], P[c + M * b]);
-                XP[a][b] = acc;
-            }
-#pragma unroll
-        for (int a = 0; a < M; ++a)
-#pragma unroll
-            for (int b = 0; b < M; ++b) {
-                double2 acc = Q[a][b];
-#pragma unroll
-                for (int c = 0; c < M; ++c) cfmac(acc, XP[a][c], X[b + M * c]);
-                Q[a][b] = acc;
-            }
-        ++s;
-    }
-    bool finite = true;
-#pragma unroll
-    for (int a = 0; a < M; ++a)
-#pragma unroll
-        for (int b = 0; b < M; ++b) finite = finite && isfinite(Q[a][b].x) && isfinite(Q[a][b].y);
-    bool pd = finite;
-    double dmax = 0.0, dmin = 1e308;
-#pragma unroll
-    for (int c = 0; c < M; ++c) {
-        double d = Q[c][c].x;
-#pragma unroll
-        for (int k2 = 0; k2 < c; ++k2) d -= Q[c][k2].x * Q[c][k2].x + Q[c][k2].y * Q[c][k2].y;
-        pd = pd && (d > 0.0);
-        const double inv = rsqrt(fmax(d, 1e-300));
-        const double lcc = fmax(d, 1e-300) * inv;
-        dmax = fmax(dmax, lcc);
-        dmin = fmin(dmin, lcc);
-        Q[c][c] = make_double2(lcc, inv);  // .y keeps 1/l_cc for the solves
-#pragma unroll
-        for (int r = c + 1; r < M; ++r) {
-            double2 sacc = Q[r][c];
-#pragma unroll
-            for (int k2 = 0; k2 < c; ++k2) {
-                sacc.x -= Q[r][k2].x * Q[c][k2].x + Q[r][k2].y * Q[c][k2].y;
-                sacc.y -= Q[r][k2].y * Q[c][k2].x - Q[r][k2].x * Q[c][k2].y;
-            }
-            Q[r][c] = make_double2(sacc.x * inv, sacc.y * inv);
-        }
-    }
-    if (!finite) st = 4;
-    else if (!pd) st = 1;
-    else if ((dmax / dmin) * (dmax / dmin) > 1e14) st = 2;
-    const int64_t orow = (gidx * Ftot + f0 + ft0 + f) * users + u;
-    double* so = sinr + orow * L;
-    double* sg = signal + orow * L;
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-        if (rank[r] >= L) continue;
-        double gamma = 0.0;
-        if (st != 1 && st != 2 && st != 4) {
-            double2 y[M];
-#pragma unroll
-            for (int a = 0; a < M; ++a) {
-                double2 acc = V[a][r];
-#pragma unroll
-                for (int k2 = 0; k2 < a; ++k2) {
-                    acc.x -= Q[a][k2].x * y[k2].x - Q[a][k2].y * y[k2].y;
-                    acc.y -= Q[a][k2].x * y[k2].y + Q[a][k2].y * y[k2].x;
-                }
-                y[a] = make_double2(acc.x * Q[a][a].y, acc.y * Q[a][a].y);
-            }
-            double nn = 0.0;
-#pragma unroll
-            for (int a = 0; a < M; ++a) nn += y[a].x * y[a].x + y[a].y * y[a].y;
-            gamma = fmax(lam[r], 0.0) * nn;
-        }
-        const double sp = gamma * gamma;
-        double den = gamma * (1.0 - gamma);
-        if (den <= -1e-12 && st == 0) st = 3;
-        den = fmax(den, 2.2250738585072014e-308);
-        so[rank[r]] = sp / den;
-        sg[rank[r]] = sp;
-    }
-    status[orow] = st;
-}
-
-template <class T, int M>
-static cudaError_t launch_fused_m(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot, double sigma,
-                                  const void* Cd, const void* G, const double* tau, const double* freqs, int uniform,
-                                  double df, const void* coeffs, double2* GU, double* sinr, double* signal,
-                                  int* status, cudaStream_t st) {
-    const size_t cs = sizeof(cplx_t<T>);
-    const int users = t.users();
-    const int mn = M * t.n;
-    cudaError_t e = cudaSuccess;
-    const char* eft = std::getenv("GWT_RG_FT");
-    int gFT = 0;  // whole-group kernel tile (0 = does not fit)
-    for (int cand : {8, 4, 2})
-        if (!gFT && group_smem<T, M>(t, cand) <= (cand >= 4 ? 110 * 1024 : 200 * 1024)) gFT = cand;
-    if (eft) gFT = std::atoi(eft) == 8 || std::atoi(eft) == 4 || std::atoi(eft) == 2 ? std::atoi(eft) : gFT;
-    if (gFT && group_smem<T, M>(t, gFT) <= 220 * 1024) {
-        auto rung = [&](auto ftc) {
-            constexpr int FT = decltype(ftc)::value;
-            const size_t sm = group_smem<T, M>(t, FT);
-            e = cudaFuncSetAttribute(k_sinr_group<T, M, FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            if (e != cudaSuccess) return;
-            dim3 g((Fc + FT - 1) / FT, ngroups);
-            k_sinr_group<T, M, FT><<<g, 256, sm, st>>>(t, Fc, f0, Ftot, (const cplx_t<T>*)Cd, (const cplx_t<T>*)G, tau,
-                                                       freqs, (const cplx_t<T>*)coeffs, GU);
-            e = cudaGetLastError();
-        };
-        if (gFT == 8) rung(std::integral_constant<int, 8>{});
-        else if (gFT == 4) rung(std::integral_constant<int, 4>{});
-        else rung(std::integral_constant<int, 2>{});
-        if (e != cudaSuccess) return e;
-    } else {
-    // rebuild+Gram: FT subcarriers per CTA tile, a group of WG threads per user (named barriers).
-    // GWT_RG_FT / GWT_RG_WG override the defaults (tuning).
-    const int FTsel = eft ? std::atoi(eft) : 16;
-    const char* ewg = std::getenv("GWT_RG_WG");
-    int WG = ewg ? std::atoi(ewg) : (mn <= 128 ? 128 : 256);
-    if (WG < 32 || 256 % WG) WG = 256;
-    const int NG = 256 / WG;
-    FusedShape fs;
-    fs.B = std::min(users, 32);
-    fs.fsplit = WG;
-    auto run = [&](auto ftc) {
-        constexpr int FT = decltype(ftc)::value;
-        fs.FT = FT;
-        const size_t tile = (size_t)mn * (FT + 1);
-        const size_t sm1 = cs * ((size_t)t.J * tile + (size_t)NG * (2 * tile + (size_t)2 * FT * (t.P + t.p)));
-        if (sm1 > 220 * 1024) { e = cudaErrorInvalidValue; return; }
-        dim3 g1((Fc + FT - 1) / FT, (users + fs.B - 1) / fs.B, ngroups);
-        e = cudaFuncSetAttribute(k_rebuild_gram<T, M, FT, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-        if (e != cudaSuccess) return;
-        k_rebuild_gram<T, M, FT, 8><<<g1, 256, sm1, st>>>(t, fs, Fc, f0, Ftot, (const cplx_t<T>*)Cd,
-                                                          (const cplx_t<T>*)G, tau, freqs, uniform, df,
-                                                          (const cplx_t<T>*)coeffs, GU);
-        e = cudaGetLastError();
-    };
-    if (FTsel == 8) run(std::integral_constant<int, 8>{});
-    else run(std::integral_constant<int, 16>{});
-    if (e != cudaSuccess) return e;
-    }
-    // solve: (users x FT2) threads per CTA, FT2 = 128 / users (>= 1)
-    const int FT2 = std::max(1, 128 / users);
-    const size_t sm2 = (size_t)FT2 * t.J * (16 * M * M + 4) + 16;
-    dim3 g2((Fc + FT2 - 1) / FT2, ngroups);
-    k_sinr_solve<M><<<g2, std::max(32, ((FT2 * users + 31) / 32) * 32), sm2, st>>>(t, FT2, Fc, f0, Ftot, sigma, GU,
-                                                                                sinr, signal, status);
-    return cudaGetLastError();
-}
-
-template <class T>
-cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot, double sigma,
-                              const void* Cd, const void* G, const double* tau, const double* freqs, int uniform,
-                              double df, const void* coeffs, double2* GU, double* sinr, double* signal, int* status,
-                              cudaStream_t st) {
-    if (t.users() > 128) return cudaErrorInvalidValue;
-    switch (t.m) {
-#define GWT_FUSED_CASE(MM)                                                                                         \
-    case MM:                                                                                                       \
-        return launch_fused_m<T, MM>(t, ngroups, Fc, f0, Ftot, sigma, Cd, G, tau, freqs, uniform, df, coeffs, GU, \
-                                     sinr, signal, status, st);
-        GWT_FUSED_CASE(1) GWT_FUSED_CASE(2) GWT_FUSED_CASE(3) GWT_FUSED_CASE(4)
-        GWT_FUSED_CASE(5) GWT_FUSED_CASE(6) GWT_FUSED_CASE(7) GWT_FUSED_CASE(8)
-#undef GWT_FUSED_CASE
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-template cudaError_t launch_sinr_fused<float>(const Topo&, int, int, int64_t, int64_t, double, const void*,
-                                              const void*, const double*, const double*, int, double, const void*,
-                                              double2*, double*, double*, int*, cudaStream_t);
-template cudaError_t launch_sinr_fused<double>(const Topo&, int, int, int64_t, int64_t, double, const void*,
-                                               const void*, const double*, const double*, int, double, const void*,
-                                               double2*, double*, double*, int*, cudaStream_t);
 
 // ---------------------------------------------------------------------------
 // launchers
@@ -1948,13 +1108,6 @@ cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64
                            cudaStream_t st) {
     using C = cplx_t<T>;
     constexpr int FT = 16;
-    const char* rtc = std::getenv("GWT_REBUILD_TC");
-    if (sizeof(T) == 4 && !coeffs && rtc && std::atoi(rtc) != 0) {
-        // tensor-core rebuild (k_tc.cu, opt-in) when the shape fits; else the CUDA-core kernels below
-        cudaError_t e = launch_rebuild_tc(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st);
-        if (e != cudaErrorNotSupported) return e;
-        cudaGetLastError();
-    }
     if (sizeof(T) == 4 && !coeffs && rebuild_mm_fits(t) && !std::getenv("GWT_REBUILD_RB")) {
         cudaError_t e = launch_rebuild_mm(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st);
         if (e != cudaErrorNotSupported) return e;
@@ -2004,26 +1157,6 @@ cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroup
     const int64_t items = (int64_t)ngroups * Fc * t.users();
     const int wpb = 4;
     const size_t smf = sizeof(double2) * (size_t)t.links() * t.m * t.n;
-    if (sizeof(T) == 4 && scope == 1 && smf <= 48 * 1024 && t.m <= 8 && ((t.links() * t.m * t.n) % 2 == 0) &&
-        std::getenv("GWT_PG_PIPE")) {
-        const size_t sm = 2 * smf;  // two raw complex64 buffers + one binary64 buffer
-        const int64_t nsl = (int64_t)ngroups * Fc;
-        const int thr = (int)std::min<int64_t>(256, ((int64_t)t.users() * t.J * t.m * t.m + 31) / 32 * 32);
-        int per_sm = 0;
-        cudaError_t e = cudaSuccess;
-        switch (t.m) {
-#define GWT_PGP(MM)                                                                                               \
-    case MM:                                                                                                      \
-        e = cudaFuncSetAttribute(k_pair_gram_pipe<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
-        if (e != cudaSuccess) return e;                                                                           \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pair_gram_pipe<MM>, thr, sm);                   \
-        k_pair_gram_pipe<MM><<<(unsigned)std::min<int64_t>(nsl, 148 * std::max(per_sm, 1)), thr, sm, st>>>(       \
-            t, Fc, f0, Ftot, nsl, (const float2*)H, PG);                                                          \
-        return cudaGetLastError();
-            GWT_PGP(1) GWT_PGP(2) GWT_PGP(3) GWT_PGP(4) GWT_PGP(5) GWT_PGP(6) GWT_PGP(7) GWT_PGP(8)
-#undef GWT_PGP
-        }
-    }
     if (scope == 1 && smf <= 64 * 1024 && t.m <= 8 && !std::getenv("GWT_PG_STAGED")) {
         const int mn = t.m * t.n, LS = mn + ((4 - mn % 8) + 8) % 8;
         const size_t smp = sizeof(double2) * (size_t)t.links() * LS;

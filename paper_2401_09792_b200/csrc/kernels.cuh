@@ -68,8 +68,6 @@ template <class T> cudaError_t launch_broadcast(const void* src, void* dst, int6
                                                 cudaStream_t st);
 cudaError_t launch_gram_tc(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V,
                            void* out, cudaStream_t st);  // k_tc.cu (c64, 3xTF32 tcgen05)
-cudaError_t launch_rebuild_tc(const Topo& t, int ngroups, int Fc, int64_t f0, const void* Cd, const void* G,
-                              const double* tau, const double* freqs, void* H, cudaStream_t st);  // k_tc.cu
 // k_eig.cu
 template <class T> cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, void* out,
                                                 double* evals, double2* ws_a, double* ws_z, double2* ws_x, int* fail,
@@ -84,18 +82,8 @@ size_t heev_ws_z_elems(int D, int count);
 template <class T> cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
                                               const void* Cd, const void* G, const double* tau, const double* freqs,
                                               const void* coeffs, void* H, cudaStream_t st);
-template <class T> cudaError_t launch_rebuild_pg(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
-                                                 int64_t pf0, int64_t pfs, const void* Cd, const void* G,
-                                                 const double* tau, const double* freqs, const void* coeffs,
-                                                 double2* PG, cudaStream_t st);  // k_sinr.cu, fused K1+K2
-bool rebuild_pg_fits(const Topo& t, size_t csize);
 template <class T> cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroups, int64_t f0,
                                                 int64_t Ftot, const void* H, double2* PG, cudaStream_t st);
-template <class T> cudaError_t launch_sinr_fused(const Topo& t, int ngroups, int Fc, int64_t f0, int64_t Ftot,
-                                                 double sigma, const void* Cd, const void* G, const double* tau,
-                                                 const double* freqs, int uniform, double df, const void* coeffs,
-                                                 double2* GU, double* sinr, double* signal, int* status,
-                                                 cudaStream_t st);
 // k_rebuild.cu: SGEMM-tiled rebuild for large cores (c64, m n >= 256)
 bool rebuild_mm_fits(const Topo& t);
 cudaError_t launch_rebuild_mm(const Topo& t, int ngroups, int Fc, int64_t f0, const void* Cd, const void* G,

@@ -23,6 +23,24 @@
 
 namespace gwt {
 
+// decompose.cpp:42-56
+const char* model_name(ModelKind model) {
+    switch (model) {
+        case ModelKind::individual: return "individual";
+        case ModelKind::shared: return "shared";
+        case ModelKind::groupwise: return "groupwise";
+    }
+    return "unknown";
+}
+
+ModelKind model_from_name(const std::string& name) {
+    static const std::pair<const char*, ModelKind> known[] = {
+        {"individual", ModelKind::individual}, {"shared", ModelKind::shared}, {"groupwise", ModelKind::groupwise}};
+    for (const auto& k : known)
+        if (name == k.first) return k.second;
+    throw std::invalid_argument("unknown model '" + name + "' (expected individual, shared or groupwise)");
+}
+
 namespace {
 
 struct Ctx {

@@ -120,3 +120,43 @@ def test_paper_metrics_reference_values():
     with pytest.raises(gw.InvalidArgument, match="zero at flat index 1"):
         metrics.sinr_error([1.0, 0.0], [1.0, 1.0])
     assert metrics.speedup(6.0, 2.0) == 3.0
+
+
+def test_runner_callsites_compile():
+    """The reference control plane's hot-path call sites (runner.cpp:82-140: the model switch over
+    groupwise/shared/individual solves, both compressed pipelines, the full-size comparator with its
+    seconds/ledger fields, model_name/model_from_name) compile against the drop-in headers."""
+    cxx = shutil.which("g++")
+    if not cxx:
+        pytest.skip("g++ not available")
+    inc = os.path.join(ROOT, "paper_2401_09792_b200", "host", "include")
+    src = os.path.join(ROOT, "tests", "cpp", "runner_callsites.cpp")
+    r = subprocess.run([cxx, "-std=c++17", "-fsyntax-only", "-I", inc, src], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_model_name_roundtrip_cpp(tmp_path):
+    """gwt::model_name / model_from_name of the C++ drop-in (decompose.cpp:42-56), including the error text."""
+    cxx = shutil.which("g++")
+    if not cxx:
+        pytest.skip("g++ not available")
+    inc = os.path.join(ROOT, "paper_2401_09792_b200", "host", "include")
+    libdir = os.path.join(ROOT, "paper_2401_09792_b200", "_build")
+    src = tmp_path / "m.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <stdexcept>
+#include "gwtucker/decompose.hpp"
+int main() {
+    for (auto k : {gwt::ModelKind::individual, gwt::ModelKind::shared, gwt::ModelKind::groupwise})
+        if (gwt::model_from_name(gwt::model_name(k)) != k) return 1;
+    try { gwt::model_from_name("tucker"); } catch (const std::invalid_argument& e) { std::puts(e.what()); return 0; }
+    return 2;
+}''')
+    exe = tmp_path / "m"
+    r = subprocess.run([cxx, "-std=c++17", "-I", inc, str(src), "-o", str(exe), "-L", libdir, "-lgwtucker_b200",
+                        "-lgwt_b200", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0
+    assert out.stdout.strip() == "unknown model 'tucker' (expected individual, shared or groupwise)"

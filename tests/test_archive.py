@@ -69,3 +69,81 @@ def test_corruption_is_detected(tmp_path):
         ar.load_archive(tmp_path / "tag.gwtk")
     with pytest.raises(gw.InvalidArgument, match="coefficient grid has 3 entries, expected 8"):
         ar.save_archive(tmp_path / "x.gwtk", "groupwise", fs, co[:3], 2, 2)
+
+
+CPP_ROUNDTRIP = r'''
+#include <cstdio>
+#include <string>
+#include "gwtucker/archive.hpp"
+int main(int argc, char** argv) {
+    // argv: mode in out   (mode "rt": load + re-save;  mode "err": print the loader's error text)
+    const std::string mode = argv[1];
+    try {
+        gwt::LoadedArchive a = gwt::load_archive(argv[2]);
+        if (mode == "err") { std::puts("no error"); return 0; }
+        if (a.model == gwt::ModelKind::individual)
+            gwt::save_archive(argv[3], a.links, a.num_cells, a.users_per_cell, a.coeffs);
+        else
+            gwt::save_archive(argv[3], a.model, a.factors, a.coeffs);
+        std::puts(gwt::model_name(a.model));
+    } catch (const gwt::BadMagicError& e) { std::printf("BadMagicError: %s\n", e.what());
+    } catch (const gwt::VersionMismatchError& e) { std::printf("VersionMismatchError: %s\n", e.what());
+    } catch (const gwt::TruncatedArchiveError& e) { std::printf("TruncatedArchiveError: %s\n", e.what());
+    } catch (const gwt::ArchiveError& e) { std::printf("ArchiveError: %s\n", e.what());
+    } catch (const std::invalid_argument& e) { std::printf("invalid_argument: %s\n", e.what()); }
+    return 0;
+}
+'''
+
+
+@pytest.fixture(scope="module")
+def cpp_archive_tool(tmp_path_factory):
+    import shutil
+    import subprocess
+    cxx = shutil.which("g++")
+    if not cxx:
+        pytest.skip("g++ not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    d = tmp_path_factory.mktemp("cpparchive")
+    (d / "rt.cpp").write_text(CPP_ROUNDTRIP)
+    libdir = os.path.join(root, "paper_2401_09792_b200", "_build")
+    r = subprocess.run([cxx, "-std=c++17", "-I", os.path.join(root, "paper_2401_09792_b200", "host", "include"),
+                        str(d / "rt.cpp"), "-o", str(d / "rt"), "-L", libdir, "-lgwtucker_b200", "-lgwt_b200",
+                        f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return lambda *a: subprocess.run([str(d / "rt"), *map(str, a)], capture_output=True, text=True).stdout.strip()
+
+
+@pytest.mark.parametrize("model", ["groupwise", "shared", "individual"])
+def test_cpp_dropin_archive_bytes_equal_python(tmp_path, cpp_archive_tool, model):
+    """gwt::save_archive / load_archive of the C++ drop-in (archive.cpp:178-311) read what archive.py writes
+    and write back the identical bytes, for all three models."""
+    rng = np.random.default_rng(7)
+    fs, co = _factors(rng)
+    src = tmp_path / f"{model}.gwtk"
+    if model == "individual":
+        links = 8
+        c = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)
+        ar.save_archive_individual(src, c(links, 4, 6), c(links, 5, 8), c(links, 3, 5), c(links, 3, 5, 4), co, 2, 2)
+    else:
+        ar.save_archive(src, model, fs, co, 2, 2)
+    out = tmp_path / f"{model}_cpp.gwtk"
+    assert cpp_archive_tool("rt", src, out) == model
+    assert out.read_bytes() == src.read_bytes()
+
+
+def test_cpp_dropin_archive_errors_match_python(tmp_path, cpp_archive_tool):
+    rng = np.random.default_rng(8)
+    fs, co = _factors(rng)
+    good = tmp_path / "g.gwtk"
+    ar.save_archive(good, "groupwise", fs, co, 2, 2)
+    data = good.read_bytes()
+    cases = {"magic": b"XXXX" + data[4:], "version": data[:4] + struct.pack("<I", 9) + data[8:],
+             "short": data[:-16], "header": data[:20]}
+    for name, blob in cases.items():
+        p = tmp_path / f"{name}.gwtk"
+        p.write_bytes(blob)
+        got = cpp_archive_tool("err", p)
+        with pytest.raises(ar.ArchiveError) as ei:
+            ar.load_archive(p)
+        assert got == f"{type(ei.value).__name__}: {ei.value}", (name, got)
