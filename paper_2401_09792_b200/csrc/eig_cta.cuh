@@ -528,9 +528,50 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
         if (t < count && s == 0) lamv[t] = 0.5 * ((double)lo + (double)hi) * tnorm;
     }
     __syncthreads();
+    if constexpr (sizeof(R) == 8) {
+        // 3a'. binary64 storage: refine each eigenvalue by binary64 multisection inside a bracket around the
+        // fp32 estimate (checked, else the Gershgorin interval). With shifts accurate to ~eps64 ||T|| the
+        // inverse iterations only need joint orthogonalisation for eigenvalues closer than 1e-9 ||T||
+        // (the fp32 shifts forced it below 1e-3 ||T||: for the graded delay-mode spectra, p_q ~ e^-0.3q,
+        // most kept eigenvalues formed one cluster and were solved one after another).
+        int S = NT / count;
+        S = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1));
+        const int t = tid / S, s = tid % S;
+        const int gl = lane / S;
+        const int want = D - 1 - t;
+        bool done = t >= count;
+        const double lam0 = done ? 0.0 : lamv[t];
+        double lo = lam0 - 4e-6 * tnorm, hi = lam0 + 4e-6 * tnorm;
+        if (!done && !(sturm_count_f64(D, (const double*)sd, (const double*)se2, lo) <= want &&
+                       sturm_count_f64(D, (const double*)sd, (const double*)se2, hi) > want)) {
+            lo = glo;
+            hi = ghi;
+        }
+        for (int it = 0; it < 80; ++it) {
+            if (!done && hi - lo <= 8.0 * 2.220446049250313e-16 * fmax(fmax(fabs(lo), fabs(hi)), 1e-14 * tnorm))
+                done = true;
+            if (__all_sync(0xffffffffu, done)) break;
+            const double step = (hi - lo) / (double)(S + 1);
+            const double pt = lo + (double)(s + 1) * step;
+            const bool le = !done && sturm_count_f64(D, (const double*)sd, (const double*)se2, pt) <= want;
+            const unsigned bits = __ballot_sync(0xffffffffu, le);
+            if (!done) {
+                const int j = __popc((bits >> (gl * S)) & ((S == 32 ? 0u : (1u << S)) - 1u));
+                const double nlo = j > 0 ? lo + (double)j * step : lo;
+                const double nhi = j < S ? lo + (double)(j + 1) * step : hi;
+                if (!(nlo >= lo && nhi <= hi && nlo < nhi) || (nlo == lo && nhi == hi)) done = true;
+                else {
+                    lo = nlo;
+                    hi = nhi;
+                }
+            }
+        }
+        if (t < count && s == 0) lamv[t] = 0.5 * (lo + hi);
+        __syncthreads();
+    }
     __shared__ int s_rounds;
     if (tid == 0) {
-        const double ctol = 1e-3 * fmax(tnorm, 1e-300);
+        const double ctol = (sizeof(R) == 8 ? 1e-9 : 1e-3) * fmax(tnorm, 1e-300);
         int pos = 0, maxr = 0;
         for (int t = 0; t < count; ++t) {
             pos = (t > 0 && fabs(lamv[t - 1] - lamv[t]) <= ctol) ? pos + 1 : 0;

@@ -153,6 +153,26 @@ __device__ __forceinline__ int sturm_count_f32(int D, const float* d, const floa
     }
     return cnt;
 }
+// binary64 Sturm count on the unnormalised tridiagonal (e2[i] couples rows i, i+1); MUFU-seeded reciprocal
+// with two Newton steps in place of the division (the count stays backward stable)
+__device__ __forceinline__ int sturm_count_f64(int D, const double* d, const double* e2, double x) {
+    const double pivmin = 1e-290;
+    int cnt = 0;
+    double q = d[0] - x;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+    for (int i = 1; i < D; ++i) {
+        double y;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q));
+        y = fma(y, fma(-q, y, 1.0), y);
+        y = fma(y, fma(-q, y, 1.0), y);
+        q = d[i] - x - e2[i - 1] * y;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+    }
+    return cnt;
+}
+
 template <class R>
 __device__ __forceinline__ int sturm_count_r(int D, const float* d, const float* e2, float x) {
     if constexpr (sizeof(R) == 4) return sturm_count_p32(D, d, e2, x);
