@@ -23,7 +23,7 @@ __host__ __device__ inline size_t eig_big_smem(int D, int count) {
            (size_t)D * count * 4 + 64;
 }
 
-__global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, const float2* __restrict__ in,
+__global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, double ctol_rel, const float2* __restrict__ in,
                                                         float2* __restrict__ out, double* __restrict__ evals,
                                                         float2* __restrict__ ws_a, float* __restrict__ ws_lu,
                                                         int* __restrict__ fail) {
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, const 
     }
     __syncthreads();
     if (tid == 0) {
-        const double ctol = 1e-3 * fmax(tnorm, 1e-300);
+        const double ctol = ctol_rel * fmax(tnorm, 1e-300);
         int pos = 0, maxr = 0;
         for (int t = 0; t < count; ++t) {
             pos = (t > 0 && fabs(lamv[t - 1] - lamv[t]) <= ctol) ? pos + 1 : 0;

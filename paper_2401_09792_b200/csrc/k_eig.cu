@@ -1159,7 +1159,12 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
         const size_t sm = eig_big_smem(D, count);
         cudaError_t e = cudaFuncSetAttribute(k_heev_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
-        k_heev_big<<<(unsigned)batch, kBigNT, sm, st>>>(D, count, (const float2*)in, (float2*)out, evals,
+        // joint-orthogonalisation threshold of the inverse iterations (relative to ||T||)
+        static const double big_ctol = [] {
+            const char* v = std::getenv("GWT_EIG_BIG_CTOL");
+            return v ? std::atof(v) : 1e-3;
+        }();
+        k_heev_big<<<(unsigned)batch, kBigNT, sm, st>>>(D, count, big_ctol, (const float2*)in, (float2*)out, evals,
                                                         reinterpret_cast<float2*>(ws_a), reinterpret_cast<float*>(ws_z),
                                                         fail);
         return cudaGetLastError();

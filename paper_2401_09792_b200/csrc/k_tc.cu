@@ -113,141 +113,196 @@ __device__ __forceinline__ int tc_set_link(const Topo& t, int kind, int s, int r
     }
 }
 
-__global__ void __launch_bounds__(256) k_gram_tc(Topo t, GramDesc d, int sets_per_group, const float2* __restrict__ V,
-                                                 float2* __restrict__ out) {
-    constexpr int KC = 32, TILE_R = 128;
-    constexpr uint32_t TB = TILE_R * KC * 4;  // 16 KB per operand tile
+// ---------------------------------------------------------------------------------------------
+// Tucker Gram on the tensor cores for unfoldings whose rows are contiguous blocks of T1 complex values
+// (GramDesc xs == T1, t1s == 1): the transmit-mode Gram of W2 = Y1 x1 A^H ([link][p][N][m], T1 = m,
+// decompose.cpp:160-176), Out[set](x, y) = sum over the set's links and t2 of V(x, :) V(y, :)^H.
+//
+// One CTA per (128 x 128 lower tile pair, set). For every (link, t2) chunk the x rows of the tile
+// are one contiguous 128 T1-complex block, so
+//   warp 8 (one thread): TMA bulk copy of the raw x / y blocks (cp.async.bulk, 3 raw stages);
+//   warps 0-7          : convert raw -> canonical K-major tf32 operand tiles, 3xTF32 split:
+//                        A = [vr, vi] (x rows), B = [vr, vi] and P = [-vi, vr] (y rows), hi / lo each
+//                        (2 tile stages);
+//   warp 9 (one thread): 12 tcgen05.mma per chunk: Re += A_h B_h + A_h B_l + A_l B_h and
+//                        Im += A_h P_h + A_h P_l + A_l P_h (M = N = 128, K = 2 T1), accumulators in TMEM;
+//   warps 0-7          : epilogue, TMEM -> Gram tile (Re warps 0-3, Im warps 4-7).
+namespace {
+constexpr int kGT = 128;
+constexpr int kGTThreads = 320;
+}  // namespace
+
+template <int T1>
+__global__ void __launch_bounds__(kGTThreads, 1) k_gram_tcb(Topo t, GramDesc d, int sets_per_group,
+                                                           const float2* __restrict__ V, float2* __restrict__ out) {
+    constexpr int KC = 2 * T1;                             // real K per chunk
+    constexpr uint32_t TILE = kGT * KC * 4;                // one operand tile (bytes)
+    constexpr uint32_t RAW = kGT * T1 * 8;                 // one raw block
+    constexpr uint32_t SBO = (KC / 4) * 128;
     extern __shared__ __align__(1024) unsigned char smem[];
-    // per stage: Ah Al (Wh of x-rows), Th Tl (Wt of x-rows), Bh Bl (Wh of y-rows)
-    __shared__ uint64_t mbar[2];
+    unsigned char* raw = smem;                              // [3][x | y] RAW each
+    unsigned char* tiles = smem + 6 * RAW;                  // [2][Ah Al Bh Bl Ph Pl] TILE each
+    __shared__ uint64_t raw_full[3], raw_empty[3], tile_full[2], tile_empty[2], acc_full;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int64_t set = blockIdx.y;
     const int64_t g = set / sets_per_group;
     const int s = (int)(set % sets_per_group);
-    const int tiles = (d.D + TILE_R - 1) / TILE_R;
-    const int x0 = (blockIdx.x % tiles) * TILE_R, y0 = (blockIdx.x / tiles) * TILE_R;
-    const bool diag = x0 == y0;
+    // lower tile pair index -> (xt >= yt)
+    int xt = 0, rem = blockIdx.x;
+    while (rem > xt) { rem -= xt + 1; ++xt; }
+    const int yt = rem;
+    const int x0 = xt * kGT, y0 = yt * kGT;
+    const bool diag = xt == yt;
+    const int nx = min(kGT, d.D - x0), ny = min(kGT, d.D - y0);
+    const int nl = tc_set_size(t, d.set_kind);
+    const int nch = nl * d.T2;
     if (warp == 0) tc::tmem_alloc(&tmem_base, 256);
     if (tid == 0) {
-        tc::mbar_init(&mbar[0], 1);
-        tc::mbar_init(&mbar[1], 1);
+        for (int i = 0; i < 3; ++i) {
+            tc::mbar_init(&raw_full[i], 1);
+            tc::mbar_init(&raw_empty[i], 256);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&tile_full[i], 256);
+            tc::mbar_init(&tile_empty[i], 1);
+        }
+        tc::mbar_init(&acc_full, 1);
         tc::fence_barrier_init();
     }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tre = tmem_base, tim = tmem_base + 128;
-    constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
-    const int nl = tc_set_size(t, d.set_kind);
-    const int Tn = d.T1 * d.T2;
-    const int64_t ktot = (int64_t)nl * Tn;  // complex reduction length
-    const int nchunks = (int)((ktot + KC / 2 - 1) / (KC / 2));
-    uint32_t phase[2] = {0, 0};
-    for (int ch = 0; ch < nchunks; ++ch) {
-        const int st = ch & 1;
-        unsigned char* base = smem + (size_t)st * 6 * TB;
-        if (ch >= 2) {  // wait until the MMAs that read this stage (chunk ch-2) are done
-            tc::mbar_wait(&mbar[st], phase[st]);
-            phase[st] ^= 1;
-        }
-        // stage 16 complex columns of the x-tile and y-tile rows
-        for (int idx = tid; idx < TILE_R * (KC / 2); idx += blockDim.x) {
-            const int tc_ = idx % (KC / 2), r = idx / (KC / 2);
-            const int64_t kt = (int64_t)ch * (KC / 2) + tc_;
-            float2 vx = make_float2(0.f, 0.f), vy = make_float2(0.f, 0.f);
-            if (kt < ktot) {
-                const int li = (int)(kt / Tn), tt = (int)(kt % Tn);
-                const int l = tc_set_link(t, d.set_kind, s, li);
-                const float2* vb = V + (g * t.links() + l) * d.v_item +
-                                   (int64_t)(tt % d.T1) * d.t1s + (int64_t)(tt / d.T1) * d.t2s;
-                if (x0 + r < d.D) vx = vb[(int64_t)(x0 + r) * d.xs];
-                if (!diag && y0 + r < d.D) vy = vb[(int64_t)(y0 + r) * d.xs];
-            }
-            const int k = 2 * tc_;
-            const uint32_t o0 = tc::kmajor_off(r, k, KC), o1 = tc::kmajor_off(r, k + 1, KC);
-            float h, l_;
-            tc::split_tf32(vx.x, h, l_);
-            *reinterpret_cast<float*>(base + 0 * TB + o0) = h;
-            *reinterpret_cast<float*>(base + 1 * TB + o0) = l_;
-            *reinterpret_cast<float*>(base + 3 * TB + o1) = -h;
-            *reinterpret_cast<float*>(base + 4 * TB + o1) = -l_;
-            tc::split_tf32(vx.y, h, l_);
-            *reinterpret_cast<float*>(base + 0 * TB + o1) = h;
-            *reinterpret_cast<float*>(base + 1 * TB + o1) = l_;
-            *reinterpret_cast<float*>(base + 3 * TB + o0) = h;
-            *reinterpret_cast<float*>(base + 4 * TB + o0) = l_;
-            if (!diag) {
-                tc::split_tf32(vy.x, h, l_);
-                *reinterpret_cast<float*>(base + 2 * TB + o0) = h;
-                *reinterpret_cast<float*>(base + 5 * TB + o0) = l_;
-                tc::split_tf32(vy.y, h, l_);
-                *reinterpret_cast<float*>(base + 2 * TB + o1) = h;
-                *reinterpret_cast<float*>(base + 5 * TB + o1) = l_;
+    auto src_block = [&](int c, int r0) -> const float2* {
+        const int li = c / d.T2, t2 = c % d.T2;
+        const int l = tc_set_link(t, d.set_kind, s, li);
+        return V + (g * t.links() + l) * d.v_item + (int64_t)t2 * d.t2s + (int64_t)r0 * T1;
+    };
+    if (warp == 8) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            for (int c = 0; c < nch; ++c) {
+                const int st = c % 3, use = c / 3;
+                if (use > 0) tc::mbar_wait(&raw_empty[st], (use - 1) & 1);
+                const uint32_t bx = (uint32_t)nx * T1 * 8, by = diag ? 0u : (uint32_t)ny * T1 * 8;
+                tc::mbar_arrive_expect_tx(&raw_full[st], bx + by);
+                tc::bulk_g2s(raw + (size_t)st * 2 * RAW, src_block(c, x0), bx, &raw_full[st]);
+                if (!diag) tc::bulk_g2s(raw + (size_t)st * 2 * RAW + RAW, src_block(c, y0), by, &raw_full[st]);
             }
         }
-        tc::fence_async_shared();
-        __syncthreads();
-        if (tid == 0) {
-            tc::fence_after_sync();
-            const uint32_t ah = tc::smem_u32(base), al = ah + TB;
-            const uint32_t bh = diag ? ah : ah + 2 * TB, bl = diag ? al : ah + 5 * TB;
-            const uint32_t th = ah + 3 * TB, tl = ah + 4 * TB;
-            constexpr uint32_t LBO = 128, SBO = (KC / 4) * 128;
+        __syncwarp();
+    } else if (warp == 9) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_tf32(kGT, kGT);
+            for (int c = 0; c < nch; ++c) {
+                const int st = c & 1, use = c >> 1;
+                tc::mbar_wait(&tile_full[st], use & 1);
+                tc::fence_after_sync();
+                const uint32_t b0 = tc::smem_u32(tiles + (size_t)st * 6 * TILE);
+                const uint64_t dAh = tc::smem_desc(b0, 128, SBO), dAl = tc::smem_desc(b0 + TILE, 128, SBO);
+                const uint64_t dBh = tc::smem_desc(b0 + 2 * TILE, 128, SBO), dBl = tc::smem_desc(b0 + 3 * TILE, 128, SBO);
+                const uint64_t dPh = tc::smem_desc(b0 + 4 * TILE, 128, SBO), dPl = tc::smem_desc(b0 + 5 * TILE, 128, SBO);
 #pragma unroll
-            for (int k8 = 0; k8 < KC / 8; ++k8) {
-                const uint32_t o = k8 * 256;
-                const uint32_t acc = (ch > 0 || k8 > 0) ? 1u : 0u;
-                const uint64_t dbh = tc::smem_desc(bh + o, LBO, SBO), dbl = tc::smem_desc(bl + o, LBO, SBO);
-                tc::mma_tf32(tre, tc::smem_desc(ah + o, LBO, SBO), dbh, idesc, acc);
-                tc::mma_tf32(tre, tc::smem_desc(ah + o, LBO, SBO), dbl, idesc, 1u);
-                tc::mma_tf32(tre, tc::smem_desc(al + o, LBO, SBO), dbh, idesc, 1u);
-                tc::mma_tf32(tim, tc::smem_desc(th + o, LBO, SBO), dbh, idesc, acc);
-                tc::mma_tf32(tim, tc::smem_desc(th + o, LBO, SBO), dbl, idesc, 1u);
-                tc::mma_tf32(tim, tc::smem_desc(tl + o, LBO, SBO), dbh, idesc, 1u);
+                for (int kk = 0; kk < KC / 8; ++kk) {
+                    const uint64_t o = (uint64_t)kk * 16;  // 256-byte k-step in the 16-byte address field
+                    const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+                    tc::mma_tf32(tre, dAh + o, dBh + o, idesc, acc);
+                    tc::mma_tf32(tre, dAh + o, dBl + o, idesc, 1u);
+                    tc::mma_tf32(tre, dAl + o, dBh + o, idesc, 1u);
+                    tc::mma_tf32(tim, dAh + o, dPh + o, idesc, acc);
+                    tc::mma_tf32(tim, dAh + o, dPl + o, idesc, 1u);
+                    tc::mma_tf32(tim, dAl + o, dPh + o, idesc, 1u);
+                }
+                tc::commit(&tile_empty[st]);
             }
-            tc::commit(&mbar[st]);
+            tc::commit(&acc_full);
         }
-    }
-    // drain: the last one or two chunks' commits
-    for (int st = 0; st < 2; ++st) {
-        const int used = nchunks > st ? (nchunks - 1 - st) / 2 + 1 : 0;  // chunks that used stage st
-        const int waited = nchunks > st + 2 ? (nchunks - st - 2 + 1) / 2 : 0;
-        if (used > waited) tc::mbar_wait(&mbar[st], phase[st]);
-    }
-    tc::fence_after_sync();
-    // epilogue: warps 0-3 read Re, warps 4-7 read Im; warp w owns TMEM lanes 32*(w%4)..
-    const int q = warp % 4;
-    const bool im = warp >= 4;
-    const int x = x0 + 32 * q + lane;
-    float2* ob = out + set * (int64_t)d.D * d.D;
-    for (int c0 = 0; c0 < 128; c0 += 16) {
-        float v[16];
-        tc::tmem_ld16((im ? tim : tre) + ((uint32_t)(32 * q) << 16) + c0, v);
-        if (x < d.D) {
+        __syncwarp();
+    } else {
+        // ---------------- converters (256 threads): 16-byte units (2 complex) of the raw blocks
+        for (int c = 0; c < nch; ++c) {
+            const int rs = c % 3, ru = c / 3, ts = c & 1, tu = c >> 1;
+            tc::mbar_wait(&raw_full[rs], ru & 1);
+            if (tu > 0) tc::mbar_wait(&tile_empty[ts], (tu - 1) & 1);
+            const unsigned char* rx = raw + (size_t)rs * 2 * RAW;
+            const unsigned char* ry = diag ? rx : rx + RAW;
+            unsigned char* tb = tiles + (size_t)ts * 6 * TILE;
+            constexpr int UNITS = kGT * T1 / 2;  // float4 units per block
+            for (int u = tid; u < UNITS; u += 256) {
+                const int r = u / (T1 / 2), k4 = (u % (T1 / 2)) * 4;  // row, first real K of the unit
+                const uint32_t o = (uint32_t)((r >> 3) * SBO + (k4 >> 2) * 128 + (r & 7) * 16);
+                float4 v = r < nx ? reinterpret_cast<const float4*>(rx)[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 h, l;
+                tc::split_tf32_rn(v.x, h.x, l.x);
+                tc::split_tf32_rn(v.y, h.y, l.y);
+                tc::split_tf32_rn(v.z, h.z, l.z);
+                tc::split_tf32_rn(v.w, h.w, l.w);
+                *reinterpret_cast<float4*>(tb + o) = h;
+                *reinterpret_cast<float4*>(tb + TILE + o) = l;
+                if (!diag) {
+                    v = r < ny ? reinterpret_cast<const float4*>(ry)[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    tc::split_tf32_rn(v.x, h.x, l.x);
+                    tc::split_tf32_rn(v.y, h.y, l.y);
+                    tc::split_tf32_rn(v.z, h.z, l.z);
+                    tc::split_tf32_rn(v.w, h.w, l.w);
+                }
+                *reinterpret_cast<float4*>(tb + 2 * TILE + o) = h;
+                *reinterpret_cast<float4*>(tb + 3 * TILE + o) = l;
+                // P = [-vi, vr] per complex
+                *reinterpret_cast<float4*>(tb + 4 * TILE + o) = make_float4(-h.y, h.x, -h.w, h.z);
+                *reinterpret_cast<float4*>(tb + 5 * TILE + o) = make_float4(-l.y, l.x, -l.w, l.z);
+            }
+            tc::fence_async_shared();
+            tc::mbar_arrive(&tile_full[ts]);
+            tc::mbar_arrive(&raw_empty[rs]);
+        }
+        // ---------------- epilogue
+        tc::mbar_wait(&acc_full, 0);
+        tc::fence_after_sync();
+        const int q = warp % 4;
+        const bool im = warp >= 4;
+        const int x = x0 + 32 * q + lane;
+        float2* ob = out + set * (int64_t)d.D * d.D;
+        for (int c0 = 0; c0 < kGT; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16((im ? tim : tre) + ((uint32_t)(32 * q) << 16) + c0, v);
+            if (x < d.D) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int y = y0 + c0 + i;
-                if (y < d.D) {
-                    float* o = reinterpret_cast<float*>(ob + x + (int64_t)d.D * y);
-                    o[im ? 1 : 0] = v[i];
+                for (int i = 0; i < 16; ++i) {
+                    const int y = y0 + c0 + i;
+                    if (y < d.D) reinterpret_cast<float*>(ob + x + (int64_t)d.D * y)[im ? 1 : 0] = v[i];
                 }
             }
         }
     }
     tc::fence_before_sync();
     __syncthreads();
+    tc::fence_after_sync();
     if (warp == 0) tc::tmem_dealloc(tmem_base, 256);
+}
+
+bool gram_tc_fits(const GramDesc& d) {
+    return d.xs == d.T1 && d.t1s == 1 && (d.T1 == 4 || d.T1 == 8) && d.D >= 128 && d.D % 8 == 0;
 }
 
 cudaError_t launch_gram_tc(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V,
                            void* out, cudaStream_t st) {
-    const size_t sm = 2 * 6 * 128 * 32 * 4;  // 192 KB: two stages x six 16 KB operand tiles
-    cudaError_t e = cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    const int tiles = (d.D + 127) / 128;
-    dim3 grid(tiles * tiles, (unsigned)(ngroups * sets_per_group));
-    k_gram_tc<<<grid, 256, sm, st>>>(t, d, sets_per_group, (const float2*)V, (float2*)out);
+    if (!gram_tc_fits(d)) return cudaErrorNotSupported;
+    const int tiles = (d.D + kGT - 1) / kGT;
+    dim3 grid(tiles * (tiles + 1) / 2, (unsigned)(ngroups * sets_per_group));
+    cudaError_t e;
+#define GWT_GTC(TT)                                                                                                \
+    do {                                                                                                           \
+        const size_t sm = 6 * (size_t)kGT * TT * 8 + 2 * 6 * (size_t)kGT * 2 * TT * 4;                             \
+        e = cudaFuncSetAttribute(k_gram_tcb<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);            \
+        if (e != cudaSuccess) return e;                                                                            \
+        k_gram_tcb<TT><<<grid, kGTThreads, sm, st>>>(t, d, sets_per_group, (const float2*)V, (float2*)out);        \
+    } while (0)
+    if (d.T1 == 8) GWT_GTC(8);
+    else GWT_GTC(4);
+#undef GWT_GTC
     return cudaGetLastError();
 }
 

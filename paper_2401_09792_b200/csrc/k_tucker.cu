@@ -562,11 +562,14 @@ cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, cons
 template <class T>
 cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V, void* out,
                         void* part, size_t part_bytes, cudaStream_t st) {
-    // complex64 Grams with D >= 64 on the tensor cores (3xTF32 tcgen05, k_tc.cu): opt-in (GWT_GRAM_TC=1)
-    // until its staging pipeline beats the CUDA-core kernel
-    if (sizeof(T) == 4 && d.D >= 64) {
-        const char* e = std::getenv("GWT_GRAM_TC");
-        if (e && std::atoi(e) != 0) return launch_gram_tc(t, d, ngroups, sets_per_group, V, out, st);
+    // complex64 Grams whose rows are contiguous blocks (the tx Gram of W2, N >= 128: C3, C4, C5) on the tensor
+    // cores (k_tc.cu, TMA bulk-staged 3xTF32); GWT_GRAM_TC=0 keeps the CUDA-core kernel
+    if (sizeof(T) == 4 && gram_tc_fits(d)) {
+        static const bool tc_on = [] {
+            const char* e = std::getenv("GWT_GRAM_TC");
+            return !(e && std::atoi(e) == 0);
+        }();
+        if (tc_on) return launch_gram_tc(t, d, ngroups, sets_per_group, V, out, st);
     }
     if (d.D <= 8 && d.xs == 1) {
         const unsigned blocks = (unsigned)(ngroups * sets_per_group);

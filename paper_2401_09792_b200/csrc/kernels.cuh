@@ -66,6 +66,7 @@ cudaError_t launch_objective(int64_t ngroups, const double* energy, const double
                              int slot, cudaStream_t st);
 template <class T> cudaError_t launch_broadcast(const void* src, void* dst, int64_t elems, int copies, int64_t ngroups,
                                                 cudaStream_t st);
+bool gram_tc_fits(const GramDesc& d);  // k_tc.cu: rows = contiguous T1-complex blocks (tx Gram of W2), D >= 128
 cudaError_t launch_gram_tc(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V,
                            void* out, cudaStream_t st);  // k_tc.cu (c64, 3xTF32 tcgen05)
 // k_eig.cu
