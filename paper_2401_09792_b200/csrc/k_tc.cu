@@ -118,46 +118,46 @@ __device__ __forceinline__ int tc_set_link(const Topo& t, int kind, int s, int r
 // (GramDesc xs == T1, t1s == 1): the transmit-mode Gram of W2 = Y1 x1 A^H ([link][p][N][m], T1 = m,
 // decompose.cpp:160-176), Out[set](x, y) = sum over the set's links and t2 of V(x, :) V(y, :)^H.
 //
-// One CTA per (128 x 128 lower tile pair, set). For every (link, t2) chunk the x rows of the tile
-// are one contiguous 128 T1-complex block, so
-//   warp 8 (one thread): TMA bulk copy of the raw x / y blocks (cp.async.bulk, 3 raw stages);
-//   warps 0-7          : convert raw -> canonical K-major tf32 operand tiles, 3xTF32 split:
-//                        A = [vr, vi] (x rows), B = [vr, vi] and P = [-vi, vr] (y rows), hi / lo each
-//                        (2 tile stages);
-//   warp 9 (one thread): 12 tcgen05.mma per chunk: Re += A_h B_h + A_h B_l + A_l B_h and
-//                        Im += A_h P_h + A_h P_l + A_l P_h (M = N = 128, K = 2 T1), accumulators in TMEM;
-//   warps 0-7          : epilogue, TMEM -> Gram tile (Re warps 0-3, Im warps 4-7).
+// One CTA per (128-row x strip, set): the B operand is rows [0, nb) with nb = 128 (xt + 1) (so the strip
+// covers every y <= x, the lower triangle, with no wasted tile) and the A operand is the strip's own rows,
+// i.e. the last 128 rows of the B tile (descriptor offset, no separate A tile). Per (link, t2) chunk the nb
+// rows are ONE contiguous block of nb T1 complex values:
+//   warp 8 (one thread): TMA bulk copy of the raw block (cp.async.bulk, 3 raw stages);
+//   warps 0-7          : convert raw -> canonical K-major tf32 tiles, 3xTF32 split: B = [vr, vi] and
+//                        P = [-vi, vr], hi / lo each (2 tile stages);
+//   warp 9 (one thread): 12 tcgen05.mma per chunk (M = 128, N = nb <= 256, K = 2 T1):
+//                        Re += A_h B_h + A_h B_l + A_l B_h, Im += A_h P_h + A_h P_l + A_l P_h, TMEM;
+//   warps 0-7          : epilogue, TMEM -> Gram strip (Re warps 0-3, Im warps 4-7).
+// N = 256 halves the shared-memory operand bytes per MAC of 128 x 128 tiles (the previous form was
+// shared-pipe bound at 52 % with the tensor pipe at 34 %).
 namespace {
 constexpr int kGT = 128;
 constexpr int kGTThreads = 320;
+constexpr int kGMaxRows = 256;
 }  // namespace
 
 template <int T1>
 __global__ void __launch_bounds__(kGTThreads, 1) k_gram_tcb(Topo t, GramDesc d, int sets_per_group,
                                                            const float2* __restrict__ V, float2* __restrict__ out) {
     constexpr int KC = 2 * T1;                             // real K per chunk
-    constexpr uint32_t TILE = kGT * KC * 4;                // one operand tile (bytes)
-    constexpr uint32_t RAW = kGT * T1 * 8;                 // one raw block
+    constexpr uint32_t TILE = kGMaxRows * KC * 4;          // one operand tile of up to 256 rows (bytes)
+    constexpr uint32_t RAW = kGMaxRows * T1 * 8;           // one raw block of up to 256 rows
     constexpr uint32_t SBO = (KC / 4) * 128;
     extern __shared__ __align__(1024) unsigned char smem[];
-    unsigned char* raw = smem;                              // [3][x | y] RAW each
-    unsigned char* tiles = smem + 6 * RAW;                  // [2][Ah Al Bh Bl Ph Pl] TILE each
+    unsigned char* raw = smem;                              // [3] RAW each
+    unsigned char* tiles = smem + 3 * RAW;                  // [2][Bh Bl Ph Pl] TILE each
     __shared__ uint64_t raw_full[3], raw_empty[3], tile_full[2], tile_empty[2], acc_full;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int64_t set = blockIdx.y;
     const int64_t g = set / sets_per_group;
     const int s = (int)(set % sets_per_group);
-    // lower tile pair index -> (xt >= yt)
-    int xt = 0, rem = blockIdx.x;
-    while (rem > xt) { rem -= xt + 1; ++xt; }
-    const int yt = rem;
-    const int x0 = xt * kGT, y0 = yt * kGT;
-    const bool diag = xt == yt;
-    const int nx = min(kGT, d.D - x0), ny = min(kGT, d.D - y0);
+    const int xt = blockIdx.x, x0 = xt * kGT;
+    const int nb = min(kGT * (xt + 1), d.D);                // B rows: [0, nb)
+    const int nbp = (nb + 15) / 16 * 16;                     // MMA N (multiple of 16)
     const int nl = tc_set_size(t, d.set_kind);
     const int nch = nl * d.T2;
-    if (warp == 0) tc::tmem_alloc(&tmem_base, 256);
+    if (warp == 0) tc::tmem_alloc(&tmem_base, 512);
     if (tid == 0) {
         for (int i = 0; i < 3; ++i) {
             tc::mbar_init(&raw_full[i], 1);
@@ -173,37 +173,35 @@ __global__ void __launch_bounds__(kGTThreads, 1) k_gram_tcb(Topo t, GramDesc d, 
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    const uint32_t tre = tmem_base, tim = tmem_base + 128;
-    auto src_block = [&](int c, int r0) -> const float2* {
-        const int li = c / d.T2, t2 = c % d.T2;
-        const int l = tc_set_link(t, d.set_kind, s, li);
-        return V + (g * t.links() + l) * d.v_item + (int64_t)t2 * d.t2s + (int64_t)r0 * T1;
-    };
+    const uint32_t tre = tmem_base, tim = tmem_base + 256;
     if (warp == 8) {
         // ---------------- TMA producer
         if (lane == 0) {
+            const uint32_t bytes = (uint32_t)nb * T1 * 8;
             for (int c = 0; c < nch; ++c) {
                 const int st = c % 3, use = c / 3;
                 if (use > 0) tc::mbar_wait(&raw_empty[st], (use - 1) & 1);
-                const uint32_t bx = (uint32_t)nx * T1 * 8, by = diag ? 0u : (uint32_t)ny * T1 * 8;
-                tc::mbar_arrive_expect_tx(&raw_full[st], bx + by);
-                tc::bulk_g2s(raw + (size_t)st * 2 * RAW, src_block(c, x0), bx, &raw_full[st]);
-                if (!diag) tc::bulk_g2s(raw + (size_t)st * 2 * RAW + RAW, src_block(c, y0), by, &raw_full[st]);
+                const int li = c / d.T2, t2 = c % d.T2;
+                const int l = tc_set_link(t, d.set_kind, s, li);
+                tc::mbar_arrive_expect_tx(&raw_full[st], bytes);
+                tc::bulk_g2s(raw + (size_t)st * RAW, V + (g * t.links() + l) * d.v_item + (int64_t)t2 * d.t2s, bytes,
+                             &raw_full[st]);
             }
         }
         __syncwarp();
     } else if (warp == 9) {
         // ---------------- MMA issuer
         if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_tf32(kGT, kGT);
+            const uint32_t idesc = tc::idesc_tf32(kGT, nbp);
+            const uint32_t aoff = (uint32_t)(x0 / 8) * SBO;  // the strip's rows inside the B tiles
             for (int c = 0; c < nch; ++c) {
                 const int st = c & 1, use = c >> 1;
                 tc::mbar_wait(&tile_full[st], use & 1);
                 tc::fence_after_sync();
-                const uint32_t b0 = tc::smem_u32(tiles + (size_t)st * 6 * TILE);
-                const uint64_t dAh = tc::smem_desc(b0, 128, SBO), dAl = tc::smem_desc(b0 + TILE, 128, SBO);
-                const uint64_t dBh = tc::smem_desc(b0 + 2 * TILE, 128, SBO), dBl = tc::smem_desc(b0 + 3 * TILE, 128, SBO);
-                const uint64_t dPh = tc::smem_desc(b0 + 4 * TILE, 128, SBO), dPl = tc::smem_desc(b0 + 5 * TILE, 128, SBO);
+                const uint32_t b0 = tc::smem_u32(tiles + (size_t)st * 4 * TILE);
+                const uint64_t dBh = tc::smem_desc(b0, 128, SBO), dBl = tc::smem_desc(b0 + TILE, 128, SBO);
+                const uint64_t dPh = tc::smem_desc(b0 + 2 * TILE, 128, SBO), dPl = tc::smem_desc(b0 + 3 * TILE, 128, SBO);
+                const uint64_t dAh = tc::smem_desc(b0 + aoff, 128, SBO), dAl = tc::smem_desc(b0 + TILE + aoff, 128, SBO);
 #pragma unroll
                 for (int kk = 0; kk < KC / 8; ++kk) {
                     const uint64_t o = (uint64_t)kk * 16;  // 256-byte k-step in the 16-byte address field
@@ -221,19 +219,18 @@ __global__ void __launch_bounds__(kGTThreads, 1) k_gram_tcb(Topo t, GramDesc d, 
         }
         __syncwarp();
     } else {
-        // ---------------- converters (256 threads): 16-byte units (2 complex) of the raw blocks
+        // ---------------- converters (256 threads): 16-byte units (2 complex) of the raw block
+        const int units = nbp * T1 / 2;
         for (int c = 0; c < nch; ++c) {
             const int rs = c % 3, ru = c / 3, ts = c & 1, tu = c >> 1;
             tc::mbar_wait(&raw_full[rs], ru & 1);
             if (tu > 0) tc::mbar_wait(&tile_empty[ts], (tu - 1) & 1);
-            const unsigned char* rx = raw + (size_t)rs * 2 * RAW;
-            const unsigned char* ry = diag ? rx : rx + RAW;
-            unsigned char* tb = tiles + (size_t)ts * 6 * TILE;
-            constexpr int UNITS = kGT * T1 / 2;  // float4 units per block
-            for (int u = tid; u < UNITS; u += 256) {
+            const float4* rv = reinterpret_cast<const float4*>(raw + (size_t)rs * RAW);
+            unsigned char* tb = tiles + (size_t)ts * 4 * TILE;
+            for (int u = tid; u < units; u += 256) {
                 const int r = u / (T1 / 2), k4 = (u % (T1 / 2)) * 4;  // row, first real K of the unit
                 const uint32_t o = (uint32_t)((r >> 3) * SBO + (k4 >> 2) * 128 + (r & 7) * 16);
-                float4 v = r < nx ? reinterpret_cast<const float4*>(rx)[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 v = r < nb ? rv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
                 float4 h, l;
                 tc::split_tf32_rn(v.x, h.x, l.x);
                 tc::split_tf32_rn(v.y, h.y, l.y);
@@ -241,38 +238,30 @@ __global__ void __launch_bounds__(kGTThreads, 1) k_gram_tcb(Topo t, GramDesc d, 
                 tc::split_tf32_rn(v.w, h.w, l.w);
                 *reinterpret_cast<float4*>(tb + o) = h;
                 *reinterpret_cast<float4*>(tb + TILE + o) = l;
-                if (!diag) {
-                    v = r < ny ? reinterpret_cast<const float4*>(ry)[u] : make_float4(0.f, 0.f, 0.f, 0.f);
-                    tc::split_tf32_rn(v.x, h.x, l.x);
-                    tc::split_tf32_rn(v.y, h.y, l.y);
-                    tc::split_tf32_rn(v.z, h.z, l.z);
-                    tc::split_tf32_rn(v.w, h.w, l.w);
-                }
-                *reinterpret_cast<float4*>(tb + 2 * TILE + o) = h;
-                *reinterpret_cast<float4*>(tb + 3 * TILE + o) = l;
                 // P = [-vi, vr] per complex
-                *reinterpret_cast<float4*>(tb + 4 * TILE + o) = make_float4(-h.y, h.x, -h.w, h.z);
-                *reinterpret_cast<float4*>(tb + 5 * TILE + o) = make_float4(-l.y, l.x, -l.w, l.z);
+                *reinterpret_cast<float4*>(tb + 2 * TILE + o) = make_float4(-h.y, h.x, -h.w, h.z);
+                *reinterpret_cast<float4*>(tb + 3 * TILE + o) = make_float4(-l.y, l.x, -l.w, l.z);
             }
             tc::fence_async_shared();
             tc::mbar_arrive(&tile_full[ts]);
             tc::mbar_arrive(&raw_empty[rs]);
         }
-        // ---------------- epilogue
+        // ---------------- epilogue: rows x of the strip, columns y < nb (the strictly lower part and the whole
+        // diagonal block, as the CUDA-core Gram writes them)
         tc::mbar_wait(&acc_full, 0);
         tc::fence_after_sync();
         const int q = warp % 4;
         const bool im = warp >= 4;
         const int x = x0 + 32 * q + lane;
         float2* ob = out + set * (int64_t)d.D * d.D;
-        for (int c0 = 0; c0 < kGT; c0 += 16) {
+        for (int c0 = 0; c0 < nbp; c0 += 16) {
             float v[16];
             tc::tmem_ld16((im ? tim : tre) + ((uint32_t)(32 * q) << 16) + c0, v);
             if (x < d.D) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    const int y = y0 + c0 + i;
-                    if (y < d.D) reinterpret_cast<float*>(ob + x + (int64_t)d.D * y)[im ? 1 : 0] = v[i];
+                    const int y = c0 + i;
+                    if (y < nb && (y <= x || y >= x0)) reinterpret_cast<float*>(ob + x + (int64_t)d.D * y)[im ? 1 : 0] = v[i];
                 }
             }
         }
@@ -280,22 +269,22 @@ __global__ void __launch_bounds__(kGTThreads, 1) k_gram_tcb(Topo t, GramDesc d, 
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
-    if (warp == 0) tc::tmem_dealloc(tmem_base, 256);
+    if (warp == 0) tc::tmem_dealloc(tmem_base, 512);
 }
 
 bool gram_tc_fits(const GramDesc& d) {
-    return d.xs == d.T1 && d.t1s == 1 && (d.T1 == 4 || d.T1 == 8) && d.D >= 128 && d.D % 8 == 0;
+    return d.xs == d.T1 && d.t1s == 1 && (d.T1 == 4 || d.T1 == 8) && d.D >= 128 && d.D <= kGMaxRows && d.D % 8 == 0;
 }
 
 cudaError_t launch_gram_tc(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V,
                            void* out, cudaStream_t st) {
     if (!gram_tc_fits(d)) return cudaErrorNotSupported;
-    const int tiles = (d.D + kGT - 1) / kGT;
-    dim3 grid(tiles * (tiles + 1) / 2, (unsigned)(ngroups * sets_per_group));
+    const int strips = (d.D + kGT - 1) / kGT;
+    dim3 grid(strips, (unsigned)(ngroups * sets_per_group));
     cudaError_t e;
 #define GWT_GTC(TT)                                                                                                \
     do {                                                                                                           \
-        const size_t sm = 6 * (size_t)kGT * TT * 8 + 2 * 6 * (size_t)kGT * 2 * TT * 4;                             \
+        const size_t sm = 3 * (size_t)kGMaxRows * TT * 8 + 2 * 4 * (size_t)kGMaxRows * 2 * TT * 4;                 \
         e = cudaFuncSetAttribute(k_gram_tcb<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);            \
         if (e != cudaSuccess) return e;                                                                            \
         k_gram_tcb<TT><<<grid, kGTThreads, sm, st>>>(t, d, sets_per_group, (const float2*)V, (float2*)out);        \
