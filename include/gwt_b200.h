@@ -68,7 +68,11 @@ typedef enum { GWT_MEM_HOST = 0, GWT_MEM_DEVICE = 1 } gwt_mem;
 typedef enum { GWT_SCOPE_FULL = 0, GWT_SCOPE_PAPER = 1 } gwt_scope; /* InterferenceScope channel.hpp:33 */
 
 /* Per-(subcarrier, user) outcome of the batched SINR; the C++ wrapper rethrows
- * the reference's exception for the first failing item in reference order. */
+ * the reference's exception for the first failing item in reference order. The low
+ * byte is the code; GWT_ITEM_NEG_DENOM carries the first failing stream r in bits
+ * 8+ (status = 3 + 256 r) for the reference's "... negative for stream r ..." text.
+ * GWT_ITEM_RANK_DEFICIENT raises nothing (the reference's SVD completes such a
+ * precoder with arbitrary null-space columns; the Gram route flags the item). */
 typedef enum {
     GWT_ITEM_OK = 0,
     GWT_ITEM_NOT_PD = 1,        /* "woodbury_inverse_apply: covariance is numerically singular" sinr.cpp:211-212 */

@@ -45,7 +45,8 @@ SCOPE = {"full": L.GWT_SCOPE_FULL, "paper_experiment": L.GWT_SCOPE_PAPER}
 ITEM_ERRORS = {
     1: (NumericalError, "woodbury_inverse_apply: covariance is numerically singular"),
     2: (NumericalError, "woodbury_inverse_apply: covariance is numerically singular (condition estimate above 1e14)"),
-    3: (NumericalError, "sinr: interference-plus-noise power is negative (numerically invalid configuration)"),
+    3: (NumericalError, "sinr: interference-plus-noise power is negative for stream {stream} (numerically invalid "
+                        "configuration)"),
     4: (InvalidArgument, "woodbury_inverse_apply: non-finite input"),
 }
 
@@ -134,11 +135,20 @@ class SinrReport:
     def raise_first_error(self):
         """Rethrow the reference's exception for the first failing (subcarrier, user) in reference order."""
         st = self.status.cpu().numpy() if hasattr(self.status, "cpu") else np.asarray(self.status)
-        bad = np.flatnonzero((st != 0) & (st != 5))
+        code = st & 0xFF  # status code; code 3 carries the first failing stream in bits 8+
+        bad = np.flatnonzero((code != 0) & (code != 5))
         if bad.size:
-            code = int(st.reshape(-1)[bad[0]])
-            exc, msg = ITEM_ERRORS[code]
-            raise exc(msg)
+            v = int(st.reshape(-1)[bad[0]])
+            exc, msg = ITEM_ERRORS[v & 0xFF]
+            raise exc(msg.format(stream=v >> 8))
+
+    @property
+    def rank_deficient(self):
+        """Items whose interfering anchor had a zero singular value among its L kept streams (status 5): the
+        reference's SVD completes that precoder with arbitrary null-space columns, which the Gram route cannot
+        reproduce; the reference raises nothing there, so neither does raise_first_error."""
+        st = self.status.cpu().numpy() if hasattr(self.status, "cpu") else np.asarray(self.status)
+        return (st & 0xFF) == 5
 
 
 # ---------------------------------------------------------------------------

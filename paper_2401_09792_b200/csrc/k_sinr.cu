@@ -762,7 +762,7 @@ __device__ __forceinline__ void mmse_item(const Topo& t, int scope, int S, int64
         }
         const double sp = gamma * gamma;
         double den = gamma * (1.0 - gamma);  // w^H Q w - |w^H g|^2
-        if (den <= -1e-12 && st == 0) st = 3;
+        if (den <= -1e-12 && st == 0) st = 3 + (r << 8);  // code 3, first failing stream in bits 8+
         den = fmax(den, 2.2250738585072014e-308);
         so[r] = sp / den;
         sg[r] = sp;
@@ -1092,8 +1092,9 @@ __global__ void __launch_bounds__(256) k_small_grp(Topo t, int scope, int S, int
     }
     // status: lanes agree on 5/4/1/2; a negative denominator (3) can come from any stream lane
     {
-        const unsigned any3 = __ballot_sync(0xffffffffu, st == 3);
-        if (valid && j == 0) status[orow] = (st == 0 && ((any3 >> base) & 0xffu)) ? 3 : st;
+        // code 3 carries the first failing stream (the lowest lane) in bits 8+
+        const unsigned m3 = (__ballot_sync(0xffffffffu, st == 3) >> base) & 0xffu;
+        if (valid && j == 0) status[orow] = ((st == 0 || st == 3) && m3) ? 3 + ((__ffs(m3) - 1) << 8) : st;
     }
 }
 

@@ -601,8 +601,9 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
         sinr[orow * L + r] = sp / den;
         signal[orow * L + r] = sp;
     }
-    const unsigned any3 = __ballot_sync(0xffffffffu, st3 == 3);
-    if (active && r == 0) status[orow] = (st == 0 && (any3 & seg_mask<MP>(lane))) ? 3 : st;
+    // code 3 carries the first failing stream (the user's lowest lane) in bits 8+
+    const unsigned m3 = (__ballot_sync(0xffffffffu, st3 == 3) & seg_mask<MP>(lane)) >> (lane & ~(MP - 1));
+    if (active && r == 0) status[orow] = (st == 0 && m3) ? 3 + ((__ffs(m3) - 1) << 8) : st;
 }
 
 bool sinr_users_fits(const Topo& t, size_t csize) {

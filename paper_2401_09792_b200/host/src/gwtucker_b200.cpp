@@ -926,14 +926,19 @@ void pack_compressed(const GroupwiseFactorSet& f, std::vector<Cplx>& C, std::vec
     }
 }
 
-const char* item_error(int st, bool& runtime) {
-    runtime = st != 4;
-    switch (st) {
+// per-item status of the batched kernels -> the reference's exception text (sinr.cpp:28-43, 205-227); code 3
+// carries the first failing stream in bits 8+; code 5 (rank-deficient anchor precoder) raises nothing, as in
+// the reference
+std::string item_error(int st, bool& runtime) {
+    runtime = (st & 0xFF) != 4;
+    switch (st & 0xFF) {
         case 1: return "woodbury_inverse_apply: covariance is numerically singular";
         case 2: return "woodbury_inverse_apply: covariance is numerically singular (condition estimate above 1e14)";
-        case 3: return "sinr: interference-plus-noise power is negative (numerically invalid configuration)";
+        case 3:
+            return "sinr: interference-plus-noise power is negative for stream " + std::to_string(st >> 8) +
+                   " (numerically invalid configuration)";
         case 4: return "woodbury_inverse_apply: non-finite input";
-        default: return nullptr;
+        default: return std::string();
     }
 }
 
@@ -1008,7 +1013,8 @@ std::vector<SinrReport> run_compressed_pipeline_batched(const SystemTopology& to
                                      sig.data(), st.data(), &led));
     for (std::size_t i = 0; i < st.size(); ++i) {  // first failure in reference order (grid, then i, then j)
         bool runtime = false;
-        if (const char* msg = item_error(st[i], runtime)) {
+        const std::string msg = item_error(st[i], runtime);
+        if (!msg.empty()) {
             if (runtime) throw std::runtime_error(msg);
             throw std::invalid_argument(msg);
         }
@@ -1065,7 +1071,8 @@ SinrReport run_full_pipeline(const ChannelSet& channels, InterferenceScope scope
                         st.data(), &led));
     for (std::size_t i = 0; i < st.size(); ++i) {
         bool runtime = false;
-        if (const char* msg = item_error(st[i], runtime)) {
+        const std::string msg = item_error(st[i], runtime);
+        if (!msg.empty()) {
             if (runtime) throw std::runtime_error(msg);
             throw std::invalid_argument(msg);
         }
