@@ -536,6 +536,24 @@ def run_gpu_config(gw, O, torch, cfg, ctx, dev, stream, flush, rank, world, step
     return res
 
 
+def c5_sweep(gw, torch, ctx, dev, groups=64):
+    """The storage / error trade-off of BASELINE configs[4] on `groups` C5 groups, all 816 subcarriers: one
+    run_sweep per axis (n with p = 16, p with n = 64), 20 ALS sweeps per point (paper_2401_09792_b200.sweep)."""
+    from paper_2401_09792_b200 import sweep
+    cfg = gw.CONFIGS["C5"]
+    X, tau = gw.generate_channels(cfg.topology(), groups, seed=0, dtype=np.complex64, nthreads=host_cores())
+    Xd, taud = torch.from_numpy(X).to(dev), torch.from_numpy(tau).to(dev)
+    fd = torch.from_numpy(cfg.freqs()).to(dev)
+    out = {"groups": groups, "subcarriers": cfg.F, "sweeps": cfg.sweeps,
+           "columns": "value, R_s (storage ratio), R_t (t_full / t_compressed, device), e_c (mean rel. SINR error), "
+                      "nmse, t_full_ms, t_compressed_ms, tucker_ms"}
+    for axis, values in (("n", (16, 32, 64, 96)), ("p", (8, 16, 32))):
+        rows = sweep.run_sweep(ctx, cfg.topology(), cfg.ranks(), axis, values, Xd, taud, fd, sweeps=cfg.sweeps,
+                               repetitions=3)
+        out[axis] = [[r.value, r.r_s, r.r_t, r.e_c, r.nmse, r.t_full_ms, r.t_compressed_ms, r.tucker_ms] for r in rows]
+    return out
+
+
 def e2e_sinr(gw, torch, cfg, fac, tau_h, local, warmup, steps):
     """SINR step through the public API with pinned host buffers (copies inside the timed region)."""
     topo, ranks = cfg.topology(), cfg.ranks()
@@ -680,6 +698,14 @@ def main(argv=None):
             except Exception as ex:  # a secondary config must not hide the headline line
                 extra[name] = {"error": f"{type(ex).__name__}: {ex}"}
             torch.cuda.empty_cache()
+
+    # ---------------- C5 rank sweep (BASELINE configs[4]: n in {16,32,64,96}, p in {8,16,32}; runner.cpp:193-211)
+    if world == 1 and args.extra and "C5" in args.extra.split(","):
+        try:
+            extra["C5_sweep"] = c5_sweep(gw, torch, ctx, dev)
+        except Exception as ex:  # a secondary line must not hide the headline
+            extra["C5_sweep"] = {"error": f"{type(ex).__name__}: {ex}"}
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

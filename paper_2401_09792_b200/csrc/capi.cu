@@ -33,8 +33,44 @@ void ck(cudaError_t e, const char* what) {
 
 }  // namespace
 
+// Tuning switches, read from the environment ONCE when the context is created (INTEGRATION.md lists them)
+struct GwtOptions {
+    int64_t ws_bytes = int64_t(16) << 30;  // GWT_WS_BYTES: workspace budget for Tucker intermediates
+    int solve_lanes = 4;                   // GWT_SOLVE_LANES
+    bool solve_side = true;                // GWT_SOLVE_NO_SIDE unset
+    bool poll = true;                      // GWT_NO_POLL unset
+    int eig64_min_d = 1 << 30;             // GWT_EIG64_MIN_D
+    bool gram_tc = true;                   // GWT_GRAM_TC != 0
+    int sinr_path = 0;                     // GWT_SINR_PATH: 0 auto, 1 tc, 2 users, 3 pg
+    int64_t sinr_chunk_bytes = int64_t(2) << 30;  // GWT_SINR_CHUNK_BYTES
+    int sinr_pipeline = 4;                 // GWT_SINR_PIPELINE: host-path group chunks
+    int sinr_dev_lanes = 0;                // GWT_SINR_DEV_LANES (0: by path)
+    int sinr_lanes = 0;                    // GWT_SINR_LANES: host-path compute lanes (0: by path)
+    bool sinr_copy_streams = true;         // GWT_SINR_COPY_STREAMS != 0
+    bool pg_small = false;                 // GWT_PG_SMALL: m > 4 tensor path -> the 8-lanes Jacobi solver
+    void read() {
+        auto num = [](const char* k, int64_t& v) { if (const char* e = std::getenv(k)) v = std::strtoll(e, nullptr, 10); };
+        auto inum = [](const char* k, int& v) { if (const char* e = std::getenv(k)) v = std::atoi(e); };
+        num("GWT_WS_BYTES", ws_bytes);
+        inum("GWT_SOLVE_LANES", solve_lanes);
+        solve_side = !std::getenv("GWT_SOLVE_NO_SIDE");
+        poll = !std::getenv("GWT_NO_POLL");
+        inum("GWT_EIG64_MIN_D", eig64_min_d);
+        if (const char* e = std::getenv("GWT_GRAM_TC")) gram_tc = std::atoi(e) != 0;
+        if (const char* e = std::getenv("GWT_SINR_PATH"))
+            sinr_path = !std::strcmp(e, "tc") ? 1 : !std::strcmp(e, "users") ? 2 : !std::strcmp(e, "pg") ? 3 : 0;
+        num("GWT_SINR_CHUNK_BYTES", sinr_chunk_bytes);
+        inum("GWT_SINR_PIPELINE", sinr_pipeline);
+        inum("GWT_SINR_DEV_LANES", sinr_dev_lanes);
+        inum("GWT_SINR_LANES", sinr_lanes);
+        if (const char* e = std::getenv("GWT_SINR_COPY_STREAMS")) sinr_copy_streams = std::atoi(e) != 0;
+        pg_small = std::getenv("GWT_PG_SMALL") != nullptr;
+    }
+};
+
 struct gwt_ctx {
     int device = 0;
+    GwtOptions opt;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
     std::string last_error;
@@ -113,11 +149,6 @@ enum {
     WS_STATUS, WS_MISC, WS_PART, WS_GPART, WS_STOP, WS_EIG64, WS_BREADY, WS_EREADY
 };
 
-size_t ws_budget() {
-    const char* e = std::getenv("GWT_WS_BYTES");
-    if (e) return static_cast<size_t>(std::strtoull(e, nullptr, 10));
-    return size_t(16) << 30;  // 16 GiB of the 180 GB HBM for intermediates
-}
 
 template <class F>
 int guarded(gwt_ctx* ctx, F&& f) {
@@ -226,13 +257,6 @@ struct SolveLane {
     size_t a_sz = 0, b_sz = 0, c_sz = 0, g_sz = 0;
 
     void* ws(int slot, size_t bytes) { return ctx->lws(lane, slot, bytes); }
-    static int eig64_min_d() {
-        static const int v = [] {
-            const char* e = std::getenv("GWT_EIG64_MIN_D");
-            return e ? std::atoi(e) : 1 << 30;
-        }();
-        return v;
-    }
     void gemm(const GemmDesc& d, const void* in, const void* U, void* out) {
         ctx->launched(launch_cgemm<T>(t, d, G, in, U, out, st));
     }
@@ -240,10 +264,10 @@ struct SolveLane {
         // copies > 0: pooled (one set per group) broadcast to `copies` factors
         const int users = t.users(), links = t.links();
         const int sets = d.set_kind == FI_USER ? users : d.set_kind == FI_BASE ? t.J : d.set_kind == FI_LINK ? links : 1;
-        ctx->launched(launch_gram<T>(t, d, G, sets, V, gram, gpart, gpart_bytes, st));
+        ctx->launched(launch_gram<T>(t, d, G, sets, V, gram, gpart, gpart_bytes, st, ctx->opt.gram_tc));
         void* dst = copies > 0 ? pool : out_factor;
         const int64_t batch = G * sets;
-        if (sizeof(T) == 4 && D > 8 && (D >= eig64_min_d() || (delay && D >= 64))) {
+        if (sizeof(T) == 4 && D > 8 && (D >= ctx->opt.eig64_min_d || (delay && D >= 64))) {
             // c64 Gram decomposed in binary64: the delay Gram carries the power-delay profile's graded
             // spectrum (p_q ~ e^-0.3q: 1e-3 at the 24th of 64 taps), and the fp32 Householder's eps32 ||A||
             // backward error moves its trailing kept eigenvectors (C4: NMSE +1.3e-6 vs the oracle; 6e-8 in
@@ -354,7 +378,7 @@ struct SolveLane {
         done = false;
         tail_pending = false;
         side = nullptr;
-        if (!early && sweeps > 0 && !std::getenv("GWT_SOLVE_NO_SIDE")) {
+        if (!early && sweeps > 0 && ctx->opt.solve_side) {
             side = ctx->side_stream(lane);
             evc = ctx->side_ev[lane][0];
             evo = ctx->side_ev[lane][1];
@@ -436,12 +460,7 @@ struct SolveLane {
     }
 };
 
-int solve_lanes() {
-    const char* e = std::getenv("GWT_SOLVE_LANES");
-    return e ? std::max(1, std::min(8, std::atoi(e))) : 4;
-}
-
-// Solve one chunk of G groups (device pointers) on up to solve_lanes() concurrent lanes.
+// Solve one chunk of G groups (device pointers) on up to ctx->opt.solve_lanes concurrent lanes.
 template <class T>
 void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int sweeps, unsigned flags, void* A, void* B,
                  void* Cf, void* Gc, double* trace_d, double* energy_d, std::vector<int>& iters, double* ms) {
@@ -451,7 +470,7 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
     const int64_t x_g = (int64_t)links * t.M * t.N * t.P, a_g = (int64_t)users * t.M * t.m,
                   b_g = (int64_t)t.J * t.N * t.n, c_g = (int64_t)links * t.P * t.p,
                   g_g = (int64_t)links * t.m * t.n * t.p;
-    const int L = (int)std::min<int64_t>(solve_lanes(), G);
+    const int L = (int)std::min<int64_t>(std::max(1, std::min(8, ctx->opt.solve_lanes)), G);
     while ((int)ctx->lanes.size() < L - 1) {
         gwt_ctx::Lane ln;
         ck(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -498,7 +517,7 @@ void solve_chunk(gwt_ctx* ctx, const Topo& t, int64_t G, const void* X, int swee
                 any = true;
             }
         if (!any) break;
-        if (early && s >= 1 && !std::getenv("GWT_NO_POLL"))
+        if (early && s >= 1 && ctx->opt.poll)
             for (auto& ln : lanes)
                 if (!ln.done) ln.poll(s - 1);
     }
@@ -547,7 +566,7 @@ void groupwise_solve_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_rank
                                     std::max({(int64_t)users * t.M * t.M, (int64_t)t.J * t.N * t.N,
                                               (int64_t)links * t.P * t.P}) * 3) +
                               (mem == GWT_MEM_HOST ? cs * (x_g + a_g + b_g + c_g + g_g) : 0);
-    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(ngroups, (int64_t)(ws_budget() / std::max<int64_t>(per_group, 1))));
+    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(ngroups, (int64_t)(ctx->opt.ws_bytes / std::max<int64_t>(per_group, 1))));
     double ms[2] = {0, 0};
     Timer tm(ctx);
     tm.mark(0);
@@ -657,12 +676,8 @@ struct StageEvents {
 
 // the tensor-core rebuild + pair-Gram path (k_rgram.cu) for large cores (m n >= 256: C3, C4, C5); the small
 // C2 cores (m n = 96) measured faster on the CUDA-core rebuild + pair-Gram kernels (0.54 vs 0.63 ms)
-bool tc_sinr_shape(const Topo& t) {
-    static const bool force = [] {
-        const char* p = std::getenv("GWT_SINR_PATH");
-        return p && std::strcmp(p, "tc") == 0;
-    }();
-    return rgram_fits(t) && (force || t.m * t.n >= 256);
+bool tc_sinr_shape(const gwt_ctx* ctx, const Topo& t) {
+    return rgram_fits(t) && (ctx->opt.sinr_path == 1 || t.m * t.n >= 256);
 }
 
 // Generic device pipeline (any scope) for ngroups groups on device pointers, on solver/SINR lane
@@ -677,22 +692,21 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
     const size_t cs = sizeof(Cx);
     const int links = t.links(), users = t.users();
     const int S = scope == GWT_SCOPE_PAPER ? t.J : t.J * t.K;
-    const char* path = std::getenv("GWT_SINR_PATH");
+    const int path = ctx->opt.sinr_path;
     {
         // generic path (any scope): rebuild -> pair Grams per subcarrier chunk sized so H~ stays resident in
         // L2 between producer and consumer; then ONE eig+MMSE launch over all subcarriers (full occupancy)
         const int64_t per_f_h = (int64_t)cs * ngroups * links * t.m * t.n;
-        const char* cb = std::getenv("GWT_SINR_CHUNK_BYTES");
         // (measured on C2: L2-sized chunks are slower - fewer CTAs per launch - so default to 2 GiB)
-        const int64_t chunk_bytes = cb ? std::atoll(cb) : (int64_t)(2ll << 30);
+        const int64_t chunk_bytes = ctx->opt.sinr_chunk_bytes;
         const int64_t Fc = std::max<int64_t>(1, std::min<int64_t>(F, chunk_bytes / std::max<int64_t>(per_f_h, 1)));
         // stage S: the per-user kernel (k_users.cu) for m > 4; for m <= 4 the pair-Gram route
         // (K2 + thread-per-user K3) measured faster (C2: 0.21 vs 0.31 ms). GWT_SINR_PATH=users|pg forces one.
-        const bool force_users = path && std::strcmp(path, "users") == 0, force_pg = path && std::strcmp(path, "pg") == 0;
+        const bool force_users = path == 2, force_pg = path == 3;
         const bool users_path = scope == GWT_SCOPE_PAPER && sinr_users_fits(t, cs) && !force_pg && (t.m > 4 || force_users);
         // c64 paper scope, m in {4, 8}: rebuild fused with the pair Grams on the tensor cores (k_rgram.cu)
-        const bool tc_path = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !cod && tc_sinr_shape(t) &&
-                             !(path && (std::strcmp(path, "users") == 0 || std::strcmp(path, "pg") == 0));
+        const bool tc_path = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !cod && tc_sinr_shape(ctx, t) && !force_users &&
+                             !force_pg;
         if (tc_path) {
             const int64_t Ft = std::min<int64_t>(F, 256);
             double2* PGt = (double2*)ctx->lws(lane, WS_PG, 16 * ngroups * Ft * users * S * t.m * t.m);
@@ -721,7 +735,7 @@ void sinr_device(gwt_ctx* ctx, int lane, cudaStream_t st, const Topo& t, const g
                 rec();
                 kind.push_back(1);
                 // m > 4: the per-user Householder/QL kernel in PG mode; m <= 4: the thread-per-user Jacobi kernel
-                if (t.m > 4 && sinr_users_pg_fits(t) && !std::getenv("GWT_PG_SMALL"))
+                if (t.m > 4 && sinr_users_pg_fits(t) && !ctx->opt.pg_small)
                     ctx->launched(launch_sinr_users_pg(t, ngroups * fc, fc, F, f0, topo->noise_std, PGt, sd, sgd, std_, st));
                 else
                     ctx->launched(launch_sinr_small(t, scope, S, ngroups * fc * users, topo->noise_std, fc, F, f0, PGt,
@@ -821,13 +835,11 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     double *sd = sinr, *sgd = signal;
     int* std_ = (int*)status;
     const int64_t out_rows = ngroups * F * users;
-    const char* pl = std::getenv("GWT_SINR_PIPELINE");
-    const int64_t nch = std::min<int64_t>(ngroups, pl ? std::max(1, std::atoi(pl)) : 4);
-    const char* dl = std::getenv("GWT_SINR_DEV_LANES");
+    const int64_t nch = std::min<int64_t>(ngroups, std::max(1, ctx->opt.sinr_pipeline));
     // two stream lanes overlap the CUDA-core rebuild of one group half with the Gram / eig stages of the
     // other; the tensor-core path keeps every SM busy with one lane (C4: 710 ms single lane vs 839 ms)
-    const bool tc_shape = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !coeffs && tc_sinr_shape(t);
-    const int64_t ndev = std::min<int64_t>(ngroups, dl ? std::max(1, std::atoi(dl)) : (tc_shape ? 1 : 2));
+    const bool tc_shape = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !coeffs && tc_sinr_shape(ctx, t);
+    const int64_t ndev = std::min<int64_t>(ngroups, ctx->opt.sinr_dev_lanes > 0 ? ctx->opt.sinr_dev_lanes : (tc_shape ? 1 : 2));
     if (mem == GWT_MEM_DEVICE && ndev > 1 && !coeffs) {
         // device-resident: group chunks on ndev stream lanes so the FP32-issue-bound rebuild of one
         // chunk overlaps the memory/fp64-bound Gram and small-matrix stages of the others
@@ -865,14 +877,12 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
         ctx->stage_ms[6] = ds;
         return;
     }
-    const char* cpp = std::getenv("GWT_SINR_COPY_STREAMS");
-    if (mem == GWT_MEM_HOST && nch > 1 && !(cpp && std::atoi(cpp) == 0)) {
+    if (mem == GWT_MEM_HOST && nch > 1 && ctx->opt.sinr_copy_streams) {
         // host buffers: group chunks flow through three engines — one H2D copy stream, NS compute lanes,
         // one D2H copy stream — chained by per-chunk events, so PCIe traffic in both directions overlaps
         // the kernels while the kernels keep the device-resident 2-lane concurrency (4 compute lanes of
         // the older scheme contended: 0.38 vs 0.36 ms device time on C2)
-        const char* nl = std::getenv("GWT_SINR_LANES");
-        const int NS = (int)std::min<int64_t>(nl ? std::max(1, std::atoi(nl)) : (tc_shape ? 1 : 2), nch);
+        const int NS = (int)std::min<int64_t>(ctx->opt.sinr_lanes > 0 ? ctx->opt.sinr_lanes : (tc_shape ? 1 : 2), nch);
         while ((int)ctx->lanes.size() < NS - 1) {
             gwt_ctx::Lane ln;
             ck(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -946,8 +956,7 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     if (mem == GWT_MEM_HOST && nch > 1) {
         // host buffers: 4 group chunks on 4 stream lanes (GWT_SINR_PIPELINE / GWT_SINR_LANES), each chunk H2D -> device
         // pipeline -> D2H on its lane, so copies in both directions overlap the other chunks' kernels
-        const char* nl = std::getenv("GWT_SINR_LANES");
-        const int NS = (int)std::min<int64_t>(nl ? std::max(1, std::atoi(nl)) : 4, nch);
+        const int NS = (int)std::min<int64_t>(ctx->opt.sinr_lanes > 0 ? ctx->opt.sinr_lanes : 4, nch);
         while ((int)ctx->lanes.size() < NS - 1) {
             gwt_ctx::Lane ln;
             ck(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -1079,6 +1088,7 @@ int gwt_ctx_create(gwt_ctx** out, int device) {
     if (device < 0 || device >= n) return GWT_INVALID_ARGUMENT;
     gwt_ctx* c = new gwt_ctx();
     c->device = device;
+    c->opt.read();
     if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete c;
         return GWT_CUDA_ERROR;

@@ -1070,7 +1070,7 @@ template <class T>
 cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, void* out, double* evals, double2* ws_a,
                              double* ws_z, double2* ws_x, int* fail, cudaStream_t st) {
     if (D > 256 || D < 1 || count < 1 || count > D) return cudaErrorInvalidValue;
-    const char* mode = std::getenv("GWT_EIG_MODE");  // tuning override: "warp", "cta"
+    const char* mode = env_once("GWT_EIG_MODE");  // tuning override: "warp", "cta"
     const bool force_warp = mode && std::strcmp(mode, "warp") == 0, force_cta = mode && std::strcmp(mode, "cta") == 0;
     const bool legacy_warp = mode && std::strcmp(mode, "warp_old") == 0;
     if (!force_warp && !force_cta && D <= 8) {
@@ -1083,7 +1083,7 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
         }
         return cudaGetLastError();
     }
-    const char* jmode = std::getenv("GWT_EIG_JACOBI");
+    const char* jmode = env_once("GWT_EIG_JACOBI");
     if (jmode && D <= kSmemMaxD) {
         // parallel cyclic Jacobi, one CTA per matrix (kept for comparison; slower than Householder on B200)
         const size_t sm = sizeof(double2) * ((size_t)2 * D * (D + 1) + 4 * 32) + sizeof(int) * 64;
@@ -1161,7 +1161,7 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
         if (e != cudaSuccess) return e;
         // joint-orthogonalisation threshold of the inverse iterations (relative to ||T||)
         static const double big_ctol = [] {
-            const char* v = std::getenv("GWT_EIG_BIG_CTOL");
+            const char* v = env_once("GWT_EIG_BIG_CTOL");
             return v ? std::atof(v) : 1e-3;
         }();
         k_heev_big<<<(unsigned)batch, kBigNT, sm, st>>>(D, count, big_ctol, (const float2*)in, (float2*)out, evals,

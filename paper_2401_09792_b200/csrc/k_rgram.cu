@@ -587,7 +587,7 @@ cudaError_t launch_rgram(const Topo& t, int64_t ngroups, int Fc, int64_t f0, int
     if (e != cudaSuccess) return e;
     dim3 grid(t.users(), (unsigned)ngroups);
     static const bool split = [] {
-        const char* v = std::getenv("GWT_RGRAM_SPLIT");
+        const char* v = env_once("GWT_RGRAM_SPLIT");
         return v && std::atoi(v) != 0;
     }();
 #define GWT_RG(MPV, SPV)                                                                                            \

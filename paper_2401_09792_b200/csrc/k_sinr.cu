@@ -359,7 +359,7 @@ static cudaError_t launch_rebuild_rb(const Topo& t, int ngroups, int Fc, int64_t
     const int mn = t.m * t.n;
     const int ph = (t.p + QG - 1) / QG;
     const int rb = (sizeof(T) == 4 && mn % 96 == 0) ? 3 : (mn % 64 == 0 ? 2 : 1);
-    const char* gse = std::getenv("GWT_REBUILD_GSMEM");
+    const char* gse = env_once("GWT_REBUILD_GSMEM");
     const bool gs = gse ? std::atoi(gse) != 0 : (size_t)mn * t.p * sizeof(cplx_t<T>) <= 32 * 1024;
 #define GWT_RB(RBV, PHV)                                                                                        \
     if (rb == RBV && ph <= PHV)                                                                                 \
@@ -1109,15 +1109,15 @@ cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64
                            cudaStream_t st) {
     using C = cplx_t<T>;
     constexpr int FT = 16;
-    if (sizeof(T) == 4 && !coeffs && rebuild_mm_fits(t) && !std::getenv("GWT_REBUILD_RB")) {
+    if (sizeof(T) == 4 && !coeffs && rebuild_mm_fits(t) && !env_once("GWT_REBUILD_RB")) {
         cudaError_t e = launch_rebuild_mm(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st);
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();
     }
-    if (!coeffs && !std::getenv("GWT_REBUILD_V1")) {
+    if (!coeffs && !env_once("GWT_REBUILD_V1")) {
         // subcarrier tile: 64 while the phasor tile (P x 64) stays <= 16 KB (C1/C2), else 32 (C3-C5:
         // P = 48/64, where FT = 64 halves the resident CTAs); GWT_REBUILD_FT overrides
-        const char* ftv = std::getenv("GWT_REBUILD_FT");
+        const char* ftv = env_once("GWT_REBUILD_FT");
         const int ft = ftv ? std::atoi(ftv) : (t.P * 64 * (int)sizeof(C) <= 16 * 1024 ? 64 : 32);
         cudaError_t e = (ft == 32)
                             ? launch_rebuild_rb<T, 32>(t, ngroups, Fc, f0, Cd, G, tau, freqs, H, st)
@@ -1129,7 +1129,7 @@ cudaError_t launch_rebuild(const Topo& t, int ngroups, int Fc, int64_t f0, int64
         constexpr int FTL = 32;
         const size_t sm = sizeof(C) * ((size_t)t.p * t.m * t.n + (size_t)t.p * t.P + (size_t)t.P * FTL + (size_t)t.p * FTL) +
                           8 * (size_t)t.P;
-        if (!coeffs && sm <= 200 * 1024 && !std::getenv("GWT_REBUILD_TILED")) {
+        if (!coeffs && sm <= 200 * 1024 && !env_once("GWT_REBUILD_TILED")) {
             // split the subcarriers so the grid covers >= ~8 CTAs per SM
             const int64_t base = (int64_t)ngroups * t.links();
             int nz = (int)std::max<int64_t>(1, std::min<int64_t>((148 * 8 + base - 1) / base, (Fc + 2 * FTL - 1) / (2 * FTL)));
@@ -1158,7 +1158,7 @@ cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroup
     const int64_t items = (int64_t)ngroups * Fc * t.users();
     const int wpb = 4;
     const size_t smf = sizeof(double2) * (size_t)t.links() * t.m * t.n;
-    if (scope == 1 && smf <= 64 * 1024 && t.m <= 8 && !std::getenv("GWT_PG_STAGED")) {
+    if (scope == 1 && smf <= 64 * 1024 && t.m <= 8 && !env_once("GWT_PG_STAGED")) {
         const int mn = t.m * t.n, LS = mn + ((4 - mn % 8) + 8) % 8;
         const size_t smp = sizeof(double2) * (size_t)t.links() * LS;
         const int thr = (int)std::min<int64_t>(256, ((int64_t)t.users() * t.J * t.m * t.m + 31) / 32 * 32);
@@ -1176,7 +1176,7 @@ cudaError_t launch_pair_gram(const Topo& t, int scope, int S, int Fc, int ngroup
         }
     }
     const size_t sm = sizeof(double2) * (size_t)wpb * (2 * t.J - 1) * t.m * t.n;
-    if (scope == 1 && sm <= 96 * 1024 && !std::getenv("GWT_PG_UNSTAGED")) {
+    if (scope == 1 && sm <= 96 * 1024 && !env_once("GWT_PG_UNSTAGED")) {
         cudaError_t e = cudaSuccess;
         switch (t.m) {
 #define GWT_PGS(MM)                                                                                                  \
@@ -1201,7 +1201,7 @@ static cudaError_t launch_small_m(const Topo& t, int scope, int S, int64_t items
                                   int64_t f0, const double2* PG, double* EG, double* sinr, double* signal, int* status,
                                   cudaStream_t st) {
     const int users = t.users();
-    if (users <= 128 && !std::getenv("GWT_SMALL_SPLIT")) {
+    if (users <= 128 && !env_once("GWT_SMALL_SPLIT")) {
         const int thr = (128 / users) * users;  // whole (group, subcarrier) slices per CTA
         const int Lp = (t.L + 1) & ~1;
         const size_t sm = (size_t)thr * (Lp + 2 * M * t.L) * 8;
@@ -1238,7 +1238,7 @@ static cudaError_t launch_small_grp(const Topo& t, int scope, int S, int64_t ite
 cudaError_t launch_sinr_small(const Topo& t, int scope, int S, int64_t items, double sigma, int fc, int64_t Ftot,
                               int64_t f0, const double2* PG, double* EG, double* sinr, double* signal, int* status,
                               cudaStream_t st) {
-    const char* grp = std::getenv("GWT_SMALL_GRP");  // 1: force the 8-lanes-per-user kernel, 0: never
+    const char* grp = env_once("GWT_SMALL_GRP");  // 1: force the 8-lanes-per-user kernel, 0: never
     const bool use_grp = t.users() * 8 <= 256 && (grp ? std::atoi(grp) != 0 : t.m > 4);
     if (use_grp) {
         switch (t.m) {

@@ -12,7 +12,24 @@
 
 #include "kernels.cuh"
 
+#include <map>
+#include <mutex>
+#include <string>
+
 namespace gwtk {
+
+const char* env_once(const char* name) {
+    static std::mutex mu;
+    static std::map<std::string, std::pair<bool, std::string>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(name);
+    if (it == cache.end()) {
+        const char* v = std::getenv(name);
+        it = cache.emplace(name, std::make_pair(v != nullptr, v ? std::string(v) : std::string())).first;
+    }
+    return it->second.first ? it->second.second.c_str() : nullptr;
+}
+
 
 // Tiled strided batched complex GEMM with conj(U) (GemmDesc): CTA tile TR rows x TC cols of one item,
 // 256 threads as NR x NC (NR = TR/RT, NC = TC/CT), RT x CT outputs per thread. The global offsets of
@@ -538,7 +555,7 @@ cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, cons
     }
     // short items (rows <= 64, e.g. W = Y1 x2 B^H with M*p = 48 rows at C2): 64-row tiles instead of
     // 128-row tiles that would run 60 % empty
-    static const bool tr64 = !(std::getenv("GWT_GEMM_TR64") && std::atoi(std::getenv("GWT_GEMM_TR64")) == 0);
+    static const bool tr64 = !(env_once("GWT_GEMM_TR64") && std::atoi(env_once("GWT_GEMM_TR64")) == 0);
     if (tr64 && rows <= 64 && d.Cols <= 32) {
         if (d.Cols <= 8) GWT_GEMM(64, 8, 1, 2)
         else if (d.Cols <= 12) GWT_GEMM(64, 12, 1, 3)
@@ -561,16 +578,10 @@ cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, cons
 
 template <class T>
 cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group, const void* V, void* out,
-                        void* part, size_t part_bytes, cudaStream_t st) {
+                        void* part, size_t part_bytes, cudaStream_t st, bool allow_tc) {
     // complex64 Grams whose rows are contiguous blocks (the tx Gram of W2, N >= 128: C3, C4, C5) on the tensor
     // cores (k_tc.cu, TMA bulk-staged 3xTF32); GWT_GRAM_TC=0 keeps the CUDA-core kernel
-    if (sizeof(T) == 4 && gram_tc_fits(d)) {
-        static const bool tc_on = [] {
-            const char* e = std::getenv("GWT_GRAM_TC");
-            return !(e && std::atoi(e) == 0);
-        }();
-        if (tc_on) return launch_gram_tc(t, d, ngroups, sets_per_group, V, out, st);
-    }
+    if (sizeof(T) == 4 && allow_tc && gram_tc_fits(d)) return launch_gram_tc(t, d, ngroups, sets_per_group, V, out, st);
     if (d.D <= 8 && d.xs == 1) {
         const unsigned blocks = (unsigned)(ngroups * sets_per_group);
         switch (d.D) {
@@ -592,7 +603,7 @@ cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int s
         if (part && ctas < 148 * 4) {
             // >= 2 chunks of KC per split (was 8): C2's per-sweep tx Grams (32 sets per lane, K = 384)
             // now split 6 ways instead of running 32 CTAs
-            static const int minch = std::getenv("GWT_GRAM_MINCH") ? std::max(1, std::atoi(std::getenv("GWT_GRAM_MINCH"))) : 2;
+            static const int minch = env_once("GWT_GRAM_MINCH") ? std::max(1, std::atoi(env_once("GWT_GRAM_MINCH"))) : 2;
             nsplit = (int)std::min<int64_t>((148 * 4 + ctas - 1) / ctas, std::max<int64_t>(1, ktot / (minch * KC)));
             const int64_t cap = (int64_t)(part_bytes / (sizeof(cplx_t<T>) * (size_t)d.D * d.D * sets));
             nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit, cap));
@@ -615,7 +626,7 @@ cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int s
     constexpr int KCb = sizeof(T) == 4 ? 32 : 16;
     // 32 x 32 lower-triangle tiles up to D = 64 (3 tiles instead of one full 64 x 64: 25 % less work,
     // 3x the CTAs; C2 Tucker 16.9 -> 16.2 ms with the split above); 64 x 64 tiles beyond
-    static const char* td = std::getenv("GWT_GRAM_TD");
+    static const char* td = env_once("GWT_GRAM_TD");
     const int tdmax = td ? std::atoi(td) : 64;
     if (d.D <= 32 || d.D <= tdmax) return run(k_gram<T, 2, KCb>, 32, KCb);
     return run(k_gram<T, 4, KCb>, 64, KCb);
@@ -654,7 +665,7 @@ cudaError_t launch_broadcast(const void* src, void* dst, int64_t elems, int copi
     template cudaError_t launch_cgemm<T>(const Topo&, const GemmDesc&, int64_t, const void*, const void*, void*, \
                                          cudaStream_t);                                                      \
     template cudaError_t launch_gram<T>(const Topo&, const GramDesc&, int64_t, int, const void*, void*, void*,   \
-                                        size_t, cudaStream_t);                                                       \
+                                        size_t, cudaStream_t, bool);                                                 \
     template cudaError_t launch_group_sqnorm<T>(const void*, int64_t, int64_t, double*, double*, cudaStream_t);          \
     template cudaError_t launch_broadcast<T>(const void*, void*, int64_t, int, int64_t, cudaStream_t);
 GWT_INST(float)

@@ -48,8 +48,12 @@ struct GramDesc {
 template <class T> cudaError_t launch_cgemm(const Topo& t, const GemmDesc& d, int64_t ngroups, const void* in,
                                             const void* U, void* out, cudaStream_t st);
 // part (nullable): scratch for K-split partial Grams (used when few sets would leave SMs idle)
+// allow_tc: the tensor-core Gram for row-block unfoldings (the context's GWT_GRAM_TC, read at ctx creation)
 template <class T> cudaError_t launch_gram(const Topo& t, const GramDesc& d, int64_t ngroups, int sets_per_group,
-                                           const void* V, void* out, void* part, size_t part_bytes, cudaStream_t st);
+                                           const void* V, void* out, void* part, size_t part_bytes, cudaStream_t st,
+                                           bool allow_tc = true);
+// tuning / diagnostic switch read once per process (the per-call hot paths never call getenv)
+const char* env_once(const char* name);
 // per-group ||v||^2 in fp64; deterministic two-level reduction through `partial`
 // (ngroups * kSqnormMaxBlocks doubles) when a group spans many blocks
 constexpr int kSqnormMaxBlocks = 128;

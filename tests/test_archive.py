@@ -147,3 +147,12 @@ def test_cpp_dropin_archive_errors_match_python(tmp_path, cpp_archive_tool):
         with pytest.raises(ar.ArchiveError) as ei:
             ar.load_archive(p)
         assert got == f"{type(ei.value).__name__}: {ei.value}", (name, got)
+
+
+def test_sweep_csv_text_and_axis_error():
+    """sweep.csv text as runner.cpp:288-298 writes it; a missing / unknown axis raises the reference's text."""
+    from paper_2401_09792_b200 import sweep
+    rows = [sweep.SweepRow(16, 12.5, 3.25, 0.0123), sweep.SweepRow(32, 6.25, 2.0, 0.001)]
+    assert sweep.sweep_csv_text(rows) == "axis,Rs,Rt,ec\n16,12.500000,3.250000,0.01230000\n32,6.250000,2.000000,0.00100000\n"
+    with pytest.raises(gw.InvalidArgument, match="run_sweep: config has no sweep axis"):
+        sweep.run_sweep(None, None, gw.CompressionRanks(4, 16, 8), "m", [1], None, None, None)

@@ -124,3 +124,32 @@ def test_bench_self_check_on_c2(ctx):
                                       freqs=torch.from_numpy(cfg.freqs()).cuda())
     out = bench.parity_sample(O, cfg, fac, Xd, tau, rep, groups=2, nfreq=16, nthreads=NT)
     assert out["ok"], out
+
+
+def test_rank_sweep_c5_matches_oracle(ctx):
+    """run_sweep (runner.cpp:193-211) over the C5 transmit rank on 4 groups x 64 subcarriers: R_s is the closed
+    form, e_c equals the oracle's mean relative error between ITS full-size and compressed SINR on the GPU's
+    factors (metrics.cpp:36-56), and the NMSE falls as the rank grows."""
+    torch = pytest.importorskip("torch")
+    from paper_2401_09792_b200 import metrics, sweep
+    cfg = gw.CONFIGS["C5"]
+    X, X128, tau = baseline_inputs(cfg, 4)
+    freqs = cfg.freqs()[:64]
+    Xd = torch.from_numpy(X).cuda()
+    rows = sweep.run_sweep(ctx, cfg.topology(), cfg.ranks(), "n", [16, 64], Xd, torch.from_numpy(tau).cuda(),
+                           torch.from_numpy(freqs).cuda(), sweeps=4, repetitions=1)
+    assert [r.value for r in rows] == [16, 64]
+    assert rows[0].nmse > rows[1].nmse
+    dims_full = dims_of(cfg)
+    co = O.coeffs_from_tau(tau, freqs)
+    want_full, _ = O.sinr_full(dims_full, X128, co, cfg.sigma, cfg.L, O.SCOPE_PAPER, nthreads=NT)
+    for r in rows:
+        rk = gw.CompressionRanks(cfg.m, r.value, cfg.p)
+        assert r.r_s == pytest.approx(metrics.storage_ratio(cfg.topology(), rk))
+        fac = ctx.groupwise_solve(cfg.topology(), Xd, rk, 4, early_stop=False)
+        d = dict(dims_full, n=r.value)
+        want_c, _ = O.sinr_compressed(d, fac.delay.cpu().numpy().astype(np.complex128),
+                                      fac.cores.cpu().numpy().astype(np.complex128), co, cfg.sigma, cfg.L,
+                                      O.SCOPE_PAPER, nthreads=NT)
+        e_oracle = metrics.sinr_error(want_full, want_c)
+        assert abs(r.e_c - e_oracle) <= 1e-4 * max(e_oracle, 1e-3), (r.e_c, e_oracle)

@@ -25,19 +25,21 @@ def test_tc_gemm_tile(K, split3):
     assert err < (1e-5 if split3 else 3e-3), err
 
 
-@pytest.mark.parametrize("name,ngroups,sweeps", [("C2", 2, 3), ("C4", 1, 1)])
+@pytest.mark.parametrize("name,ngroups,sweeps", [("C3", 2, 3), ("C5", 2, 3), ("C4", 1, 2)])
 def test_gram_tc_matches_cuda_core_gram(name, ngroups, sweeps, monkeypatch):
-    """The tcgen05 3xTF32 complex Gram (c64, D >= 64; C4's N = 256 exercises off-diagonal 128x128
-    tiles) gives the same Tucker solve as the FP32 CUDA-core Gram (GWT_GRAM_TC=0)."""
+    """The tcgen05 3xTF32 transmit Gram (row-block unfoldings, N = 128 at C3 / C5: one 128 x 128 strip;
+    N = 256 at C4: the 128 x 256 strip) gives the same Tucker solve as the FP32 CUDA-core Gram
+    (GWT_GRAM_TC=0). The switch is read when a Context is created, so each setting gets its own."""
     import paper_2401_09792_b200 as gw
     from tests.helpers import baseline_inputs
     cfg = gw.CONFIGS[name]
     X, _, _ = baseline_inputs(cfg, ngroups)
-    ctx = gw.Context(0)
     out = {}
     for tcv in ("0", "1"):
         monkeypatch.setenv("GWT_GRAM_TC", tcv)
+        ctx = gw.Context(0)
         out[tcv] = ctx.groupwise_solve(cfg.topology(), X, cfg.ranks(), sweeps, early_stop=False)
+        ctx.close()
     a, b = out["0"], out["1"]
     assert np.max(np.abs(a.trace / a.energy[:, None] - b.trace / b.energy[:, None])) <= 1e-6
     assert np.max(np.abs(a.energy - b.energy) / a.energy) <= 1e-6
