@@ -1,4 +1,4 @@
-// CTA-per-matrix Hermitian top-k eigensolver for 128 < D <= 256 in fp32 (c64 Grams, e.g. the C4
+// CTA-per-matrix Hermitian top-k eigensolver for 64 < D <= 256 in fp32 (c64 Grams, e.g. the C4
 // transmit factor, N = 256). Included by k_eig.cu (inside namespace gwtk) after eig_cta.cuh.
 //
 // Same algorithm and conventions as k_heev_cr (reference leading_eigenvectors,
@@ -6,21 +6,35 @@
 // (512 KB) does not fit in shared memory, so it lives in the per-matrix global workspace where
 // it stays L2-resident (148 concurrent matrices = 76 MB of the 126 MB L2); everything on the
 // serial chains is in shared memory or registers:
-//  1. Householder, 512 threads = 2 per row, 2 CTA barriers per reflector (as k_heev_cr), loads of
-//     4-column batches issued before use.
+//  1. Householder in panels of kPanel reflectors (the LAPACK latrd / her2k split): inside a panel the
+//     trailing matrix is not rewritten; each step reads it once (p = A v, 16 loads in flight per
+//     thread) and corrects with the panel's V, W columns held in shared memory
+//     (p -= V (W^H v) + W (V^H v)); one rank-2*kPanel update per panel (4x4 register tiles) then
+//     rewrites the trailing matrix. The per-reflector read-modify-write of the whole trailing matrix
+//     (the old form: two L2 passes + one write per step, latency bound) is gone.
 //  2. fp32 multisection on Sturm counts (8 lanes per wanted eigenvalue).
 //  3. Inverse iteration, thread per eigenvalue, iterate in shared memory ([i][t], conflict free),
 //     pivoted LU in the global workspace (L1-resident per thread column).
 //  4. Back-transform with 8 threads per eigenvector (32 rows each in registers), vectors in
-//     batches of 64 (counts up to 128: the C5 rank sweep n = 96).
+//     batches of 64 (counts up to 128: the C5 rank sweep n = 96); the reflectors are staged into
+//     shared memory 32 at a time (zero-padded, so the apply loop runs unpredicated).
 #pragma once
 
 constexpr int kBigNT = 512;
+constexpr int kPanel = 32;
+
+__host__ __device__ inline size_t eig_big_region(int D, int count) {
+    // union of the Householder panel (V, W: kPanel columns each) and the iterate XR [i][t] + the
+    // back-transform staging of kPanel reflectors
+    const size_t vw = (size_t)2 * kPanel * D * 8;
+    const size_t xs = (((size_t)D * count * 4 + 15) & ~size_t(15)) + (size_t)kPanel * D * 8;
+    return vw > xs ? vw : xs;
+}
 
 __host__ __device__ inline size_t eig_big_smem(int D, int count) {
-    // tau, sub, dlt, sd, se, se2, fd, fe2, lam, scl, red, pp, XR
-    return (size_t)D * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4) + (size_t)count * (8 + 4) + 2 * 16 * 8 + (size_t)D * 8 +
-           (size_t)D * count * 4 + 64;
+    // tau, sub, dlt, sd, se, se2, fd, fe2, pA, lam, scl, red, xy, region
+    return (size_t)D * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + 8) + (size_t)count * (8 + 4) + 2 * 16 * 8 + 2 * kPanel * 8 +
+           eig_big_region(D, count) + 16 * 16;
 }
 
 __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, double ctol_rel, const float2* __restrict__ in,
@@ -52,8 +66,14 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, double
     double* lamv = reinterpret_cast<double*>(take((size_t)count * 8));
     int* scl = reinterpret_cast<int*>(take((size_t)count * 4));
     R* red = reinterpret_cast<R*>(take(2 * 16 * 8));
-    C* pp = reinterpret_cast<C*>(take((size_t)D * 8));
-    R* XR = reinterpret_cast<R*>(take((size_t)D * count * 4));  // [i][t] iterate / final z
+    C* xy = reinterpret_cast<C*>(take(2 * kPanel * 8));  // W^H v, V^H v of the current step
+    C* pA = reinterpret_cast<C*>(take((size_t)D * 8));   // A v of the current step
+    unsigned char* region = take(eig_big_region(D, count));
+    C* Vp = reinterpret_cast<C*>(region);                       // [kPanel][D] panel reflectors
+    C* Wp = Vp + (size_t)kPanel * D;                            // [kPanel][D] panel w vectors
+    R* XR = reinterpret_cast<R*>(region);                       // [i][t] iterate / final z (after phase 1)
+    C* Sg = reinterpret_cast<C*>(region + (((size_t)D * count * 4 + 15) & ~size_t(15)));  // staged reflectors
+    __shared__ C s_x0;
     __shared__ int s_rounds;
     C* A = ws_a + b * (int64_t)D * D;
     const C* H = in + b * (int64_t)D * D;
@@ -68,121 +88,222 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, double
     }
     __syncthreads();
     GWT_CLK(t_ph0);
+#ifdef GWT_PHASE_TIMERS
+    long long hs[5] = {0, 0, 0, 0, 0}, hc = 0, hn = 0;
+#define GWT_HS(slot) GWT_TICK(hn); hs[slot] += hn - hc; hc = hn;
+#else
+#define GWT_HS(slot)
+#endif
     const int r = tid / Q, q = tid % Q;
+    const bool row_ok = r < D;
     R* rt2 = red;
     R* rkp = red + NW;
-    {
-        R part = 0.f;
-        if (q == 0 && r > 1 && r < D) {
-            const C a = A[r];
-            part = a.x * a.x + a.y * a.y;
-        }
-        part = rows_sum<Q>(part);
-        if (lane == 0) rt2[wid] = part;
-    }
-    for (int k = 0; k + 2 < D; ++k) {
-        const bool act = r > k && r < D;
-        __syncthreads();  // [A]
-        R t2 = 0.f;
+    for (int k0 = 0; k0 + 2 < D; k0 += kPanel) {
+        const int kend = min(k0 + kPanel, D - 2);  // steps k in [k0, kend)
+        for (int k = k0; k < kend; ++k) {
+            const int j = k - k0;
+            GWT_TICK(hc);
+            // (1) column k of the effective trailing matrix, rows >= k: A - sum_{i<j} (V_i W_i^H + W_i V_i^H)
+            C a = make_float2(0.f, 0.f), corr = make_float2(0.f, 0.f);
+            if (row_ok && r >= k) {
+                for (int i = q; i < j; i += Q) {
+                    cfmac(corr, Vp[i * D + r], Wp[i * D + k]);
+                    cfmac(corr, Wp[i * D + r], Vp[i * D + k]);
+                }
+            }
+            corr.x += __shfl_xor_sync(0xffffffffu, corr.x, 1);
+            corr.y += __shfl_xor_sync(0xffffffffu, corr.y, 1);
+            if (row_ok && r >= k) {
+                const C a0 = A[r + LD * k];
+                a = make_float2(a0.x - corr.x, a0.y - corr.y);
+                if (q == 0 && r == k) A[k + LD * k] = make_float2(a.x, 0.f);
+                if (q == 0 && r == k + 1) s_x0 = a;
+            }
+            {
+                R part = (q == 0 && row_ok && r > k + 1) ? a.x * a.x + a.y * a.y : 0.f;
+                part = rows_sum<Q>(part);
+                if (lane == 0) rt2[wid] = part;
+            }
+            __syncthreads();  // [1] norm partials, x0
+            GWT_HS(0)
+            R t2 = 0.f;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) t2 += rt2[w];
-        const C x0 = A[(k + 1) + LD * k];
-        const C* colk = A + LD * k;
-        if (t2 == 0.f) {
+            for (int w = 0; w < NW; ++w) t2 += rt2[w];
+            const C x0 = s_x0;
+            C al, v0;
+            R tk;
+            if (t2 == 0.f) {  // column already reduced: H = I (v = 0, w = 0)
+                al = x0;
+                v0 = make_float2(0.f, 0.f);
+                tk = 0.f;
+            } else {
+                reflector(x0, t2, al, v0, tk);
+            }
+            const C v = (row_ok && r > k && t2 != 0.f) ? (r == k + 1 ? v0 : a) : make_float2(0.f, 0.f);
+            if (q == 0 && row_ok) {
+                Vp[j * D + r] = v;
+                if (r > k) A[r + LD * k] = v;
+            }
             if (tid == 0) {
-                tau[k] = 0.f;
-                sub[k] = x0;
+                tau[k] = tk;
+                sub[k] = al;
             }
-            __syncthreads();
-            R part = 0.f;
-            if (q == 0 && r > k + 2 && r < D) {
-                const C a = A[r + LD * (k + 1)];
-                part = a.x * a.x + a.y * a.y;
-            }
-            part = rows_sum<Q>(part);
-            if (lane == 0) rt2[wid] = part;
-            continue;
-        }
-        C al, v0;
-        R tk;
-        reflector(x0, t2, al, v0, tk);
-        const C v = act ? (r == k + 1 ? v0 : colk[r]) : make_float2(0.f, 0.f);
-        C p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
-        if (act) {
-            const C* arow = A + r;
-            int c = k + 1 + q;
-            for (; c + 3 * Q < D; c += 4 * Q) {
-                C a[4], bb[4];
+            __syncthreads();  // [2] v visible
+            GWT_HS(1)
+            // (2) x = W^H v, y = V^H v over the panel's previous columns: warp w takes dot products
+            // w, w + 16, w + 32, w + 48 as four independent chains
+            const C* vj = Vp + j * D;
+            if (wid < 2 * j) {
+                const int nd = 2 * j;
+                const C* src[4];
+                C sacc[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    a[u] = arow[LD * (c + u * Q)];
-                    bb[u] = colk[c + u * Q];
+                    const int d = wid + NW * u;
+                    src[u] = d < nd ? ((d & 1) ? Vp + (d >> 1) * D : Wp + (d >> 1) * D) : vj;
+                    sacc[u] = make_float2(0.f, 0.f);
                 }
-                if (c == k + 1) bb[0] = v0;
-                cfma(p0, a[0], bb[0]);
-                cfma(p1, a[1], bb[1]);
-                cfma(p0, a[2], bb[2]);
-                cfma(p1, a[3], bb[3]);
+                for (int c = k + 1 + lane; c < D; c += 32) {
+                    const C vc = vj[c];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (wid + NW * u < nd) cfmaconj(sacc[u], src[u][c], vc);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        sacc[u].x += __shfl_xor_sync(0xffffffffu, sacc[u].x, o);
+                        sacc[u].y += __shfl_xor_sync(0xffffffffu, sacc[u].y, o);
+                    }
+                if (lane == 0) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int d = wid + NW * u;
+                        if (d < nd) xy[(d & 1) * kPanel + (d >> 1)] = sacc[u];
+                    }
+                }
             }
-            for (; c < D; c += Q) cfma(p0, arow[LD * c], c == k + 1 ? v0 : colk[c]);
-        }
-        C pv = make_float2(p0.x + p1.x, p0.y + p1.y);
+            GWT_HS(2)
+            // (3) p = A v over the rows k < r < D (the trailing matrix as of the panel start) by all threads:
+            // Qm = 2..16 threads per active row as the trailing block shrinks, 16 loads in flight
+            {
+                const int nr = D - k - 1;
+                const int Qm = nr > 128 ? 2 : nr > 64 ? 4 : nr > 32 ? 8 : 16;
+                const int rr = k + 1 + tid / Qm, qm = tid % Qm;
+                C p0 = make_float2(0.f, 0.f), p1 = make_float2(0.f, 0.f);
+                if (rr < D) {
+                    const C* arow = A + rr;
+                    int c = k + 1 + qm;
+                    for (; c + 15 * Qm < D; c += 16 * Qm) {
+                        C av[16];
 #pragma unroll
-        for (int o = 1; o < Q; o <<= 1) {
-            pv.x += __shfl_xor_sync(0xffffffffu, pv.x, o);
-            pv.y += __shfl_xor_sync(0xffffffffu, pv.y, o);
-        }
-        pv = make_float2(pv.x * tk, pv.y * tk);
-        R kp = (q == 0 && act) ? v.x * pv.x + v.y * pv.y : 0.f;
-        kp = rows_sum<Q>(kp);
-        if (lane == 0) rkp[wid] = kp;
-        if (act && q == 0) pp[r] = pv;
-        __syncthreads();  // [B]
-        R ks = 0.f;
+                        for (int u = 0; u < 16; ++u) av[u] = arow[LD * (c + u * Qm)];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) ks += rkp[w];
-        const R kk = 0.5f * tk * ks;
-        const C w = make_float2(pv.x - kk * v.x, pv.y - kk * v.y);
-        if (tid == 0) {
-            tau[k] = tk;
-            sub[k] = al;
+                        for (int u = 0; u < 16; u += 2) {
+                            cfma(p0, av[u], vj[c + u * Qm]);
+                            cfma(p1, av[u + 1], vj[c + (u + 1) * Qm]);
+                        }
+                    }
+                    for (; c + 3 * Qm < D; c += 4 * Qm) {
+                        C av[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) av[u] = arow[LD * (c + u * Qm)];
+                        cfma(p0, av[0], vj[c]);
+                        cfma(p1, av[1], vj[c + Qm]);
+                        cfma(p0, av[2], vj[c + 2 * Qm]);
+                        cfma(p1, av[3], vj[c + 3 * Qm]);
+                    }
+                    for (; c < D; c += Qm) cfma(p0, arow[LD * c], vj[c]);
+                }
+                C ps = make_float2(p0.x + p1.x, p0.y + p1.y);
+                for (int o = 1; o < Qm; o <<= 1) {
+                    ps.x += __shfl_xor_sync(0xffffffffu, ps.x, o);
+                    ps.y += __shfl_xor_sync(0xffffffffu, ps.y, o);
+                }
+                if (qm == 0 && rr < D) pA[rr] = ps;
+            }
+            GWT_HS(3)
+            __syncthreads();  // [3] x, y visible
+            C pv = (q == 0 && row_ok && r > k) ? pA[r] : make_float2(0.f, 0.f);
+            if (row_ok && r > k) {
+                for (int i = q; i < j; i += Q) {
+                    const C xi = xy[i], yi = xy[kPanel + i];
+                    const C vr = Vp[i * D + r], wr = Wp[i * D + r];
+                    pv.x -= vr.x * xi.x - vr.y * xi.y + wr.x * yi.x - wr.y * yi.y;
+                    pv.y -= vr.x * xi.y + vr.y * xi.x + wr.x * yi.y + wr.y * yi.x;
+                }
+            }
+            pv.x += __shfl_xor_sync(0xffffffffu, pv.x, 1);
+            pv.y += __shfl_xor_sync(0xffffffffu, pv.y, 1);
+            pv = make_float2(pv.x * tk, pv.y * tk);
+            {
+                R kp = (q == 0 && row_ok && r > k) ? v.x * pv.x + v.y * pv.y : 0.f;
+                kp = rows_sum<Q>(kp);
+                if (lane == 0) rkp[wid] = kp;
+            }
+            __syncthreads();  // [4] v^H p partials
+            R ks = 0.f;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) ks += rkp[w];
+            const R kk = 0.5f * tk * ks;
+            if (q == 0 && row_ok)
+                Wp[j * D + r] = (r > k) ? make_float2(pv.x - kk * v.x, pv.y - kk * v.y) : make_float2(0.f, 0.f);
+            __syncthreads();  // [5] w visible (next column update, next dots)
+            GWT_HS(4)
         }
-        R part = 0.f;
-        if (act) {
-            C* arow = A + r;
-            int c = k + 1 + q;
-            for (; c + 3 * Q < D; c += 4 * Q) {
-                C a[4], vc[4], pc[4];
+        // Hermitian rank-2*nj update of the trailing matrix, rows and columns >= kend: warp tiles of 32 rows x 16
+        // columns, lane (lr, lc) = (lane % 8, lane / 8) owns rows lr + 8x and columns lc + 4y (x, y < 4),
+        // so every shared load is a broadcast of 8 (rows) or 4 (columns) consecutive entries
+        const int nj = kend - k0;
+        const int kb = kend & ~7;
+        const int nwr = (D - kb + 31) / 32, nwc = (D - kb + 15) / 16;
+        const int lr = lane % 8, lc = lane / 8;
+        for (int wt = wid; wt < nwr * nwc; wt += NW) {
+            // the lower triangle is computed, the upper mirrored (tiles wholly above the diagonal skip)
+            if (kb + 32 * (wt % nwr) + 31 < kb + 16 * (wt / nwr)) continue;
+            const int rb = kb + 32 * (wt % nwr) + lr, cb = kb + 16 * (wt / nwr) + lc;
+            C acc[4][4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+                for (int y = 0; y < 4; ++y) acc[x][y] = make_float2(0.f, 0.f);
+            for (int i = 0; i < nj; ++i) {
+                const C* vi = Vp + i * D;
+                const C* wi = Wp + i * D;
+                C vr[4], wr[4], vc[4], wc[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    a[u] = arow[LD * (c + u * Q)];
-                    vc[u] = colk[c + u * Q];
-                    pc[u] = pp[c + u * Q];
+                    const int rr = min(rb + 8 * u, D - 1), cc = min(cb + 4 * u, D - 1);
+                    vr[u] = vi[rr];
+                    wr[u] = wi[rr];
+                    vc[u] = vi[cc];
+                    wc[u] = wi[cc];
                 }
-                if (c == k + 1) vc[0] = v0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const C wc = make_float2(pc[u].x - kk * vc[u].x, pc[u].y - kk * vc[u].y);
-                    a[u].x -= v.x * wc.x + v.y * wc.y + w.x * vc[u].x + w.y * vc[u].y;
-                    a[u].y -= v.y * wc.x - v.x * wc.y + w.y * vc[u].x - w.x * vc[u].y;
-                    arow[LD * (c + u * Q)] = a[u];
+                for (int x = 0; x < 4; ++x)
+#pragma unroll
+                    for (int y = 0; y < 4; ++y) {
+                        cfmac(acc[x][y], vr[x], wc[y]);
+                        cfmac(acc[x][y], wr[x], vc[y]);
+                    }
+            }
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+                const int c = cb + 4 * y;
+                if (c < kend || c >= D) continue;
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    const int rr = rb + 8 * x;
+                    if (rr < c || rr >= D) continue;
+                    C& e = A[rr + LD * c];
+                    const C nv = make_float2(e.x - acc[x][y].x, e.y - acc[x][y].y);
+                    e = nv;
+                    if (rr > c) A[c + LD * rr] = make_float2(nv.x, -nv.y);
                 }
-                if (c == k + 1 && r > k + 2) part = a[0].x * a[0].x + a[0].y * a[0].y;
             }
-            for (; c < D; c += Q) {
-                const C vc = c == k + 1 ? v0 : colk[c];
-                const C pc = pp[c];
-                const C wc = make_float2(pc.x - kk * vc.x, pc.y - kk * vc.y);
-                C a = arow[LD * c];
-                a.x -= v.x * wc.x + v.y * wc.y + w.x * vc.x + w.y * vc.y;
-                a.y -= v.y * wc.x - v.x * wc.y + w.y * vc.x - w.x * vc.y;
-                arow[LD * c] = a;
-                if (c == k + 1 && r > k + 2) part = a.x * a.x + a.y * a.y;
-            }
-            if (r == k + 1 && q == 0) A[r + LD * k] = v0;
         }
-        part = rows_sum<Q>(part);
-        if (lane == 0) rt2[wid] = part;
+        __syncthreads();
     }
     __syncthreads();
     GWT_CLK(t_ph1);
@@ -394,29 +515,39 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, double
                 y[u] = make_float2(dl.x * z, dl.y * z);
             }
         }
-        for (int k = D - 3; k >= 0; --k) {
-            const R tk = tau[k];
-            if (tk == 0.f) continue;
-            const C* vk = A + LD * k;
-            C dot = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int u = 0; u < RPT; ++u) {
-                const int i = qb + QB * u;
-                if (i > k && i < D) cfmaconj(dot, vk[i], y[u]);
+        // reflectors in blocks of kPanel, staged (rows <= k zeroed) into shared memory
+        for (int khi = D - 3; khi >= 0; khi -= kPanel) {
+            const int klo = max(0, khi - kPanel + 1);
+            __syncthreads();  // previous block applied by every thread
+            for (int idx = tid; idx < (khi - klo + 1) * D; idx += NT) {
+                const int kk = idx / D, i = idx % D, k = klo + kk;
+                Sg[idx] = i > k ? A[i + LD * k] : make_float2(0.f, 0.f);
             }
+            __syncthreads();
+            for (int k = khi; k >= klo; --k) {
+                const R tk = tau[k];
+                if (tk == 0.f) continue;
+                const C* vk = Sg + (k - klo) * D;
+                C dot = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int o = 1; o < QB; o <<= 1) {
-                dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
-                dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
-            }
-            dot = make_float2(dot.x * tk, dot.y * tk);
+                for (int u = 0; u < RPT; ++u) {
+                    const int i = qb + QB * u;
+                    if (i < D) cfmaconj(dot, vk[i], y[u]);
+                }
 #pragma unroll
-            for (int u = 0; u < RPT; ++u) {
-                const int i = qb + QB * u;
-                if (i > k && i < D) {
-                    const C pr = cmul(vk[i], dot);
-                    y[u].x -= pr.x;
-                    y[u].y -= pr.y;
+                for (int o = 1; o < QB; o <<= 1) {
+                    dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
+                    dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
+                }
+                dot = make_float2(dot.x * tk, dot.y * tk);
+#pragma unroll
+                for (int u = 0; u < RPT; ++u) {
+                    const int i = qb + QB * u;
+                    if (i < D) {
+                        const C pr = cmul(vk[i], dot);
+                        y[u].x -= pr.x;
+                        y[u].y -= pr.y;
+                    }
                 }
             }
         }
@@ -462,6 +593,10 @@ __global__ void __launch_bounds__(kBigNT, 1) k_heev_big(int D, int count, double
     }
 #ifdef GWT_PHASE_TIMERS
     if (b == 0 && tid == 0) {
+        g_eig_phase[4] = hs[0] + hs[1];
+        g_eig_phase[5] = hs[2];
+        g_eig_phase[6] = hs[3];
+        g_eig_phase[7] = hs[4];
         const long long t_ph4 = clock64();
         g_eig_phase[0] = t_ph1 - t_ph0;
         g_eig_phase[1] = t_ph2 - t_ph1;

@@ -40,7 +40,7 @@ __host__ __device__ inline EigCtaLayout eig_cta_layout(int D, int count, int rs)
     GWT_TAKE(oscl, count * 4)
     GWT_TAKE(ored, 4 * 8 * 8)
     GWT_TAKE(odd, (size_t)D * count * rs)
-    GWT_TAKE(odu, (size_t)D * count * rs)
+    L.odu = o;  // no stored U superdiagonal: recomputed in the back substitution (k_heev_cr)
     GWT_TAKE(oml, (size_t)D * count * rs)
     GWT_TAKE(oxr, (size_t)D * count * rs)
 #undef GWT_TAKE
@@ -272,7 +272,7 @@ __device__ __forceinline__ void hh_cta_reg64(int D, int LD, float2* A, float2* p
 }
 
 template <class R, int DM, int NT, bool HREG = false>
-__global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, const cplx_t<R>* __restrict__ in,
+__global__ void __launch_bounds__(NT, (sizeof(R) == 8 && DM == 64) ? 2 : 256 / NT) k_heev_cr(int D, int count, const cplx_t<R>* __restrict__ in,
                                                           cplx_t<R>* __restrict__ out, double* __restrict__ evals,
                                                           int* __restrict__ fail) {
     using C = cplx_t<R>;
@@ -298,7 +298,6 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
     int* scl = reinterpret_cast<int*>(base + L.oscl);
     double* red = reinterpret_cast<double*>(base + L.ored);  // [4 slots][NW]
     R* DDv = reinterpret_cast<R*>(base + L.odd);
-    R* DUv = reinterpret_cast<R*>(base + L.odu);
     R* MLv = reinterpret_cast<R*>(base + L.oml);
     R* XR = reinterpret_cast<R*>(base + L.oxr);
     const C* H = in + b * (int64_t)D * D;
@@ -608,7 +607,6 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                     const R mult = ii_div(piv ? dcur : sb, di);
                     if (piv) sw[i >> 5] |= 1u << (i & 31);
                     LU_(DDv, i) = di;
-                    LU_(DUv, i) = piv ? dn : ucur;
                     const R ndc = piv ? ucur - mult * dn : dn - mult * ucur;
                     ucur = piv ? -mult * en : en;
                     dcur = ndc;
@@ -643,8 +641,16 @@ __global__ void __launch_bounds__(NT, 256 / NT) k_heev_cr(int D, int count, cons
                     R x1 = R(0), x2 = R(0);  // back substitution with U, x[i+1], x[i+2] in registers
                     for (int i = D - 1; i >= 0; --i) {
                         R acc = XV(i);
-                        if (i + 1 < D) acc -= LU_(DUv, i) * x1;
-                        const R u2 = (i + 2 < D && ((sw[i >> 5] >> (i & 31)) & 1u)) ? se[i + 1] : R(0);
+                        const bool pvi = (sw[i >> 5] >> (i & 31)) & 1u;
+                        if (i + 1 < D) {
+                            // U's first superdiagonal as the factorisation formed it: d_{i+1} - lam after a row
+                            // interchange, else the carried entry (e_0; -m_{i-1} e_i after an interchange at
+                            // i - 1; e_i otherwise)
+                            const bool pvm = i > 0 && ((sw[(i - 1) >> 5] >> ((i - 1) & 31)) & 1u);
+                            const R du = pvi ? sd[i + 1] - lam : (pvm ? -LU_(MLv, i - 1) * se[i] : se[i]);
+                            acc -= du * x1;
+                        }
+                        const R u2 = (i + 2 < D && pvi) ? se[i + 1] : R(0);
                         acc -= u2 * x2;
                         const R v = acc * LU_(DDv, i);
                         XV(i) = v;

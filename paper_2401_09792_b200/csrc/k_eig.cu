@@ -30,8 +30,10 @@ constexpr int kEigThreads = 256;
 #ifdef GWT_PHASE_TIMERS
 __device__ long long g_eig_phase[8];
 #define GWT_CLK(v) const long long v = clock64()
+#define GWT_TICK(v) v = clock64()
 #else
 #define GWT_CLK(v)
+#define GWT_TICK(v)
 #endif
 constexpr int kSmemMaxD = 64;
 
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(kEigThreads) k_heev_topk(int D, int count, con
 
 #ifdef GWT_PHASE_TIMERS
 extern "C" int gwt_debug_eig_phases(long long* out4) {
-    return (int)cudaMemcpyFromSymbol(out4, g_eig_phase, 4 * sizeof(long long));
+    return (int)cudaMemcpyFromSymbol(out4, g_eig_phase, 8 * sizeof(long long));
 }
 #endif
 
@@ -1141,6 +1143,9 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
             } else if (D <= 64) {
                 e = cudaFuncSetAttribute(k_heev_cr<T, 64, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
                 if (e != cudaSuccess) return e;
+                // binary64 D <= 64 (the delay Grams): 2 CTAs per SM when the layout fits (<= 113 KB each)
+                e = cudaFuncSetAttribute(k_heev_cr<T, 64, 256>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+                if (e != cudaSuccess) return e;
                 k_heev_cr<T, 64, 256><<<(unsigned)batch, 256, sm, st>>>(D, count, (const cplx_t<T>*)in, (cplx_t<T>*)out,
                                                                   evals, fail);
             } else {
@@ -1162,7 +1167,7 @@ cudaError_t launch_heev_topk(int D, int count, int64_t batch, const void* in, vo
         // joint-orthogonalisation threshold of the inverse iterations (relative to ||T||)
         static const double big_ctol = [] {
             const char* v = env_once("GWT_EIG_BIG_CTOL");
-            return v ? std::atof(v) : 1e-3;
+            return v ? std::atof(v) : 1e-4;
         }();
         k_heev_big<<<(unsigned)batch, kBigNT, sm, st>>>(D, count, big_ctol, (const float2*)in, (float2*)out, evals,
                                                         reinterpret_cast<float2*>(ws_a), reinterpret_cast<float*>(ws_z),
