@@ -190,9 +190,22 @@ template <int MP, int H> __host__ __device__ constexpr int srow_off(int idx) {
 }
 template <int MP> constexpr int kServAcc = MP == 8 ? 18 : 5;
 
+#ifdef GWT_F2D_INT
+// fp32 -> fp64 by exponent rebias on the integer pipe (F2F.F64.F32 issues at 16/clk/SM on the XU);
+// exact for normal numbers, +-0 kept, fp32 subnormals (< 1.2e-38) flush to +-0, Inf/NaN kept non-finite
+__device__ __forceinline__ double i2d(uint32_t b) {
+    const uint32_t a = b & 0x7fffffffu;
+    uint32_t hi = ((a >> 3) + 0x38000000u) | (b & 0x80000000u);
+    hi = a < 0x00800000u ? (b & 0x80000000u) : hi;
+    hi = a >= 0x7f800000u ? (hi | 0x7ff00000u) : hi;
+    return __hiloint2double((int)hi, (int)(b << 29));
+}
+__device__ __forceinline__ double2 f2d(uint32_t re, uint32_t im) { return make_double2(i2d(re), i2d(im)); }
+#else
 __device__ __forceinline__ double2 f2d(uint32_t re, uint32_t im) {
     return make_double2((double)__uint_as_float(re), (double)__uint_as_float(im));
 }
+#endif
 
 template <int MP>
 __device__ __forceinline__ void tmem_ldmp(uint32_t taddr, uint32_t (&r)[MP]);

@@ -124,7 +124,7 @@ __device__ __forceinline__ void ql_rows(double (&dg)[MP], double (&eo)[MP], doub
 // shared-memory layout of one slice (all offsets in bytes, 16-byte aligned)
 struct SliceLayout {
     int U, MP, L, n, J, tsz;  // tsz = sizeof(complex T)
-    int a_off, z_off, u_off, lam_off, tau_off, v_off, tri_off, bytes;
+    int a_off, z_off, u_off, lam_off, tau_off, v_off, bytes;
     __host__ __device__ void init(int U_, int MP_, int L_, int n_, int J_, int tsz_) {
         U = U_; MP = MP_; L = L_; n = n_; J = J_; tsz = tsz_;
         int o = 0;
@@ -136,8 +136,6 @@ struct SliceLayout {
         lam_off = o; o += U * MP * 8;                      // eigenvalues by rank
         tau_off = o; o += U * MP * 16;                     // Householder scalars
         v_off = o; o += J * n * L * tsz;                   // anchor precoders V'_k [k][y][l]
-        o = (o + 15) & ~15;
-        tri_off = o; o += U * 2 * MP * 8;                  // tridiagonal (d, e) -> eigenvalues (QL phase)
         bytes = (o + 15) & ~15;
     }
 };
@@ -298,54 +296,19 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     eo[MP - 1] = 0.0;
     // the last step (i = MP-2) may leave a complex phase only through tau (|1 - tau| = 1): e is real.
 
-    // ---------------- phase 1c: implicit QL (tql2) on (dg, eo). The scalar recurrence is serial, so it runs
-    // with 2 lanes per user (each rotating 4 rows of Z) on the first 2 U spc threads instead of being
-    // replicated over the user's 8 lanes: 4x fewer issued instructions for the same latency chain.
+    // ---------------- phase 1c (warp-local): implicit QL (tql2) on (dg, eo), the recurrence replicated over the
+    // user's MP lanes (identical inputs -> identical results), lane r rotating row r of Z; no CTA barrier.
+    // (Measured against packing the recurrence onto 2 lanes per user in 2 warps behind a CTA barrier: C4 stage
+    // 21.5 -> 21.0 ms, C3 5.2 -> 4.8 ms per 32 groups; the QL latency chain itself is ~45 % of this kernel.)
     {
-        double* stri = reinterpret_cast<double*>(sbase + lay.tri_off) + u * 2 * MP;
-        if (r == 0) {
+        double zr[1][MP];
 #pragma unroll
-            for (int k = 0; k < MP; ++k) {
-                stri[k] = dg[k];
-                stri[MP + k] = eo[k];
-            }
-        }
-        __syncthreads();
-        constexpr int LQ = 2, RL = MP / LQ;
-        const int nql = spc * U * LQ;
-        if (tid < ((nql + 31) & ~31)) {
-            const bool qv = tid < nql;
-            const int qi = qv ? tid : 0;
-            const int qs = qi / (U * LQ), qu = (qi / LQ) % U, qh = qi % LQ;
-            unsigned char* qb = smem_raw + (size_t)qs * lay.bytes;
-            double* qt = reinterpret_cast<double*>(qb + lay.tri_off) + qu * 2 * MP;
-            double d[MP], e[MP];
+        for (int c = 0; c < MP; ++c) zr[0][c] = c == r ? 1.0 : 0.0;
+        ql_rows<MP, 1>(dg, eo, zr, active);
+        __syncwarp();
 #pragma unroll
-            for (int k = 0; k < MP; ++k) {
-                d[k] = qt[k];
-                e[k] = qt[MP + k];
-            }
-            double zq[RL][MP];
-#pragma unroll
-            for (int q = 0; q < RL; ++q)
-#pragma unroll
-                for (int c = 0; c < MP; ++c) zq[q][c] = c == qh * RL + q ? 1.0 : 0.0;
-            ql_rows<MP, RL>(d, e, zq, qv);
-            __syncwarp();
-            if (qv) {
-                double* zs = reinterpret_cast<double*>(qb + lay.z_off) + qu * MP * (MP + 1);
-#pragma unroll
-                for (int q = 0; q < RL; ++q)
-#pragma unroll
-                    for (int c = 0; c < MP; ++c) zs[(qh * RL + q) * (MP + 1) + c] = zq[q][c];
-                if (qh == 0)
-#pragma unroll
-                    for (int k = 0; k < MP; ++k) qt[k] = d[k];
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < MP; ++k) dg[k] = stri[k];
+        for (int c = 0; c < MP; ++c) sZ[r * (MP + 1) + c] = zr[0][c];
+        __syncwarp();
     }
     // ---------------- phase 1d: back-transform, lane j = eigenvector j: u = H_0 ... H_{MP-2} z_j
     double2 uv[MP];
