@@ -40,10 +40,17 @@ $(DROPIN): tests/cpp/test_dropin.cpp $(HOSTLIB)
 phase:
 	$(MAKE) OBJ=$(PKG)/_build/phase/obj LIB=$(PKG)/_build/phase/libgwt_b200.so NVFLAGS="$(NVFLAGS) -DGWT_PHASE_TIMERS" $(PKG)/_build/phase/libgwt_b200.so
 
+# A/B variant build: make variant V=name DEFS="-DGWT_..."  ->  $(PKG)/_build/name/libgwt_b200.so (GWT_LIB_PATH)
+variant:
+	$(MAKE) OBJ=$(PKG)/_build/$(V)/obj LIB=$(PKG)/_build/$(V)/libgwt_b200.so NVFLAGS="$(NVFLAGS) $(DEFS)" $(PKG)/_build/$(V)/libgwt_b200.so
+
+micro:
+	for f in f2f dfma_occ dmma gram_mix; do $(NVCC) $(ARCH) -O3 -o tools/micro/$$f tools/micro/$$f.cu; done
+
 oracle:
 	$(MAKE) -s -C oracle
 
 clean:
 	rm -rf $(PKG)/_build oracle/_build
 
-.PHONY: all oracle clean phase
+.PHONY: all oracle clean phase variant micro

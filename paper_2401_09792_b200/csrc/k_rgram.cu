@@ -13,16 +13,18 @@
 // E(q, f) = sum_r C(r, q) conj(c_r(f)), x = r + m c (the core's storage order). It runs as a real
 // GEMM on tcgen05.mma.kind::tf32 with 3xTF32 splitting (hi*hi + hi*lo + lo*hi ~ fp32 accuracy):
 //     A  = [Er | Ei]                       (128 subcarriers x 2p, K-major, from k_esplit)
-//     B  = [Gi | Gr | -Gi]                 (x chunk of XC rows x 3p, K-major, from k_bsplit)
-//     Hi = A * B[:, 0:2p]^T,   Hr = A * B[:, p:3p]^T        (two MMAs sharing A, k-step pointer offsets)
-// so the real-form doubling costs no extra operand storage. Both operands are staged by TMA bulk
+//     B  = [Gi | Gr ; Gr | -Gi]            (2 XC rows x 2p, K-major, from k_bsplit: rows [0, XC) give Hi of the
+//                                           x chunk, rows [XC, 2 XC) its Hr)
+//     [Hi | Hr] = A * B^T                  (one MMA of N = 2 XC per k-step: the A slice is fetched once for both)
+// (measured against two N = XC MMAs per k-step on B = [Gi | Gr | -Gi]: the small-N MMAs are paced by their
+// operand fetch, not by the math). Both operands are staged by TMA bulk
 // copies (cp.async.bulk + mbarrier complete_tx) from pre-split global buffers; the accumulators (Hr,
 // Hi per link slot, two stages) live in TMEM with lane = subcarrier.
 //
 // CTA = (user, group); it walks the subcarrier tiles and, per tile, its J "jobs": job 0 = the
 // serving link, job k = (interfering link (k,i,j), anchor link (k,k,0)). Warp roles:
 //   warp 8  (one thread): TMA producer   E tile (A) per job, G chunk (B) per chunk, 2 B stages
-//   warp 9  (one thread): MMA issuer     per chunk 3 passes x p/4 k-steps x {Hi, Hr} x slots
+//   warp 9  (one thread): MMA issuer     per chunk 3 passes x p/4 k-steps x slots
 //   warps 0-7           : Gram epilogue  two threads per subcarrier (TMEM lane quarter = warp % 4);
 //                         tcgen05.ld -> binary64 -> DFMA accumulation of the entries of its rows
 // Binary64 accumulation of the exact products of the fp32 H~ values keeps the Gram route free of
@@ -42,7 +44,7 @@ constexpr int kRgThreads = (kEpiWarps + 2) * 32;  // + MMA warp + TMA warp
 
 struct RgCfg {
     int m, n, p, mn, XC, nch, ks, tcols;
-    uint32_t TA, TB;  // bytes of one A operand (128 x 2p fp32) / one B operand (XC x 3p fp32)
+    uint32_t TA, TB;  // bytes of one A operand (128 x 2p fp32) / one B operand (2 XC x 2p fp32)
     uint32_t sbo_a, sbo_b;
     size_t smem;
 };
@@ -57,9 +59,9 @@ RgCfg rg_cfg(const Topo& t, int XC) {
     c.nch = c.mn / XC;
     c.ks = 2 * t.p / 8;
     c.TA = (uint32_t)kFT * 2 * t.p * 4;
-    c.TB = (uint32_t)XC * 3 * t.p * 4;
+    c.TB = (uint32_t)2 * XC * 2 * t.p * 4;
     c.sbo_a = (uint32_t)(2 * t.p / 4) * 128;
-    c.sbo_b = (uint32_t)(3 * t.p / 4) * 128;
+    c.sbo_b = (uint32_t)(2 * t.p / 4) * 128;
     c.smem = (size_t)4 * c.TA + (size_t)8 * c.TB;
     c.tcols = 8 * XC <= 32 ? 32 : (8 * XC <= 64 ? 64 : (8 * XC <= 128 ? 128 : 256));
     return c;
@@ -73,7 +75,7 @@ __device__ __forceinline__ uint32_t kmaj(int row, int k, uint32_t sbo) {
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
-// B operands: Bready[g][l][chunk][hi|lo] = [Gi | Gr | -Gi] rows x = chunk*XC + n, K-major canonical.
+// B operands: Bready[g][l][chunk][hi|lo] = rows n: [Gi | Gr], rows XC + n: [Gr | -Gi] (x = chunk*XC + n), K-major canonical.
 __global__ void __launch_bounds__(256) k_bsplit(Topo t, RgCfg c, const float2* __restrict__ G,
                                                unsigned char* __restrict__ Bready) {
     const int ch = blockIdx.x, l = blockIdx.y;
@@ -85,12 +87,12 @@ __global__ void __launch_bounds__(256) k_bsplit(Topo t, RgCfg c, const float2* _
     for (int e = threadIdx.x; e < XC * p; e += blockDim.x) {
         const int n = e % XC, q = e / XC;
         const float2 v = Gl[(int64_t)q * c.mn + x0 + n];
-        const float vals[3] = {v.y, v.x, -v.y};
+        const float vals[4] = {v.y, v.x, v.x, -v.y};
 #pragma unroll
-        for (int b = 0; b < 3; ++b) {
+        for (int b = 0; b < 4; ++b) {
             float h, r;
             tc::split_tf32_rn(vals[b], h, r);
-            const uint32_t o = kmaj(n, b * p + q, c.sbo_b);
+            const uint32_t o = kmaj((b >> 1) * XC + n, (b & 1) * p + q, c.sbo_b);
             *reinterpret_cast<float*>(hi + o) = h;
             *reinterpret_cast<float*>(lo + o) = r;
         }
@@ -427,16 +429,14 @@ struct RgCtrl {
         tc::mbar_wait(&b_full[st], use & 1);
         if (use > 0) tc::mbar_wait(&t_empty[st], (use - 1) & 1);
         tc::fence_after_sync();
-        const uint32_t idesc = tc::idesc_tf32(kFT, XC);
-        const uint32_t roff = (uint32_t)(c->p / 4) * 128;  // B[:, p:3p] = [Gr | -Gi]
+        const uint32_t idesc = tc::idesc_tf32(kFT, 2 * XC);
         for (int sl = 0; sl < ns; ++sl) {
-            const uint32_t dI = tb + (uint32_t)(st * 4 * XC + sl * 2 * XC), dR = dI + XC;
+            const uint32_t dI = tb + (uint32_t)(st * 4 * XC + sl * 2 * XC);  // columns [Hi | Hr] of this slot
             const uint32_t ab = tc::smem_u32(sA + (size_t)sl * 2 * c->TA);
             const uint32_t bb = tc::smem_u32(sB + ((size_t)st * 2 + sl) * 2 * c->TB);
             // descriptor start-address field = addr >> 4 (14 bits, smem < 256 KB): k-step kk adds 16
             const uint64_t dAh = tc::smem_desc(ab, 128, c->sbo_a), dAl = tc::smem_desc(ab + c->TA, 128, c->sbo_a);
             const uint64_t dBh = tc::smem_desc(bb, 128, c->sbo_b), dBl = tc::smem_desc(bb + c->TB, 128, c->sbo_b);
-            const uint64_t rr = roff >> 4;
 #pragma unroll 1
             for (int pass = 0; pass < 3; ++pass) {
                 const uint64_t da = pass == 2 ? dAl : dAh;
@@ -445,7 +445,6 @@ struct RgCtrl {
                     const uint32_t acc = (pass > 0 || kk > 0) ? 1u : 0u;
                     const uint64_t o = (uint64_t)kk * 16;
                     tc::mma_tf32(dI, da + o, db + o, idesc, acc);
-                    tc::mma_tf32(dR, da + o, db + rr + o, idesc, acc);
                 }
             }
         }

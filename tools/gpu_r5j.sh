@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+echo "dmma coop, ATS" > gpurun_out/r5j_ab.log
+timeout 300 python tools/sinr_real.py C4 64 2 3 >> gpurun_out/r5j_ab.log 2>&1
+timeout 300 python tools/sinr_real.py C3 64 2 3 >> gpurun_out/r5j_ab.log 2>&1
+echo "dmma coop, no ATS" >> gpurun_out/r5j_ab.log
+GWT_RGRAM_ATS=0 timeout 300 python tools/sinr_real.py C4 64 2 3 >> gpurun_out/r5j_ab.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_scale.py -m gpu -q -x > gpurun_out/r5j_pytest.log 2>&1; echo "rc $?" >> gpurun_out/r5j_pytest.log
