@@ -29,6 +29,7 @@
 //                         tcgen05.ld -> binary64 -> DFMA accumulation of the entries of its rows
 // Binary64 accumulation of the exact products of the fp32 H~ values keeps the Gram route free of
 // the kappa^2 loss an fp32 Gram would add.
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -350,6 +351,9 @@ __device__ __forceinline__ void epi_job(const EpiCtx& e, uint32_t& cnt, bool val
         tc::mbar_wait(&e.t_full[st], use & 1);
         tc::fence_after_sync();
         const uint32_t col0 = e.tcol + (uint32_t)(st * 4 * e.XC);
+#ifdef GWT_RG_PROBE_NOEPI
+        if (ch == 0)
+#endif
         if constexpr (KIND == 0) serving_chunk<MP, H>(col0, e.XC, acc);
         else if constexpr (KIND == 3) pair_chunk_full<MP, H>(col0, e.XC, acc);
         else pair_chunk<MP, H, KIND - 1>(col0, e.XC, acc);
@@ -405,7 +409,38 @@ struct RgCtrl {
         const int64_t gl = g * links + job_link(jb, sl);
         tc::bulk_g2s(sA + (size_t)sl * 2 * c->TA, Eready + ((size_t)gl * ntiles + ti) * 2 * c->TA, 2 * c->TA, a_full);
     }
+#ifdef GWT_RG_TIMERS
+#define RG_T0 long long t0_ = clock64()
+#define RG_TA(i) do { long long t1_ = clock64(); tm[i] += t1_ - t0_; t0_ = t1_; } while (0)
+    mutable long long tm[4] = {0, 0, 0, 0};
+#else
+#define RG_T0
+#define RG_TA(i)
+#endif
+    // The MMA warp walks the chunk sequence as a whole warp (the waits are warp-wide) and issues TMA / tcgen05.mma /
+    // tcgen05.commit under elect.sync: in a `lane == 0` region the compiler wraps every uniform-datapath instruction
+    // (UTCHMMA, UTCBAR) in an ELECT / BRA.U.ANY loop — 126 cycles per MMA on the lone issuing thread
+    // (tools/micro/mma_fetch.cu: 242 vs 48 cycles per N = 64 MMA) — while under elect.sync with the k-steps
+    // unrolled the MMAs issue back to back and run at their shared-memory operand fetch rate.
+    template <int KS>
+    __device__ __forceinline__ void issue(uint32_t d, uint64_t dAh, uint64_t dAl, uint64_t dBh, uint64_t dBl,
+                                          uint32_t idesc) const {
+#ifdef GWT_RG_PROBE_1PASS
+        constexpr int NP = 1;
+#else
+        constexpr int NP = 3;
+#endif
+#pragma unroll
+        for (int pass = 0; pass < NP; ++pass) {
+            const uint64_t da = pass == 2 ? dAl : dAh;
+            const uint64_t db = pass == 1 ? dBl : dBh;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk)
+                tc::mma_tf32(d, da + 16 * kk, db + 16 * kk, idesc, (pass > 0 || kk > 0) ? 1u : 0u);
+        }
+    }
     __device__ __forceinline__ void mma(int k) const {  // all MMAs of flat chunk k (loads the job's A first)
+        RG_T0;
         const int st = k & 1, use = k >> 1;
         const int job = k / nch, ch = k % nch, jb = job % njobs;
         const int ns = jb == 0 ? 1 : 2;
@@ -414,43 +449,50 @@ struct RgCtrl {
             // A of this job: job 0 uses slot 0 and prefetches the first pair's anchor into slot 1; the first
             // pair's quarter 0 then loads slot 0 alone; quarter 1 reuses both slots; later pairs load both
             if (job > 0) tc::mbar_wait(a_empty, (job - 1) & 1);
-            const int pk = (jb - 1) / split, q = (jb - 1) % split;
-            const int nload = jb == 0 ? (njobs > 1 ? 2 : 1) : (q == 1 ? 0 : (pk == 0 ? 1 : 2));
-            tc::mbar_arrive_expect_tx(a_full, (uint32_t)nload * 2 * c->TA);
-            if (jb == 0) {
-                tma_a(job, 0);
-                if (njobs > 1) tma_a(job + 1, 1);
-            } else if (q == 0) {
-                tma_a(job, 0);
-                if (pk > 0) tma_a(job, 1);
-            }
-            tc::mbar_wait(a_full, job & 1);
-        }
-        tc::mbar_wait(&b_full[st], use & 1);
-        if (use > 0) tc::mbar_wait(&t_empty[st], (use - 1) & 1);
-        tc::fence_after_sync();
-        const uint32_t idesc = tc::idesc_tf32(kFT, 2 * XC);
-        for (int sl = 0; sl < ns; ++sl) {
-            const uint32_t dI = tb + (uint32_t)(st * 4 * XC + sl * 2 * XC);  // columns [Hi | Hr] of this slot
-            const uint32_t ab = tc::smem_u32(sA + (size_t)sl * 2 * c->TA);
-            const uint32_t bb = tc::smem_u32(sB + ((size_t)st * 2 + sl) * 2 * c->TB);
-            // descriptor start-address field = addr >> 4 (14 bits, smem < 256 KB): k-step kk adds 16
-            const uint64_t dAh = tc::smem_desc(ab, 128, c->sbo_a), dAl = tc::smem_desc(ab + c->TA, 128, c->sbo_a);
-            const uint64_t dBh = tc::smem_desc(bb, 128, c->sbo_b), dBl = tc::smem_desc(bb + c->TB, 128, c->sbo_b);
-#pragma unroll 1
-            for (int pass = 0; pass < 3; ++pass) {
-                const uint64_t da = pass == 2 ? dAl : dAh;
-                const uint64_t db = pass == 1 ? dBl : dBh;
-                for (int kk = 0; kk < c->ks; ++kk) {
-                    const uint32_t acc = (pass > 0 || kk > 0) ? 1u : 0u;
-                    const uint64_t o = (uint64_t)kk * 16;
-                    tc::mma_tf32(dI, da + o, db + o, idesc, acc);
+            if (tc::elect_one()) {
+                const int pk = (jb - 1) / split, q = (jb - 1) % split;
+                const int nload = jb == 0 ? (njobs > 1 ? 2 : 1) : (q == 1 ? 0 : (pk == 0 ? 1 : 2));
+                tc::mbar_arrive_expect_tx(a_full, (uint32_t)nload * 2 * c->TA);
+                if (jb == 0) {
+                    tma_a(job, 0);
+                    if (njobs > 1) tma_a(job + 1, 1);
+                } else if (q == 0) {
+                    tma_a(job, 0);
+                    if (pk > 0) tma_a(job, 1);
                 }
             }
+            __syncwarp();
+            tc::mbar_wait(a_full, job & 1);
         }
-        tc::commit(&b_empty[st]);
-        tc::commit(&t_full[st]);
-        if (ch == nch - 1) tc::commit(a_empty);
+        RG_TA(0);
+        tc::mbar_wait(&b_full[st], use & 1);
+        RG_TA(1);
+        if (use > 0) tc::mbar_wait(&t_empty[st], (use - 1) & 1);
+        RG_TA(2);
+        tc::fence_after_sync();
+        const uint32_t idesc = tc::idesc_tf32(kFT, 2 * XC);
+        if (tc::elect_one()) {
+            for (int sl = 0; sl < ns; ++sl) {
+                const uint32_t dI = tb + (uint32_t)(st * 4 * XC + sl * 2 * XC);  // columns [Hi | Hr] of this slot
+                const uint32_t ab = tc::smem_u32(sA + (size_t)sl * 2 * c->TA);
+                const uint32_t bb = tc::smem_u32(sB + ((size_t)st * 2 + sl) * 2 * c->TB);
+                // descriptor start-address field = addr >> 4 (14 bits, smem < 256 KB): k-step kk adds 16
+                const uint64_t dAh = tc::smem_desc(ab, 128, c->sbo_a), dAl = tc::smem_desc(ab + c->TA, 128, c->sbo_a);
+                const uint64_t dBh = tc::smem_desc(bb, 128, c->sbo_b), dBl = tc::smem_desc(bb + c->TB, 128, c->sbo_b);
+                switch (c->ks) {
+                    case 2: issue<2>(dI, dAh, dAl, dBh, dBl, idesc); break;
+                    case 3: issue<3>(dI, dAh, dAl, dBh, dBl, idesc); break;
+                    case 4: issue<4>(dI, dAh, dAl, dBh, dBl, idesc); break;
+                    case 6: issue<6>(dI, dAh, dAl, dBh, dBl, idesc); break;
+                    default: issue<8>(dI, dAh, dAl, dBh, dBl, idesc); break;
+                }
+            }
+            tc::commit(&b_empty[st]);
+            tc::commit(&t_full[st]);
+            if (ch == nch - 1) tc::commit(a_empty);
+        }
+        __syncwarp();
+        RG_TA(3);
     }
 };
 
@@ -489,8 +531,12 @@ __global__ void __launch_bounds__(kRgThreads, 1) k_rgram(Topo t, RgCfg c, int Fc
     const RgCtrl ctl{&c, smem, smem + 4 * c.TA, Bready, Eready, &a_full, &a_empty, b_full, b_empty, t_full, t_empty,
                      tb, g, t.links(), ntiles, njobs, nch, total, u / K, u % K, J, K, SP};
     if (warp == kEpiWarps) {  // MMA warp
-        if (lane == 0)
-            for (int k = 0; k < total; ++k) ctl.mma(k);
+        for (int k = 0; k < total; ++k) ctl.mma(k);
+#ifdef GWT_RG_TIMERS
+        if (lane == 0 && blockIdx.x == 3 && blockIdx.y == 5)
+            printf("mma thread: chunks %d  a_full %lld  b_full %lld  t_empty %lld  issue %lld (cycles per chunk)\n", total,
+                   ctl.tm[0] / total, ctl.tm[1] / total, ctl.tm[2] / total, ctl.tm[3] / total);
+#endif
         __syncwarp();
     } else if (warp == kEpiWarps + 1) {  // TMA warp
         if (lane == 0)
