@@ -190,22 +190,25 @@ __global__ void __launch_bounds__(kGTThreads, 1) k_gram_tcb(Topo t, GramDesc d, 
         }
         __syncwarp();
     } else if (warp == 9) {
-        // ---------------- MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc = tc::idesc_tf32(kGT, nbp);
-            const uint32_t aoff = (uint32_t)(x0 / 8) * SBO;  // the strip's rows inside the B tiles
-            for (int c = 0; c < nch; ++c) {
-                const int st = c & 1, use = c >> 1;
-                tc::mbar_wait(&tile_full[st], use & 1);
-                tc::fence_after_sync();
+        // ---------------- MMA issuer: the whole warp waits, one elected lane issues (under elect.sync the
+        // UTCHMMAs compile back to back; in a `lane == 0` region each sits in an ELECT / BRA.U.ANY loop, ~240
+        // cycles per MMA on the lone thread against the 128-cycle floor of N = 256, tools/micro/mma_fetch.cu)
+        const uint32_t idesc = tc::idesc_tf32(kGT, nbp);
+        const uint32_t aoff = (uint32_t)(x0 / 8) * SBO;  // the strip's rows inside the B tiles
+        for (int c = 0; c < nch; ++c) {
+            const int st = c & 1, use = c >> 1;
+            tc::mbar_wait(&tile_full[st], use & 1);
+            tc::fence_after_sync();
+            if (tc::elect_one()) {
                 const uint32_t b0 = tc::smem_u32(tiles + (size_t)st * 4 * TILE);
                 const uint64_t dBh = tc::smem_desc(b0, 128, SBO), dBl = tc::smem_desc(b0 + TILE, 128, SBO);
                 const uint64_t dPh = tc::smem_desc(b0 + 2 * TILE, 128, SBO), dPl = tc::smem_desc(b0 + 3 * TILE, 128, SBO);
                 const uint64_t dAh = tc::smem_desc(b0 + aoff, 128, SBO), dAl = tc::smem_desc(b0 + TILE + aoff, 128, SBO);
+                const uint32_t acc0 = c > 0 ? 1u : 0u;
 #pragma unroll
                 for (int kk = 0; kk < KC / 8; ++kk) {
                     const uint64_t o = (uint64_t)kk * 16;  // 256-byte k-step in the 16-byte address field
-                    const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+                    const uint32_t acc = kk > 0 ? 1u : acc0;
                     tc::mma_tf32(tre, dAh + o, dBh + o, idesc, acc);
                     tc::mma_tf32(tre, dAh + o, dBl + o, idesc, 1u);
                     tc::mma_tf32(tre, dAl + o, dBh + o, idesc, 1u);
@@ -214,10 +217,10 @@ __global__ void __launch_bounds__(kGTThreads, 1) k_gram_tcb(Topo t, GramDesc d, 
                     tc::mma_tf32(tim, dAl + o, dPh + o, idesc, 1u);
                 }
                 tc::commit(&tile_empty[st]);
+                if (c == nch - 1) tc::commit(&acc_full);
             }
-            tc::commit(&acc_full);
+            __syncwarp();
         }
-        __syncwarp();
     } else {
         // ---------------- converters (256 threads): 16-byte units (2 complex) of the raw block
         const int units = nbp * T1 / 2;
