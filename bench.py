@@ -504,7 +504,9 @@ def run_gpu_config(gw, O, torch, cfg, ctx, dev, stream, flush, rank, world, step
     with ClockSampler(dev.index or 0) as clk:
         rep, step_ms = timed(torch, stream, flush, step, steps)
     launches = ctx.launches - launches0
-    ms = float(np.mean(step_ms))
+    # headline: mean of the K timed steps (the contract's "time exactly K steps"); the side configs' sub-millisecond
+    # steps report the median (one allocator hiccup in 3-10 steps would otherwise set the figure), all steps listed
+    ms = float(np.mean(step_ms)) if headline else float(np.median(step_ms))
     st = np.array(ctx.stage_ms())
     evals = ng * cfg.F * cfg.J * cfg.K
     bad = int(rep.status.ne(0).sum())
@@ -691,8 +693,6 @@ def main(argv=None):
                         "R_t_gpu": float(np.mean(fms)) / e["ms"], "t_full_ms": float(np.mean(fms)),
                         "e_c": pm.sinr_error(full.sinr.cpu().numpy(), rep_e.sinr.cpu().numpy()),
                         "R_s": pm.storage_ratio(topo, c2.ranks())}
-                for k in ("step_ms_all",):
-                    e.pop(k, None)
                 extra[name] = e
                 del Xe, fac_e, rep_e
             except Exception as ex:  # a secondary config must not hide the headline line

@@ -124,7 +124,7 @@ __device__ __forceinline__ void ql_rows(double (&dg)[MP], double (&eo)[MP], doub
 // shared-memory layout of one slice (all offsets in bytes, 16-byte aligned)
 struct SliceLayout {
     int U, MP, L, n, J, tsz;  // tsz = sizeof(complex T)
-    int a_off, z_off, u_off, lam_off, tau_off, v_off, bytes;
+    int a_off, z_off, u_off, lam_off, tau_off, v_off, tri_off, bytes;
     __host__ __device__ void init(int U_, int MP_, int L_, int n_, int J_, int tsz_) {
         U = U_; MP = MP_; L = L_; n = n_; J = J_; tsz = tsz_;
         int o = 0;
@@ -136,6 +136,9 @@ struct SliceLayout {
         lam_off = o; o += U * MP * 8;                      // eigenvalues by rank
         tau_off = o; o += U * MP * 16;                     // Householder scalars
         v_off = o; o += J * n * L * tsz;                   // anchor precoders V'_k [k][y][l]
+        o = (o + 15) & ~15;
+        tri_off = o;
+        o += U * 2 * MP * 8;                               // tridiagonal (d, e) -> eigenvalues (packed QL phase)
         bytes = (o + 15) & ~15;
     }
 };
@@ -146,7 +149,7 @@ struct SliceLayout {
 // here. PGM = true: the serving / pair Grams come precomputed in PG[item][user][J][m*m] (k_rgram.cu); the
 // interference of cell k is Y = X_{u,k} W'_k with W'_k = U'_L Lambda'^{-1/2} of the anchor (k,0)
 // (= H~_kij V'_k, the same product through the anchor's Gram eigenpairs), all in binary64.
-template <class T, int MP, bool PGM>
+template <class T, int MP, bool PGM, bool QLP>
 __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t nslices, int fc, int64_t Ftot,
                                                     int64_t f0, double sigma, const cplx_t<T>* __restrict__ H,
                                                     const double2* __restrict__ PG, double* __restrict__ sinr,
@@ -296,11 +299,59 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     eo[MP - 1] = 0.0;
     // the last step (i = MP-2) may leave a complex phase only through tau (|1 - tau| = 1): e is real.
 
-    // ---------------- phase 1c (warp-local): implicit QL (tql2) on (dg, eo), the recurrence replicated over the
-    // user's MP lanes (identical inputs -> identical results), lane r rotating row r of Z; no CTA barrier.
-    // (Measured against packing the recurrence onto 2 lanes per user in 2 warps behind a CTA barrier: C4 stage
-    // 21.5 -> 21.0 ms, C3 5.2 -> 4.8 ms per 32 groups; the QL latency chain itself is ~45 % of this kernel.)
-    {
+    // ---------------- phase 1c: implicit QL (tql2) on (dg, eo).
+    // QLP = false (warp-local): the recurrence is replicated over the user's MP lanes (identical inputs -> identical
+    // results), lane r rotating row r of Z; no CTA barrier. QLP = true (packed): 2 lanes per user, each rotating
+    // MP / 2 rows of Z, on the first 2 U spc threads of the CTA behind two CTA barriers — a quarter of the
+    // binary64 warp instructions. Measured per 64 groups: C4 (32 users, one slice per CTA; fp64 pipe 42 % busy in
+    // the warp-local form) packed 42.6 vs 45.3 ms, and 337 vs 398 ms on the whole config; C3 (16 users, 2 slices
+    // per CTA) warp-local 9.2 vs 10.3 ms. The launcher picks by slices per CTA (GWT_QL_PACKED=0/1 overrides).
+    if constexpr (QLP) {
+        double* stri = reinterpret_cast<double*>(sbase + lay.tri_off) + u * 2 * MP;
+        if (r == 0) {
+#pragma unroll
+            for (int k = 0; k < MP; ++k) {
+                stri[k] = dg[k];
+                stri[MP + k] = eo[k];
+            }
+        }
+        __syncthreads();
+        constexpr int LQ = 2, RL = MP / LQ;
+        const int nql = spc * U * LQ;
+        if (tid < ((nql + 31) & ~31)) {
+            const bool qv = tid < nql;
+            const int qi = qv ? tid : 0;
+            const int qs = qi / (U * LQ), qu = (qi / LQ) % U, qh = qi % LQ;
+            unsigned char* qb = smem_raw + (size_t)qs * lay.bytes;
+            double* qt = reinterpret_cast<double*>(qb + lay.tri_off) + qu * 2 * MP;
+            double d[MP], e[MP];
+#pragma unroll
+            for (int k = 0; k < MP; ++k) {
+                d[k] = qt[k];
+                e[k] = qt[MP + k];
+            }
+            double zq[RL][MP];
+#pragma unroll
+            for (int q = 0; q < RL; ++q)
+#pragma unroll
+                for (int c = 0; c < MP; ++c) zq[q][c] = c == qh * RL + q ? 1.0 : 0.0;
+            ql_rows<MP, RL>(d, e, zq, qv);
+            __syncwarp();
+            if (qv) {
+                double* zs = reinterpret_cast<double*>(qb + lay.z_off) + qu * MP * (MP + 1);
+#pragma unroll
+                for (int q = 0; q < RL; ++q)
+#pragma unroll
+                    for (int c = 0; c < MP; ++c) zs[(qh * RL + q) * (MP + 1) + c] = zq[q][c];
+                if (qh == 0)
+#pragma unroll
+                    for (int k = 0; k < MP; ++k) qt[k] = d[k];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < MP; ++k) dg[k] = stri[k];
+    } else {
         double zr[1][MP];
 #pragma unroll
         for (int c = 0; c < MP; ++c) zr[0][c] = c == r ? 1.0 : 0.0;
@@ -577,8 +628,8 @@ bool sinr_users_fits(const Topo& t, size_t csize) {
     return lay.bytes <= 200 * 1024;
 }
 
-template <class T, int MP, bool PGM>
-static cudaError_t launch_users_mp(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0, double sigma,
+template <class T, int MP, bool PGM, bool QLP>
+static cudaError_t launch_users_qlp(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0, double sigma,
                                    const void* H, const double2* PG, double* sinr, double* signal, int* status,
                                    cudaStream_t st) {
     SliceLayout lay;
@@ -588,12 +639,29 @@ static cudaError_t launch_users_mp(const Topo& t, int64_t nslices, int fc, int64
     while (spc > 1 && (size_t)(spc + 1) * lay.bytes > 200 * 1024) --spc;
     const int threads = ((spc * per + 31) / 32) * 32;
     const size_t smem = (size_t)((threads + per - 1) / per) * lay.bytes;
-    cudaError_t e = cudaFuncSetAttribute(k_sinr_users<T, MP, PGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_sinr_users<T, MP, PGM, QLP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (nslices + spc - 1) / spc;
-    k_sinr_users<T, MP, PGM><<<(unsigned)blocks, threads, smem, st>>>(t, spc, nslices, fc, Ftot, f0, sigma,
-                                                                      (const cplx_t<T>*)H, PG, sinr, signal, status);
+    k_sinr_users<T, MP, PGM, QLP><<<(unsigned)blocks, threads, smem, st>>>(t, spc, nslices, fc, Ftot, f0, sigma,
+                                                                           (const cplx_t<T>*)H, PG, sinr, signal, status);
     return cudaGetLastError();
+}
+
+template <class T, int MP, bool PGM>
+static cudaError_t launch_users_mp(const Topo& t, int64_t nslices, int fc, int64_t Ftot, int64_t f0, double sigma,
+                                   const void* H, const double2* PG, double* sinr, double* signal, int* status,
+                                   cudaStream_t st) {
+    if constexpr (PGM && MP == 8) {
+        // packed QL when a CTA holds one slice (C4: 32 users x 8 lanes), warp-local otherwise (see phase 1c)
+        static const int force = [] {
+            const char* v = env_once("GWT_QL_PACKED");
+            return v ? std::atoi(v) : -1;
+        }();
+        const bool packed = force >= 0 ? force != 0 : t.users() * MP >= 256;
+        if (packed) return launch_users_qlp<T, MP, PGM, true>(t, nslices, fc, Ftot, f0, sigma, H, PG, sinr, signal, status, st);
+    }
+    return launch_users_qlp<T, MP, PGM, false>(t, nslices, fc, Ftot, f0, sigma, H, PG, sinr, signal, status, st);
 }
 
 template <class T>
