@@ -23,8 +23,9 @@
 //
 // CTA = (user, group); it walks the subcarrier tiles and, per tile, its J "jobs": job 0 = the
 // serving link, job k = (interfering link (k,i,j), anchor link (k,k,0)). Warp roles:
-//   warp 8  (one thread): TMA producer   E tile (A) per job, G chunk (B) per chunk, 2 B stages
-//   warp 9  (one thread): MMA issuer     per chunk 3 passes x p/4 k-steps x slots
+//   warp 8  (whole warp, elect.sync issue): MMA issuer  per chunk 3 passes x p/4 k-steps x slots; loads the job's
+//                         E tiles (A) itself
+//   warp 9  (one thread): TMA producer   G chunk (B) per chunk, 2 B stages
 //   warps 0-7           : Gram epilogue  two threads per subcarrier (TMEM lane quarter = warp % 4);
 //                         tcgen05.ld -> binary64 -> DFMA accumulation of the entries of its rows
 // Binary64 accumulation of the exact products of the fp32 H~ values keeps the Gram route free of
