@@ -52,6 +52,16 @@ __device__ __forceinline__ double frcp(double x) {
     return fma(y, fma(-x, y, 1.0), y);
 }
 
+// binary64 reciprocal square root of a positive normal number: MUFU seed (~2^-22) + two Newton steps, no special-case
+// branches (libdevice's rsqrt carries a slow path and was the top stall line of the QL chain)
+__device__ __forceinline__ double frsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = fma(y, fma(-hx * y, y, 0.5), y);
+    return fma(y, fma(-hx * y, y, 0.5), y);
+}
+
 // Implicit QL (tql2 with Wilkinson shift) on the real tridiagonal (d, e); this lane rotates RL rows of Z
 // (rows row0 .. row0 + RL - 1). `valid` lanes only; every lane of the warp must call it (warp votes).
 template <int MP, int RL>
@@ -70,7 +80,7 @@ __device__ __forceinline__ void ql_rows(double (&dg)[MP], double (&eo)[MP], doub
             if (go) {
                 double g = (dg[l + 1] - dg[l]) * (0.5 * frcp(eo[l]));
                 const double t1 = fma(g, g, 1.0);
-                double rr = t1 * rsqrt(t1);
+                double rr = t1 * frsqrt(t1);
                 double dm = dg[MP - 1];
 #pragma unroll
                 for (int k = l + 1; k < MP - 1; ++k)
@@ -83,8 +93,8 @@ __device__ __forceinline__ void ql_rows(double (&dg)[MP], double (&eo)[MP], doub
                     if (i < mm && !brk) {
                         const double f = s * eo[i], b = c * eo[i];
                         const double t2 = f * f + g * g;
-                        const double inv = rsqrt(t2);
-                        rr = t2 * inv;
+                        const double inv = frsqrt(t2);
+                        rr = t2 == 0.0 ? 0.0 : t2 * inv;
                         eo[i + 1] = rr;
                         if (t2 == 0.0) {
                             dg[i + 1] -= p;
@@ -242,12 +252,16 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
         double beta = alpha.x;
         double2 v = make_double2(r == i + 1 ? 1.0 : 0.0, 0.0);
         if (xn2 > 0.0 || alpha.y != 0.0) {
-            const double nrm = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xn2);
+            // branch-free reciprocals / square roots (MUFU seed + Newton, ~1 ulp): the division and sqrt sequences
+            // of libdevice sit on the serial chain of every reflector
+            const double s2n = fmax(alpha.x * alpha.x + alpha.y * alpha.y + xn2, 1e-280);
+            const double nrm = s2n * frsqrt(s2n);
             beta = alpha.x >= 0.0 ? -nrm : nrm;
-            tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+            const double rb = frcp(beta);
+            tau = make_double2((beta - alpha.x) * rb, -alpha.y * rb);
             // scale = 1 / (alpha - beta)
             const double2 am = make_double2(alpha.x - beta, alpha.y);
-            const double den = 1.0 / (am.x * am.x + am.y * am.y);
+            const double den = frcp(am.x * am.x + am.y * am.y);
             const double2 sc = make_double2(am.x * den, -am.y * den);
             if (r > i + 1) v = dmul(xr, sc);
         }
@@ -554,12 +568,13 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
         if (kc < m) {
             const double dkk = __shfl_sync(0xffffffffu, q[kc].x, (lane & ~(MP - 1)) + kc);
             pd = pd && (dkk > 0.0);
-            const double lkk = sqrt(fmax(dkk, 1e-300));
+            const double dk = fmax(dkk, 1e-300);
+            const double rl = frsqrt(dk), lkk = dk * rl;  // 1 / L_kk rides in the (otherwise zero) imaginary slot
             dmax = fmax(dmax, lkk);
             dmin = fmin(dmin, lkk);
             double2 lrk;
-            if (r == kc) lrk = make_double2(lkk, 0.0);
-            else lrk = make_double2(q[kc].x / lkk, q[kc].y / lkk);
+            if (r == kc) lrk = make_double2(lkk, rl);
+            else lrk = make_double2(q[kc].x * rl, q[kc].y * rl);
             if (r >= kc) sLf[r * (MP + 1) + kc] = lrk;
             __syncwarp();
             if (r > kc && r < m) {
@@ -599,8 +614,8 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
                         acc2.x -= pr.x;
                         acc2.y -= pr.y;
                     }
-                    const double laa = sLf[a * (MP + 1) + a].x;
-                    yv[a] = make_double2(acc2.x / laa, acc2.y / laa);
+                    const double rla = sLf[a * (MP + 1) + a].y;  // 1 / L_aa
+                    yv[a] = make_double2(acc2.x * rla, acc2.y * rla);
                     nn += yv[a].x * yv[a].x + yv[a].y * yv[a].y;
                 } else {
                     yv[a] = make_double2(0.0, 0.0);
