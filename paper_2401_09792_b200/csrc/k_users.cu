@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
             const double2* U2 = reinterpret_cast<const double2*>(sb2 + lay.u_off) + (k * K) * L * MP;
             const double* l2 = reinterpret_cast<const double*>(sb2 + lay.lam_off) + (k * K) * MP;
             const double lam = l2[l];
-            const double sc = lam > 0.0 ? 1.0 / sqrt(lam) : 0.0;
+            const double sc = lam > 0.0 ? frsqrt(fmax(lam, 1e-300)) : 0.0;
             const double2 v = U2[l * MP + a];
             reinterpret_cast<double2*>(sb2 + lay.v_off)[(k * MP + a) * L + l] = make_double2(v.x * sc, v.y * sc);
         }
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
                 double2 s = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int a = 0; a < MP; ++a) cfmaconj(s, h[a], U2[l * MP + a]);
-                const double sc = lam > 0.0 ? 1.0 / sqrt(lam) : 0.0;
+                const double sc = lam > 0.0 ? frsqrt(fmax(lam, 1e-300)) : 0.0;
                 V2[l] = from_d2<C>(make_double2(s.x * sc, s.y * sc));
             }
         }
@@ -592,8 +592,15 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     }
     if (!finite) st = 4;
     else if (!pd) st = 1;
-    else if ((dmax / dmin) * (dmax / dmin) > 1e14) st = 2;
-    const int64_t g = sl_c / fc, fl = sl_c % fc;
+    else if (dmax * dmax > 1e14 * (dmin * dmin)) st = 2;  // (dmax / dmin)^2 > 1e14 without the divisions
+    int64_t g, fl;
+    if (sl_c < (int64_t(1) << 31)) {  // 32-bit division when the slice index allows it
+        g = (uint32_t)sl_c / (uint32_t)fc;
+        fl = (uint32_t)sl_c % (uint32_t)fc;
+    } else {
+        g = sl_c / fc;
+        fl = sl_c % fc;
+    }
     const int64_t orow = (g * Ftot + f0 + fl) * U + u;
     int st3 = 0;
     if (active && r < L) {
@@ -627,7 +634,7 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
         double den = gamma * (1.0 - gamma);
         if (den <= -1e-12 && st == 0) st3 = 3;
         den = fmax(den, 2.2250738585072014e-308);
-        sinr[orow * L + r] = sp / den;
+        sinr[orow * L + r] = sp * frcp(den);
         signal[orow * L + r] = sp;
     }
     // code 3 carries the first failing stream (the user's lowest lane) in bits 8+
