@@ -398,6 +398,22 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
             }
         }
     }
+    // PG mode: the pair Gram of the first interfering cell is copied asynchronously into the user's (now free)
+    // Householder area, entry (row, b) at b (MP + 1) + row, so its global-memory latency passes behind the ranking,
+    // the CTA barriers and the anchor precoders without holding registers (at its use in phase 3 the plain loads
+    // were 14 % of the kernel's stall samples)
+    if constexpr (PGM) {
+        __syncwarp();  // every lane of the user is done with the Householder vectors
+        if (J > 1 && active && r < m) {
+#pragma unroll
+            for (int b = 0; b < MP; ++b)
+                if (b < m) {
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(sA + b * (MP + 1) + r);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(Pu + MM + r + m * b) : "memory");
+                }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     // rank (descending, lower index first on ties) over the real rows; keep the top L
     {
         const double lam = dg[0];
@@ -504,12 +520,17 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
 #pragma unroll
         for (int l = 0; l < MP; ++l) yrow[l] = czero<C>();
         if constexpr (PGM) {
-            const double2* Xg = Pu + (int64_t)(1 + (k < i_cell ? k : k - 1)) * MM;  // slot of cell k
+            const int slot = 1 + (k < i_cell ? k : k - 1);
+            const double2* Xg = Pu + (int64_t)slot * MM;  // slot of cell k
+            if (slot == 1) {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncwarp();
+            }
             if (active && r < m) {
 #pragma unroll
                 for (int b = 0; b < MP; ++b) {
                     if (b < m) {
-                        const double2 xv = Xg[r + m * b];
+                        const double2 xv = slot == 1 ? sA[b * (MP + 1) + r] : Xg[r + m * b];
                         const double2* wb = Vk + (size_t)b * L;
 #pragma unroll
                         for (int l = 0; l < MP; ++l)
