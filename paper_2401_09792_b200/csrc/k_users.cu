@@ -28,6 +28,10 @@
 
 #include "kernels.cuh"
 
+#ifndef GWT_QL_LANES
+#define GWT_QL_LANES 4  // lanes per user in the packed QL phase (each rotates MP / GWT_QL_LANES rows of Z)
+#endif
+
 namespace gwtk {
 
 namespace {
@@ -314,12 +318,14 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     // the last step (i = MP-2) may leave a complex phase only through tau (|1 - tau| = 1): e is real.
 
     // ---------------- phase 1c: implicit QL (tql2) on (dg, eo).
-    // QLP = false (warp-local): the recurrence is replicated over the user's MP lanes (identical inputs -> identical
-    // results), lane r rotating row r of Z; no CTA barrier. QLP = true (packed): 2 lanes per user, each rotating
-    // MP / 2 rows of Z, on the first 2 U spc threads of the CTA behind two CTA barriers — a quarter of the
-    // binary64 warp instructions. Measured per 64 groups: C4 (32 users, one slice per CTA; fp64 pipe 42 % busy in
-    // the warp-local form) packed 42.6 vs 45.3 ms, and 337 vs 398 ms on the whole config; C3 (16 users, 2 slices
-    // per CTA) warp-local 9.2 vs 10.3 ms. The launcher picks by slices per CTA (GWT_QL_PACKED=0/1 overrides).
+    // QLP = true (packed, default): GWT_QL_LANES = 4 lanes per user, each rotating MP / 4 rows of Z, on the first
+    // 4 U spc threads of the CTA behind two CTA barriers. QLP = false (warp-local): the recurrence replicated over the
+    // user's MP lanes, lane r rotating row r of Z; no CTA barrier, but twice the binary64 warp instructions (fp64 pipe
+    // 42 % busy). A warp advances its users in lockstep (every user of the warp converges on eigenvalue l before l + 1),
+    // so fewer users per warp shorten the phase while more lanes per user replicate the recurrence. Measured per 64
+    // groups (C4 / C3 solve): 1 lane 51.6 / 10.5 ms, 2 lanes 35.8 / -, 4 lanes 33.6 / 7.5, 8 lanes (warp-local)
+    // 38.5 / 7.6; on the whole C4 config the warp-local form ran 398 ms against 337 ms for 2 packed lanes.
+    // GWT_QL_PACKED=0 selects the warp-local form.
     if constexpr (QLP) {
         double* stri = reinterpret_cast<double*>(sbase + lay.tri_off) + u * 2 * MP;
         if (r == 0) {
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
             }
         }
         __syncthreads();
-        constexpr int LQ = 2, RL = MP / LQ;
+        constexpr int LQ = GWT_QL_LANES, RL = MP / LQ;
         const int nql = spc * U * LQ;
         if (tid < ((nql + 31) & ~31)) {
             const bool qv = tid < nql;
@@ -696,12 +702,11 @@ static cudaError_t launch_users_mp(const Topo& t, int64_t nslices, int fc, int64
                                    const void* H, const double2* PG, double* sinr, double* signal, int* status,
                                    cudaStream_t st) {
     if constexpr (PGM && MP == 8) {
-        // packed QL when a CTA holds one slice (C4: 32 users x 8 lanes), warp-local otherwise (see phase 1c)
         static const int force = [] {
             const char* v = env_once("GWT_QL_PACKED");
             return v ? std::atoi(v) : -1;
         }();
-        const bool packed = force >= 0 ? force != 0 : t.users() * MP >= 256;
+        const bool packed = force != 0;  // see phase 1c
         if (packed) return launch_users_qlp<T, MP, PGM, true>(t, nslices, fc, Ftot, f0, sigma, H, PG, sinr, signal, status, st);
     }
     return launch_users_qlp<T, MP, PGM, false>(t, nslices, fc, Ftot, f0, sigma, H, PG, sinr, signal, status, st);
