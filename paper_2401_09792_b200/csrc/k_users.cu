@@ -323,8 +323,9 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
     // user's MP lanes, lane r rotating row r of Z; no CTA barrier, but twice the binary64 warp instructions (fp64 pipe
     // 42 % busy). A warp advances its users in lockstep (every user of the warp converges on eigenvalue l before l + 1),
     // so fewer users per warp shorten the phase while more lanes per user replicate the recurrence. Measured per 64
-    // groups (C4 / C3 solve): 1 lane 51.6 / 10.5 ms, 2 lanes 35.8 / -, 4 lanes 33.6 / 7.5, 8 lanes (warp-local)
-    // 38.5 / 7.6; on the whole C4 config the warp-local form ran 398 ms against 337 ms for 2 packed lanes.
+    // groups (C4 / C3 solve): 1 lane 51.6 / 10.5 ms, 2 lanes 35.8 / -, 4 lanes 33.6 / 7.5, warp-local - / 7.6
+    // (C4 warp-local against 2 packed lanes, before the fast reciprocals: 45.3 vs 42.6 ms, and 398 vs 337 ms on the
+    // whole 512-group config).
     // GWT_QL_PACKED=0 selects the warp-local form.
     if constexpr (QLP) {
         double* stri = reinterpret_cast<double*>(sbase + lay.tri_off) + u * 2 * MP;
