@@ -88,4 +88,23 @@ struct Topo {
     __host__ __device__ int links() const { return J * J * K; }
 };
 
+// binary64 reciprocal: MUFU seed + two Newton steps (no division sequence on the QL's serial chain)
+__device__ __forceinline__ double frcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(y, fma(-x, y, 1.0), y);
+    return fma(y, fma(-x, y, 1.0), y);
+}
+
+// binary64 reciprocal square root of a positive normal number: MUFU seed (~2^-22) + two Newton steps, no special-case
+// branches (libdevice's rsqrt carries a slow path and was the top stall line of the QL chain)
+__device__ __forceinline__ double frsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = fma(y, fma(-hx * y, y, 0.5), y);
+    return fma(y, fma(-hx * y, y, 0.5), y);
+}
+
+
 }  // namespace gwtk

@@ -682,7 +682,7 @@ __device__ __forceinline__ void mmse_item(const Topo& t, int scope, int S, int64
                 st = st ? st : 5;
                 continue;
             }
-            const double sc = 1.0 / sqrt(lr);
+            const double sc = frsqrt(fmax(lr, 1e-300));
             double2 z[M];  // z = X u'_r / sqrt(lambda'_r)  (= H~_{kij} v_{kl,r})
 #pragma unroll
             for (int a = 0; a < M; ++a) {
@@ -712,11 +712,11 @@ __device__ __forceinline__ void mmse_item(const Topo& t, int scope, int S, int64
 #pragma unroll
         for (int k2 = 0; k2 < c; ++k2) d -= Q[c][k2].x * Q[c][k2].x + Q[c][k2].y * Q[c][k2].y;
         pd = pd && (d > 0.0);
-        const double lcc = sqrt(fmax(d, 1e-300));
+        const double dc = fmax(d, 1e-300);
+        const double inv = frsqrt(dc), lcc = dc * inv;  // 1 / L_cc rides in the diagonal's imaginary slot
         dmax = fmax(dmax, lcc);
         dmin = fmin(dmin, lcc);
-        Q[c][c] = make_double2(lcc, 0.0);
-        const double inv = 1.0 / lcc;
+        Q[c][c] = make_double2(lcc, inv);
 #pragma unroll
         for (int r = c + 1; r < M; ++r) {
             double2 s = Q[r][c];
@@ -732,7 +732,7 @@ __device__ __forceinline__ void mmse_item(const Topo& t, int scope, int S, int64
     }
     if (!finite) st = 4;
     else if (!pd) st = 1;
-    else if ((dmax / dmin) * (dmax / dmin) > 1e14) st = 2;
+    else if (dmax * dmax > 1e14 * (dmin * dmin)) st = 2;
     // output row: items are (g, f in chunk, u); outputs are [g][Ftot][users]
     const int64_t g = gf / fc, fl = gf % fc;
     const int64_t orow = (g * Ftot + f0 + fl) * users + u;
@@ -753,7 +753,7 @@ __device__ __forceinline__ void mmse_item(const Topo& t, int scope, int S, int64
                     acc.x -= pr.x;
                     acc.y -= pr.y;
                 }
-                y[a] = make_double2(acc.x / Q[a][a].x, acc.y / Q[a][a].x);
+                y[a] = make_double2(acc.x * Q[a][a].y, acc.y * Q[a][a].y);
             }
             double nn = 0.0;
 #pragma unroll
@@ -764,7 +764,7 @@ __device__ __forceinline__ void mmse_item(const Topo& t, int scope, int S, int64
         double den = gamma * (1.0 - gamma);  // w^H Q w - |w^H g|^2
         if (den <= -1e-12 && st == 0) st = 3 + (r << 8);  // code 3, first failing stream in bits 8+
         den = fmax(den, 2.2250738585072014e-308);
-        so[r] = sp / den;
+        so[r] = sp * frcp(den);
         sg[r] = sp;
     }
     status[orow] = st;
@@ -889,13 +889,13 @@ __global__ void __launch_bounds__(256) k_small_grp(Topo t, int scope, int S, int
             double c = 1.0, sn = 0.0, phr = 1.0, phi = 0.0;
             const double b2 = apq.x * apq.x + apq.y * apq.y;
             if (b2 > 1e-300) {
-                const double rb = rsqrt(b2);
+                const double rb = frsqrt(b2);
                 phr = apq.x * rb;
                 phi = apq.y * rb;
                 const float tau = (float)((aqq.x - app.x) * (0.5 * rb));
                 const float tf = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 1.0f)));
                 const double tt = (double)tf;
-                c = rsqrt(fma(tt, tt, 1.0));
+                c = frsqrt(fma(tt, tt, 1.0));
                 sn = tt * c;
             }
             const double2 uqp = make_double2(-sn * phr, sn * phi), uqq = make_double2(c * phr, -c * phi);
@@ -1050,7 +1050,7 @@ __global__ void __launch_bounds__(256) k_small_grp(Topo t, int scope, int S, int
     __syncwarp();
     if (!finite) st = 4;
     else if (!pd) st = 1;
-    else if ((dmax / dmin) * (dmax / dmin) > 1e14) st = 2;
+    else if (dmax * dmax > 1e14 * (dmin * dmin)) st = 2;
     const int64_t gf = item / users;
     const int64_t g = gf / fc, fl = gf % fc;
     const int64_t orow = (g * Ftot + f0 + fl) * users + u;

@@ -48,24 +48,6 @@ template <int MP> __device__ __forceinline__ double seg_sum(double v) {
 
 __device__ __forceinline__ double2 dmul(double2 a, double2 b) { return cmul(a, b); }
 
-// binary64 reciprocal: MUFU seed + two Newton steps (no division sequence on the QL's serial chain)
-__device__ __forceinline__ double frcp(double x) {
-    double y;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    y = fma(y, fma(-x, y, 1.0), y);
-    return fma(y, fma(-x, y, 1.0), y);
-}
-
-// binary64 reciprocal square root of a positive normal number: MUFU seed (~2^-22) + two Newton steps, no special-case
-// branches (libdevice's rsqrt carries a slow path and was the top stall line of the QL chain)
-__device__ __forceinline__ double frsqrt(double x) {
-    double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    const double hx = 0.5 * x;
-    y = fma(y, fma(-hx * y, y, 0.5), y);
-    return fma(y, fma(-hx * y, y, 0.5), y);
-}
-
 // Implicit QL (tql2 with Wilkinson shift) on the real tridiagonal (d, e); this lane rotates RL rows of Z
 // (rows row0 .. row0 + RL - 1). `valid` lanes only; every lane of the warp must call it (warp votes).
 template <int MP, int RL>

@@ -53,12 +53,12 @@ __device__ __forceinline__ void jacobi_herm(double2 (&A)[M][M], double2 (&V)[M][
                 if (b2 > 1e-300) {
                     // rotation angle in fp32 (only the convergence rate depends on it); the rotation
                     // itself (unit phase, c = 1/sqrt(1+t^2), s = t c) is exact in binary64
-                    const double rb = rsqrt(b2);
+                    const double rb = frsqrt(b2);
                     const double phr = aqp.x * rb, phi = -aqp.y * rb;  // phase = apq/|apq|
                     const float tau = (float)((A[q][q].x - A[p][p].x) * (0.5 * rb));
                     const float tf = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 1.0f)));
                     const double tt = (double)tf;
-                    const double c = rsqrt(fma(tt, tt, 1.0));
+                    const double c = frsqrt(fma(tt, tt, 1.0));
                     const double s = tt * c;
                     // U = [[c, s], [-s conj(ph), c conj(ph)]]
                     const double2 uqp = make_double2(-s * phr, s * phi);
