@@ -419,25 +419,22 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
             slam[u * MP + rank] = fmax(lj, 0.0);
 #pragma unroll
             for (int a = 0; a < MP; ++a) sU[(u * L + rank) * MP + a] = uv[a];
+            if constexpr (PGM) {
+                // the anchor (k, 0) publishes W'_k = U'_L Lambda'^{-1/2} (m x L) itself: no separate phase, one CTA
+                // barrier less
+                if (j_user == 0) {
+                    const double sc = lj > 0.0 ? frsqrt(fmax(lj, 1e-300)) : 0.0;
+#pragma unroll
+                    for (int a = 0; a < MP; ++a) sV[(i_cell * MP + a) * L + rank] = make_double2(uv[a].x * sc, uv[a].y * sc);
+                }
+            }
         }
     }
     __syncthreads();
 
-    // ---------------- phase 2: anchor precoders V'_k = H~_kk0^H U'_L L'^-1/2 (all threads of the CTA);
-    // PG mode: W'_k = U'_L L'^-1/2 (m x L) instead
-    if constexpr (PGM) {
-        const int per = J * MP * L;
-        for (int e = tid; e < spc * per; e += blockDim.x) {
-            const int s2 = e / per, rem = e % per, k = rem / (MP * L), a = (rem / L) % MP, l = rem % L;
-            unsigned char* sb2 = smem_raw + (size_t)s2 * lay.bytes;
-            const double2* U2 = reinterpret_cast<const double2*>(sb2 + lay.u_off) + (k * K) * L * MP;
-            const double* l2 = reinterpret_cast<const double*>(sb2 + lay.lam_off) + (k * K) * MP;
-            const double lam = l2[l];
-            const double sc = lam > 0.0 ? frsqrt(fmax(lam, 1e-300)) : 0.0;
-            const double2 v = U2[l * MP + a];
-            reinterpret_cast<double2*>(sb2 + lay.v_off)[(k * MP + a) * L + l] = make_double2(v.x * sc, v.y * sc);
-        }
-    } else {
+    // ---------------- phase 2 (H~ mode): anchor precoders V'_k = H~_kk0^H U'_L L'^-1/2 (all threads of the CTA);
+    // PG mode uses W'_k = U'_L L'^-1/2 (m x L), written by the anchors' own lanes above
+    if constexpr (!PGM) {
         const int per = J * n;
         for (int e = tid; e < spc * per; e += blockDim.x) {
             const int s2 = e / per, rem = e % per, k = rem / n, y = rem % n;
@@ -460,8 +457,8 @@ __global__ void __launch_bounds__(256, 2) k_sinr_users(Topo t, int spc, int64_t 
                 V2[l] = from_d2<C>(make_double2(s.x * sc, s.y * sc));
             }
         }
+        __syncthreads();
     }
-    __syncthreads();
 
     // ---------------- phase 3: covariance, Cholesky, per-stream SINR
     int st = 0;

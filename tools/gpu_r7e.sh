@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+echo "anchor precoders at the rank step" > gpurun_out/r7e_ab.log
+timeout 300 python tools/sinr_real.py C4 64 2 3 >> gpurun_out/r7e_ab.log 2>&1
+timeout 300 python tools/sinr_real.py C3 64 2 3 >> gpurun_out/r7e_ab.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_scale.py tests/test_gpu_parity.py -m gpu -q -x > gpurun_out/r7e_pytest.log 2>&1; echo "rc $?" >> gpurun_out/r7e_pytest.log
