@@ -153,3 +153,26 @@ def test_rank_sweep_c5_matches_oracle(ctx):
                                       O.SCOPE_PAPER, nthreads=NT)
         e_oracle = metrics.sinr_error(want_full, want_c)
         assert abs(r.e_c - e_oracle) <= 1e-4 * max(e_oracle, 1e-3), (r.e_c, e_oracle)
+
+
+@pytest.mark.parametrize("name,dt,tol", [("C2", np.complex128, 1e-12), ("C2", np.complex64, 2e-6),
+                                         ("C4", np.complex128, 1e-12), ("C4", np.complex64, 2e-6)])
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_mode_product_baseline_shapes(ctx, name, dt, tol, mode):
+    """gwt::mode_product (tensor.cpp:96-116) at the BASELINE tensor shapes and ranks: a batch of channel tensors
+    [P, N, M] times U^H-shaped factors (rank x dim), against the oracle's mode_product on the same values."""
+    cfg = gw.CONFIGS[name]
+    rng = np.random.default_rng(17 + mode)
+    M, N, P = cfg.M, cfg.N, cfg.P
+    rank = (cfg.m, cfg.n, cfg.p)[mode - 1]
+    d = (M, N, P)[mode - 1]
+    b = 3
+    X = (rng.standard_normal((b, P, N, M)) + 1j * rng.standard_normal((b, P, N, M))).astype(dt)
+    U = (rng.standard_normal((rank, d)) + 1j * rng.standard_normal((rank, d))).astype(dt)
+    Y = ctx.mode_product(X, U, mode)
+    assert Y.dtype == dt
+    for i in range(b):
+        want = O.mode_product(np.transpose(X[i].astype(np.complex128), (2, 1, 0)), U.astype(np.complex128), mode)
+        got = np.transpose(Y[i], (2, 1, 0))
+        assert got.shape == want.shape
+        assert np.max(np.abs(got - want)) <= tol * np.abs(want).max()
