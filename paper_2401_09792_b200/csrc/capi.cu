@@ -43,7 +43,7 @@ struct GwtOptions {
     bool gram_tc = true;                   // GWT_GRAM_TC != 0
     int sinr_path = 0;                     // GWT_SINR_PATH: 0 auto, 1 tc, 2 users, 3 pg
     int64_t sinr_chunk_bytes = int64_t(2) << 30;  // GWT_SINR_CHUNK_BYTES
-    int sinr_pipeline = 4;                 // GWT_SINR_PIPELINE: host-path group chunks
+    int sinr_pipeline = 0;                 // GWT_SINR_PIPELINE: host-path group chunks (0: 8 on the tensor-core path, else 4)
     int sinr_dev_lanes = 0;                // GWT_SINR_DEV_LANES (0: by path)
     int sinr_lanes = 0;                    // GWT_SINR_LANES: host-path compute lanes (0: by path)
     bool sinr_copy_streams = true;         // GWT_SINR_COPY_STREAMS != 0
@@ -835,10 +835,13 @@ void sinr_impl(gwt_ctx* ctx, const gwt_topology* topo, const gwt_ranks* ranks, i
     double *sd = sinr, *sgd = signal;
     int* std_ = (int*)status;
     const int64_t out_rows = ngroups * F * users;
-    const int64_t nch = std::min<int64_t>(ngroups, std::max(1, ctx->opt.sinr_pipeline));
     // two stream lanes overlap the CUDA-core rebuild of one group half with the Gram / eig stages of the
     // other; the tensor-core path keeps every SM busy with one lane (C4: 710 ms single lane vs 839 ms)
     const bool tc_shape = sizeof(T) == 4 && scope == GWT_SCOPE_PAPER && !coeffs && tc_sinr_shape(ctx, t);
+    // host-buffer calls: group chunks through the copy / compute / copy engines; the exposed copies are the first
+    // chunk's H2D and the last chunk's D2H (C4, 10.7 GB per step: 4 / 8 / 16 chunks 610 / 591 / 588 ms against
+    // 557 ms device-resident)
+    const int64_t nch = std::min<int64_t>(ngroups, ctx->opt.sinr_pipeline > 0 ? ctx->opt.sinr_pipeline : (tc_shape ? 8 : 4));
     const int64_t ndev = std::min<int64_t>(ngroups, ctx->opt.sinr_dev_lanes > 0 ? ctx->opt.sinr_dev_lanes : (tc_shape ? 1 : 2));
     if (mem == GWT_MEM_DEVICE && ndev > 1 && !coeffs) {
         // device-resident: group chunks on ndev stream lanes so the FP32-issue-bound rebuild of one
