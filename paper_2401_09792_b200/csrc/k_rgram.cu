@@ -298,27 +298,35 @@ __device__ __forceinline__ void pair_chunk_full(uint32_t col0, int XC, double2 (
     }
 }
 
-template <int MP, int H>
-__device__ __forceinline__ void write_serving(double2* __restrict__ out, int m, const double2 (&acc)[kServAcc<MP>]) {
-#pragma unroll
-    for (int idx = 0; idx < srow_n<MP, H>(); ++idx) {
-        const int row = srow<MP, H>(idx);
-#pragma unroll
-        for (int r2 = 0; r2 < MP; ++r2) {
-            if (r2 <= row) {
-                double2 v = acc[srow_off<MP, H>(idx) + r2];
-                if (r2 == row) v.y = 0.0;
-                out[row + m * r2] = v;
-                if (r2 != row) out[r2 + m * row] = make_double2(v.x, -v.y);
-            }
-        }
-    }
-}
 // 32-byte store (two adjacent double2; sm_100 256-bit global stores): the thread's rows are contiguous per column,
 // and the PG rows of the warp's 32 subcarriers are 64 KB apart, so every store instruction is 32 separate requests
 // (16-byte stores: 8 % of the kernel's stall samples on the LSU queue; C4 R+Gram 41.2 -> 38.9 ms per 64 groups)
 __device__ __forceinline__ void st_pair32(double2* p, double2 a, double2 b) {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
+}
+template <int MP, int H>
+__device__ __forceinline__ void write_serving(double2* __restrict__ out, int m, const double2 (&acc)[kServAcc<MP>]) {
+#pragma unroll
+    for (int idx = 0; idx < srow_n<MP, H>(); ++idx) {
+        const int row = srow<MP, H>(idx);
+        // lower-triangle entries (row, r2 < row): strided by a column, one 16-byte store each
+#pragma unroll
+        for (int r2 = 0; r2 < MP; ++r2)
+            if (r2 < row) out[row + m * r2] = acc[srow_off<MP, H>(idx) + r2];
+        // their conjugates and the diagonal fill column `row`, rows 0..row: contiguous, 32-byte stores
+        double2 cj[MP];
+#pragma unroll
+        for (int r2 = 0; r2 < MP; ++r2)
+            if (r2 <= row) cj[r2] = make_double2(acc[srow_off<MP, H>(idx) + r2].x, r2 == row ? 0.0 : -acc[srow_off<MP, H>(idx) + r2].y);
+#pragma unroll
+        for (int r2 = 0; r2 < MP; r2 += 2) {
+            if (r2 + 1 <= row && m == MP) st_pair32(out + r2 + m * row, cj[r2], cj[r2 + 1]);
+            else {
+                if (r2 <= row) out[r2 + m * row] = cj[r2];
+                if (r2 + 1 <= row) out[r2 + 1 + m * row] = cj[r2 + 1];
+            }
+        }
+    }
 }
 template <int MP, int H>
 __device__ __forceinline__ void write_pair_full(double2* __restrict__ out, int m, const double2 (&acc)[MP * MP / 2]) {
