@@ -141,7 +141,12 @@ __device__ __forceinline__ int sturm_count_p32(int D, const float* d, const floa
 // inverse-iteration arithmetic in the storage precision: fp32 uses the fast reciprocal (the LU of
 // T - lambda I only has to be backward stable; the eigenvalue is the binary64 Rayleigh quotient)
 __device__ __forceinline__ float ii_div(float a, float b) { return __fdividef(a, b); }
-__device__ __forceinline__ double ii_div(double a, double b) { return a * frcp(b); }  // pivots are guarded (>= tiny), ~1 ulp
+// binary64: MUFU-seeded reciprocal (~1 ulp) instead of the division sequence; the seed flushes subnormal inputs, so a
+// (never observed) subnormal divisor is clamped to the smallest magnitude the callers' own `tiny` guards use
+__device__ __forceinline__ double ii_div(double a, double b) {
+    const double bb = fabs(b) < 1e-290 ? copysign(1e-290, b) : b;
+    return a * frcp(bb);
+}
 
 __device__ __forceinline__ int sturm_count_f32(int D, const float* d, const float* e2, float x, float pivmin) {
     int cnt = 0;
